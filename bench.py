@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 DRGraph layout path (driver contract: one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload mesh|rgg|grid|rmat]
+                    [--impl ours|reference]
+
+A *step* is one complete multilevel layout stage of the workload (T iterations at
+every level, coarsest to finest, with prolongation) -- ``value`` is layout
+iterations/s over the K timed steps with the graph, P and the hierarchy resident
+in HBM.  One GPU iteration at level l applies the expected displacement of one
+reference epoch at that level, so iters/s is directly
+comparable with the reference's epochs/s.  ``interactions_per_s`` reports the
+(P-edges + negative samples) updated per second.  ``e2e`` is the same metric
+through the public API (``layout_graph``) from pinned host CSR to host positions,
+preprocessing (k-hop BFS, similarity, hierarchy) and both copies included.
+
+Default workload: BASELINE config C4 (120^3 26-neighbour mesh, k=2, perplexity
+50, M=5, 800 iterations per level, 4 levels) -- the north star's 1-GPU roofline
+target; its level-0 working set (3.5 GB/iteration) is far above the 126 MB L2.
+
+``--impl reference`` times the reference algorithm on the host cores instead (the
+oracle port of _kernels.sgd_steps / sgd_epoch, Hogwild over all threads): each
+step is one epoch at every level of the same hierarchy.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "layout iters/s"
+UNIT = "iters/s"
+
+WORKLOADS = {
+    # name: (description, generator, k, perplexity, iters, M, hierarchy kwargs, init)
+    "grid": dict(desc="C1: 100x100 grid, k=2, perplexity 30, M=5, 300 iterations, single level",
+                 gen=("grid", (100, 100)), k=2, perplexity=30.0, iters=300, M=5,
+                 hier=dict(max_levels=1), init="uniform"),
+    "rgg": dict(desc="C2: RGG 200k (mean degree 10), k=3, perplexity 30, M=5, 500 iterations, "
+                     "3 levels", gen=("rgg", (200_000,)), k=3, perplexity=30.0, iters=500, M=5,
+                hier=dict(max_levels=3), init="normal"),
+    "mesh": dict(desc="C4: 120^3 26-neighbour mesh, k=2, perplexity 50, M=5, 800 iterations per "
+                      "level, 4 levels", gen=("mesh3d", (120,)), k=2, perplexity=50.0, iters=800,
+                 M=5, hier=dict(max_levels=4), init="normal"),
+    "rmat": dict(desc="C5: R-MAT scale 24 edge factor 16, k=1, M=5, 500 iterations, 5 levels",
+                 gen=("rmat", (24, 16)), k=1, perplexity="auto", iters=500, M=5,
+                 hier=dict(force_levels=5, max_levels=5), init="normal"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="mesh", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--iters", type=int, default=None, help="override iterations per level")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--update", default="jacobi", choices=["jacobi", "inplace"])
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = [r.split(", ") for r in (self.out or "").strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        busy = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- workload
+def build_workload(name):
+    from paper_2008_07799_b200 import synthetic
+    w = WORKLOADS[name]
+    fn, args = w["gen"]
+    return getattr(synthetic, fn)(*args)
+
+
+def params_for(name, iters_override=None, update="jacobi"):
+    import paper_2008_07799_b200 as B
+    w = WORKLOADS[name]
+    sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"])
+    opt = B.OptimizerParams(neg_samples=w["M"], iters=iters_override or w["iters"], seed=0,
+                            init=w["init"], update=update)
+    return sim, opt, dict(w["hier"])
+
+
+# ----------------------------------------------------------------------------- CPU arm
+def cpu_reference_setup(ns_host, maps, level_sizes, neg_power=0.75):
+    """Reference-form samplers (optimizer.py:291-300) and level maps for the oracle
+    port of the step loop.  Built from P and the (bit-exact) hierarchy maps."""
+    from oracle import oracle as O
+    samplers = O.build_samplers(ns_host, neg_power)
+    h = O.Hierarchy([_Sized(n) for n in level_sizes], list(maps), 0.8, 16)
+    return samplers, h
+
+
+class _Sized:
+    def __init__(self, n):
+        self.node_count = n
+
+
+def cpu_reference_step(samplers, h, opt, threads):
+    """One epoch at every level (the bounded sample of one layout step)."""
+    from oracle import oracle as O
+    oopt = O.OptimizerParams(neg_samples=opt.neg_samples, gamma=opt.gamma,
+                             gamma_coarsest=opt.gamma_coarsest, iters=opt.iters, b=opt.b,
+                             lr0=opt.lr0, grad_clip=opt.grad_clip, eps=opt.eps, seed=opt.seed,
+                             threads=threads)
+    t0 = time.perf_counter()
+    for level in range(h.depth, -1, -1):
+        n = h.levels[level].node_count
+        pos = np.random.default_rng(level).normal(0, 1.0, size=(n, 2))
+        O.sgd_epoch(pos, h, samplers, oopt, t=opt.iters // 2, level=level, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_prepare_reference(name, sim, opt, hier):
+    """The reference path on the host (oracle port): graph -> k-hop -> P ->
+    hierarchy.  Returns (ns, maps, level sizes, preprocessing seconds)."""
+    from oracle import oracle as O
+    from paper_2008_07799_b200 import synthetic
+    import torch
+    w = WORKLOADS[name]
+    fn, args = w["gen"]
+    if torch.cuda.is_available():   # input generation only (not timed, not the path)
+        g_dev = getattr(synthetic, fn)(*args)
+        g = O.Graph(g_dev.indptr.cpu().numpy(), g_dev.indices.cpu().numpy())
+        del g_dev
+    else:
+        raise RuntimeError("the synthetic generators run on the device")
+    t = {}
+    t0 = time.perf_counter()
+    nd = O.all_k_neighborhoods(g, sim.k)
+    t["khop_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ns = O.build_sparse_similarity(nd, sim.perplexity)
+    del nd
+    t["similarity_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    h = O.build_hierarchy(g, 0.8, 16, O.derive_seed(opt.seed, O.HIERARCHY_TAG), **hier)
+    t["hierarchy_s"] = time.perf_counter() - t0
+    return ns, h.maps, [lv.node_count for lv in h.levels], t
+
+
+def run_reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    name = args.workload
+    sim, opt, hier = params_for(name, args.iters)
+    threads = os.cpu_count() or 1
+    ns, maps, sizes, prep_t = cpu_prepare_reference(name, sim, opt, hier)
+    t0 = time.perf_counter()
+    samplers, h = cpu_reference_setup(ns, maps, sizes, opt.neg_power)
+    prep_t["samplers_s"] = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        cpu_reference_step(samplers, h, opt, threads)
+    times = [cpu_reference_step(samplers, h, opt, threads) for _ in range(args.steps)]
+    total = sum(times)
+    L = len(sizes)
+    value = L * args.steps / total
+    inter = sum(n * (1 + opt.neg_samples) for n in sizes) * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": name, "desc": WORKLOADS[name]["desc"], "levels": sizes,
+                   "step": "one epoch at every level (bounded sample of the layout stage)"},
+        "interactions_per_s": inter,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} x (1 epoch at each of {L} levels), Hogwild "
+                                   f"over {threads} threads (oracle C port of "
+                                   f"_kernels.sgd_steps)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "preprocess_s": prep_t,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2008_07799_b200 as B
+    from paper_2008_07799_b200 import _lib
+    from paper_2008_07799_b200.optimizer import layout_device, prepare_layout
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    name = args.workload
+    sim, opt, hier = params_for(name, args.iters, args.update)
+
+    dg = build_workload(name)
+    torch.cuda.synchronize()
+    prep = prepare_layout(dg, sim, opt, max_levels=hier.get("max_levels"),
+                          force_levels=hier.get("force_levels"), timed=True)
+    plan = prep.plan
+    sizes = prep.hierarchy.sizes
+    nnzs = [lv.nnz for lv in plan.levels]
+    prep_ms = {k: round(v, 3) for k, v in prep.timings.items()}
+    L0 = plan.levels[0]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    lvl_events = {}
+
+    def on_level(level, what):
+        if level == 0:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            lvl_events[what] = e
+
+    def step():
+        return plan.run(group=group, on_level=on_level)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    launches0 = _lib.launch_count()
+    step_ms, l0_ms = [], []
+    sampler = ClockSampler(local)
+    with sampler:
+        for _ in range(args.steps):
+            flush.zero_()                       # L2 flush between steps (untimed)
+            if group is not None:
+                dist.barrier(group)
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            step()
+            e.record()
+            torch.cuda.synchronize()
+            if group is not None:
+                dist.barrier(group)
+            step_ms.append(s.elapsed_time(e))
+            l0_ms.append(lvl_events["start"].elapsed_time(lvl_events["end"]))
+    launches = _lib.launch_count() - launches0
+    total_ms = sum(step_ms)
+    if group is not None:
+        t = torch.tensor([total_ms, sum(l0_ms)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        total_ms, l0_total = float(t[0]), float(t[1])
+    else:
+        l0_total = sum(l0_ms)
+    iters = plan.iterations()
+    value = iters * args.steps / (total_ms / 1e3)
+    inter = plan.interactions() * args.steps / (total_ms / 1e3)
+
+    # roofline of the dominant kernel: K7 at level 0
+    peak, peak_kind = measured_peaks()
+    T = opt.iters
+    l0_launch_s = (l0_total / args.steps / T) / 1e3
+    alg_bytes = L0.algorithmic_bytes(opt.neg_samples)
+    if group is not None:
+        alg_bytes = alg_bytes // world   # rows per rank
+    achieved = alg_bytes / l0_launch_s / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "kernel": "layout_iter_kernel (level 0)",
+                "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes,
+                "launch_us": l0_launch_s * 1e6}
+    prof = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                roofline["traffic"] = json.load(f).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            pass
+
+    # e2e through the public API: pinned host CSR in, host positions out
+    e2e = None
+    if not args.no_e2e:
+        gh = dg.to_host()
+        ip = torch.from_numpy(gh.indptr).pin_memory()
+        ix = torch.from_numpy(gh.indices).pin_memory()
+        g_pinned = B.Graph(ip.numpy(), ix.numpy())
+        h2d = ip.numel() * 8 + ix.numel() * 4
+        d2h = sizes[0] * 2 * 4
+        del prep, plan
+        torch.cuda.empty_cache()
+        kw = dict(max_levels=hier.get("max_levels"), force_levels=hier.get("force_levels"))
+        B.layout_graph(g_pinned, sim, opt, group=group, **kw)      # warm-up
+        walls = []
+        n_e2e = max(1, min(args.steps, 2))
+        for _ in range(n_e2e):
+            if group is not None:
+                dist.barrier(group)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            lay = B.layout_graph(g_pinned, sim, opt, group=group, **kw)
+            walls.append(time.perf_counter() - t0)
+        wall = max(walls) if group is None else walls[-1]
+        if group is not None:
+            tw = torch.tensor([sum(walls) / len(walls)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX, group=group)
+            wall = float(tw[0])
+        else:
+            wall = sum(walls) / len(walls)
+        e2e = {"value": iters / wall, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "wall_s": wall,
+               "interactions_per_s": lay.stats["interactions"] / wall}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_from_gpu(dg, sim, opt, sizes, hier)
+
+    if rank == 0:
+        clocks = sampler.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": name, "desc": WORKLOADS[name]["desc"], "levels": sizes,
+                       "nnz_per_level": nnzs,
+                       "iters_per_level": T, "update": opt.update,
+                       "l2": "256 MiB flush between steps; level-0 stream "
+                             f"{alg_bytes / 1e9:.2f} GB/iteration > 126 MB L2",
+                       "parallelism": f"node-range x{world}" if world > 1 else "single GPU"},
+            "interactions_per_s": inter,
+            "iters_per_step": iters,
+            "gpu_launches": launches,
+            "gpu_launches_per_step": launches / args.steps,
+            "roofline": roofline,
+            "clocks": clocks,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "preprocess_ms": prep_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        dist.barrier(group)
+        dist.destroy_process_group()
+
+
+def cpu_baseline_from_gpu(dg, sim, opt, sizes, hier):
+    """Oracle port of the reference step loop on this box's host cores, on the same
+    P and hierarchy (copied from the device), one epoch at every level."""
+    from oracle import oracle as O
+    from paper_2008_07799_b200.graph import device_k_neighborhoods
+    from paper_2008_07799_b200.multilevel import device_build_hierarchy
+    from paper_2008_07799_b200.optimizer import _HIERARCHY_TAG, _derive_seed
+    from paper_2008_07799_b200.similarity import device_similarity
+    threads = os.cpu_count() or 1
+    ds = device_similarity(device_k_neighborhoods(dg, sim.k), sim)
+    ns = O.SparseSimilarity(ds.indptr.cpu().numpy(), ds.targets.cpu().numpy(),
+                            ds.weights.cpu().numpy(), ds.total_mass, ds.sigma.cpu().numpy(),
+                            ds.k)
+    del ds
+    dh = device_build_hierarchy(dg, 0.8, 16, _derive_seed(opt.seed, _HIERARCHY_TAG),
+                                hier.get("max_levels"), hier.get("force_levels"))
+    maps = [m.cpu().numpy() for m in dh.maps]
+    t0 = time.perf_counter()
+    samplers, h = cpu_reference_setup(ns, maps, sizes, opt.neg_power)
+    setup = time.perf_counter() - t0
+    dt = cpu_reference_step(samplers, h, opt, threads)
+    L = len(sizes)
+    return {"value": L / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"1 epoch at each of {L} levels, Hogwild over {threads} threads "
+                      f"(oracle C port of _kernels.sgd_steps, same P and hierarchy)",
+            "interactions_per_s": sum(n * (1 + opt.neg_samples) for n in sizes) / dt,
+            "setup_s": setup}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * drgraph_b200.h -- C ABI of the B200-native DRGraph layout path.
+ *
+ * One shared library (paper_2008_07799_b200/libdrgraph_b200.so, sm_100a) exports
+ * every entry point below.  The ABI is plain C: raw DEVICE pointers the caller
+ * allocates and owns, sizes as int64_t, and a cudaStream_t passed as `void *`
+ * (NULL = legacy default stream).  Every call returns an int status:
+ *
+ *     DRG_OK (0)            success
+ *     DRG_ERR_INVALID (-1)  bad argument             -> Python ValueError
+ *     DRG_ERR_CUDA (-2)     CUDA runtime error       -> RuntimeError
+ *     DRG_ERR_NONFINITE(-3) non-finite coordinate    -> FloatingPointError
+ *     DRG_ERR_UNSUPPORTED(-4) input outside a kernel tier (e.g. a k-hop ball
+ *                           larger than the block tier holds) -> RuntimeError
+ *     DRG_ERR_NOMEM (-5)    device allocation failed -> MemoryError
+ *
+ * drg_last_error() returns a thread-local message for the last failure.  No C++
+ * exception crosses the ABI.  Variable-size outputs are two-phase (a count call,
+ * then a fill into caller-allocated buffers) or take a documented upper bound.
+ * Calls that return a host scalar synchronise `stream`; all others are
+ * asynchronous on it.  All calls release nothing they did not allocate.
+ *
+ * Each entry point names the reference function it replaces
+ * (/root/reference/pkg/src/drgraph/<file>:<line>).
+ */
+#ifndef DRGRAPH_B200_H
+#define DRGRAPH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DRG_OK 0
+#define DRG_ERR_INVALID (-1)
+#define DRG_ERR_CUDA (-2)
+#define DRG_ERR_NONFINITE (-3)
+#define DRG_ERR_UNSUPPORTED (-4)
+#define DRG_ERR_NOMEM (-5)
+
+#define DRG_ABI_VERSION 1
+
+/* --- library --------------------------------------------------------------- */
+int drg_abi_version(void);
+const char *drg_last_error(void);
+/* Number of kernels this library has launched since it was loaded. */
+uint64_t drg_launch_count(void);
+
+/* --- K1: k-hop neighbourhoods ----------------------------------------------
+ * Replaces all_k_neighborhoods (graph.py:308-366) / bfs_k_neighborhood
+ * (graph.py:280-305).  Input: canonical CSR (graph.py:27-36): indptr int64[n+1],
+ * indices int32[2E], rows sorted.  Output rows hold every node within k hops
+ * (excluding the source) sorted by (dist, id); `cap` > 0 keeps the sorted prefix
+ * of length cap (BASELINE config C3 extension; cap <= 0 = reference behaviour).
+ * Phase 1 writes out_indptr[n+1] (device) and *out_nnz (host); phase 2 fills
+ * out_ids[nnz] / out_dists[nnz].  1 <= k <= 6, n < 2^29. */
+int drg_khop_count(const int64_t *indptr, const int32_t *indices, int64_t n, int k,
+                   int64_t cap, int64_t *out_indptr, int64_t *out_nnz, void *stream);
+int drg_khop_fill(const int64_t *indptr, const int32_t *indices, int64_t n, int k,
+                  int64_t cap, const int64_t *out_indptr, int32_t *out_ids,
+                  int32_t *out_dists, void *stream);
+
+/* --- K2 + K3: Gaussian similarity --------------------------------------------
+ * Replaces build_sparse_similarity (similarity.py:216-278) with search_sigma
+ * (similarity.py:167-199), _row_perplexity (148-164), conditional_similarity_row
+ * (122-145), the k=1 / all-ones closed form (202-213) and
+ * SparseSimilarity.row_masses (84-91).  Input: a NeighborDistances CSR
+ * (graph.py:252-263, mirror-complete rows).  perplexity <= 0 means "auto".
+ * Outputs (device): sigma[n], weights[nnz] (pair masses, bitwise symmetric),
+ * row_mass[n]; host: *out_total_mass (sum of weights), *out_n_nonisolated. */
+int drg_similarity(const int64_t *nd_indptr, const int32_t *nd_ids, const int32_t *nd_dists,
+                   int64_t n, int64_t nnz, int k, double perplexity, double tol,
+                   int max_iter, double sigma_min, double sigma_max, double *out_sigma,
+                   double *out_weights, double *out_row_mass, double *out_total_mass,
+                   int64_t *out_n_nonisolated, void *stream);
+
+/* --- K4: coarsening ------------------------------------------------------------
+ * Replaces coarsen_with_order (multilevel.py:48-79).  `order` (device int64[n])
+ * is the visiting permutation (multilevel.py:91 draws it with numpy PCG64; the
+ * caller passes the same array).  out_parent[n] = coarse id, dense in seed
+ * creation order; *out_n_coarse (host).  Bit-exact with the greedy pass. */
+int drg_coarsen(const int64_t *indptr, const int32_t *indices, int64_t n,
+                const int64_t *order, int32_t *out_parent, int64_t *out_n_coarse,
+                int32_t *out_rounds, void *stream);
+/* Coarse CSR (multilevel.py:70-78 + from_edges graph.py:80-125): deduplicated
+ * images of the fine edges with different parents, rows sorted.  out_indices
+ * must hold nnz(fine) entries (upper bound); *out_nnz (host) is the used size. */
+int drg_coarse_graph(const int64_t *indptr, const int32_t *indices, int64_t n,
+                     const int32_t *parent, int64_t n_coarse, int64_t *out_indptr,
+                     int32_t *out_indices, int64_t *out_nnz, void *stream);
+/* compose_maps step (multilevel.py:116-123): out[i] = second[first[i]]. */
+int drg_compose_maps(const int32_t *first, const int32_t *second, int64_t n, int32_t *out,
+                     void *stream);
+
+/* --- A10: level aggregation ----------------------------
+ * P^l from P^{l-1}: sum of pair masses over (parent[i], parent[j]) with
+ * parent[i] != parent[j].  Output capacity = nnz (upper bound). */
+int drg_aggregate_pairs(const int64_t *indptr, const int32_t *targets, const double *weights,
+                        int64_t n, int64_t nnz, const int32_t *parent, int64_t n_coarse,
+                        int64_t *out_indptr, int32_t *out_targets, double *out_weights,
+                        int64_t *out_nnz, void *stream);
+/* out[c] = sum of values[v] over parent[v] == c (every c has >= 1 child). */
+int drg_aggregate_nodes(const double *values, const int32_t *parent, int64_t n,
+                        int64_t n_coarse, double *out, void *stream);
+
+/* --- A8: negative sampler ------------------------------------------------------
+ * Node weights of build_negative_sampler (optimizer.py:243-259): mass^power,
+ * zero -> 1e-8 * max, power 0 -> uniform.  out_w[n] device. */
+int drg_negative_weights(const double *row_mass, int64_t n, double power, double *out_w,
+                         void *stream);
+/* Vose alias table (optimizer.py:111-139) over weights[n] (device), packed as
+ * uint64 records {float32 threshold (low word), int32 alias (high word)};
+ * *out_total (host, may be NULL) receives the weight sum. */
+int drg_alias_build(const double *weights, int64_t n, uint64_t *out_table, double *out_total,
+                    void *stream);
+
+/* --- K7 / K8: layout iterations --------------------------------------------------
+ * Pack a level for the gradient kernel: rec[e] = {int32 target, float32 2*n*P[e]},
+ * V[a] = n * (R[a] + q_scale * Q[a])  (SURVEY §8(a) A12 expectation-matching
+ * weights; Q may be unnormalised negative weights with q_scale = 1 / sum). */
+int drg_level_pack(const int32_t *targets, const double *P, const double *R, const double *Q,
+                   double q_scale, int64_t n, int64_t nnz, uint64_t *out_rec, float *out_V,
+                   void *stream);
+
+#define DRG_FLAG_INPLACE 1u   /* Hogwild-style in-place update (y_out == y_in) */
+
+/* n_iter node-parallel iterations t = t0 .. t0+n_iter-1 of level `level`
+ * (replaces the sgd_epoch loop of layout_graph, optimizer.py:310-353, 405-407,
+ * and the step kernel _kernels.py:48-141):
+ *   y_a += lr_t * ( sum_b W_ab clip(g_att(y_a, y_b)) + V_a sum_m clip(g_rep(y_a, y_cm)) )
+ * lr_t = lr0 * max(1 - t/iters, 0); negatives c_m ~ alias table, Philox keyed by
+ * (seed, level, t, node, m, attempt), redrawn up to 9 times if c_m == a.
+ * Only rows [row_lo, row_hi) are updated (node-range sharding).  Jacobi: reads
+ * y_in, writes y_out (ping-pong; the result is in y_out).  With
+ * DRG_FLAG_INPLACE, y_in must equal y_out.  neg_idx (optional, n*M int32, -1 =
+ * skip) replaces the sampled negatives (parity mode, n_iter must be 1).
+ * nonfinite (optional device int, init INT_MAX) receives the first t whose
+ * update produced a non-finite coordinate. */
+int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, const float *V,
+                     const uint64_t *alias, int64_t n, int64_t row_lo, int64_t row_hi,
+                     float *y_in, float *y_out, int t0, int n_iter, int iters, double lr0,
+                     double gamma, double eps, double clip, int b, int M, uint64_t seed,
+                     int level, const int32_t *neg_idx, int32_t *nonfinite, unsigned flags,
+                     void *stream);
+
+/* --- K6: prolongation ---------------------------------------------------------------
+ * _layout_radius (optimizer.py:356-358): max distance to the centroid (host). */
+int drg_layout_radius(const float *y, int64_t n, double *out_radius, void *stream);
+/* prolong (multilevel.py:126-138): y_fine[i] = y_coarse[parent[i]] + N(0, jitter)
+ * (Philox Box-Muller keyed by (seed, i); jitter <= 0 copies). */
+int drg_prolong(const float *y_coarse, const int32_t *parent, int64_t n_fine, double jitter,
+                uint64_t seed, float *y_fine, void *stream);
+
+/* --- graph construction and diagnostics ---------------------------------------------
+ * from_edges (graph.py:80-125): canonical CSR from m (u, v) pairs (device int64
+ * [m][2]), self-loops dropped, duplicates and reversed pairs merged, rows sorted.
+ * out_indices must hold 2*m entries; *out_nnz (host) = 2 * edge_count.  Ids must
+ * lie in [0, n). */
+int drg_from_edges(const int64_t *pairs, int64_t m, int64_t n, int64_t *out_indptr,
+                   int32_t *out_indices, int64_t *out_nnz, void *stream);
+/* connected_components (graph.py:369-388): out_labels[n] (device, may be NULL)
+ * numbered 0..C-1 in first-seen order (component of the smallest unlabelled id),
+ * *out_count (host) = C.  layout_graph uses it for a warning and
+ * stats["components"] (optimizer.py:374-378). */
+int drg_components(const int64_t *indptr, const int32_t *indices, int64_t n,
+                   int32_t *out_labels, int64_t *out_count, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DRGRAPH_B200_H */

@@ -1,0 +1,32 @@
+"""paper_2008_07799_b200: B200-native DRGraph layout path (arxiv 2008.07799).
+
+Drop-in for the reference package ``drgraph`` on its hot path: the same public
+names, signatures, result types and exceptions, computed by hand-written sm_100a
+kernels in ``libdrgraph_b200.so`` (C ABI: include/drgraph_b200.h) -- no CPU path.
+"""
+
+from .graph import (DeviceGraph, DeviceNeighborDistances, Graph, NeighborDistances, ParseError,
+                    all_k_neighborhoods, connected_components, device_from_edges,
+                    device_k_neighborhoods, from_edges)
+from .multilevel import (DeviceHierarchy, Hierarchy, build_hierarchy, coarsen_once,
+                         coarsen_with_order, compose_maps, device_build_hierarchy, prolong)
+from .optimizer import (AliasTable, Layout, LayoutPlan, OptimizerParams, Samplers,
+                        build_alias_table, build_negative_sampler, build_samplers,
+                        layout_device, layout_graph, prepare_layout, sgd_epoch)
+from .similarity import (DeviceSimilarity, SimilarityParams, SparseSimilarity,
+                         build_sparse_similarity, device_similarity)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Graph", "NeighborDistances", "ParseError", "from_edges", "all_k_neighborhoods",
+    "connected_components", "SimilarityParams", "SparseSimilarity", "build_sparse_similarity",
+    "Hierarchy", "coarsen_once", "coarsen_with_order", "build_hierarchy", "compose_maps",
+    "prolong", "OptimizerParams", "Layout", "AliasTable", "build_alias_table",
+    "build_negative_sampler", "build_samplers", "Samplers", "sgd_epoch", "layout_graph",
+    # device-resident API
+    "DeviceGraph", "DeviceNeighborDistances", "DeviceSimilarity", "DeviceHierarchy",
+    "LayoutPlan", "device_from_edges", "device_k_neighborhoods", "device_similarity",
+    "device_build_hierarchy", "prepare_layout", "layout_device",
+    "__version__",
+]

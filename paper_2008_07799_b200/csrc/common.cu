@@ -1,0 +1,31 @@
+// Library state: error messages, launch counter, version.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+namespace drg {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local char g_msg[1024] = "";
+
+int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_msg, sizeof(g_msg), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    int code = (e == cudaErrorMemoryAllocation) ? DRG_ERR_NOMEM : DRG_ERR_CUDA;
+    return fail(code, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+}  // namespace drg
+
+extern "C" int drg_abi_version(void) { return DRG_ABI_VERSION; }
+extern "C" const char *drg_last_error(void) { return drg::g_msg; }
+extern "C" uint64_t drg_launch_count(void) {
+    return drg::g_launches.load(std::memory_order_relaxed);
+}

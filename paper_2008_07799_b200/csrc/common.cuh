@@ -1,0 +1,94 @@
+// Shared helpers for the sm_100a kernels of the DRGraph layout path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "../../include/drgraph_b200.h"
+
+namespace drg {
+
+extern std::atomic<uint64_t> g_launches;
+
+int fail(int code, const char *fmt, ...);
+int cuda_fail(cudaError_t e, const char *what);
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Stream-ordered scratch allocation (freed on the same stream at scope exit).
+struct Scratch {
+    void *p = nullptr;
+    cudaStream_t s;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    Scratch(const Scratch &) = delete;
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    cudaError_t alloc(size_t bytes) {
+        if (p) {
+            cudaFreeAsync(p, s);
+            p = nullptr;
+        }
+        return cudaMallocAsync(&p, bytes ? bytes : 16, s);
+    }
+    template <class T>
+    T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// grid size for warp-per-item kernels: one warp per item, `wpb` warps per block
+inline unsigned warp_grid(int64_t items, int wpb) {
+    int64_t g = ceil_div(items, wpb);
+    if (g < 1) g = 1;
+    if (g > 0x7fffffffLL) g = 0x7fffffffLL;
+    return (unsigned)g;
+}
+
+// ---- Philox4x32-10 counter-based RNG ----------------------------------------
+struct u32x4 {
+    uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ u32x4 philox4x32(u32x4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = u32x4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+__device__ __forceinline__ float u32_to_unit(uint32_t v) {  // [0, 1), 24 bits
+    return (float)(v >> 8) * (1.0f / 16777216.0f);
+}
+
+}  // namespace drg
+
+#define DRG_LAUNCHED(name)                                          \
+    do {                                                            \
+        drg::g_launches.fetch_add(1, std::memory_order_relaxed);   \
+        cudaError_t _e = cudaGetLastError();                        \
+        if (_e != cudaSuccess) return drg::cuda_fail(_e, name);     \
+    } while (0)
+
+#define DRG_CUDA(call)                                              \
+    do {                                                            \
+        cudaError_t _e = (call);                                    \
+        if (_e != cudaSuccess) return drg::cuda_fail(_e, #call);    \
+    } while (0)
+
+#define DRG_TRY(call)                                               \
+    do {                                                            \
+        int _rc = (call);                                           \
+        if (_rc != DRG_OK) return _rc;                              \
+    } while (0)

@@ -1,0 +1,414 @@
+// K7/K8: the node-parallel layout iteration and its level scheduler, K6
+// prolongation + radius, and the negative-sampler tables (A8).
+//
+// K7 replaces the sgd_steps loop (_kernels.py:48-141) driven by sgd_epoch
+// (optimizer.py:310-353).  One reference epoch at level l draws n_l positive
+// pairs ~ P and M negatives ~ Q per pair; its expected displacement of node a is
+//
+//     lr * [ sum_b 2 n_l P^l_ab clip(g_att(a,b)) + M n_l (R_a + Q_a) E_c clip(g_rep(a,c)) ]
+// The kernel applies exactly that, gathering: one warp per node streams the
+// node's CSR row as packed 8-byte records {int32 target, fp32 W_ab = 2 n_l P_ab}
+// (one coalesced LDG.64 per entry) and gathers y_b (8 bytes, L2-resident for
+// every config here), then lanes 0..M-1 draw one negative each (Philox keyed by
+// seed/level/t/node/m/attempt -> alias pick, redraw if c == a, <= 9 attempts like
+// _kernels.py:108-117) and add V_a clip(g_rep).  Warp-shuffle reduction, lane 0
+// writes y_a.  fp32 throughout; per-interaction math follows
+// attractive_gradient / repulsive_gradient (optimizer.py:174-203) with the
+// kernel's clip (_kernels.py:94-101, 126-135).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "common.cuh"
+
+namespace drg {
+namespace {
+
+constexpr int kWpb = 8;  // warps per block of the layout kernel
+
+__device__ __forceinline__ float ipowf(float x, int n) {
+    float r = 1.0f;
+    for (int i = 0; i < n; ++i) r *= x;
+    return r;
+}
+
+__device__ __forceinline__ float clampf(float g, float c) { return fminf(fmaxf(g, -c), c); }
+
+struct IterArgs {
+    const int64_t *indptr;
+    const uint2 *rec;     // {target, W bits}
+    const float *V;
+    const uint2 *alias;   // {prob bits, alias}
+    int64_t n, row_lo, row_hi;
+    float lr, gamma, eps, clip;
+    int b, M;
+    uint32_t key0, key1;
+    uint32_t level;
+    int t;
+    const int32_t *neg_idx;
+    int32_t *nonfinite;
+};
+
+// Draw the m-th negative of node a at iteration t (level-l node id, or -1).
+__device__ __forceinline__ int64_t draw_negative(const IterArgs &A, int64_t a, int m) {
+    for (int attempt = 0; attempt < 9; ++attempt) {
+        u32x4 r = philox4x32(u32x4{(uint32_t)a, (uint32_t)(a >> 32) ^ ((uint32_t)A.t << 1),
+                                   (A.level << 24) | ((uint32_t)m << 8) | (uint32_t)attempt,
+                                   0x5eed1e55u},
+                             A.key0, A.key1);
+        const uint64_t r64 = ((uint64_t)r.x << 32) | r.y;
+        const int64_t idx = (int64_t)__umul64hi(r64, (uint64_t)A.n);
+        const uint2 rec = __ldg(A.alias + idx);
+        const int64_t c = (u32_to_unit(r.z) < __uint_as_float(rec.x)) ? idx : (int64_t)rec.y;
+        if (c != a) return c;
+    }
+    return -1;
+}
+
+template <bool INPLACE>
+__global__ void __launch_bounds__(kWpb * 32)
+    layout_iter_kernel(IterArgs A, const float2 *y_in, float2 *y_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t a = A.row_lo + (int64_t)blockIdx.x * kWpb + (threadIdx.x >> 5);
+    if (a >= A.row_hi) return;
+    const float2 ya = y_in[a];
+    const int64_t lo = __ldg(A.indptr + a), hi = __ldg(A.indptr + a + 1);
+    const float two_b = 2.0f * (float)A.b;
+    float ax = 0.f, ay = 0.f;
+    // attractive: sum_b W_ab clip(g_att(y_a, y_b))
+#pragma unroll 4
+    for (int64_t e = lo + lane; e < hi; e += 32) {
+        const uint2 r = __ldg(A.rec + e);
+        const float2 yb = y_in[r.x];
+        const float dx = ya.x - yb.x, dy = ya.y - yb.y;
+        const float ld2 = dx * dx + dy * dy;
+        if (ld2 > 0.f) {
+            const float pw = ipowf(ld2, A.b - 1);
+            const float coef = -two_b * pw / (1.0f + pw * ld2);
+            const float w = __uint_as_float(r.y);
+            ax += w * clampf(coef * dx, A.clip);
+            ay += w * clampf(coef * dy, A.clip);
+        }
+    }
+    // repulsive: lanes 0..M-1, one negative each
+    float rx = 0.f, ry = 0.f;
+    for (int m = lane; m < A.M; m += 32) {
+        const int64_t c = A.neg_idx ? (int64_t)A.neg_idx[a * A.M + m] : draw_negative(A, a, m);
+        if (c >= 0) {
+            const float2 yc = y_in[c];
+            const float dx = ya.x - yc.x, dy = ya.y - yc.y;
+            const float ld2 = dx * dx + dy * dy;
+            if (ld2 + A.eps > 0.f) {
+                const float pw = ipowf(ld2, A.b - 1);
+                const float coef = A.gamma * two_b / ((ld2 + A.eps) * (1.0f + pw * ld2));
+                rx += clampf(coef * dx, A.clip);
+                ry += clampf(coef * dy, A.clip);
+            }
+        }
+    }
+    const float Va = __ldg(A.V + a);
+    float gx = ax + Va * rx, gy = ay + Va * ry;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        gx += __shfl_xor_sync(kFull, gx, o);
+        gy += __shfl_xor_sync(kFull, gy, o);
+    }
+    if (lane == 0) {
+        float2 out = make_float2(ya.x + A.lr * gx, ya.y + A.lr * gy);
+        if (!isfinite(out.x) || !isfinite(out.y)) {
+            if (A.nonfinite) atomicMin(A.nonfinite, A.t);
+        }
+        y_out[a] = out;
+    }
+}
+
+__global__ void level_pack_kernel(const int32_t *__restrict__ targets, const double *__restrict__ P,
+                                  int64_t nnz, double scale, uint2 *rec) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x)
+        rec[e] = make_uint2((uint32_t)targets[e], __float_as_uint((float)(scale * P[e])));
+}
+
+__global__ void node_pack_kernel(const double *__restrict__ R, const double *__restrict__ Q,
+                                 double q_scale, int64_t n, double scale, float *V) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        V[i] = (float)(scale * (R[i] + q_scale * Q[i]));
+}
+
+// w = mass^power (zero -> 0), block max into *top (optimizer.py:249-255)
+__global__ void neg_pow_kernel(const double *__restrict__ mass, int64_t n, double power, double *w,
+                               unsigned long long *top_bits) {
+    double local = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double m = mass[i];
+        double v = (power == 0.0) ? 1.0 : (m > 0.0 ? pow(m, power) : 0.0);
+        w[i] = v;
+        local = fmax(local, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) local = fmax(local, __shfl_xor_sync(kFull, local, o));
+    if ((threadIdx.x & 31) == 0 && local > 0.0)
+        atomicMax(top_bits, (unsigned long long)__double_as_longlong(local));
+}
+
+// zero -> 1e-8 * top (optimizer.py:256-258); top == 0 -> all ones
+__global__ void neg_floor_kernel(double *w, int64_t n, const unsigned long long *top_bits) {
+    const double top = __longlong_as_double((long long)*top_bits);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (top <= 0.0) w[i] = 1.0;
+        else if (!(w[i] > 0.0)) w[i] = 1e-8 * top;
+    }
+}
+
+__global__ void centroid_kernel(const float2 *__restrict__ y, int64_t n, double *partial) {
+    double sx = 0.0, sy = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float2 v = y[i];
+        sx += v.x;
+        sy += v.y;
+    }
+    typedef cub::BlockReduce<double, 256> BR;
+    __shared__ typename BR::TempStorage t1, t2;
+    double bx = BR(t1).Sum(sx);
+    double by = BR(t2).Sum(sy);
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = bx;
+        partial[2 * blockIdx.x + 1] = by;
+    }
+}
+
+__global__ void radius_kernel(const float2 *__restrict__ y, int64_t n, const double *partial,
+                              int nparts, unsigned long long *rmax_bits) {
+    double cx = 0.0, cy = 0.0;
+    for (int p = 0; p < nparts; ++p) {  // fixed order: deterministic centroid
+        cx += partial[2 * p];
+        cy += partial[2 * p + 1];
+    }
+    cx /= (double)n;
+    cy /= (double)n;
+    double local = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float2 v = y[i];
+        double dx = (double)v.x - cx, dy = (double)v.y - cy;
+        local = fmax(local, sqrt(dx * dx + dy * dy));
+    }
+    for (int o = 16; o > 0; o >>= 1) local = fmax(local, __shfl_xor_sync(kFull, local, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(rmax_bits, (unsigned long long)__double_as_longlong(local));
+}
+
+__global__ void prolong_kernel(const float2 *__restrict__ yc, const int32_t *__restrict__ parent,
+                               int64_t n, float jitter, uint32_t k0, uint32_t k1, float2 *yf) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float2 v = yc[parent[i]];
+        if (jitter > 0.f) {
+            u32x4 r = philox4x32(u32x4{(uint32_t)i, (uint32_t)(i >> 32), 0x9a55u, 0x1e7u}, k0, k1);
+            // Box-Muller: two independent N(0,1)
+            const float u1 = ((float)(r.x >> 8) + 1.0f) * (1.0f / 16777216.0f);  // (0, 1]
+            const float u2 = u32_to_unit(r.y);
+            const float rad = sqrtf(-2.0f * logf(u1));
+            float s, c;
+            sincospif(2.0f * u2, &s, &c);
+            v.x += jitter * rad * c;
+            v.y += jitter * rad * s;
+        }
+        yf[i] = v;
+    }
+}
+
+inline unsigned flat_grid(int64_t n, int threads = 256) {
+    return (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n, threads), 1), kSMs * 32);
+}
+
+}  // namespace
+}  // namespace drg
+
+using namespace drg;
+
+extern "C" int drg_level_pack(const int32_t *targets, const double *P, const double *R,
+                              const double *Q, double q_scale, int64_t n, int64_t nnz,
+                              uint64_t *out_rec, float *out_V, void *stream) {
+    if (n < 0 || nnz < 0) return fail(DRG_ERR_INVALID, "negative size");
+    cudaStream_t st = as_stream(stream);
+    if (nnz > 0) {
+        level_pack_kernel<<<flat_grid(nnz), 256, 0, st>>>(targets, P, nnz, 2.0 * (double)n,
+                                                          reinterpret_cast<uint2 *>(out_rec));
+        DRG_LAUNCHED("level_pack_kernel");
+    }
+    if (n > 0) {
+        node_pack_kernel<<<flat_grid(n), 256, 0, st>>>(R, Q, q_scale, n, (double)n, out_V);
+        DRG_LAUNCHED("node_pack_kernel");
+    }
+    return DRG_OK;
+}
+
+extern "C" int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, const float *V,
+                                const uint64_t *alias, int64_t n, int64_t row_lo, int64_t row_hi,
+                                float *y_in, float *y_out, int t0, int n_iter, int iters,
+                                double lr0, double gamma, double eps, double clip, int b, int M,
+                                uint64_t seed, int level, const int32_t *neg_idx,
+                                int32_t *nonfinite, unsigned flags, void *stream) {
+    if (n <= 0 || n_iter < 0) return DRG_OK;
+    if (row_lo < 0 || row_hi > n || row_lo > row_hi)
+        return fail(DRG_ERR_INVALID, "row range [%lld, %lld) outside [0, %lld)",
+                    (long long)row_lo, (long long)row_hi, (long long)n);
+    if (b < 1 || M < 0 || iters < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
+    if (neg_idx && n_iter != 1) return fail(DRG_ERR_INVALID, "neg_idx needs n_iter == 1");
+    const bool inplace = (flags & DRG_FLAG_INPLACE) != 0;
+    if (inplace && y_in != y_out) return fail(DRG_ERR_INVALID, "in-place needs y_in == y_out");
+    if (!inplace && y_in == y_out) return fail(DRG_ERR_INVALID, "Jacobi needs two buffers");
+    cudaStream_t st = as_stream(stream);
+    IterArgs A;
+    A.indptr = indptr;
+    A.rec = reinterpret_cast<const uint2 *>(rec);
+    A.V = V;
+    A.alias = reinterpret_cast<const uint2 *>(alias);
+    A.n = n;
+    A.row_lo = row_lo;
+    A.row_hi = row_hi;
+    A.gamma = (float)gamma;
+    A.eps = (float)eps;
+    A.clip = (float)clip;
+    A.b = b;
+    A.M = M;
+    A.key0 = (uint32_t)seed;
+    A.key1 = (uint32_t)(seed >> 32);
+    A.level = (uint32_t)level;
+    A.neg_idx = neg_idx;
+    A.nonfinite = nonfinite;
+    const int64_t rows = row_hi - row_lo;
+    if (rows == 0) return DRG_OK;
+    const unsigned grid = (unsigned)ceil_div(rows, kWpb);
+    if (n_iter > 1 && (row_lo != 0 || row_hi != n))
+        return fail(DRG_ERR_INVALID, "n_iter > 1 needs the full row range");
+    float2 *src = reinterpret_cast<float2 *>(y_in);
+    float2 *dst = reinterpret_cast<float2 *>(y_out);
+    if (!inplace && n_iter > 1 && n_iter % 2 == 0) {
+        // Jacobi ping-pong with the last write landing in y_out: an even count
+        // starts from a copy of the input in y_out (y_in becomes scratch).
+        DRG_CUDA(cudaMemcpyAsync(dst, src, sizeof(float2) * (size_t)n, cudaMemcpyDeviceToDevice,
+                                 st));
+        std::swap(src, dst);
+    }
+    for (int j = 0; j < n_iter; ++j) {
+        const int t = t0 + j;
+        A.t = t;
+        A.lr = (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0);  // optimizer.py:322
+        if (inplace) {
+            layout_iter_kernel<true><<<grid, kWpb * 32, 0, st>>>(A, src, src);
+        } else {
+            layout_iter_kernel<false><<<grid, kWpb * 32, 0, st>>>(A, src, dst);
+            std::swap(src, dst);
+        }
+        DRG_LAUNCHED("layout_iter_kernel");
+    }
+    return DRG_OK;
+}
+
+extern "C" int drg_layout_radius(const float *y, int64_t n, double *out_radius, void *stream) {
+    if (n <= 0) return fail(DRG_ERR_INVALID, "empty layout");
+    cudaStream_t st = as_stream(stream);
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 256), 256);
+    Scratch partial(st), rmax(st);
+    DRG_CUDA(partial.alloc(sizeof(double) * 2 * g));
+    DRG_CUDA(rmax.alloc(sizeof(unsigned long long)));
+    DRG_CUDA(cudaMemsetAsync(rmax.p, 0, sizeof(unsigned long long), st));
+    centroid_kernel<<<g, 256, 0, st>>>(reinterpret_cast<const float2 *>(y), n, partial.as<double>());
+    DRG_LAUNCHED("centroid_kernel");
+    radius_kernel<<<flat_grid(n), 256, 0, st>>>(reinterpret_cast<const float2 *>(y), n,
+                                                partial.as<double>(), (int)g,
+                                                rmax.as<unsigned long long>());
+    DRG_LAUNCHED("radius_kernel");
+    unsigned long long bits = 0;
+    DRG_CUDA(cudaMemcpyAsync(&bits, rmax.p, sizeof(bits), cudaMemcpyDeviceToHost, st));
+    DRG_CUDA(cudaStreamSynchronize(st));
+    double r;
+    memcpy(&r, &bits, sizeof(r));
+    *out_radius = r;
+    return DRG_OK;
+}
+
+extern "C" int drg_prolong(const float *y_coarse, const int32_t *parent, int64_t n_fine,
+                           double jitter, uint64_t seed, float *y_fine, void *stream) {
+    if (n_fine <= 0) return DRG_OK;
+    cudaStream_t st = as_stream(stream);
+    prolong_kernel<<<flat_grid(n_fine), 256, 0, st>>>(
+        reinterpret_cast<const float2 *>(y_coarse), parent, n_fine, (float)jitter, (uint32_t)seed,
+        (uint32_t)(seed >> 32), reinterpret_cast<float2 *>(y_fine));
+    DRG_LAUNCHED("prolong_kernel");
+    return DRG_OK;
+}
+
+extern "C" int drg_negative_weights(const double *row_mass, int64_t n, double power,
+                                    double *out_w, void *stream) {
+    if (n <= 0) return DRG_OK;
+    cudaStream_t st = as_stream(stream);
+    Scratch top(st);
+    DRG_CUDA(top.alloc(sizeof(unsigned long long)));
+    DRG_CUDA(cudaMemsetAsync(top.p, 0, sizeof(unsigned long long), st));
+    neg_pow_kernel<<<flat_grid(n), 256, 0, st>>>(row_mass, n, power, out_w,
+                                                 top.as<unsigned long long>());
+    DRG_LAUNCHED("neg_pow_kernel");
+    neg_floor_kernel<<<flat_grid(n), 256, 0, st>>>(out_w, n, top.as<unsigned long long>());
+    DRG_LAUNCHED("neg_floor_kernel");
+    return DRG_OK;
+}
+
+// Vose's alias method (optimizer.py:111-139), host side: the weights come down
+// once per level, the packed table goes back up.  Same stack discipline as the
+// reference (small/large built in index order, pop from the back).
+extern "C" int drg_alias_build(const double *weights, int64_t n, uint64_t *out_table,
+                               double *out_total, void *stream) {
+    if (n <= 0) return fail(DRG_ERR_INVALID, "cannot build an alias table over zero items");
+    cudaStream_t st = as_stream(stream);
+    std::vector<double> w((size_t)n);
+    DRG_CUDA(cudaMemcpyAsync(w.data(), weights, sizeof(double) * (size_t)n,
+                             cudaMemcpyDeviceToHost, st));
+    DRG_CUDA(cudaStreamSynchronize(st));
+    double total = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (w[i] < 0) return fail(DRG_ERR_INVALID, "negative weight");
+        total += w[i];
+    }
+    if (!(total > 0)) return fail(DRG_ERR_INVALID, "all weights are zero");
+    if (out_total) *out_total = total;
+    const double f = (double)n / total;
+    std::vector<double> prob((size_t)n, 1.0);
+    std::vector<int32_t> alias((size_t)n);
+    std::vector<int64_t> small, large;
+    small.reserve((size_t)n);
+    large.reserve((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        w[i] *= f;
+        alias[i] = (int32_t)i;
+    }
+    for (int64_t i = 0; i < n; ++i) (w[i] < 1.0 ? small : large).push_back(i);
+    while (!small.empty() && !large.empty()) {
+        int64_t s = small.back();
+        small.pop_back();
+        int64_t l = large.back();
+        large.pop_back();
+        prob[s] = w[s];
+        alias[s] = (int32_t)l;
+        w[l] = (w[l] + w[s]) - 1.0;
+        (w[l] < 1.0 ? small : large).push_back(l);
+    }
+    for (int64_t i : small) prob[i] = 1.0;
+    std::vector<uint64_t> packed((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        float p = (float)prob[i];
+        uint32_t pb;
+        memcpy(&pb, &p, 4);
+        packed[i] = (uint64_t)pb | ((uint64_t)(uint32_t)alias[i] << 32);
+    }
+    DRG_CUDA(cudaMemcpyAsync(out_table, packed.data(), sizeof(uint64_t) * (size_t)n,
+                             cudaMemcpyHostToDevice, st));
+    DRG_CUDA(cudaStreamSynchronize(st));
+    return DRG_OK;
+}

@@ -1,0 +1,569 @@
+"""Multilevel layout optimisation on the GPU (drop-in for drgraph.optimizer).
+
+``layout_graph`` keeps the reference signature (optimizer.py:361-413) and returns
+the same ``Layout``; everything after ingestion runs on the device:
+
+    K1 k-hop rows -> K2/K3 similarity -> K4 hierarchy -> A10 level aggregation
+    -> per-level Vose tables + packed rows -> K7 iterations (K8 scheduler) -> K6
+    prolongation, coarsest to finest.
+
+One K7 iteration at level l stands in for one reference epoch (n_l sampled
+steps): it applies the epoch's expected displacement.  The
+reference's bitwise splitmix64 trajectories are not reproduced (allowed by the
+north star); parity is single-step (tests/test_gpu_parity.py) and final-layout
+KL / neighbourhood preservation (tests/test_gpu_quality.py).
+
+Multi-GPU: with a torch.distributed process group, levels with at least
+``shard_min_nodes`` nodes are node-range sharded -- each rank updates its rows and
+an all-gather (NCCL over NVLink) refreshes the replicated Y every iteration;
+smaller levels run replicated (identical on every rank, no traffic).
+"""
+
+from __future__ import annotations
+
+import logging
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import _lib
+from .graph import DeviceGraph, Graph, device_components, device_k_neighborhoods
+from .multilevel import (DeviceHierarchy, Hierarchy, compose_maps, device_build_hierarchy,
+                         device_prolong)
+from .similarity import (DeviceSimilarity, SimilarityParams, SparseSimilarity,
+                         device_similarity)
+
+logger = logging.getLogger("drgraph")
+
+_HIERARCHY_TAG = 1
+_INIT_TAG = 2
+_JITTER_TAG = 3
+_EPOCH_TAG = 4
+_INT_MAX = 2**31 - 1
+
+
+def _derive_seed(seed: int, *tags: int) -> int:
+    """Deterministic uint64 child seed (optimizer.py:32-34)."""
+    return int(np.random.SeedSequence([seed, *tags]).generate_state(1, np.uint64)[0])
+
+
+@dataclass
+class OptimizerParams:
+    """optimizer.py:37-74 (same fields, defaults and validation) plus B200
+    extensions: ``init`` ("normal" = reference N(0, init_scale); "uniform" =
+    U[-init_scale, init_scale], BASELINE config C1), ``update`` ("jacobi" =
+    deterministic double buffer; "inplace" = Hogwild-style in-place gather, closer
+    to the reference's sequential order), ``shard_min_nodes`` (multi-GPU).
+    ``threads`` is accepted and ignored (the GPU replaces the Hogwild threads)."""
+
+    neg_samples: int = 5
+    gamma: float = 0.1
+    gamma_coarsest: float = 0.01
+    iters: int = 400
+    b: int = 2
+    lr0: float = 1.0
+    grad_clip: float = 5.0
+    eps: float = 1e-3
+    neg_power: float = 0.75
+    init_scale: float = 1e-4
+    jitter_rel: float = 1e-3
+    seed: int = 0
+    threads: int = 1
+    init: str = "normal"
+    update: str = "jacobi"
+    shard_min_nodes: int = 65536
+
+    def __post_init__(self) -> None:
+        if self.neg_samples < 0:
+            raise ValueError("neg_samples must be >= 0")
+        if self.gamma <= 0 or self.gamma_coarsest <= 0:
+            raise ValueError("gamma must be positive")
+        if self.iters < 1:
+            raise ValueError("iters must be >= 1")
+        if self.b < 1:
+            raise ValueError("b must be >= 1")
+        if self.lr0 <= 0:
+            raise ValueError("lr0 must be positive")
+        if self.threads < 1:
+            raise ValueError("threads must be >= 1")
+        if self.seed < 0:
+            raise ValueError("seed must be non-negative")
+        if self.init not in ("normal", "uniform"):
+            raise ValueError("init must be 'normal' or 'uniform'")
+        if self.update not in ("jacobi", "inplace"):
+            raise ValueError("update must be 'jacobi' or 'inplace'")
+
+
+@dataclass
+class Layout:
+    """2-D position per node plus bookkeeping (optimizer.py:77-82)."""
+
+    positions: np.ndarray
+    stats: dict = field(default_factory=dict)
+
+
+@dataclass(frozen=True)
+class AliasTable:
+    """Vose table (optimizer.py:85-108): fp32 thresholds as stored on device."""
+
+    prob: np.ndarray
+    alias: np.ndarray
+    total_weight: float
+
+    def __len__(self) -> int:
+        return len(self.prob)
+
+
+def _alias_device(w: torch.Tensor) -> tuple[torch.Tensor, float]:
+    n = w.numel()
+    table = torch.empty(n, dtype=torch.int64, device=w.device)
+    total = _lib.out_f64()
+    _lib.call("drg_alias_build", _lib.ptr(w), n, _lib.ptr(table), _lib.byref(total),
+              _lib.stream_ptr())
+    return table, total.value
+
+
+def _unpack_alias(table: torch.Tensor, total: float) -> AliasTable:
+    raw = table.cpu().numpy().view(np.uint32).reshape(-1, 2)
+    return AliasTable(raw[:, 0].view(np.float32).astype(np.float64),
+                      raw[:, 1].astype(np.int32), total)
+
+
+def build_alias_table(weights) -> AliasTable:
+    """optimizer.py:111-139 (built by the library's Vose routine)."""
+    w = np.asarray(weights, dtype=np.float64)
+    if len(w) == 0:
+        raise ValueError("cannot build an alias table over zero items")
+    _lib.load()
+    table, total = _alias_device(torch.from_numpy(np.ascontiguousarray(w)).cuda())
+    return _unpack_alias(table, total)
+
+
+def device_negative_weights(row_mass: torch.Tensor, power: float) -> torch.Tensor:
+    """optimizer.py:243-259 weights on device (drg_negative_weights)."""
+    w = torch.empty_like(row_mass)
+    _lib.call("drg_negative_weights", _lib.ptr(row_mass), row_mass.numel(), float(power),
+              _lib.ptr(w), _lib.stream_ptr())
+    return w
+
+
+def build_negative_sampler(ns: SparseSimilarity, power: float = 0.75) -> AliasTable:
+    """O(1) node sampler by (incident mass)**power, floor 1e-8*max (optimizer.py:243-259)."""
+    _lib.load()
+    r = torch.from_numpy(np.ascontiguousarray(ns.row_masses())).cuda()
+    table, total = _alias_device(device_negative_weights(r, power))
+    return _unpack_alias(table, total)
+
+
+# ---------------------------------------------------------------------------
+# per-level device data
+# ---------------------------------------------------------------------------
+
+@dataclass
+class LevelData:
+    """What K7 reads at one level: CSR row offsets, packed {target, W} records,
+    per-node repulsion weight V, and the level's Vose table over Q^l."""
+
+    n: int
+    nnz: int
+    indptr: torch.Tensor   # int64 [n+1]
+    rec: torch.Tensor      # int64 [nnz]  (int32 target | fp32 W << 32)
+    V: torch.Tensor        # fp32 [n]
+    alias: torch.Tensor    # int64 [n]    (fp32 prob | int32 alias << 32)
+
+    def algorithmic_bytes(self, M: int) -> int:
+        """16 B per P entry + (24 + 16 M) B per node (level 0) --
+        col 4 + W 4 + y_j 8 per entry; rowptr 4 + y_a 8 + y_a' 8 + V 4 and per
+        negative an 8 B alias record + 8 B y_c per node."""
+        return 16 * self.nnz + (24 + 16 * M) * self.n
+
+
+def _aggregate_pairs(indptr, targets, weights, parent, n_coarse):
+    n = indptr.numel() - 1
+    nnz = targets.numel()
+    dev = indptr.device
+    o_ip = torch.empty(n_coarse + 1, dtype=torch.int64, device=dev)
+    o_tg = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    o_w = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+    out_nnz = _lib.out_i64()
+    _lib.call("drg_aggregate_pairs", _lib.ptr(indptr), _lib.ptr(targets), _lib.ptr(weights), n,
+              nnz, _lib.ptr(parent), n_coarse, _lib.ptr(o_ip), _lib.ptr(o_tg), _lib.ptr(o_w),
+              _lib.byref(out_nnz), _lib.stream_ptr())
+    k = out_nnz.value
+    return o_ip, o_tg[:k].clone(), o_w[:k].clone()
+
+
+def _aggregate_nodes(values, parent, n_coarse):
+    out = torch.empty(n_coarse, dtype=torch.float64, device=values.device)
+    _lib.call("drg_aggregate_nodes", _lib.ptr(values), _lib.ptr(parent), values.numel(),
+              n_coarse, _lib.ptr(out), _lib.stream_ptr())
+    return out
+
+
+def pack_level(targets, P, R, Wn, q_scale, n) -> tuple[torch.Tensor, torch.Tensor]:
+    nnz = targets.numel()
+    rec = torch.empty(max(nnz, 1), dtype=torch.int64, device=R.device)
+    V = torch.empty(max(n, 1), dtype=torch.float32, device=R.device)
+    _lib.call("drg_level_pack", _lib.ptr(targets), _lib.ptr(P), _lib.ptr(R), _lib.ptr(Wn),
+              float(q_scale), n, nnz, _lib.ptr(rec), _lib.ptr(V), _lib.stream_ptr())
+    return rec[:nnz], V[:n]
+
+
+def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float = 0.75
+                     ) -> list[LevelData]:
+    """P^l, R^l, Q^l for every level, pulled up level by level through the parent
+    maps (drg_aggregate_pairs / drg_aggregate_nodes), then packed (drg_level_pack)
+    with a Vose table per level (drg_alias_build)."""
+    ip, tg, P = ds.indptr, ds.targets, ds.weights
+    R = ds.row_mass
+    Wn = device_negative_weights(R, neg_power)
+    out = []
+    for level in range(dh.depth + 1):
+        n_l = dh.levels[level].node_count
+        if level > 0:
+            parent = dh.maps[level - 1]
+            ip, tg, P = _aggregate_pairs(ip, tg, P, parent, n_l)
+            R = _aggregate_nodes(R, parent, n_l)
+            Wn = _aggregate_nodes(Wn, parent, n_l)
+        alias, total = _alias_device(Wn)
+        rec, V = pack_level(tg, P, R, Wn, 1.0 / total, n_l)
+        out.append(LevelData(n_l, tg.numel(), ip, rec, V, alias))
+    return out
+
+
+StepFn = Callable[[torch.Tensor, torch.Tensor, int, int, int], None]
+
+
+@dataclass
+class LayoutPlan:
+    """Prepared device state of one layout: level data, parent maps, params."""
+
+    levels: list
+    maps: list
+    opt: OptimizerParams
+    nonfinite: torch.Tensor = None
+
+    @property
+    def depth(self) -> int:
+        return len(self.levels) - 1
+
+    def iterations(self) -> int:
+        return self.opt.iters * len(self.levels)
+
+    def interactions(self) -> int:
+        """(P entries + M negatives) updated over the whole layout stage."""
+        M = self.opt.neg_samples
+        return self.opt.iters * sum(L.nnz + M * L.n for L in self.levels)
+
+    def init_positions(self) -> torch.Tensor:
+        """Coarsest-level start (optimizer.py:393-395): the reference's numpy draw
+        (tag 2), so both implementations start from the same Y0."""
+        n = self.levels[-1].n
+        rng = np.random.default_rng(_derive_seed(self.opt.seed, _INIT_TAG))
+        if self.opt.init == "uniform":
+            y = rng.uniform(-self.opt.init_scale, self.opt.init_scale, size=(n, 2))
+        else:
+            y = rng.normal(0.0, self.opt.init_scale, size=(n, 2))
+        return torch.from_numpy(y.astype(np.float32)).cuda()
+
+    def _level_args(self, level: int):
+        L = self.levels[level]
+        o = self.opt
+        gamma = o.gamma_coarsest if level == self.depth else o.gamma   # optimizer.py:321
+        seed = _derive_seed(o.seed, _EPOCH_TAG, level) & 0xFFFFFFFFFFFFFFFF
+        return L, gamma, seed
+
+    def kernel_step(self, level: int, y_in: torch.Tensor, y_out: torch.Tensor, row_lo: int,
+                    row_hi: int, t0: int, n_iter: int = 1, neg_idx: torch.Tensor | None = None,
+                    stream=None) -> None:
+        """drg_layout_iters for iterations t0..t0+n_iter-1 of ``level``."""
+        L, gamma, seed = self._level_args(level)
+        o = self.opt
+        flags = _lib.DRG_FLAG_INPLACE if y_in.data_ptr() == y_out.data_ptr() else 0
+        if self.nonfinite is None:
+            self.nonfinite = torch.full((1,), _INT_MAX, dtype=torch.int32, device=y_in.device)
+        _lib.call("drg_layout_iters", _lib.ptr(L.indptr), _lib.ptr(L.rec), _lib.ptr(L.V),
+                  _lib.ptr(L.alias), L.n, row_lo, row_hi, _lib.ptr(y_in), _lib.ptr(y_out),
+                  t0, n_iter, o.iters, float(o.lr0), float(gamma), float(o.eps),
+                  float(o.grad_clip), o.b, o.neg_samples, seed, level, _lib.ptr(neg_idx),
+                  _lib.ptr(self.nonfinite), flags, _lib.stream_ptr(stream))
+
+    def check_finite(self, level: int) -> None:
+        if self.nonfinite is None:
+            return
+        t = int(self.nonfinite.item())
+        if t != _INT_MAX:
+            self.nonfinite.fill_(_INT_MAX)
+            raise FloatingPointError(f"non-finite coordinate after epoch {t} at level {level}")
+
+    def run_level(self, level: int, y: torch.Tensor, t0: int = 0, n_iter: int | None = None,
+                  group=None, step_fn: StepFn | None = None) -> torch.Tensor:
+        """Iterations t0.. of one level; returns the new positions (y may be reused
+        as scratch).  With a process group of >1 ranks and a level of at least
+        ``shard_min_nodes`` nodes, rows are node-range sharded + all-gathered."""
+        n_iter = self.opt.iters - t0 if n_iter is None else n_iter
+        L = self.levels[level]
+        world = 1
+        if group is not None:
+            import torch.distributed as dist
+            world = dist.get_world_size(group)
+        inplace = self.opt.update == "inplace"
+        if world > 1 and L.n >= self.opt.shard_min_nodes:
+            return self._run_level_sharded(level, y, t0, n_iter, group, step_fn)
+        if step_fn is not None:   # host-injected step (multi-rank CPU tests)
+            out = y if inplace else torch.empty_like(y)
+            a, b = y, out
+            for j in range(n_iter):
+                step_fn(a, b, 0, L.n, t0 + j)
+                if not inplace:
+                    a, b = b, a
+            return a
+        if inplace:
+            self.kernel_step(level, y, y, 0, L.n, t0, n_iter)
+            return y
+        out = torch.empty_like(y)
+        self.kernel_step(level, y, out, 0, L.n, t0, n_iter)
+        return out
+
+    def _run_level_sharded(self, level, y, t0, n_iter, group, step_fn):
+        import torch.distributed as dist
+        L = self.levels[level]
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        chunk = -(-L.n // world)
+        lo, hi = rank * chunk, min(rank * chunk + chunk, L.n)
+        inplace = self.opt.update == "inplace"
+        a = torch.zeros((world * chunk, 2), dtype=torch.float32, device=y.device)
+        a[:L.n] = y
+        b = a if inplace else torch.zeros_like(a)
+        nccl = dist.get_backend(group) == "nccl"
+        for j in range(n_iter):
+            t = t0 + j
+            if step_fn is not None:
+                step_fn(a, b, lo, hi, t)
+            else:
+                self.kernel_step(level, a, b, lo, hi, t, 1)
+            mine = b[rank * chunk:(rank + 1) * chunk]
+            dist.all_gather_into_tensor(b, mine if nccl else mine.clone(), group=group)
+            if not inplace:
+                a, b = b, a
+        return a[:L.n].contiguous()
+
+    def run(self, y0: torch.Tensor | None = None, group=None, step_fn: StepFn | None = None,
+            on_level: Callable | None = None) -> torch.Tensor:
+        """All levels, coarsest to finest (optimizer.py:405-412)."""
+        y = self.init_positions() if y0 is None else y0
+        o = self.opt
+        for level in range(self.depth, -1, -1):
+            if on_level is not None:
+                on_level(level, "start")
+            y = self.run_level(level, y, group=group, step_fn=step_fn)
+            if on_level is not None:
+                on_level(level, "end")
+            self.check_finite(level)
+            if level > 0:
+                radius = device_radius(y)
+                jitter = o.jitter_rel * radius if radius > 0 else o.init_scale
+                y = device_prolong(y, self.maps[level - 1], jitter,
+                                   _derive_seed(o.seed, _JITTER_TAG, level))
+        return y
+
+
+def device_radius(y: torch.Tensor) -> float:
+    """_layout_radius (optimizer.py:356-358) on device."""
+    r = _lib.out_f64()
+    _lib.call("drg_layout_radius", _lib.ptr(y), y.shape[0], _lib.byref(r), _lib.stream_ptr())
+    return r.value
+
+
+def build_plan(ds: DeviceSimilarity, dh: DeviceHierarchy, opt: OptimizerParams) -> LayoutPlan:
+    return LayoutPlan(build_level_data(ds, dh, opt.neg_power), list(dh.maps), opt)
+
+
+@dataclass
+class PreparedLayout:
+    """Everything layout_device computed before the optimisation."""
+
+    plan: LayoutPlan | None
+    similarity: DeviceSimilarity
+    hierarchy: DeviceHierarchy
+    stats: dict
+    timings: dict
+
+
+def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
+                   rho: float = 0.8, min_size: int = 16, max_levels: int | None = None,
+                   force_levels: int | None = None, timed: bool = False) -> PreparedLayout:
+    """Preprocessing stages of layout_graph (optimizer.py:372-391) on device."""
+    if dg.node_count < 1:
+        raise ValueError("cannot lay out an empty graph")
+    timings = {}
+    ev = [] if timed else None
+
+    def stamp(name):
+        if ev is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            ev.append((name, e))
+
+    stamp("start")
+    n_comp = device_components(dg)
+    if n_comp > 1:
+        logger.warning("input has %d connected components; repulsion alone separates them",
+                       n_comp)
+    stamp("components")
+    nd = device_k_neighborhoods(dg, sim.k, sim.neighbor_cap)
+    stamp("khop")
+    ds = device_similarity(nd, sim)
+    del nd
+    stamp("similarity")
+    dh = device_build_hierarchy(dg, rho, min_size, _derive_seed(opt.seed, _HIERARCHY_TAG),
+                                max_levels, force_levels)
+    stamp("hierarchy")
+    stats = {
+        "components": n_comp,
+        "levels": dh.sizes,
+        "similarity_nbytes": ds.nbytes(),
+        "hierarchy_nbytes": dh.nbytes(),
+        "gradient_steps": 0,
+        "distance_evals": 0,
+    }
+    plan = None
+    if ds.entry_count > 0:
+        plan = build_plan(ds, dh, opt)
+        stamp("level_data")
+    if ev is not None:
+        torch.cuda.synchronize()
+        for (a, ea), (b, eb) in zip(ev[:-1], ev[1:]):
+            timings[b + "_ms"] = ea.elapsed_time(eb)
+    return PreparedLayout(plan, ds, dh, stats, timings)
+
+
+def layout_device(dg: DeviceGraph, sim: SimilarityParams | None = None,
+                  opt: OptimizerParams | None = None, rho: float = 0.8, min_size: int = 16,
+                  max_levels: int | None = None, force_levels: int | None = None,
+                  init_positions: np.ndarray | torch.Tensor | None = None, group=None
+                  ) -> tuple[torch.Tensor, dict, PreparedLayout]:
+    """layout_graph on a resident graph; returns (Y on device, stats, prepared)."""
+    sim = sim or SimilarityParams()
+    opt = opt or OptimizerParams()
+    prep = prepare_layout(dg, sim, opt, rho, min_size, max_levels, force_levels)
+    stats, dh = prep.stats, prep.hierarchy
+    if init_positions is not None:
+        y0 = torch.as_tensor(np.asarray(init_positions, dtype=np.float32)).cuda() \
+            if not isinstance(init_positions, torch.Tensor) else init_positions.float().cuda()
+    else:
+        y0 = None
+    if prep.plan is None:
+        # no similarity mass (edgeless input): broadcast the coarsest init
+        # through the maps without jitter (optimizer.py:397-402)
+        stats["skipped_optimization"] = True
+        n_top = dh.levels[-1].node_count
+        tmp = LayoutPlan([LevelData(n_top, 0, None, None, None, None)], [], opt)
+        y = tmp.init_positions() if y0 is None else y0
+        for level in range(dh.depth, 0, -1):
+            y = device_prolong(y, dh.maps[level - 1], 0.0, 0)
+        return y, stats, prep
+    y = prep.plan.run(y0, group=group)
+    M = opt.neg_samples
+    stats["gradient_steps"] = opt.iters * sum(dh.sizes)
+    # reference-equivalent interaction count: each iteration stands for n_l steps of
+    # (1 + M) interactions (an upper bound, like the reference's counter)
+    stats["distance_evals"] = opt.iters * (1 + M) * sum(dh.sizes)
+    stats["interactions"] = prep.plan.interactions()
+    return y, stats, prep
+
+
+def layout_graph(g: Graph, sim_params: SimilarityParams | None = None,
+                 opt_params: OptimizerParams | None = None, rho: float = 0.8,
+                 min_size: int = 16, *, max_levels: int | None = None,
+                 force_levels: int | None = None, init_positions=None, group=None) -> Layout:
+    """Full pipeline (optimizer.py:361-413) on the GPU.  Graph in (host CSR),
+    positions out (host float64 [n, 2]).  Deterministic for a fixed seed with the
+    default Jacobi update."""
+    if g.node_count < 1:
+        raise ValueError("cannot lay out an empty graph")
+    _lib.load()
+    dg = DeviceGraph.from_host(g)
+    y, stats, _ = layout_device(dg, sim_params, opt_params, rho, min_size, max_levels,
+                                force_levels, init_positions, group)
+    return Layout(positions=y.cpu().numpy().astype(np.float64), stats=stats)
+
+
+# ---------------------------------------------------------------------------
+# sgd_epoch drop-in: one K7 iteration at the level inferred from len(positions)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Samplers:
+    """Sampling state shared across levels (optimizer.py:270-288).  Holds the
+    similarity and lazily builds the per-level device tables for a hierarchy."""
+
+    ns: SparseSimilarity
+    neg_power: float = 0.75
+    _plans: dict = field(default_factory=dict)
+
+    def level_map(self, h: Hierarchy, level: int) -> np.ndarray:
+        return compose_maps(h, level)
+
+    def plan_for(self, h: Hierarchy, params: OptimizerParams) -> LayoutPlan:
+        key = id(h)
+        if key not in self._plans:
+            levels = h.device_levels or [DeviceGraph.from_host(g) for g in h.levels]
+            maps = h.device_maps or [torch.from_numpy(np.ascontiguousarray(m, dtype=np.int32))
+                                     .cuda() for m in h.maps]
+            dh = DeviceHierarchy(list(levels), list(maps), h.rho, h.min_size)
+            ns = self.ns
+            ds = DeviceSimilarity(
+                torch.from_numpy(np.ascontiguousarray(ns.indptr, dtype=np.int64)).cuda(),
+                torch.from_numpy(np.ascontiguousarray(ns.targets, dtype=np.int32)).cuda(),
+                torch.from_numpy(np.ascontiguousarray(ns.weights, dtype=np.float64)).cuda(),
+                torch.from_numpy(np.ascontiguousarray(ns.sigma)).cuda(),
+                torch.from_numpy(np.ascontiguousarray(ns.row_masses())).cuda(),
+                ns.total_mass, int((np.diff(ns.indptr) > 0).sum()), ns.k)
+            self._plans[key] = (h, LayoutPlan(build_level_data(ds, dh, self.neg_power),
+                                              list(dh.maps), params))
+        plan = self._plans[key][1]
+        plan.opt = params
+        return plan
+
+
+def build_samplers(ns: SparseSimilarity, neg_power: float = 0.75) -> Samplers:
+    """optimizer.py:291-300."""
+    if ns.entry_count == 0 or float(ns.weights.sum()) <= 0.0:
+        raise ValueError("similarity carries no mass; nothing to sample")
+    _lib.load()
+    return Samplers(ns, neg_power)
+
+
+def _infer_level(h: Hierarchy, n: int) -> int:
+    for level, g in enumerate(h.levels):
+        if g.node_count == n:
+            return level
+    raise ValueError(f"no hierarchy level has {n} nodes")
+
+
+def sgd_epoch(positions: np.ndarray, h: Hierarchy, samplers: Samplers,
+              params: OptimizerParams, t: int, stats: dict | None = None) -> np.ndarray:
+    """One epoch in place (optimizer.py:310-353): one K7 iteration t at the level
+    inferred from the position count."""
+    n = len(positions)
+    level = _infer_level(h, n)
+    plan = samplers.plan_for(h, params)
+    y = torch.from_numpy(np.ascontiguousarray(positions, dtype=np.float32)).cuda()
+    y = plan.run_level(level, y, t0=t, n_iter=1)
+    plan.check_finite(level)
+    positions[:] = y.cpu().numpy()
+    if stats is not None:
+        stats["gradient_steps"] = stats.get("gradient_steps", 0) + n
+        stats["distance_evals"] = stats.get("distance_evals", 0) + n * (1 + params.neg_samples)
+    return positions
+
+
+
+__all__ = ["OptimizerParams", "Layout", "AliasTable", "build_alias_table",
+           "build_negative_sampler", "build_samplers", "Samplers", "sgd_epoch", "layout_graph",
+           "layout_device", "prepare_layout", "LayoutPlan", "LevelData", "build_level_data",
+           "device_radius"]

@@ -1,0 +1,76 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads and exports every
+symbol include/drgraph_b200.h declares (no compute calls -- no GPU here), the
+Python binding covers the same set, and the host-side parameter validation
+matches the reference (similarity.py:44-53, optimizer.py:60-74)."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "drgraph_b200.h")
+LIB = os.path.join(ROOT, "paper_2008_07799_b200", "libdrgraph_b200.so")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(drg_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_the_path():
+    syms = declared_symbols()
+    for name in ("drg_khop_count", "drg_khop_fill", "drg_similarity", "drg_coarsen",
+                 "drg_coarse_graph", "drg_aggregate_pairs", "drg_alias_build",
+                 "drg_layout_iters", "drg_prolong", "drg_layout_radius", "drg_from_edges"):
+        assert name in syms
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="extension not built")
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(LIB)
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    assert lib.drg_abi_version() == 1
+    lib.drg_last_error.restype = ctypes.c_char_p
+    assert isinstance(lib.drg_last_error(), bytes)
+
+
+def test_python_binding_covers_header():
+    from paper_2008_07799_b200 import _lib
+    assert set(_lib.SIGNATURES) == set(declared_symbols())
+
+
+def test_params_validation_matches_reference():
+    from paper_2008_07799_b200 import OptimizerParams, SimilarityParams
+    for bad in (dict(k=0), dict(k=7), dict(perplexity=0.5)):
+        with pytest.raises(ValueError):
+            SimilarityParams(**bad)
+    for bad in (dict(gamma=-1), dict(iters=0), dict(b=0), dict(threads=0), dict(neg_samples=-1),
+                dict(lr0=0), dict(seed=-1), dict(init="x"), dict(update="y")):
+        with pytest.raises(ValueError):
+            OptimizerParams(**bad)
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2008_07799_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            src = open(os.path.join(pkg, fn)).read()
+            assert "oracle" not in src.replace("oracle/", ""), fn
+
+
+def test_no_cpu_device_path():
+    """Without a CUDA device the product raises instead of computing on the CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import numpy as np
+    from paper_2008_07799_b200 import Graph, all_k_neighborhoods
+    g = Graph(np.array([0, 1, 2]), np.array([1, 0], dtype=np.int32))
+    with pytest.raises(RuntimeError):
+        all_k_neighborhoods(g, 2)
