@@ -21,6 +21,10 @@ constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Keep freed stream-ordered allocations reserved in the device pool (no re-map
+// of multi-GB scratch on every call).
+void keep_pool_reserved();
+
 // Stream-ordered scratch allocation (freed on the same stream at scope exit).
 struct Scratch {
     void *p = nullptr;
@@ -35,6 +39,7 @@ struct Scratch {
             cudaFreeAsync(p, s);
             p = nullptr;
         }
+        keep_pool_reserved();
         return cudaMallocAsync(&p, bytes ? bytes : 16, s);
     }
     template <class T>

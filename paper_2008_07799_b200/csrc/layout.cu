@@ -51,76 +51,170 @@ struct IterArgs {
     int32_t *nonfinite;
 };
 
-// Draw the m-th negative of node a at iteration t (level-l node id, or -1).
-__device__ __forceinline__ int64_t draw_negative(const IterArgs &A, int64_t a, int m) {
-    for (int attempt = 0; attempt < 9; ++attempt) {
-        u32x4 r = philox4x32(u32x4{(uint32_t)a, (uint32_t)(a >> 32) ^ ((uint32_t)A.t << 1),
-                                   (A.level << 24) | ((uint32_t)m << 8) | (uint32_t)attempt,
-                                   0x5eed1e55u},
-                             A.key0, A.key1);
-        const uint64_t r64 = ((uint64_t)r.x << 32) | r.y;
-        const int64_t idx = (int64_t)__umul64hi(r64, (uint64_t)A.n);
-        const uint2 rec = __ldg(A.alias + idx);
-        const int64_t c = (u32_to_unit(r.z) < __uint_as_float(rec.x)) ? idx : (int64_t)rec.y;
-        if (c != a) return c;
-    }
-    return -1;
+__device__ __forceinline__ u32x4 neg_bits(const IterArgs &A, int64_t a, int m, int attempt) {
+    return philox4x32(u32x4{(uint32_t)a, (uint32_t)(a >> 32) ^ ((uint32_t)A.t << 1),
+                            (A.level << 24) | ((uint32_t)m << 8) | (uint32_t)attempt,
+                            0x5eed1e55u},
+                      A.key0, A.key1);
 }
 
+__device__ __forceinline__ int64_t alias_index(const IterArgs &A, const u32x4 &r) {
+    const uint64_t r64 = ((uint64_t)r.x << 32) | r.y;
+    return (int64_t)__umul64hi(r64, (uint64_t)A.n);
+}
+
+// y gathers: read-only path when the kernel never writes y_in (Jacobi); L2-coherent
+// loads in the in-place mode, where other warps update y while it is read.
 template <bool INPLACE>
-__global__ void __launch_bounds__(kWpb * 32)
+__device__ __forceinline__ float2 load_y(const float2 *y, int64_t i) {
+    if (INPLACE) return __ldcg(y + i);
+    return __ldg(y + i);
+}
+
+// (ld2)^(b-1) by repeated multiply (optimizer.py:142-147); B > 0 is compile-time.
+template <int B>
+__device__ __forceinline__ float powbm1(float ld2, int b) {
+    if (B > 0) {
+        float r = 1.0f;
+#pragma unroll
+        for (int i = 0; i < B - 1; ++i) r *= ld2;
+        return r;
+    }
+    return ipowf(ld2, b - 1);
+}
+
+constexpr int kDepth = 4;   // row entries in flight per lane (4 x 32 = 128 per warp pass)
+
+template <bool INPLACE, int B>
+__global__ void __launch_bounds__(kWpb * 32, 5)
     layout_iter_kernel(IterArgs A, const float2 *y_in, float2 *y_out) {
     const int lane = threadIdx.x & 31;
     const int64_t a = A.row_lo + (int64_t)blockIdx.x * kWpb + (threadIdx.x >> 5);
     if (a >= A.row_hi) return;
-    const float2 ya = y_in[a];
-    const int64_t lo = __ldg(A.indptr + a), hi = __ldg(A.indptr + a + 1);
-    const float two_b = 2.0f * (float)A.b;
-    float ax = 0.f, ay = 0.f;
-    // attractive: sum_b W_ab clip(g_att(y_a, y_b))
-#pragma unroll 4
-    for (int64_t e = lo + lane; e < hi; e += 32) {
-        const uint2 r = __ldg(A.rec + e);
-        const float2 yb = y_in[r.x];
-        const float dx = ya.x - yb.x, dy = ya.y - yb.y;
-        const float ld2 = dx * dx + dy * dy;
-        if (ld2 > 0.f) {
-            const float pw = ipowf(ld2, A.b - 1);
-            const float coef = -two_b * pw / (1.0f + pw * ld2);
-            const float w = __uint_as_float(r.y);
-            ax += w * clampf(coef * dx, A.clip);
-            ay += w * clampf(coef * dy, A.clip);
+    const int b = B > 0 ? B : A.b;
+    const float two_b = 2.0f * (float)b;
+
+    // Negatives first (lanes 0..M-1): the Philox draw and the alias-record load are
+    // issued before the row stream so their latency overlaps it.
+    int64_t c = -1;
+    u32x4 nb = {0, 0, 0, 0};
+    uint2 arec = make_uint2(0, 0);
+    int64_t aidx = 0;
+    const bool neg_lane = lane < A.M;
+    if (neg_lane) {
+        if (A.neg_idx) {
+            c = (int64_t)A.neg_idx[a * A.M + lane];
+        } else {
+            nb = neg_bits(A, a, lane, 0);
+            aidx = alias_index(A, nb);
+            arec = __ldg(A.alias + aidx);
         }
     }
-    // repulsive: lanes 0..M-1, one negative each
-    float rx = 0.f, ry = 0.f;
-    for (int m = lane; m < A.M; m += 32) {
-        const int64_t c = A.neg_idx ? (int64_t)A.neg_idx[a * A.M + m] : draw_negative(A, a, m);
-        if (c >= 0) {
-            const float2 yc = y_in[c];
-            const float dx = ya.x - yc.x, dy = ya.y - yc.y;
+
+    const int64_t lo = __ldg(A.indptr + a), hi = __ldg(A.indptr + a + 1);
+    const float2 ya = load_y<INPLACE>(y_in, a);
+    const float Va = __ldg(A.V + a);
+    float ax = 0.f, ay = 0.f;
+    // attractive: sum_b W_ab clip(g_att(y_a, y_b)), kDepth records then kDepth
+    // gathers in flight per lane
+    for (int64_t base = lo; base < hi; base += 32 * kDepth) {
+        uint2 r[kDepth];
+#pragma unroll
+        for (int j = 0; j < kDepth; ++j) {
+            const int64_t e = base + j * 32 + lane;
+            r[j] = e < hi ? __ldcs(A.rec + e) : make_uint2(0xffffffffu, 0u);
+        }
+        float2 yb[kDepth];
+#pragma unroll
+        for (int j = 0; j < kDepth; ++j)
+            yb[j] = r[j].x != 0xffffffffu ? load_y<INPLACE>(y_in, r[j].x) : ya;
+#pragma unroll
+        for (int j = 0; j < kDepth; ++j) {
+            const float dx = ya.x - yb[j].x, dy = ya.y - yb[j].y;
             const float ld2 = dx * dx + dy * dy;
-            if (ld2 + A.eps > 0.f) {
-                const float pw = ipowf(ld2, A.b - 1);
-                const float coef = A.gamma * two_b / ((ld2 + A.eps) * (1.0f + pw * ld2));
-                rx += clampf(coef * dx, A.clip);
-                ry += clampf(coef * dy, A.clip);
+            if (ld2 > 0.f) {
+                const float pw = powbm1<B>(ld2, b);
+                const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
+                const float w = __uint_as_float(r[j].y);
+                ax = fmaf(w, clampf(coef * dx, A.clip), ax);
+                ay = fmaf(w, clampf(coef * dy, A.clip), ay);
             }
         }
     }
-    const float Va = __ldg(A.V + a);
-    float gx = ax + Va * rx, gy = ay + Va * ry;
+
+    // repulsive: finish the draws (redraw if the image is a, <= 9 attempts,
+    // _kernels.py:108-117), gather y_c, clip(g_rep)
+    float rx = 0.f, ry = 0.f;
+    if (neg_lane) {
+        if (!A.neg_idx) {
+            c = (u32_to_unit(nb.z) < __uint_as_float(arec.x)) ? aidx : (int64_t)arec.y;
+            for (int attempt = 1; c == a && attempt < 9; ++attempt) {
+                nb = neg_bits(A, a, lane, attempt);
+                aidx = alias_index(A, nb);
+                arec = __ldg(A.alias + aidx);
+                c = (u32_to_unit(nb.z) < __uint_as_float(arec.x)) ? aidx : (int64_t)arec.y;
+            }
+            if (c == a) c = -1;
+        }
+        if (c >= 0) {
+            const float2 yc = load_y<INPLACE>(y_in, c);
+            const float dx = ya.x - yc.x, dy = ya.y - yc.y;
+            const float ld2 = dx * dx + dy * dy;
+            if (ld2 + A.eps > 0.f) {
+                const float pw = powbm1<B>(ld2, b);
+                const float coef = __fdividef(A.gamma * two_b, (ld2 + A.eps) * (1.0f + pw * ld2));
+                rx = clampf(coef * dx, A.clip);
+                ry = clampf(coef * dy, A.clip);
+            }
+        }
+    }
+    for (int m = lane + 32; m < A.M; m += 32) {   // M > 32: extra negatives, serial
+        int64_t cm = -1;
+        if (A.neg_idx) {
+            cm = A.neg_idx[a * A.M + m];
+        } else {
+            for (int attempt = 0; attempt < 9; ++attempt) {
+                u32x4 q = neg_bits(A, a, m, attempt);
+                int64_t qi = alias_index(A, q);
+                uint2 qr = __ldg(A.alias + qi);
+                cm = (u32_to_unit(q.z) < __uint_as_float(qr.x)) ? qi : (int64_t)qr.y;
+                if (cm != a) break;
+                cm = -1;
+            }
+        }
+        if (cm >= 0) {
+            const float2 yc = load_y<INPLACE>(y_in, cm);
+            const float dx = ya.x - yc.x, dy = ya.y - yc.y;
+            const float ld2 = dx * dx + dy * dy;
+            const float pw = powbm1<B>(ld2, b);
+            const float coef = __fdividef(A.gamma * two_b, (ld2 + A.eps) * (1.0f + pw * ld2));
+            rx += clampf(coef * dx, A.clip);
+            ry += clampf(coef * dy, A.clip);
+        }
+    }
+    float gx = fmaf(Va, rx, ax), gy = fmaf(Va, ry, ay);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         gx += __shfl_xor_sync(kFull, gx, o);
         gy += __shfl_xor_sync(kFull, gy, o);
     }
     if (lane == 0) {
-        float2 out = make_float2(ya.x + A.lr * gx, ya.y + A.lr * gy);
+        float2 out = make_float2(fmaf(A.lr, gx, ya.x), fmaf(A.lr, gy, ya.y));
         if (!isfinite(out.x) || !isfinite(out.y)) {
             if (A.nonfinite) atomicMin(A.nonfinite, A.t);
         }
         y_out[a] = out;
+    }
+}
+
+template <bool INPLACE>
+void launch_iter(unsigned grid, cudaStream_t st, const IterArgs &A, const float2 *src,
+                 float2 *dst) {
+    switch (A.b) {
+        case 1: layout_iter_kernel<INPLACE, 1><<<grid, kWpb * 32, 0, st>>>(A, src, dst); break;
+        case 2: layout_iter_kernel<INPLACE, 2><<<grid, kWpb * 32, 0, st>>>(A, src, dst); break;
+        case 3: layout_iter_kernel<INPLACE, 3><<<grid, kWpb * 32, 0, st>>>(A, src, dst); break;
+        default: layout_iter_kernel<INPLACE, 0><<<grid, kWpb * 32, 0, st>>>(A, src, dst); break;
     }
 }
 
@@ -301,9 +395,9 @@ extern "C" int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, cons
         A.t = t;
         A.lr = (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0);  // optimizer.py:322
         if (inplace) {
-            layout_iter_kernel<true><<<grid, kWpb * 32, 0, st>>>(A, src, src);
+            launch_iter<true>(grid, st, A, src, src);
         } else {
-            layout_iter_kernel<false><<<grid, kWpb * 32, 0, st>>>(A, src, dst);
+            launch_iter<false>(grid, st, A, src, dst);
             std::swap(src, dst);
         }
         DRG_LAUNCHED("layout_iter_kernel");

@@ -262,8 +262,11 @@ def test_level_data_vs_oracle(golden):
         ip, tg, P, R, Q = O.level_data(ns, oh, level)
         assert np.array_equal(L.indptr.cpu().numpy(), ip)
         rec = L.rec.cpu().numpy().view(np.uint32).reshape(-1, 2)
-        assert np.array_equal(rec[:, 0].astype(np.int32), tg)
-        W = rec[:, 1].view(np.float32)
+        # level 0 keeps the reference's (dist, id) row order; compare row-sorted
+        rows = np.repeat(np.arange(L.n), np.diff(ip))
+        order = np.lexsort((rec[:, 0].astype(np.int64), rows))
+        assert np.array_equal(rec[order, 0].astype(np.int32), tg)
+        W = rec[order, 1].view(np.float32)
         np.testing.assert_allclose(W, 2 * L.n * P, rtol=1e-6)
         np.testing.assert_allclose(L.V.cpu().numpy(), L.n * (R + Q), rtol=1e-6)
 
