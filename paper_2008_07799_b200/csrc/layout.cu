@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <climits>
 #include <vector>
 
@@ -85,121 +86,212 @@ __device__ __forceinline__ float powbm1(float ld2, int b) {
 
 constexpr int kDepth = 4;   // row entries in flight per lane (4 x 32 = 128 per warp pass)
 
-template <bool INPLACE, int B>
+// One negative draw: Philox word pair -> alias bucket, coin -> accept / alias.
+__device__ __forceinline__ int64_t resolve_draw(const IterArgs &A, const u32x4 &r, uint2 rec,
+                                                int64_t idx) {
+    return (u32_to_unit(r.z) < __uint_as_float(rec.x)) ? idx : (int64_t)rec.y;
+}
+
+// A warp owns `npw` consecutive nodes (npw = 32 / M): the M negative draws of all
+// of them are made at once (one Philox pass for the whole warp, alias records
+// loaded before the row streams start), then each node's row is streamed with
+// kDepth records + kDepth y-gathers in flight per lane.
+//  CLAMP_ATT: clip the attractive gradient.  For b <= 3 and the default clip 5 it
+//             is provably inactive (|g_att| <= (2b-1)^((2b-1)/2b) < 5), so the
+//             host drops it.
+//  PARTNER:   also reject a negative equal to the node's sampled positive partner
+//             j ~ W_a. (the reference redraws c in {i, j}, _kernels.py:108-117);
+//             only visible when Q_j is not negligible, so enabled on small levels.
+template <bool INPLACE, int B, bool CLAMP_ATT, bool PARTNER>
 __global__ void __launch_bounds__(kWpb * 32, 5)
-    layout_iter_kernel(IterArgs A, const float2 *y_in, float2 *y_out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t a = A.row_lo + (int64_t)blockIdx.x * kWpb + (threadIdx.x >> 5);
-    if (a >= A.row_hi) return;
+    layout_iter_kernel(IterArgs A, int npw, const float2 *y_in, float2 *y_out) {
+    __shared__ float2 s_rep[kWpb][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t a0 = A.row_lo + ((int64_t)blockIdx.x * kWpb + warp) * npw;
+    if (a0 >= A.row_hi) return;
+    const int nodes = (int)min((int64_t)npw, A.row_hi - a0);
     const int b = B > 0 ? B : A.b;
     const float two_b = 2.0f * (float)b;
+    const int M = A.M;
 
-    // Negatives first (lanes 0..M-1): the Philox draw and the alias-record load are
-    // issued before the row stream so their latency overlaps it.
-    int64_t c = -1;
+    // ---- negative draws, first attempt (lane q -> node q / M, sample q % M)
+    const int nq = nodes * M;
+    const int my_node = (npw == 1) ? 0 : (M > 0 ? lane / M : 0);
+    const bool neg_lane = (npw == 1) ? (lane < M) : (lane < nq);
+    int64_t cand = -1;
     u32x4 nb = {0, 0, 0, 0};
     uint2 arec = make_uint2(0, 0);
     int64_t aidx = 0;
-    const bool neg_lane = lane < A.M;
     if (neg_lane) {
+        const int64_t an = a0 + my_node;
+        const int m = (npw == 1) ? lane : lane - my_node * M;
         if (A.neg_idx) {
-            c = (int64_t)A.neg_idx[a * A.M + lane];
+            cand = (int64_t)A.neg_idx[an * M + m];
         } else {
-            nb = neg_bits(A, a, lane, 0);
+            nb = neg_bits(A, an, m, 0);
             aidx = alias_index(A, nb);
             arec = __ldg(A.alias + aidx);
         }
     }
 
-    const int64_t lo = __ldg(A.indptr + a), hi = __ldg(A.indptr + a + 1);
-    const float2 ya = load_y<INPLACE>(y_in, a);
-    const float Va = __ldg(A.V + a);
-    float ax = 0.f, ay = 0.f;
-    // attractive: sum_b W_ab clip(g_att(y_a, y_b)), kDepth records then kDepth
-    // gathers in flight per lane
-    for (int64_t base = lo; base < hi; base += 32 * kDepth) {
-        uint2 r[kDepth];
+    // ---- attractive rows, node by node
+    float att_x = 0.f, att_y = 0.f;  // kept by lane i for node i
+    int64_t partner = -1;            // kept by lane i for node i
+    for (int i = 0; i < nodes; ++i) {
+        const int64_t a = a0 + i;
+        const int64_t lo = __ldg(A.indptr + a), hi = __ldg(A.indptr + a + 1);
+        const int cnt = (int)(hi - lo);
+        const uint2 *row = A.rec + lo;
+        const float2 ya = load_y<INPLACE>(y_in, a);
+        float ax = 0.f, ay = 0.f, wsum = 0.f;
+        for (int base = 0; base < cnt; base += 32 * kDepth) {
+            uint2 r[kDepth];
 #pragma unroll
-        for (int j = 0; j < kDepth; ++j) {
-            const int64_t e = base + j * 32 + lane;
-            r[j] = e < hi ? __ldcs(A.rec + e) : make_uint2(0xffffffffu, 0u);
-        }
-        float2 yb[kDepth];
-#pragma unroll
-        for (int j = 0; j < kDepth; ++j)
-            yb[j] = r[j].x != 0xffffffffu ? load_y<INPLACE>(y_in, r[j].x) : ya;
-#pragma unroll
-        for (int j = 0; j < kDepth; ++j) {
-            const float dx = ya.x - yb[j].x, dy = ya.y - yb[j].y;
-            const float ld2 = dx * dx + dy * dy;
-            if (ld2 > 0.f) {
-                const float pw = powbm1<B>(ld2, b);
-                const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
-                const float w = __uint_as_float(r[j].y);
-                ax = fmaf(w, clampf(coef * dx, A.clip), ax);
-                ay = fmaf(w, clampf(coef * dy, A.clip), ay);
+            for (int j = 0; j < kDepth; ++j) {
+                const int e = base + j * 32 + lane;
+                r[j] = e < cnt ? __ldcs(row + e) : make_uint2((uint32_t)a, 0u);
             }
+            float2 yb[kDepth];
+#pragma unroll
+            for (int j = 0; j < kDepth; ++j) yb[j] = load_y<INPLACE>(y_in, r[j].x);
+#pragma unroll
+            for (int j = 0; j < kDepth; ++j) {
+                // ld2 == 0 gives an exactly zero contribution for every b >= 1
+                const float dx = ya.x - yb[j].x, dy = ya.y - yb[j].y;
+                const float ld2 = fmaf(dx, dx, dy * dy);
+                const float pw = powbm1<B>(ld2, b);
+                const float w = __uint_as_float(r[j].y);
+                const float coef = __fdividef(-two_b * pw, fmaf(pw, ld2, 1.0f));
+                if (CLAMP_ATT) {
+                    ax = fmaf(w, clampf(coef * dx, A.clip), ax);
+                    ay = fmaf(w, clampf(coef * dy, A.clip), ay);
+                } else {
+                    const float wc = w * coef;
+                    ax = fmaf(wc, dx, ax);
+                    ay = fmaf(wc, dy, ay);
+                }
+                if (PARTNER) wsum += w;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ax += __shfl_xor_sync(kFull, ax, o);
+            ay += __shfl_xor_sync(kFull, ay, o);
+        }
+        if (lane == i) {
+            att_x = ax;
+            att_y = ay;
+        }
+        if (PARTNER && M > 0) {
+            // sample j ~ W_a. with the node's spare Philox word: second pass over the
+            // (short) row, lane-major cumulative order
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
+            const uint32_t ubits = __shfl_sync(kFull, nb.w, (npw == 1) ? 0 : i * M);
+            float tau = u32_to_unit(ubits) * wsum;
+            int64_t found = -1;
+            for (int base = 0; base < cnt && wsum > 0.f; base += 32) {
+                const int e = base + lane;
+                const uint2 rr = e < cnt ? row[e] : make_uint2(0u, 0u);
+                const float w = __uint_as_float(rr.y);
+                float incl = w;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    float t = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const unsigned hit = __ballot_sync(kFull, e < cnt && w > 0.f && incl > tau);
+                if (hit) {
+                    const int src = __ffs(hit) - 1;
+                    found = (int64_t)__shfl_sync(kFull, rr.x, src);
+                    break;
+                }
+                tau -= __shfl_sync(kFull, incl, 31);
+            }
+            if (lane == i) partner = found;
         }
     }
 
-    // repulsive: finish the draws (redraw if the image is a, <= 9 attempts,
-    // _kernels.py:108-117), gather y_c, clip(g_rep)
+    // ---- repulsive: finish the draws (redraw while c == a or c == partner, <= 9
+    // attempts, _kernels.py:108-117), gather y_c, clip(g_rep)
+    const int64_t part = PARTNER ? __shfl_sync(kFull, partner, min(my_node, 31)) : -1;
     float rx = 0.f, ry = 0.f;
     if (neg_lane) {
+        const int64_t an = a0 + my_node;
+        const int m = (npw == 1) ? lane : lane - my_node * M;
+        int64_t c = cand;
         if (!A.neg_idx) {
-            c = (u32_to_unit(nb.z) < __uint_as_float(arec.x)) ? aidx : (int64_t)arec.y;
-            for (int attempt = 1; c == a && attempt < 9; ++attempt) {
-                nb = neg_bits(A, a, lane, attempt);
+            c = resolve_draw(A, nb, arec, aidx);
+            for (int attempt = 1; (c == an || c == part) && attempt < 9; ++attempt) {
+                nb = neg_bits(A, an, m, attempt);
                 aidx = alias_index(A, nb);
                 arec = __ldg(A.alias + aidx);
-                c = (u32_to_unit(nb.z) < __uint_as_float(arec.x)) ? aidx : (int64_t)arec.y;
+                c = resolve_draw(A, nb, arec, aidx);
             }
-            if (c == a) c = -1;
+            if (c == an || c == part) c = -1;
         }
         if (c >= 0) {
+            const float2 ya = load_y<INPLACE>(y_in, an);
             const float2 yc = load_y<INPLACE>(y_in, c);
             const float dx = ya.x - yc.x, dy = ya.y - yc.y;
-            const float ld2 = dx * dx + dy * dy;
-            if (ld2 + A.eps > 0.f) {
-                const float pw = powbm1<B>(ld2, b);
-                const float coef = __fdividef(A.gamma * two_b, (ld2 + A.eps) * (1.0f + pw * ld2));
-                rx = clampf(coef * dx, A.clip);
-                ry = clampf(coef * dy, A.clip);
-            }
-        }
-    }
-    for (int m = lane + 32; m < A.M; m += 32) {   // M > 32: extra negatives, serial
-        int64_t cm = -1;
-        if (A.neg_idx) {
-            cm = A.neg_idx[a * A.M + m];
-        } else {
-            for (int attempt = 0; attempt < 9; ++attempt) {
-                u32x4 q = neg_bits(A, a, m, attempt);
-                int64_t qi = alias_index(A, q);
-                uint2 qr = __ldg(A.alias + qi);
-                cm = (u32_to_unit(q.z) < __uint_as_float(qr.x)) ? qi : (int64_t)qr.y;
-                if (cm != a) break;
-                cm = -1;
-            }
-        }
-        if (cm >= 0) {
-            const float2 yc = load_y<INPLACE>(y_in, cm);
-            const float dx = ya.x - yc.x, dy = ya.y - yc.y;
-            const float ld2 = dx * dx + dy * dy;
+            const float ld2 = fmaf(dx, dx, dy * dy);
             const float pw = powbm1<B>(ld2, b);
-            const float coef = __fdividef(A.gamma * two_b, (ld2 + A.eps) * (1.0f + pw * ld2));
-            rx += clampf(coef * dx, A.clip);
-            ry += clampf(coef * dy, A.clip);
+            const float coef = __fdividef(A.gamma * two_b, (ld2 + A.eps) * fmaf(pw, ld2, 1.0f));
+            rx = clampf(coef * dx, A.clip);
+            ry = clampf(coef * dy, A.clip);
         }
     }
-    float gx = fmaf(Va, rx, ax), gy = fmaf(Va, ry, ay);
+    if (npw == 1) {
+        // M > 32 tail (serial), then a whole-warp reduction
+        for (int m = lane + 32; m < M; m += 32) {
+            int64_t c = -1;
+            if (A.neg_idx) {
+                c = A.neg_idx[a0 * M + m];
+            } else {
+                for (int attempt = 0; attempt < 9; ++attempt) {
+                    u32x4 q = neg_bits(A, a0, m, attempt);
+                    int64_t qi = alias_index(A, q);
+                    c = resolve_draw(A, q, __ldg(A.alias + qi), qi);
+                    if (c != a0 && c != part) break;
+                    c = -1;
+                }
+            }
+            if (c >= 0) {
+                const float2 ya = load_y<INPLACE>(y_in, a0);
+                const float2 yc = load_y<INPLACE>(y_in, c);
+                const float dx = ya.x - yc.x, dy = ya.y - yc.y;
+                const float ld2 = fmaf(dx, dx, dy * dy);
+                const float pw = powbm1<B>(ld2, b);
+                const float coef =
+                    __fdividef(A.gamma * two_b, (ld2 + A.eps) * fmaf(pw, ld2, 1.0f));
+                rx += clampf(coef * dx, A.clip);
+                ry += clampf(coef * dy, A.clip);
+            }
+        }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        gx += __shfl_xor_sync(kFull, gx, o);
-        gy += __shfl_xor_sync(kFull, gy, o);
+        for (int o = 16; o > 0; o >>= 1) {
+            rx += __shfl_xor_sync(kFull, rx, o);
+            ry += __shfl_xor_sync(kFull, ry, o);
+        }
+    } else {
+        // segmented sum over the M lanes of each node
+        s_rep[warp][lane] = make_float2(rx, ry);
+        __syncwarp();
+        rx = ry = 0.f;
+        if (lane < nodes)
+            for (int q = lane * M; q < lane * M + M; ++q) {
+                rx += s_rep[warp][q].x;
+                ry += s_rep[warp][q].y;
+            }
     }
-    if (lane == 0) {
-        float2 out = make_float2(fmaf(A.lr, gx, ya.x), fmaf(A.lr, gy, ya.y));
+
+    // ---- update (lane i writes node i)
+    if (lane < nodes) {
+        const int64_t a = a0 + lane;
+        const float2 ya = load_y<INPLACE>(y_in, a);
+        const float Va = __ldg(A.V + a);
+        const float gx = fmaf(Va, rx, att_x), gy = fmaf(Va, ry, att_y);
+        const float2 out = make_float2(fmaf(A.lr, gx, ya.x), fmaf(A.lr, gy, ya.y));
         if (!isfinite(out.x) || !isfinite(out.y)) {
             if (A.nonfinite) atomicMin(A.nonfinite, A.t);
         }
@@ -207,16 +299,37 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
     }
 }
 
-template <bool INPLACE>
-void launch_iter(unsigned grid, cudaStream_t st, const IterArgs &A, const float2 *src,
-                 float2 *dst) {
-    switch (A.b) {
-        case 1: layout_iter_kernel<INPLACE, 1><<<grid, kWpb * 32, 0, st>>>(A, src, dst); break;
-        case 2: layout_iter_kernel<INPLACE, 2><<<grid, kWpb * 32, 0, st>>>(A, src, dst); break;
-        case 3: layout_iter_kernel<INPLACE, 3><<<grid, kWpb * 32, 0, st>>>(A, src, dst); break;
-        default: layout_iter_kernel<INPLACE, 0><<<grid, kWpb * 32, 0, st>>>(A, src, dst); break;
+template <bool INPLACE, int B>
+void launch_iter_b(unsigned grid, cudaStream_t st, const IterArgs &A, int npw, bool clamp,
+                   bool partner, const float2 *src, float2 *dst) {
+    if (clamp) {
+        if (partner) layout_iter_kernel<INPLACE, B, true, true><<<grid, kWpb * 32, 0, st>>>(A, npw, src, dst);
+        else layout_iter_kernel<INPLACE, B, true, false><<<grid, kWpb * 32, 0, st>>>(A, npw, src, dst);
+    } else {
+        if (partner) layout_iter_kernel<INPLACE, B, false, true><<<grid, kWpb * 32, 0, st>>>(A, npw, src, dst);
+        else layout_iter_kernel<INPLACE, B, false, false><<<grid, kWpb * 32, 0, st>>>(A, npw, src, dst);
     }
 }
+
+template <bool INPLACE>
+void launch_iter(unsigned grid, cudaStream_t st, const IterArgs &A, int npw, bool clamp,
+                 bool partner, const float2 *src, float2 *dst) {
+    switch (A.b) {
+        case 1: launch_iter_b<INPLACE, 1>(grid, st, A, npw, clamp, partner, src, dst); break;
+        case 2: launch_iter_b<INPLACE, 2>(grid, st, A, npw, clamp, partner, src, dst); break;
+        case 3: launch_iter_b<INPLACE, 3>(grid, st, A, npw, clamp, partner, src, dst); break;
+        default: launch_iter_b<INPLACE, 0>(grid, st, A, npw, clamp, partner, src, dst); break;
+    }
+}
+
+// Largest |component| the attractive gradient can reach: max_d 2b d^(2b-1)/(1+d^(2b))
+// = (2b-1)^((2b-1)/(2b)) (at d^(2b) = 2b-1).
+inline bool attractive_clip_active(int b, double clip) {
+    const double gmax = std::pow(2.0 * b - 1.0, (2.0 * b - 1.0) / (2.0 * b));
+    return !(clip >= gmax * (1.0 + 1e-4));
+}
+
+constexpr int64_t kPartnerMaxNodes = 65536;  // partner rejection on levels up to this size
 
 __global__ void level_pack_kernel(const int32_t *__restrict__ targets, const double *__restrict__ P,
                                   int64_t nnz, double scale, uint2 *rec) {
@@ -378,7 +491,10 @@ extern "C" int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, cons
     A.nonfinite = nonfinite;
     const int64_t rows = row_hi - row_lo;
     if (rows == 0) return DRG_OK;
-    const unsigned grid = (unsigned)ceil_div(rows, kWpb);
+    const int npw = (M == 0) ? 8 : (M <= 32 ? std::min(8, 32 / M) : 1);
+    const unsigned grid = (unsigned)ceil_div(ceil_div(rows, npw), kWpb);
+    const bool clamp = attractive_clip_active(b, clip);
+    const bool partner = n <= kPartnerMaxNodes;
     if (n_iter > 1 && (row_lo != 0 || row_hi != n))
         return fail(DRG_ERR_INVALID, "n_iter > 1 needs the full row range");
     float2 *src = reinterpret_cast<float2 *>(y_in);
@@ -395,9 +511,9 @@ extern "C" int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, cons
         A.t = t;
         A.lr = (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0);  // optimizer.py:322
         if (inplace) {
-            launch_iter<true>(grid, st, A, src, src);
+            launch_iter<true>(grid, st, A, npw, clamp, partner, src, src);
         } else {
-            launch_iter<false>(grid, st, A, src, dst);
+            launch_iter<false>(grid, st, A, npw, clamp, partner, src, dst);
             std::swap(src, dst);
         }
         DRG_LAUNCHED("layout_iter_kernel");
