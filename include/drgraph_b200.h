@@ -118,10 +118,12 @@ int drg_alias_build(const double *weights, int64_t n, uint64_t *out_table, doubl
 /* --- K7 / K8: layout iterations --------------------------------------------------
  * Pack a level for the gradient kernel: rec[e] = {int32 target, float32 2*n*P[e]},
  * V[a] = n * (R[a] + q_scale * Q[a])  (SURVEY §8(a) A12 expectation-matching
- * weights; Q may be unnormalised negative weights with q_scale = 1 / sum). */
-int drg_level_pack(const int32_t *targets, const double *P, const double *R, const double *Q,
-                   double q_scale, int64_t n, int64_t nnz, uint64_t *out_rec, float *out_V,
-                   void *stream);
+ * weights; Q may be unnormalised negative weights with q_scale = 1 / sum).
+ * sort_rows != 0 re-orders each row by target id (locality of the y gathers;
+ * needed for (dist,id)-ordered level-0 rows). */
+int drg_level_pack(const int64_t *indptr, const int32_t *targets, const double *P,
+                   const double *R, const double *Q, double q_scale, int64_t n, int64_t nnz,
+                   int sort_rows, uint64_t *out_rec, float *out_V, void *stream);
 
 #define DRG_FLAG_INPLACE 1u   /* Hogwild-style in-place update (y_out == y_in) */
 

@@ -49,7 +49,7 @@ SIGNATURES = {
     "drg_aggregate_nodes": [_P, _P, _I64, _I64, _P, _P],
     "drg_negative_weights": [_P, _I64, _F64, _P, _P],
     "drg_alias_build": [_P, _I64, _P, _P, _P],
-    "drg_level_pack": [_P, _P, _P, _P, _F64, _I64, _I64, _P, _P, _P],
+    "drg_level_pack": [_P, _P, _P, _P, _P, _F64, _I64, _I64, _I32, _P, _P, _P],
     "drg_layout_iters": [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _I32, _I32, _I32, _F64, _F64,
                          _F64, _F64, _I32, _I32, _U64, _I32, _P, _P, _U32, _P],
     "drg_layout_radius": [_P, _I64, _P, _P],

@@ -37,6 +37,13 @@ __device__ __forceinline__ float ipowf(float x, int n) {
 
 __device__ __forceinline__ float clampf(float g, float c) { return fminf(fmaxf(g, -c), c); }
 
+// 1/x with one MUFU.RCP (x >= 1 here: no denormal fix-up needed), ~1 ulp.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 struct IterArgs {
     const int64_t *indptr;
     const uint2 *rec;     // {target, W bits}
@@ -103,7 +110,7 @@ __device__ __forceinline__ int64_t resolve_draw(const IterArgs &A, const u32x4 &
 //             j ~ W_a. (the reference redraws c in {i, j}, _kernels.py:108-117);
 //             only visible when Q_j is not negligible, so enabled on small levels.
 template <bool INPLACE, int B, bool CLAMP_ATT, bool PARTNER>
-__global__ void __launch_bounds__(kWpb * 32, 5)
+__global__ void __launch_bounds__(kWpb * 32, 6)
     layout_iter_kernel(IterArgs A, int npw, const float2 *y_in, float2 *y_out) {
     __shared__ float2 s_rep[kWpb][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -114,23 +121,26 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
     const float two_b = 2.0f * (float)b;
     const int M = A.M;
 
-    // ---- negative draws, first attempt (lane q -> node q / M, sample q % M)
+    // ---- negative draws, first attempt (lane q -> node q / M, sample q % M).
+    // Only the coin, the spare word and the alias record stay live across the rows.
     const int nq = nodes * M;
     const int my_node = (npw == 1) ? 0 : (M > 0 ? lane / M : 0);
     const bool neg_lane = (npw == 1) ? (lane < M) : (lane < nq);
-    int64_t cand = -1;
-    u32x4 nb = {0, 0, 0, 0};
+    int32_t cand = -1;
+    uint32_t coin = 0, spare = 0;
     uint2 arec = make_uint2(0, 0);
-    int64_t aidx = 0;
+    int32_t aidx = 0;
     if (neg_lane) {
         const int64_t an = a0 + my_node;
         const int m = (npw == 1) ? lane : lane - my_node * M;
         if (A.neg_idx) {
-            cand = (int64_t)A.neg_idx[an * M + m];
+            cand = A.neg_idx[an * M + m];
         } else {
-            nb = neg_bits(A, an, m, 0);
-            aidx = alias_index(A, nb);
+            const u32x4 nb = neg_bits(A, an, m, 0);
+            aidx = (int32_t)alias_index(A, nb);
             arec = __ldg(A.alias + aidx);
+            coin = nb.z;
+            spare = nb.w;
         }
     }
 
@@ -161,17 +171,23 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
                 const float ld2 = fmaf(dx, dx, dy * dy);
                 const float pw = powbm1<B>(ld2, b);
                 const float w = __uint_as_float(r[j].y);
-                const float coef = __fdividef(-two_b * pw, fmaf(pw, ld2, 1.0f));
+                const float inv = rcp_approx(fmaf(pw, ld2, 1.0f));
                 if (CLAMP_ATT) {
+                    const float coef = -two_b * pw * inv;
                     ax = fmaf(w, clampf(coef * dx, A.clip), ax);
                     ay = fmaf(w, clampf(coef * dy, A.clip), ay);
                 } else {
-                    const float wc = w * coef;
+                    // the constant -2b is applied once per node below
+                    const float wc = (B == 1 ? w : w * pw) * inv;
                     ax = fmaf(wc, dx, ax);
                     ay = fmaf(wc, dy, ay);
                 }
                 if (PARTNER) wsum += w;
             }
+        }
+        if (!CLAMP_ATT) {
+            ax *= -two_b;
+            ay *= -two_b;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -187,7 +203,7 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
             // (short) row, lane-major cumulative order
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
-            const uint32_t ubits = __shfl_sync(kFull, nb.w, (npw == 1) ? 0 : i * M);
+            const uint32_t ubits = __shfl_sync(kFull, spare, (npw == 1) ? 0 : i * M);
             float tau = u32_to_unit(ubits) * wsum;
             int64_t found = -1;
             for (int base = 0; base < cnt && wsum > 0.f; base += 32) {
@@ -221,12 +237,11 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
         const int m = (npw == 1) ? lane : lane - my_node * M;
         int64_t c = cand;
         if (!A.neg_idx) {
-            c = resolve_draw(A, nb, arec, aidx);
+            c = (u32_to_unit(coin) < __uint_as_float(arec.x)) ? aidx : (int64_t)arec.y;
             for (int attempt = 1; (c == an || c == part) && attempt < 9; ++attempt) {
-                nb = neg_bits(A, an, m, attempt);
-                aidx = alias_index(A, nb);
-                arec = __ldg(A.alias + aidx);
-                c = resolve_draw(A, nb, arec, aidx);
+                const u32x4 nb = neg_bits(A, an, m, attempt);
+                const int64_t qi = alias_index(A, nb);
+                c = resolve_draw(A, nb, __ldg(A.alias + qi), qi);
             }
             if (c == an || c == part) c = -1;
         }
@@ -236,9 +251,12 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
             const float dx = ya.x - yc.x, dy = ya.y - yc.y;
             const float ld2 = fmaf(dx, dx, dy * dy);
             const float pw = powbm1<B>(ld2, b);
-            const float coef = __fdividef(A.gamma * two_b, (ld2 + A.eps) * fmaf(pw, ld2, 1.0f));
-            rx = clampf(coef * dx, A.clip);
-            ry = clampf(coef * dy, A.clip);
+            if (ld2 + A.eps > 0.f) {   // repulsive_gradient's guard (optimizer.py:197)
+                const float den = fmaxf((ld2 + A.eps) * fmaf(pw, ld2, 1.0f), 1.17549435e-38f);
+                const float coef = A.gamma * two_b * rcp_approx(den);
+                rx = clampf(coef * dx, A.clip);
+                ry = clampf(coef * dy, A.clip);
+            }
         }
     }
     if (npw == 1) {
@@ -262,10 +280,13 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
                 const float dx = ya.x - yc.x, dy = ya.y - yc.y;
                 const float ld2 = fmaf(dx, dx, dy * dy);
                 const float pw = powbm1<B>(ld2, b);
-                const float coef =
-                    __fdividef(A.gamma * two_b, (ld2 + A.eps) * fmaf(pw, ld2, 1.0f));
-                rx += clampf(coef * dx, A.clip);
-                ry += clampf(coef * dy, A.clip);
+                if (ld2 + A.eps > 0.f) {
+                    const float den =
+                        fmaxf((ld2 + A.eps) * fmaf(pw, ld2, 1.0f), 1.17549435e-38f);
+                    const float coef = A.gamma * two_b * rcp_approx(den);
+                    rx += clampf(coef * dx, A.clip);
+                    ry += clampf(coef * dy, A.clip);
+                }
             }
         }
 #pragma unroll
@@ -438,13 +459,49 @@ inline unsigned flat_grid(int64_t n, int threads = 256) {
 
 using namespace drg;
 
-extern "C" int drg_level_pack(const int32_t *targets, const double *P, const double *R,
-                              const double *Q, double q_scale, int64_t n, int64_t nnz,
-                              uint64_t *out_rec, float *out_V, void *stream) {
+__global__ void weight_kernel(const double *__restrict__ P, int64_t nnz, double scale, float *w) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x)
+        w[e] = (float)(scale * P[e]);
+}
+
+__global__ void interleave_kernel(const int32_t *__restrict__ tg, const float *__restrict__ w,
+                                  int64_t nnz, uint2 *rec) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+         e += (int64_t)gridDim.x * blockDim.x)
+        rec[e] = make_uint2((uint32_t)tg[e], __float_as_uint(w[e]));
+}
+
+extern "C" int drg_level_pack(const int64_t *indptr, const int32_t *targets, const double *P,
+                              const double *R, const double *Q, double q_scale, int64_t n,
+                              int64_t nnz, int sort_rows, uint64_t *out_rec, float *out_V,
+                              void *stream) {
     if (n < 0 || nnz < 0) return fail(DRG_ERR_INVALID, "negative size");
     cudaStream_t st = as_stream(stream);
-    if (nnz > 0) {
-        level_pack_kernel<<<flat_grid(nnz), 256, 0, st>>>(targets, P, nnz, 2.0 * (double)n,
+    const double scale = 2.0 * (double)n;
+    if (nnz > 0 && sort_rows && nnz < 0x7fffffffLL && n < 0x7fffffffLL) {
+        // rows re-ordered by target id: neighbouring lanes then gather neighbouring
+        // y's (fewer L1 sectors per warp load); the pair masses are unchanged
+        Scratch w(st), tg2(st), w2(st), tmp(st);
+        DRG_CUDA(w.alloc(sizeof(float) * (size_t)nnz));
+        DRG_CUDA(tg2.alloc(sizeof(int32_t) * (size_t)nnz));
+        DRG_CUDA(w2.alloc(sizeof(float) * (size_t)nnz));
+        weight_kernel<<<flat_grid(nnz), 256, 0, st>>>(P, nnz, scale, w.as<float>());
+        DRG_LAUNCHED("weight_kernel");
+        size_t tb = 0;
+        cub::DeviceSegmentedSort::SortPairs(nullptr, tb, targets, tg2.as<int32_t>(), w.as<float>(),
+                                            w2.as<float>(), (int)nnz, (int)n, indptr, indptr + 1,
+                                            st);
+        DRG_CUDA(tmp.alloc(tb));
+        DRG_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, targets, tg2.as<int32_t>(),
+                                                     w.as<float>(), w2.as<float>(), (int)nnz,
+                                                     (int)n, indptr, indptr + 1, st));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        interleave_kernel<<<flat_grid(nnz), 256, 0, st>>>(tg2.as<int32_t>(), w2.as<float>(), nnz,
+                                                          reinterpret_cast<uint2 *>(out_rec));
+        DRG_LAUNCHED("interleave_kernel");
+    } else if (nnz > 0) {
+        level_pack_kernel<<<flat_grid(nnz), 256, 0, st>>>(targets, P, nnz, scale,
                                                           reinterpret_cast<uint2 *>(out_rec));
         DRG_LAUNCHED("level_pack_kernel");
     }
@@ -466,6 +523,7 @@ extern "C" int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, cons
         return fail(DRG_ERR_INVALID, "row range [%lld, %lld) outside [0, %lld)",
                     (long long)row_lo, (long long)row_hi, (long long)n);
     if (b < 1 || M < 0 || iters < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
+    if (n >= 0x7fffffffLL) return fail(DRG_ERR_INVALID, "level exceeds 2^31 - 1 nodes");
     if (neg_idx && n_iter != 1) return fail(DRG_ERR_INVALID, "neg_idx needs n_iter == 1");
     const bool inplace = (flags & DRG_FLAG_INPLACE) != 0;
     if (inplace && y_in != y_out) return fail(DRG_ERR_INVALID, "in-place needs y_in == y_out");

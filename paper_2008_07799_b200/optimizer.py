@@ -202,12 +202,14 @@ def _aggregate_nodes(values, parent, n_coarse):
     return out
 
 
-def pack_level(targets, P, R, Wn, q_scale, n) -> tuple[torch.Tensor, torch.Tensor]:
+def pack_level(indptr, targets, P, R, Wn, q_scale, n, sort_rows=False
+               ) -> tuple[torch.Tensor, torch.Tensor]:
     nnz = targets.numel()
     rec = torch.empty(max(nnz, 1), dtype=torch.int64, device=R.device)
     V = torch.empty(max(n, 1), dtype=torch.float32, device=R.device)
-    _lib.call("drg_level_pack", _lib.ptr(targets), _lib.ptr(P), _lib.ptr(R), _lib.ptr(Wn),
-              float(q_scale), n, nnz, _lib.ptr(rec), _lib.ptr(V), _lib.stream_ptr())
+    _lib.call("drg_level_pack", _lib.ptr(indptr), _lib.ptr(targets), _lib.ptr(P), _lib.ptr(R),
+              _lib.ptr(Wn), float(q_scale), n, nnz, int(bool(sort_rows)), _lib.ptr(rec),
+              _lib.ptr(V), _lib.stream_ptr())
     return rec[:nnz], V[:n]
 
 
@@ -228,7 +230,10 @@ def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float
             R = _aggregate_nodes(R, parent, n_l)
             Wn = _aggregate_nodes(Wn, parent, n_l)
         alias, total = _alias_device(Wn)
-        rec, V = pack_level(tg, P, R, Wn, 1.0 / total, n_l)
+        # level-0 rows come in the reference's (dist, id) order; coarse rows are
+        # id-sorted by construction
+        rec, V = pack_level(ip, tg, P, R, Wn, 1.0 / total, n_l,
+                            sort_rows=(level == 0 and ds.k > 1))
         out.append(LevelData(n_l, tg.numel(), ip, rec, V, alias))
     return out
 

@@ -377,7 +377,7 @@ def test_sgd_epoch_attractive_only_contracts():
     for t in range(100):
         B.sgd_epoch(pos, h, s, params, t)
         ld = float(np.linalg.norm(pos[0] - pos[1]))
-        assert ld < last
+        assert ld <= last        # fp32 positions: contraction stops at the ulp of |y|
         last = ld
     assert last < 0.2
 
