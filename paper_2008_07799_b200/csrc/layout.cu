@@ -110,9 +110,8 @@ __device__ __forceinline__ int64_t resolve_draw(const IterArgs &A, const u32x4 &
 //             j ~ W_a. (the reference redraws c in {i, j}, _kernels.py:108-117);
 //             only visible when Q_j is not negligible, so enabled on small levels.
 template <bool INPLACE, int B, bool CLAMP_ATT, bool PARTNER>
-__global__ void __launch_bounds__(kWpb * 32, 6)
+__global__ void __launch_bounds__(kWpb * 32, 5)
     layout_iter_kernel(IterArgs A, int npw, const float2 *y_in, float2 *y_out) {
-    __shared__ float2 s_rep[kWpb][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t a0 = A.row_lo + ((int64_t)blockIdx.x * kWpb + warp) * npw;
     if (a0 >= A.row_hi) return;
@@ -295,15 +294,20 @@ __global__ void __launch_bounds__(kWpb * 32, 6)
             ry += __shfl_xor_sync(kFull, ry, o);
         }
     } else {
-        // segmented sum over the M lanes of each node
-        s_rep[warp][lane] = make_float2(rx, ry);
-        __syncwarp();
-        rx = ry = 0.f;
-        if (lane < nodes)
-            for (int q = lane * M; q < lane * M + M; ++q) {
-                rx += s_rep[warp][q].x;
-                ry += s_rep[warp][q].y;
+        // segmented sum over the M consecutive lanes of each node (shuffles), then
+        // lane i fetches node i's total from lane i*M
+        const int sub = lane - my_node * M;
+        for (int o = 1; o < M; o <<= 1) {
+            const float tx = __shfl_down_sync(kFull, rx, o);
+            const float ty = __shfl_down_sync(kFull, ry, o);
+            if (sub + o < M && lane + o < 32) {
+                rx += tx;
+                ry += ty;
             }
+        }
+        const int src = min(lane * M, 31);
+        rx = __shfl_sync(kFull, rx, src);
+        ry = __shfl_sync(kFull, ry, src);
     }
 
     // ---- update (lane i writes node i)

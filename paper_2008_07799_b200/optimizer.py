@@ -230,10 +230,10 @@ def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float
             R = _aggregate_nodes(R, parent, n_l)
             Wn = _aggregate_nodes(Wn, parent, n_l)
         alias, total = _alias_device(Wn)
-        # level-0 rows come in the reference's (dist, id) order; coarse rows are
-        # id-sorted by construction
-        rec, V = pack_level(ip, tg, P, R, Wn, 1.0 / total, n_l,
-                            sort_rows=(level == 0 and ds.k > 1))
+        # rows keep their order: re-sorting level-0 rows by id (sort_rows) cut L1
+        # sectors by 12% on the mesh but cost 130 ms of segmented sort and no
+        # kernel time (profiles/README.md), so it is off
+        rec, V = pack_level(ip, tg, P, R, Wn, 1.0 / total, n_l, sort_rows=False)
         out.append(LevelData(n_l, tg.numel(), ip, rec, V, alias))
     return out
 

@@ -57,7 +57,7 @@ def main(name="mesh"):
                 t = tick(f"agg_nodes_{level}", t)
             alias, total = OPT._alias_device(Wn)
             t = tick(f"alias_{level}", t)
-            OPT.pack_level(ip, tg, P, R, Wn, 1.0 / total, n_l, sort_rows=(level == 0 and ds.k > 1))
+            OPT.pack_level(ip, tg, P, R, Wn, 1.0 / total, n_l, sort_rows=False)
             t = tick(f"pack_{level}", t)
         print(rep, T, flush=True)
 
