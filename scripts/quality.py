@@ -1,0 +1,104 @@
+"""Final-layout quality parity: GPU layouts vs the reference algorithm (oracle port)
+on the same graph, P, hierarchy and initial Y, over many seeds.
+
+    python scripts/quality.py grid 20        # C1, 20 seeds
+    python scripts/quality.py rgg 5          # C2, 5 seeds (KL by Monte-Carlo Z, sampled NP)
+
+Prints one JSON line per (workload, impl) with KL / NP medians and spreads
+(SURVEY §8(c) evaluators: KL with the unnormalised t-kernel of lp_kernel,
+optimizer.py:150-152; NP = metrics.py:114-145).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+from oracle import oracle as O  # noqa: E402
+
+CONFIGS = {
+    "grid": dict(k=2, perplexity=30.0, iters=300, max_levels=1, init="uniform", z_pairs=None,
+                 np_sample=None),
+    "rgg": dict(k=3, perplexity=30.0, iters=500, max_levels=3, init="normal", z_pairs=20_000_000,
+                np_sample=20_000),
+    "mesh_small": dict(k=2, perplexity=50.0, iters=800, max_levels=4, init="normal",
+                       z_pairs=20_000_000, np_sample=20_000),
+}
+
+
+def graph_for(name):
+    import paper_2008_07799_b200 as B
+    from paper_2008_07799_b200 import synthetic
+    if name == "grid":
+        g = synthetic.grid(100, 100, device="host")
+    elif name == "rgg":
+        g = synthetic.rgg(200_000, seed=0, device="host")
+    else:
+        g = synthetic.mesh3d(40, device="host")
+    return O.Graph(g.indptr, g.indices), B.Graph(g.indptr, g.indices)
+
+
+def init_for(cfg, n, seed):
+    rng = np.random.default_rng(O.derive_seed(seed, O.INIT_TAG))
+    if cfg["init"] == "uniform":
+        return rng.uniform(-1e-4, 1e-4, size=(n, 2)).astype(np.float32).astype(np.float64)
+    return rng.normal(0.0, 1e-4, size=(n, 2)).astype(np.float32).astype(np.float64)
+
+
+def main(name="grid", n_seeds=10, modes=("jacobi", "inplace")):
+    import paper_2008_07799_b200 as B
+    cfg = CONFIGS[name]
+    og, bg = graph_for(name)
+    nd = O.all_k_neighborhoods(og, cfg["k"])
+    ns = O.build_sparse_similarity(nd, cfg["perplexity"])
+    del nd
+    sample = None
+    if cfg["np_sample"]:
+        sample = np.random.default_rng(7).choice(og.node_count, cfg["np_sample"], replace=False)
+    results = {"reference": [], **{m: [] for m in modes}}
+    threads = os.cpu_count() if og.node_count > 50_000 else 1
+    for seed in range(n_seeds):
+        h = O.build_hierarchy(og, 0.8, 16, O.derive_seed(seed, O.HIERARCHY_TAG),
+                              max_levels=cfg["max_levels"])
+        y0 = init_for(cfg, h.levels[-1].node_count, seed)
+        t0 = time.perf_counter()
+        opt = O.OptimizerParams(iters=cfg["iters"], seed=seed, threads=threads)
+        pos, _, _, _ = O.layout_graph(og, k=cfg["k"], perplexity=cfg["perplexity"], params=opt,
+                                      max_levels=cfg["max_levels"], init=y0)
+        t_ref = time.perf_counter() - t0
+        runs = {"reference": (pos, t_ref)}
+        for m in modes:
+            t0 = time.perf_counter()
+            lay = B.layout_graph(bg, B.SimilarityParams(k=cfg["k"], perplexity=cfg["perplexity"]),
+                                 B.OptimizerParams(iters=cfg["iters"], seed=seed, update=m,
+                                                   init=cfg["init"]),
+                                 max_levels=cfg["max_levels"], init_positions=y0)
+            runs[m] = (lay.positions, time.perf_counter() - t0)
+        for key, (y, t) in runs.items():
+            kl = O.kl_divergence(ns, y, 2, z_pairs=cfg["z_pairs"], seed=11)
+            npv = O.neighborhood_preservation(og, y, 2, sample=sample)
+            results[key].append({"seed": seed, "kl": kl, "np": npv, "s": t})
+    for key, rs in results.items():
+        kls = [r["kl"] for r in rs]
+        nps = [r["np"] for r in rs]
+        line = {"workload": name, "impl": key, "seeds": len(rs),
+                "kl_median": statistics.median(kls), "kl_min": min(kls), "kl_max": max(kls),
+                "np_median": statistics.median(nps), "np_min": min(nps), "np_max": max(nps),
+                "seconds_median": statistics.median(r["s"] for r in rs)}
+        if key != "reference":
+            ref = results["reference"]
+            line["kl_rel_vs_ref"] = line["kl_median"] / statistics.median(r["kl"] for r in ref) - 1
+            line["np_rel_vs_ref"] = line["np_median"] / statistics.median(r["np"] for r in ref) - 1
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = sys.argv[1:]
+    main(a[0] if a else "grid", int(a[1]) if len(a) > 1 else 10)
