@@ -68,7 +68,7 @@ def parse():
     ap.add_argument("--iters", type=int, default=None, help="override iterations per level")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--update", default="jacobi", choices=["jacobi", "inplace"])
+    ap.add_argument("--update", default="jacobi", choices=["jacobi", "inplace", "sampled"])
     return ap.parse_args()
 
 

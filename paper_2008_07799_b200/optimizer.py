@@ -55,7 +55,8 @@ class OptimizerParams:
     extensions: ``init`` ("normal" = reference N(0, init_scale); "uniform" =
     U[-init_scale, init_scale], BASELINE config C1), ``update`` ("jacobi" =
     deterministic double buffer; "inplace" = Hogwild-style in-place gather, closer
-    to the reference's sequential order), ``shard_min_nodes`` (multi-GPU).
+    to the reference's sequential order; "sampled" = the reference's own sampled
+    steps, Hogwild with atomics), ``shard_min_nodes`` (multi-GPU).
     ``threads`` is accepted and ignored (the GPU replaces the Hogwild threads)."""
 
     neg_samples: int = 5
@@ -92,8 +93,8 @@ class OptimizerParams:
             raise ValueError("seed must be non-negative")
         if self.init not in ("normal", "uniform"):
             raise ValueError("init must be 'normal' or 'uniform'")
-        if self.update not in ("jacobi", "inplace"):
-            raise ValueError("update must be 'jacobi' or 'inplace'")
+        if self.update not in ("jacobi", "inplace", "sampled"):
+            raise ValueError("update must be 'jacobi', 'inplace' or 'sampled'")
 
 
 @dataclass
@@ -242,6 +243,41 @@ StepFn = Callable[[torch.Tensor, torch.Tensor, int, int, int], None]
 
 
 @dataclass
+class SampledData:
+    """Level-0 sampling tables of the reference-faithful mode (update="sampled"):
+    P^0 CSR with per-row cumulative weights, a Vose table over the row masses
+    (sources), the level-0 negative table, and the flat level maps."""
+
+    indptr0: torch.Tensor
+    targets0: torch.Tensor
+    cum0: torch.Tensor
+    src_alias: torch.Tensor
+    neg_alias: torch.Tensor
+    flat_maps: list   # flat_maps[l]: level-0 id -> level-l id (None at level 0)
+
+
+def build_sampled_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_alias: torch.Tensor
+                       ) -> SampledData:
+    n0 = ds.node_count
+    cum = torch.empty(max(ds.entry_count, 1), dtype=torch.float32, device=ds.weights.device)
+    _lib.call("drg_row_cumulative", _lib.ptr(ds.indptr), _lib.ptr(ds.weights), n0,
+              _lib.ptr(cum), _lib.stream_ptr())
+    src_alias, _ = _alias_device(ds.row_mass)
+    flat = [None]
+    cur = None
+    for level in range(1, dh.depth + 1):
+        nxt = torch.empty(n0, dtype=torch.int32, device=ds.weights.device)
+        if cur is None:
+            nxt.copy_(dh.maps[0])
+        else:
+            _lib.call("drg_compose_maps", _lib.ptr(cur), _lib.ptr(dh.maps[level - 1]), n0,
+                      _lib.ptr(nxt), _lib.stream_ptr())
+        flat.append(nxt)
+        cur = nxt
+    return SampledData(ds.indptr, ds.targets, cum, src_alias, neg_alias, flat)
+
+
+@dataclass
 class LayoutPlan:
     """Prepared device state of one layout: level data, parent maps, params."""
 
@@ -249,6 +285,7 @@ class LayoutPlan:
     maps: list
     opt: OptimizerParams
     nonfinite: torch.Tensor = None
+    sampled: SampledData | None = None
 
     @property
     def depth(self) -> int:
@@ -314,6 +351,8 @@ class LayoutPlan:
         if group is not None:
             import torch.distributed as dist
             world = dist.get_world_size(group)
+        if self.opt.update == "sampled":
+            return self._run_level_sampled(level, y, t0, n_iter)
         inplace = self.opt.update == "inplace"
         if world > 1 and L.n >= self.opt.shard_min_nodes:
             return self._run_level_sharded(level, y, t0, n_iter, group, step_fn)
@@ -331,6 +370,25 @@ class LayoutPlan:
         out = torch.empty_like(y)
         self.kernel_step(level, y, out, 0, L.n, t0, n_iter)
         return out
+
+    def _run_level_sampled(self, level, y, t0, n_iter):
+        """Reference-faithful epochs: n_l sampled steps each, Hogwild on y."""
+        S = self.sampled
+        if S is None:
+            raise RuntimeError("plan was built without sampled-mode tables")
+        L, gamma, seed = self._level_args(level)
+        o = self.opt
+        fm = S.flat_maps[level]
+        n0 = S.indptr0.numel() - 1
+        _lib.call("drg_layout_sampled", _lib.ptr(S.indptr0), _lib.ptr(S.targets0),
+                  _lib.ptr(S.cum0), _lib.ptr(S.src_alias), _lib.ptr(S.neg_alias), n0,
+                  _lib.ptr(fm), _lib.ptr(y), L.n, L.n, t0, n_iter, o.iters, float(o.lr0),
+                  float(gamma), float(o.eps), float(o.grad_clip), o.b, o.neg_samples, seed,
+                  level, max(256, L.n // 4), _lib.stream_ptr())
+        if not bool(torch.isfinite(y).all()):
+            raise FloatingPointError(f"non-finite coordinate in epochs {t0}..{t0 + n_iter - 1} "
+                                     f"at level {level}")
+        return y
 
     def _run_level_sharded(self, level, y, t0, n_iter, group, step_fn):
         import torch.distributed as dist
@@ -384,7 +442,10 @@ def device_radius(y: torch.Tensor) -> float:
 
 
 def build_plan(ds: DeviceSimilarity, dh: DeviceHierarchy, opt: OptimizerParams) -> LayoutPlan:
-    return LayoutPlan(build_level_data(ds, dh, opt.neg_power), list(dh.maps), opt)
+    plan = LayoutPlan(build_level_data(ds, dh, opt.neg_power), list(dh.maps), opt)
+    if opt.update == "sampled":
+        plan.sampled = build_sampled_data(ds, dh, plan.levels[0].alias)
+    return plan
 
 
 @dataclass

@@ -52,7 +52,7 @@ def init_for(cfg, n, seed):
     return rng.normal(0.0, 1e-4, size=(n, 2)).astype(np.float32).astype(np.float64)
 
 
-def main(name="grid", n_seeds=10, modes=("jacobi", "inplace")):
+def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled")):
     import paper_2008_07799_b200 as B
     cfg = CONFIGS[name]
     og, bg = graph_for(name)

@@ -404,3 +404,22 @@ def test_abi_error_mapping():
     assert rc == _lib.DRG_ERR_INVALID
     with pytest.raises(ValueError):
         _lib.check(rc)
+
+
+def test_sampled_mode_matches_reference_behaviour(golden):
+    """update="sampled" replays the reference step: on K2 every negative hits the
+    pair and is rejected (_kernels.py:108-117), so the layout stays near its init
+    scale (test_optimizer.py:260-268)."""
+    k2 = as_gpu_graph(O.from_edges(np.array([[0, 1]]), 2))
+    lay = B.layout_graph(k2, opt_params=B.OptimizerParams(seed=9, iters=100, update="sampled"))
+    ld = float(np.linalg.norm(lay.positions[0] - lay.positions[1]))
+    assert 0.0 < ld < 1e-2
+    g = as_gpu_graph(golden_graph(golden, "r500"))
+    lay = B.layout_graph(g, B.SimilarityParams(k=2),
+                         B.OptimizerParams(seed=1, iters=40, update="sampled"))
+    assert np.isfinite(lay.positions).all() and lay.positions.std() > 1e-3
+    # two components stay apart under sampled repulsion
+    two = as_gpu_graph(O.from_edges(np.array([[0, 1], [1, 2], [3, 4], [4, 5]]), 6))
+    lay = B.layout_graph(two, opt_params=B.OptimizerParams(seed=2, iters=60, update="sampled"))
+    c0, c1 = lay.positions[:3].mean(0), lay.positions[3:].mean(0)
+    assert np.linalg.norm(c0 - c1) > 1e-3
