@@ -52,6 +52,10 @@ WORKLOADS = {
     "mesh": dict(desc="C4: 120^3 26-neighbour mesh, k=2, perplexity 50, M=5, 800 iterations per "
                       "level, 4 levels", gen=("mesh3d", (120,)), k=2, perplexity=50.0, iters=800,
                  M=5, hier=dict(max_levels=4), init="normal"),
+    "ba": dict(desc="C3: Barabasi-Albert 1M (m=4), k=2 with neighbour cap 256 (union "
+                    "symmetrised), perplexity 50, M=5, 500 iterations, rho-rule levels",
+               gen=("barabasi_albert", (1_000_000, 4)), k=2, perplexity=50.0, iters=500, M=5,
+               hier=dict(), init="normal", cap=256),
     "rmat": dict(desc="C5: R-MAT scale 24 edge factor 16, k=1, M=5, 500 iterations, 5 levels",
                  gen=("rmat", (24, 16)), k=1, perplexity="auto", iters=500, M=5,
                  hier=dict(force_levels=5, max_levels=5), init="normal"),
@@ -151,7 +155,7 @@ def build_workload(name):
 def params_for(name, iters_override=None, update="jacobi"):
     import paper_2008_07799_b200 as B
     w = WORKLOADS[name]
-    sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"])
+    sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"], neighbor_cap=w.get("cap"))
     opt = B.OptimizerParams(neg_samples=w["M"], iters=iters_override or w["iters"], seed=0,
                             init=w["init"], update=update)
     return sim, opt, dict(w["hier"])
@@ -203,10 +207,11 @@ def cpu_prepare_reference(name, sim, opt, hier):
         raise RuntimeError("the synthetic generators run on the device")
     t = {}
     t0 = time.perf_counter()
-    nd = O.all_k_neighborhoods(g, sim.k)
+    nd = O.all_k_neighborhoods(g, sim.k, cap=sim.neighbor_cap or 0)
     t["khop_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
-    ns = O.build_sparse_similarity(nd, sim.perplexity)
+    ns = (O.build_capped_similarity(nd, sim.perplexity) if sim.neighbor_cap
+          else O.build_sparse_similarity(nd, sim.perplexity))
     del nd
     t["similarity_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
@@ -420,7 +425,7 @@ def cpu_baseline_from_gpu(dg, sim, opt, sizes, hier):
     from paper_2008_07799_b200.optimizer import _HIERARCHY_TAG, _derive_seed
     from paper_2008_07799_b200.similarity import device_similarity
     threads = os.cpu_count() or 1
-    ds = device_similarity(device_k_neighborhoods(dg, sim.k), sim)
+    ds = device_similarity(device_k_neighborhoods(dg, sim.k, sim.neighbor_cap), sim)
     ns = O.SparseSimilarity(ds.indptr.cpu().numpy(), ds.targets.cpu().numpy(),
                             ds.weights.cpu().numpy(), ds.total_mass, ds.sigma.cpu().numpy(),
                             ds.k)

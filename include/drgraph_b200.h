@@ -75,6 +75,20 @@ int drg_similarity(const int64_t *nd_indptr, const int32_t *nd_ids, const int32_
                    double *out_weights, double *out_row_mass, double *out_total_mass,
                    int64_t *out_n_nonisolated, void *stream);
 
+/* Capped rows (BASELINE C3, k-hop rows truncated to their (dist,id)-sorted prefix):
+ * the same per-row bisection and conditional rows, then UNION symmetrisation
+ * P_ij = (p_{j|i} + p_{i|j}) / (2 N_ne) with a missing mirror counting 0 (SURVEY
+ * §8(a) A6; the reference mis-symmetrises such rows).  The output CSR has rows
+ * sorted by target id; out_targets / out_weights must hold 2*nnz entries;
+ * *out_nnz (host) is the union size. */
+int drg_similarity_union(const int64_t *nd_indptr, const int32_t *nd_ids,
+                         const int32_t *nd_dists, int64_t n, int64_t nnz, int k,
+                         double perplexity, double tol, int max_iter, double sigma_min,
+                         double sigma_max, double *out_sigma, int64_t *out_indptr,
+                         int32_t *out_targets, double *out_weights, double *out_row_mass,
+                         int64_t *out_nnz, double *out_total_mass, int64_t *out_n_nonisolated,
+                         void *stream);
+
 /* --- K4: coarsening ------------------------------------------------------------
  * Replaces coarsen_with_order (multilevel.py:48-79).  `order` (device int64[n])
  * is the visiting permutation (multilevel.py:91 draws it with numpy PCG64; the

@@ -42,6 +42,8 @@ SIGNATURES = {
     "drg_khop_fill": [_P, _P, _I64, _I32, _I64, _P, _P, _P, _P],
     "drg_similarity": [_P, _P, _P, _I64, _I64, _I32, _F64, _F64, _I32, _F64, _F64, _P, _P, _P,
                        _P, _P, _P],
+    "drg_similarity_union": [_P, _P, _P, _I64, _I64, _I32, _F64, _F64, _I32, _F64, _F64, _P, _P,
+                             _P, _P, _P, _P, _P, _P, _P],
     "drg_coarsen": [_P, _P, _I64, _P, _P, _P, _P, _P],
     "drg_coarse_graph": [_P, _P, _I64, _P, _I64, _P, _P, _P, _P],
     "drg_compose_maps": [_P, _P, _I64, _P, _P],

@@ -176,6 +176,8 @@ inline int bits_for(uint64_t v) {
     return b;
 }
 
+}  // namespace
+
 // Sort keys (and optional fp64 values), drop the sentinel tail, reduce duplicates
 // (values summed), and emit a CSR.  Returns the unique count in *out_nnz.
 int sort_unique_csr(uint64_t *keys, double *vals, int64_t nnz, int64_t n_coarse,
@@ -240,7 +242,6 @@ int sort_unique_csr(uint64_t *keys, double *vals, int64_t nnz, int64_t n_coarse,
     return DRG_OK;
 }
 
-}  // namespace
 }  // namespace drg
 
 using namespace drg;

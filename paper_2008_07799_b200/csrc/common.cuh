@@ -48,6 +48,13 @@ struct Scratch {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Sort 64-bit (row << 32 | col) keys (+ optional fp64 values), drop keys whose row
+// is >= n_rows (sentinels), sum duplicate keys' values, emit a CSR with rows
+// sorted.  *out_nnz (host) receives the unique count.  Defined in coarsen.cu.
+int sort_unique_csr(uint64_t *keys, double *vals, int64_t nnz, int64_t n_rows,
+                    int64_t *out_indptr, int32_t *out_cols, double *out_vals, int64_t *out_nnz,
+                    cudaStream_t st);
+
 // grid size for warp-per-item kernels: one warp per item, `wpb` warps per block
 inline unsigned warp_grid(int64_t items, int wpb) {
     int64_t g = ceil_div(items, wpb);

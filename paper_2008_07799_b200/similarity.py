@@ -119,8 +119,7 @@ def device_similarity(nd: DeviceNeighborDistances, params: SimilarityParams | No
     """K2 + K3 on resident k-hop rows (drg_similarity)."""
     params = params or SimilarityParams(k=nd.k)
     if nd.cap:
-        raise NotImplementedError("neighbor_cap similarity (union symmetrisation) is not built "
-                                  "on the GPU yet")
+        return device_similarity_union(nd, params)
     n, nnz = nd.node_count, nd.nnz
     dev = nd.indptr.device
     sigma = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
@@ -137,6 +136,29 @@ def device_similarity(nd: DeviceNeighborDistances, params: SimilarityParams | No
                             total.value, n_ne.value, nd.k)
 
 
+def device_similarity_union(nd: DeviceNeighborDistances, params: SimilarityParams
+                            ) -> DeviceSimilarity:
+    """Capped rows (BASELINE C3): conditional rows over the capped prefixes, then
+    union symmetrisation (drg_similarity_union); rows of the result are id-sorted."""
+    n, nnz = nd.node_count, nd.nnz
+    dev = nd.indptr.device
+    sigma = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    indptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    targets = torch.empty(max(2 * nnz, 1), dtype=torch.int32, device=dev)
+    weights = torch.empty(max(2 * nnz, 1), dtype=torch.float64, device=dev)
+    row_mass = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    out_nnz, total, n_ne = _lib.out_i64(), _lib.out_f64(), _lib.out_i64()
+    perp = -1.0 if params.perplexity == "auto" else float(params.perplexity)
+    _lib.call("drg_similarity_union", _lib.ptr(nd.indptr), _lib.ptr(nd.ids), _lib.ptr(nd.dists),
+              n, nnz, nd.k, perp, float(params.tol), int(params.max_iter),
+              float(params.sigma_min), float(params.sigma_max), _lib.ptr(sigma), _lib.ptr(indptr),
+              _lib.ptr(targets), _lib.ptr(weights), _lib.ptr(row_mass), _lib.byref(out_nnz),
+              _lib.byref(total), _lib.byref(n_ne), _lib.stream_ptr())
+    m = out_nnz.value
+    return DeviceSimilarity(indptr, targets[:m].clone(), weights[:m].clone(), sigma[:n],
+                            row_mass[:n], total.value, n_ne.value, nd.k)
+
+
 def build_sparse_similarity(nd: NeighborDistances,
                             params: SimilarityParams | None = None) -> SparseSimilarity:
     """similarity.py:216-278 on the GPU.  P matches the reference within 1e-12
@@ -145,6 +167,9 @@ def build_sparse_similarity(nd: NeighborDistances,
     if params is None:
         params = SimilarityParams()
     _lib.load()
-    ds = device_similarity(DeviceNeighborDistances.from_host(nd), params)
+    dnd = DeviceNeighborDistances.from_host(nd)
+    if params.neighbor_cap:
+        dnd.cap = int(params.neighbor_cap)
+    ds = device_similarity(dnd, params)
     return ds.to_host()
 

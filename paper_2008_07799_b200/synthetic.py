@@ -71,32 +71,27 @@ def rgg(n: int = 200_000, seed: int = 0, mean_degree: float = 10.0, device="cuda
 
 
 def barabasi_albert(n: int = 1_000_000, m: int = 4, seed: int = 0, device="cuda"):
-    """Preferential attachment: each new node links to m distinct targets drawn
-    proportionally to degree (repeated-endpoint list), starting from a star on
-    m + 1 nodes."""
-    rng = np.random.default_rng(seed)
-    src = np.empty((n - m - 1) * m + m, dtype=np.int64)
-    dst = np.empty_like(src)
-    src[:m] = 0
-    dst[:m] = np.arange(1, m + 1)
-    ends = np.empty(2 * len(src), dtype=np.int64)
-    ends[:2 * m:2] = 0
-    ends[1:2 * m:2] = np.arange(1, m + 1)
-    fill = 2 * m
-    k = m
-    for v in range(m + 1, n):
-        chosen = set()
-        while len(chosen) < m:
-            chosen.add(int(ends[rng.integers(0, fill)]))
-        for u in chosen:
-            src[k] = v
-            dst[k] = u
-            ends[fill] = v
-            ends[fill + 1] = u
-            fill += 2
-            k += 1
-    e = torch.from_numpy(np.stack([src[:k], dst[:k]], 1)).cuda()
-    return _finish(device_from_edges(e, n), device)
+    """Preferential attachment, m edges per new node, in the linearised-chord-
+    diagram form (Bollobas-Riordan): edge e of node e // m gets endpoint slots 2e
+    (itself) and 2e+1, which copies a uniform slot r in [0, 2e+1] -- i.e. a node
+    chosen proportionally to its current degree.  Copy chains are resolved on the
+    device by pointer jumping; loops and repeated edges are dropped by
+    drg_from_edges.  Power-law degrees (exponent 3)."""
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    E = m * n
+    e = torch.arange(E, dtype=torch.int64, device="cuda")
+    span = (2 * e + 2).to(torch.float64)
+    r = torch.minimum((torch.rand(E, dtype=torch.float64, device="cuda", generator=gen)
+                       * span).to(torch.int64), 2 * e + 1)
+    ptr = r.clone()
+    for _ in range(256):
+        odd = (ptr & 1) == 1
+        if not bool(odd.any()):
+            break
+        ptr = torch.where(odd, r[torch.clamp((ptr - 1) // 2, min=0)], ptr)
+    pairs = torch.stack([e // m, (ptr // 2) // m], 1)
+    return _finish(device_from_edges(pairs, n), device)
 
 
 def rmat(scale: int = 24, edge_factor: int = 16, a=0.57, b=0.19, c=0.19, seed: int = 0,

@@ -423,3 +423,53 @@ def test_sampled_mode_matches_reference_behaviour(golden):
     lay = B.layout_graph(two, opt_params=B.OptimizerParams(seed=2, iters=60, update="sampled"))
     c0, c1 = lay.positions[:3].mean(0), lay.positions[3:].mean(0)
     assert np.linalg.norm(c0 - c1) > 1e-3
+
+
+@pytest.mark.parametrize("cap,perp", [(4, "auto"), (16, 5.0), (16, "auto"), (64, 10.0)])
+def test_capped_union_similarity_vs_oracle(golden, cap, perp):
+    """BASELINE C3: capped rows + union symmetrisation, vs the oracle restatement
+    (same arithmetic order: bitwise-equal weights except ulp differences of exp)."""
+    g = golden_graph(golden, "dense80")
+    ond = O.all_k_neighborhoods(g, 2, cap=cap)
+    want = O.build_capped_similarity(ond, perp)
+    nd = B.all_k_neighborhoods(as_gpu_graph(g), 2, cap=cap)
+    got = B.build_sparse_similarity(nd, B.SimilarityParams(k=2, perplexity=perp, neighbor_cap=cap))
+    assert np.array_equal(got.indptr, want.indptr)
+    assert np.array_equal(got.targets, want.targets)
+    np.testing.assert_allclose(got.weights, want.weights, rtol=1e-5, atol=0)
+    assert abs(got.total_mass - 1.0) <= 1e-9
+    ent = {(int(i), int(j)): w for i, j, w in zip(got.sources(), got.targets, got.weights)}
+    for (i, j), w in ent.items():
+        assert ent[(j, i)] == w
+
+
+def test_ba_capped_pipeline_runs():
+    from paper_2008_07799_b200 import synthetic
+    g = synthetic.barabasi_albert(20_000, 4, seed=1, device="host")
+    deg = np.diff(g.indptr)
+    assert deg.max() > 20 * np.median(deg)           # heavy tail
+    og = O.Graph(g.indptr, g.indices)
+    want = O.build_capped_similarity(O.all_k_neighborhoods(og, 2, cap=256), 50.0)
+    nd = B.all_k_neighborhoods(g, 2, cap=256)
+    got = B.build_sparse_similarity(nd, B.SimilarityParams(k=2, perplexity=50.0, neighbor_cap=256))
+    assert np.array_equal(got.indptr, want.indptr) and np.array_equal(got.targets, want.targets)
+    np.testing.assert_allclose(got.weights, want.weights, rtol=1e-5)
+    lay = B.layout_graph(g, B.SimilarityParams(k=2, perplexity=50.0, neighbor_cap=256),
+                         B.OptimizerParams(seed=0, iters=30))
+    assert np.isfinite(lay.positions).all()
+
+
+def test_rmat_generator_small():
+    from paper_2008_07799_b200 import synthetic
+    g = synthetic.rmat(12, 16, seed=0, device="host")
+    assert g.node_count == 4096
+    og = O.Graph(g.indptr, g.indices)
+    assert np.all(np.diff(g.indptr) >= 0)
+    # canonical: rows sorted, symmetric, no loops
+    for i in range(0, 4096, 97):
+        row = g.indices[g.indptr[i]:g.indptr[i + 1]]
+        assert np.all(np.diff(row) > 0) and i not in row
+    lay = B.layout_graph(g, B.SimilarityParams(k=1), B.OptimizerParams(seed=0, iters=20),
+                         force_levels=5, max_levels=5)
+    assert np.isfinite(lay.positions).all() and len(lay.stats["levels"]) <= 5
+    del og
