@@ -75,6 +75,7 @@ class OptimizerParams:
     init: str = "normal"
     update: str = "jacobi"
     shard_min_nodes: int = 65536
+    sampled_concurrency: int = 4   # update="sampled": n_l / this many steps in flight
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
@@ -384,7 +385,7 @@ class LayoutPlan:
                   _lib.ptr(S.cum0), _lib.ptr(S.src_alias), _lib.ptr(S.neg_alias), n0,
                   _lib.ptr(fm), _lib.ptr(y), L.n, L.n, t0, n_iter, o.iters, float(o.lr0),
                   float(gamma), float(o.eps), float(o.grad_clip), o.b, o.neg_samples, seed,
-                  level, max(256, L.n // 4), _lib.stream_ptr())
+                  level, max(256, L.n // max(1, o.sampled_concurrency)), _lib.stream_ptr())
         if not bool(torch.isfinite(y).all()):
             raise FloatingPointError(f"non-finite coordinate in epochs {t0}..{t0 + n_iter - 1} "
                                      f"at level {level}")

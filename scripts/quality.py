@@ -76,9 +76,11 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled")):
         runs = {"reference": (pos, t_ref)}
         for m in modes:
             t0 = time.perf_counter()
+            upd, _, div = m.partition(":")
+            extra = {"sampled_concurrency": int(div)} if div else {}
             lay = B.layout_graph(bg, B.SimilarityParams(k=cfg["k"], perplexity=cfg["perplexity"]),
-                                 B.OptimizerParams(iters=cfg["iters"], seed=seed, update=m,
-                                                   init=cfg["init"]),
+                                 B.OptimizerParams(iters=cfg["iters"], seed=seed, update=upd,
+                                                   init=cfg["init"], **extra),
                                  max_levels=cfg["max_levels"], init_positions=y0)
             runs[m] = (lay.positions, time.perf_counter() - t0)
         for key, (y, t) in runs.items():
@@ -101,4 +103,5 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled")):
 
 if __name__ == "__main__":
     a = sys.argv[1:]
-    main(a[0] if a else "grid", int(a[1]) if len(a) > 1 else 10)
+    main(a[0] if a else "grid", int(a[1]) if len(a) > 1 else 10,
+         tuple(a[2].split(",")) if len(a) > 2 else ("jacobi", "inplace", "sampled"))
