@@ -288,10 +288,9 @@ def run_ours(args):
     lvl_events = {}
 
     def on_level(level, what):
-        if level == 0:
-            e = torch.cuda.Event(enable_timing=True)
-            e.record()
-            lvl_events[what] = e
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        lvl_events[(level, what)] = e
 
     def step():
         return plan.run(group=group, on_level=on_level)
@@ -317,7 +316,9 @@ def run_ours(args):
             if group is not None:
                 dist.barrier(group)
             step_ms.append(s.elapsed_time(e))
-            l0_ms.append(lvl_events["start"].elapsed_time(lvl_events["end"]))
+            l0_ms.append(lvl_events[(0, "start")].elapsed_time(lvl_events[(0, "end")]))
+    level_ms = [round(lvl_events[(lv, "start")].elapsed_time(lvl_events[(lv, "end")]), 3)
+                for lv in range(len(sizes))]
     launches = _lib.launch_count() - launches0
     total_ms = sum(step_ms)
     if group is not None:
@@ -402,6 +403,7 @@ def run_ours(args):
                        "parallelism": f"node-range x{world}" if world > 1 else "single GPU"},
             "interactions_per_s": inter,
             "iters_per_step": iters,
+            "level_ms_last_step": level_ms,
             "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps,
             "roofline": roofline,

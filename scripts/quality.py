@@ -28,6 +28,8 @@ CONFIGS = {
                  np_sample=None),
     "rgg": dict(k=3, perplexity=30.0, iters=500, max_levels=3, init="normal", z_pairs=20_000_000,
                 np_sample=20_000),
+    "rgg1": dict(k=3, perplexity=30.0, iters=500, max_levels=1, init="normal",
+                 z_pairs=20_000_000, np_sample=20_000),
     "mesh_small": dict(k=2, perplexity=50.0, iters=800, max_levels=4, init="normal",
                        z_pairs=20_000_000, np_sample=20_000),
 }
@@ -38,7 +40,7 @@ def graph_for(name):
     from paper_2008_07799_b200 import synthetic
     if name == "grid":
         g = synthetic.grid(100, 100, device="host")
-    elif name == "rgg":
+    elif name in ("rgg", "rgg1"):
         g = synthetic.rgg(200_000, seed=0, device="host")
     else:
         g = synthetic.mesh3d(40, device="host")
