@@ -187,6 +187,16 @@ int drg_layout_radius(const float *y, int64_t n, double *out_radius, void *strea
 int drg_prolong(const float *y_coarse, const int32_t *parent, int64_t n_fine, double jitter,
                 uint64_t seed, float *y_fine, void *stream);
 
+/* --- parity instruments -----------------------------
+ * KL(P || Q) terms of a layout y (device fp32 [n][2]) with the unnormalised
+ * t-kernel lp_kernel (optimizer.py:150-152): out4 (host) = {sum P log P,
+ * sum P log(1 + d^(2b)), sum P, Z = sum_{i != j} 1/(1 + d_ij^(2b))}; Z is exact
+ * (tiled all-pairs) when z_pairs <= 0, else a Monte-Carlo estimate over z_pairs
+ * uniform ordered pairs.  KL = (out4[0] + out4[1]) / out4[2] + log(out4[3]). */
+int drg_kl_terms(const int64_t *indptr, const int32_t *targets, const double *P, int64_t n,
+                 const float *y, int b, int64_t z_pairs, uint64_t seed, double *out4,
+                 void *stream);
+
 /* --- graph construction and diagnostics ---------------------------------------------
  * from_edges (graph.py:80-125): canonical CSR from m (u, v) pairs (device int64
  * [m][2]), self-loops dropped, duplicates and reversed pairs merged, rows sorted.

@@ -473,3 +473,20 @@ def test_rmat_generator_small():
                          force_levels=5, max_levels=5)
     assert np.isfinite(lay.positions).all() and len(lay.stats["levels"]) <= 5
     del og
+
+
+def test_gpu_kl_matches_oracle_evaluator(golden):
+    """The device KL instrument equals the numpy evaluator (exact Z) and the
+    Monte-Carlo Z estimate is close."""
+    from paper_2008_07799_b200.quality import kl_divergence
+    g = golden_graph(golden, "r500")
+    ns = O.build_sparse_similarity(O.all_k_neighborhoods(g, 2))
+    y = np.random.default_rng(0).normal(size=(500, 2)).astype(np.float32).astype(np.float64)
+    for b in (1, 2, 3):
+        want = O.kl_divergence(ns, y, b)
+        got = kl_divergence(B.SparseSimilarity(ns.indptr, ns.targets, ns.weights, ns.total_mass,
+                                               ns.sigma, ns.k), y, b)
+        assert got == pytest.approx(want, rel=1e-5)
+    mc = kl_divergence(B.SparseSimilarity(ns.indptr, ns.targets, ns.weights, ns.total_mass,
+                                          ns.sigma, ns.k), y, 2, z_pairs=4_000_000)
+    assert mc == pytest.approx(O.kl_divergence(ns, y, 2), rel=2e-3)
