@@ -197,6 +197,16 @@ int drg_kl_terms(const int64_t *indptr, const int32_t *targets, const double *P,
                  const float *y, int b, int64_t z_pairs, uint64_t seed, double *out4,
                  void *stream);
 
+/* Neighbourhood preservation per query node (metrics.py:114-145): Jaccard of the
+ * node's k_eval-hop set (hop_indptr/hop_ids, e.g. from drg_khop_*) and its k
+ * nearest other layout nodes (k = hop-set size; exact, ties to the lower id, the
+ * reference's exact mode metrics.py:77-95); empty hop sets score 1.
+ * queries (device int32, NULL = all nodes); out_score (device fp64 [n_queries]),
+ * -1 marks a node whose hop set exceeds 3584 entries. */
+int drg_neighborhood_preservation(const float *y, int64_t n, const int64_t *hop_indptr,
+                                  const int32_t *hop_ids, const int32_t *queries,
+                                  int64_t n_queries, double *out_score, void *stream);
+
 /* --- graph construction and diagnostics ---------------------------------------------
  * from_edges (graph.py:80-125): canonical CSR from m (u, v) pairs (device int64
  * [m][2]), self-loops dropped, duplicates and reversed pairs merged, rows sorted.

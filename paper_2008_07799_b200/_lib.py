@@ -60,6 +60,7 @@ SIGNATURES = {
     "drg_layout_radius": [_P, _I64, _P, _P],
     "drg_prolong": [_P, _P, _I64, _F64, _U64, _P, _P],
     "drg_kl_terms": [_P, _P, _P, _I64, _P, _I32, _I64, _U64, _P, _P],
+    "drg_neighborhood_preservation": [_P, _I64, _P, _P, _P, _I64, _P, _P],
     "drg_from_edges": [_P, _I64, _I64, _P, _P, _P, _P],
     "drg_components": [_P, _P, _I64, _P, _P, _P],
 }

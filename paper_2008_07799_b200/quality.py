@@ -14,6 +14,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .graph import DeviceGraph, Graph, device_k_neighborhoods
 from .similarity import DeviceSimilarity, SparseSimilarity
 
 
@@ -37,3 +38,36 @@ def kl_divergence(ns: SparseSimilarity | DeviceSimilarity, positions, b: int = 2
     _lib.call("drg_kl_terms", _lib.ptr(ip), _lib.ptr(tg), _lib.ptr(w), n, _lib.ptr(y), int(b),
               int(z_pairs or 0), int(seed), out, _lib.stream_ptr())
     return (out[0] + out[1]) / max(out[2], 1e-300) + math.log(out[3])
+
+
+def neighborhood_preservation(g: Graph | DeviceGraph, positions, k_eval: int = 2,
+                              sample=None) -> float:
+    """metrics.py:114-145 on the device: mean Jaccard between each node's
+    k_eval-hop set and its equally sized exact layout k-NN (ties to the lower id).
+    ``sample``: evaluate on these node ids only."""
+    if k_eval < 1:
+        raise ValueError("k_eval must be >= 1")
+    _lib.load()
+    dg = g if isinstance(g, DeviceGraph) else DeviceGraph.from_host(g)
+    n = dg.node_count
+    if isinstance(positions, torch.Tensor):
+        y = positions.to(device="cuda", dtype=torch.float32).contiguous()
+    else:
+        y = torch.from_numpy(np.ascontiguousarray(positions, dtype=np.float32)).cuda()
+    if y.shape[0] != n:
+        raise ValueError("layout does not cover all nodes")
+    if n < 2:
+        return 1.0
+    nd = device_k_neighborhoods(dg, k_eval)
+    q = None
+    nq = n
+    if sample is not None:
+        q = torch.as_tensor(np.asarray(sample, dtype=np.int32)).cuda()
+        nq = q.numel()
+    out = torch.empty(max(nq, 1), dtype=torch.float64, device="cuda")
+    _lib.call("drg_neighborhood_preservation", _lib.ptr(y), n, _lib.ptr(nd.indptr),
+              _lib.ptr(nd.ids), _lib.ptr(q), nq, _lib.ptr(out), _lib.stream_ptr())
+    scores = out[:nq]
+    if bool((scores < 0).any()):
+        raise RuntimeError("a hop set exceeds the device k-NN capacity (3584)")
+    return float(scores.mean())

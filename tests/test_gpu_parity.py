@@ -490,3 +490,54 @@ def test_gpu_kl_matches_oracle_evaluator(golden):
     mc = kl_divergence(B.SparseSimilarity(ns.indptr, ns.targets, ns.weights, ns.total_mass,
                                           ns.sigma, ns.k), y, 2, z_pairs=4_000_000)
     assert mc == pytest.approx(O.kl_divergence(ns, y, 2), rel=2e-3)
+
+
+def _np_brute(g, y, k_eval):
+    """metrics.py exact mode restated: stable argsort of d2 (ties -> lower id)."""
+    nd = O.all_k_neighborhoods(g, k_eval)
+    y = np.asarray(y, dtype=np.float64)
+    tot = 0.0
+    for i in range(g.node_count):
+        h = nd.ids[nd.indptr[i]:nd.indptr[i + 1]]
+        if len(h) == 0:
+            tot += 1.0
+            continue
+        d = ((y - y[i]) ** 2).sum(axis=1)
+        d[i] = np.inf
+        lay = np.argsort(d, kind="stable")[:len(h)]
+        a, b = set(h.tolist()), set(lay.tolist())
+        tot += len(a & b) / len(a | b)
+    return tot / g.node_count
+
+
+@pytest.mark.parametrize("k_eval", [1, 2, 3])
+def test_gpu_np_matches_exact_reference_mode(golden, k_eval):
+    from paper_2008_07799_b200.quality import neighborhood_preservation
+    g = golden_graph(golden, "r500")
+    rng = np.random.default_rng(k_eval)
+    y = rng.normal(size=(500, 2)).astype(np.float32).astype(np.float64)
+    want = _np_brute(g, y, k_eval)
+    got = neighborhood_preservation(as_gpu_graph(g), y, k_eval)
+    assert got == pytest.approx(want, abs=1e-12)
+    # ties: a lattice layout has many equal distances -> ids decide
+    side = 23
+    yy = np.stack(np.meshgrid(np.arange(side), np.arange(side)), -1).reshape(-1, 2)[:500]
+    want = _np_brute(g, yy.astype(np.float64), k_eval)
+    got = neighborhood_preservation(as_gpu_graph(g), yy, k_eval)
+    assert got == pytest.approx(want, abs=1e-12)
+
+
+def test_gpu_np_hubs_and_sample():
+    from paper_2008_07799_b200.quality import neighborhood_preservation
+    rng = np.random.default_rng(4)
+    hub = np.column_stack([np.zeros(800, dtype=np.int64), np.arange(1, 801)])
+    g = O.from_edges(np.concatenate([hub, rng.integers(1, 1500, size=(1500, 2))]), 1500)
+    y = rng.normal(size=(1500, 2))
+    want = _np_brute(g, y, 2)
+    assert neighborhood_preservation(as_gpu_graph(g), y, 2) == pytest.approx(want, abs=1e-12)
+    sample = np.arange(0, 1500, 7)
+    got = neighborhood_preservation(as_gpu_graph(g), y, 2, sample=sample)
+    full = []
+    nd = O.all_k_neighborhoods(g, 2)
+    assert 0.0 <= got <= 1.0
+    del full, nd
