@@ -26,12 +26,12 @@ from oracle import oracle as O  # noqa: E402
 CONFIGS = {
     "grid": dict(k=2, perplexity=30.0, iters=300, max_levels=1, init="uniform", z_pairs=None,
                  np_sample=None),
-    "rgg": dict(k=3, perplexity=30.0, iters=500, max_levels=3, init="normal", z_pairs=20_000_000,
-                np_sample=20_000),
-    "rgg1": dict(k=3, perplexity=30.0, iters=500, max_levels=1, init="normal",
-                 z_pairs=20_000_000, np_sample=20_000),
+    "rgg": dict(k=3, perplexity=30.0, iters=500, max_levels=3, init="normal", z_pairs=None,
+                np_sample=None),
+    "rgg1": dict(k=3, perplexity=30.0, iters=500, max_levels=1, init="normal", z_pairs=None,
+                 np_sample=None),
     "mesh_small": dict(k=2, perplexity=50.0, iters=800, max_levels=4, init="normal",
-                       z_pairs=20_000_000, np_sample=20_000),
+                       z_pairs=None, np_sample=None),
 }
 
 
@@ -54,12 +54,14 @@ def init_for(cfg, n, seed):
     return rng.normal(0.0, 1e-4, size=(n, 2)).astype(np.float32).astype(np.float64)
 
 
-def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled")):
+def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evaluator="gpu"):
     import paper_2008_07799_b200 as B
+    from paper_2008_07799_b200 import quality as Q
     cfg = CONFIGS[name]
     og, bg = graph_for(name)
     nd = O.all_k_neighborhoods(og, cfg["k"])
     ns = O.build_sparse_similarity(nd, cfg["perplexity"])
+    bns = B.SparseSimilarity(ns.indptr, ns.targets, ns.weights, ns.total_mass, ns.sigma, ns.k)
     del nd
     sample = None
     if cfg["np_sample"]:
@@ -86,8 +88,12 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled")):
                                  max_levels=cfg["max_levels"], init_positions=y0)
             runs[m] = (lay.positions, time.perf_counter() - t0)
         for key, (y, t) in runs.items():
-            kl = O.kl_divergence(ns, y, 2, z_pairs=cfg["z_pairs"], seed=11)
-            npv = O.neighborhood_preservation(og, y, 2, sample=sample)
+            if evaluator == "gpu":   # device instruments (exact Z, exact-mode k-NN)
+                kl = Q.kl_divergence(bns, y, 2, z_pairs=cfg["z_pairs"], seed=11)
+                npv = Q.neighborhood_preservation(bg, y, 2, sample=sample)
+            else:
+                kl = O.kl_divergence(ns, y, 2, z_pairs=cfg["z_pairs"], seed=11)
+                npv = O.neighborhood_preservation(og, y, 2, sample=sample)
             results[key].append({"seed": seed, "kl": kl, "np": npv, "s": t})
     for key, rs in results.items():
         kls = [r["kl"] for r in rs]
@@ -106,4 +112,5 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled")):
 if __name__ == "__main__":
     a = sys.argv[1:]
     main(a[0] if a else "grid", int(a[1]) if len(a) > 1 else 10,
-         tuple(a[2].split(",")) if len(a) > 2 else ("jacobi", "inplace", "sampled"))
+         tuple(a[2].split(",")) if len(a) > 2 else ("jacobi", "inplace", "sampled"),
+         a[3] if len(a) > 3 else "gpu")
