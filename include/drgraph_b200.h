@@ -141,6 +141,19 @@ int drg_level_pack(const int64_t *indptr, const int32_t *targets, const double *
 
 #define DRG_FLAG_INPLACE 1u   /* Hogwild-style in-place update (y_out == y_in) */
 
+/* Heavy-row split for drg_layout_iters (heavy-tailed rows, e.g. R-MAT hubs): rows
+ * listed here are streamed by several warps in chunks of DRG_HEAVY_CHUNK entries
+ * whose partial sums the row's warp then adds (deterministic order). */
+#define DRG_HEAVY_CHUNK 2048
+typedef struct drg_heavy_split {
+    const int32_t *slot;        /* [n] heavy index of each row, -1 for normal rows */
+    const int32_t *chunk_ptr;   /* [n_heavy + 1] first chunk of each heavy row */
+    const int32_t *chunk_row;   /* [n_chunks] row of each chunk */
+    const int64_t *chunk_begin; /* [n_chunks] first entry of each chunk */
+    int64_t n_chunks;
+    float *partial;             /* [2 * n_chunks] scratch for the chunk sums */
+} drg_heavy_split;
+
 /* n_iter node-parallel iterations t = t0 .. t0+n_iter-1 of level `level`
  * (replaces the sgd_epoch loop of layout_graph, optimizer.py:310-353, 405-407,
  * and the step kernel _kernels.py:48-141):
@@ -152,13 +165,13 @@ int drg_level_pack(const int64_t *indptr, const int32_t *targets, const double *
  * DRG_FLAG_INPLACE, y_in must equal y_out.  neg_idx (optional, n*M int32, -1 =
  * skip) replaces the sampled negatives (parity mode, n_iter must be 1).
  * nonfinite (optional device int, init INT_MAX) receives the first t whose
- * update produced a non-finite coordinate. */
+ * update produced a non-finite coordinate.  heavy (optional) splits long rows. */
 int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, const float *V,
                      const uint64_t *alias, int64_t n, int64_t row_lo, int64_t row_hi,
                      float *y_in, float *y_out, int t0, int n_iter, int iters, double lr0,
                      double gamma, double eps, double clip, int b, int M, uint64_t seed,
-                     int level, const int32_t *neg_idx, int32_t *nonfinite, unsigned flags,
-                     void *stream);
+                     int level, const int32_t *neg_idx, int32_t *nonfinite,
+                     const drg_heavy_split *heavy, unsigned flags, void *stream);
 
 /* --- reference-faithful sampled epochs (update = "sampled") ----------------------
  * cum[e] = (sum of P over the row up to e) / (row sum), last entry of a non-empty

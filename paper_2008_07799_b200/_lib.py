@@ -53,7 +53,7 @@ SIGNATURES = {
     "drg_alias_build": [_P, _I64, _P, _P, _P],
     "drg_level_pack": [_P, _P, _P, _P, _P, _F64, _I64, _I64, _I32, _P, _P, _P],
     "drg_layout_iters": [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _I32, _I32, _I32, _F64, _F64,
-                         _F64, _F64, _I32, _I32, _U64, _I32, _P, _P, _U32, _P],
+                         _F64, _F64, _I32, _I32, _U64, _I32, _P, _P, _P, _U32, _P],
     "drg_row_cumulative": [_P, _P, _I64, _P, _P],
     "drg_layout_sampled": [_P, _P, _P, _P, _P, _I64, _P, _P, _I64, _I64, _I32, _I32, _I32, _F64,
                            _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _P],
@@ -65,6 +65,16 @@ SIGNATURES = {
     "drg_components": [_P, _P, _I64, _P, _P, _P],
 }
 RESTYPES = {"drg_last_error": ctypes.c_char_p, "drg_launch_count": ctypes.c_uint64}
+
+DRG_HEAVY_CHUNK = 2048
+
+
+class HeavySplit(ctypes.Structure):
+    """drg_heavy_split (include/drgraph_b200.h)."""
+    _fields_ = [("slot", ctypes.c_void_p), ("chunk_ptr", ctypes.c_void_p),
+                ("chunk_row", ctypes.c_void_p), ("chunk_begin", ctypes.c_void_p),
+                ("n_chunks", ctypes.c_int64), ("partial", ctypes.c_void_p)]
+
 
 _lib = None
 

@@ -57,6 +57,13 @@ struct IterArgs {
     int t;
     const int32_t *neg_idx;
     int32_t *nonfinite;
+    // heavy-row split (may be null)
+    const int32_t *hslot;
+    const int32_t *hptr;
+    const int32_t *hrow;
+    const int64_t *hbegin;
+    float2 *hpart;
+    int64_t hchunks;
 };
 
 __device__ __forceinline__ u32x4 neg_bits(const IterArgs &A, int64_t a, int m, int attempt) {
@@ -149,7 +156,8 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
     for (int i = 0; i < nodes; ++i) {
         const int64_t a = a0 + i;
         const int64_t lo = __ldg(A.indptr + a), hi = __ldg(A.indptr + a + 1);
-        const int cnt = (int)(hi - lo);
+        const int hs = A.hslot ? __ldg(A.hslot + a) : -1;
+        const int cnt = hs >= 0 ? 0 : (int)(hi - lo);   // heavy rows: chunk partials
         const uint2 *row = A.rec + lo;
         const float2 ya = load_y<INPLACE>(y_in, a);
         float ax = 0.f, ay = 0.f, wsum = 0.f;
@@ -188,6 +196,12 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
             ax *= -two_b;
             ay *= -two_b;
         }
+        if (hs >= 0)   // chunk sums of the heavy-row kernel (already scaled)
+            for (int c = __ldg(A.hptr + hs) + lane; c < __ldg(A.hptr + hs + 1); c += 32) {
+                const float2 p = A.hpart[c];
+                ax += p.x;
+                ay += p.y;
+            }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             ax += __shfl_xor_sync(kFull, ax, o);
@@ -324,9 +338,71 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
     }
 }
 
+// One warp per chunk of a heavy row: the same attraction math as the row loop,
+// the chunk's sum to A.hpart[c].
+template <bool INPLACE, int B, bool CLAMP_ATT>
+__global__ void __launch_bounds__(kWpb * 32)
+    heavy_chunk_kernel(IterArgs A, const float2 *y_in) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * kWpb + (threadIdx.x >> 5);
+    if (c >= A.hchunks) return;
+    const int b = B > 0 ? B : A.b;
+    const float two_b = 2.0f * (float)b;
+    const int64_t a = A.hrow[c];
+    const int64_t lo = A.hbegin[c];
+    const int cnt = (int)min((int64_t)DRG_HEAVY_CHUNK, __ldg(A.indptr + a + 1) - lo);
+    const uint2 *row = A.rec + lo;
+    const float2 ya = load_y<INPLACE>(y_in, a);
+    float ax = 0.f, ay = 0.f;
+    for (int base = 0; base < cnt; base += 32 * kDepth) {
+        uint2 r[kDepth];
+#pragma unroll
+        for (int j = 0; j < kDepth; ++j) {
+            const int e = base + j * 32 + lane;
+            r[j] = e < cnt ? __ldcs(row + e) : make_uint2((uint32_t)a, 0u);
+        }
+        float2 yb[kDepth];
+#pragma unroll
+        for (int j = 0; j < kDepth; ++j) yb[j] = load_y<INPLACE>(y_in, r[j].x);
+#pragma unroll
+        for (int j = 0; j < kDepth; ++j) {
+            const float dx = ya.x - yb[j].x, dy = ya.y - yb[j].y;
+            const float ld2 = fmaf(dx, dx, dy * dy);
+            const float pw = powbm1<B>(ld2, b);
+            const float w = __uint_as_float(r[j].y);
+            const float inv = rcp_approx(fmaf(pw, ld2, 1.0f));
+            if (CLAMP_ATT) {
+                const float coef = -two_b * pw * inv;
+                ax = fmaf(w, clampf(coef * dx, A.clip), ax);
+                ay = fmaf(w, clampf(coef * dy, A.clip), ay);
+            } else {
+                const float wc = (B == 1 ? w : w * pw) * inv;
+                ax = fmaf(wc, dx, ax);
+                ay = fmaf(wc, dy, ay);
+            }
+        }
+    }
+    if (!CLAMP_ATT) {
+        ax *= -two_b;
+        ay *= -two_b;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        ax += __shfl_xor_sync(kFull, ax, o);
+        ay += __shfl_xor_sync(kFull, ay, o);
+    }
+    if (lane == 0) A.hpart[c] = make_float2(ax, ay);
+}
+
 template <bool INPLACE, int B>
 void launch_iter_b(unsigned grid, cudaStream_t st, const IterArgs &A, int npw, bool clamp,
                    bool partner, const float2 *src, float2 *dst) {
+    if (A.hchunks > 0) {
+        const unsigned hg = (unsigned)ceil_div(A.hchunks, kWpb);
+        if (clamp) heavy_chunk_kernel<INPLACE, B, true><<<hg, kWpb * 32, 0, st>>>(A, src);
+        else heavy_chunk_kernel<INPLACE, B, false><<<hg, kWpb * 32, 0, st>>>(A, src);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
     if (clamp) {
         if (partner) layout_iter_kernel<INPLACE, B, true, true><<<grid, kWpb * 32, 0, st>>>(A, npw, src, dst);
         else layout_iter_kernel<INPLACE, B, true, false><<<grid, kWpb * 32, 0, st>>>(A, npw, src, dst);
@@ -521,7 +597,8 @@ extern "C" int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, cons
                                 float *y_in, float *y_out, int t0, int n_iter, int iters,
                                 double lr0, double gamma, double eps, double clip, int b, int M,
                                 uint64_t seed, int level, const int32_t *neg_idx,
-                                int32_t *nonfinite, unsigned flags, void *stream) {
+                                int32_t *nonfinite, const drg_heavy_split *heavy,
+                                unsigned flags, void *stream) {
     if (n <= 0 || n_iter < 0) return DRG_OK;
     if (row_lo < 0 || row_hi > n || row_lo > row_hi)
         return fail(DRG_ERR_INVALID, "row range [%lld, %lld) outside [0, %lld)",
@@ -551,6 +628,20 @@ extern "C" int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, cons
     A.level = (uint32_t)level;
     A.neg_idx = neg_idx;
     A.nonfinite = nonfinite;
+    A.hslot = nullptr;
+    A.hptr = nullptr;
+    A.hrow = nullptr;
+    A.hbegin = nullptr;
+    A.hpart = nullptr;
+    A.hchunks = 0;
+    if (heavy && heavy->n_chunks > 0) {
+        A.hslot = heavy->slot;
+        A.hptr = heavy->chunk_ptr;
+        A.hrow = heavy->chunk_row;
+        A.hbegin = heavy->chunk_begin;
+        A.hpart = reinterpret_cast<float2 *>(heavy->partial);
+        A.hchunks = heavy->n_chunks;
+    }
     const int64_t rows = row_hi - row_lo;
     if (rows == 0) return DRG_OK;
     const int npw = (M == 0) ? 8 : (M <= 32 ? std::min(8, 32 / M) : 1);

@@ -174,12 +174,40 @@ class LevelData:
     rec: torch.Tensor      # int64 [nnz]  (int32 target | fp32 W << 32)
     V: torch.Tensor        # fp32 [n]
     alias: torch.Tensor    # int64 [n]    (fp32 prob | int32 alias << 32)
+    heavy: dict | None = None   # heavy-row split tensors (rows > HEAVY_ROW entries)
 
     def algorithmic_bytes(self, M: int) -> int:
         """16 B per P entry + (24 + 16 M) B per node (level 0) --
         col 4 + W 4 + y_j 8 per entry; rowptr 4 + y_a 8 + y_a' 8 + V 4 and per
         negative an 8 B alias record + 8 B y_c per node."""
         return 16 * self.nnz + (24 + 16 * M) * self.n
+
+
+HEAVY_ROW = 4 * _lib.DRG_HEAVY_CHUNK   # rows longer than this are split across warps
+
+
+def heavy_split(indptr: torch.Tensor, threshold: int = HEAVY_ROW) -> dict | None:
+    """Chunk list of the rows with more than ``threshold`` entries (drg_heavy_split):
+    a heavy-tailed row (an R-MAT hub) is streamed by many warps instead of one."""
+    deg = indptr[1:] - indptr[:-1]
+    heavy = torch.nonzero(deg > threshold).flatten()
+    if heavy.numel() == 0:
+        return None
+    C = _lib.DRG_HEAVY_CHUNK
+    nch = (deg[heavy] + C - 1) // C
+    ptr = torch.zeros(heavy.numel() + 1, dtype=torch.int64, device=indptr.device)
+    ptr[1:] = torch.cumsum(nch, 0)
+    rows = torch.repeat_interleave(heavy, nch)
+    within = torch.arange(rows.numel(), device=indptr.device) - torch.repeat_interleave(ptr[:-1], nch)
+    slot = torch.full((deg.numel(),), -1, dtype=torch.int32, device=indptr.device)
+    slot[heavy] = torch.arange(heavy.numel(), dtype=torch.int32, device=indptr.device)
+    t = {"slot": slot, "chunk_ptr": ptr.to(torch.int32), "chunk_row": rows.to(torch.int32),
+         "chunk_begin": (indptr[rows] + within * C).contiguous(),
+         "partial": torch.empty(2 * rows.numel(), dtype=torch.float32, device=indptr.device)}
+    t["struct"] = _lib.HeavySplit(t["slot"].data_ptr(), t["chunk_ptr"].data_ptr(),
+                                  t["chunk_row"].data_ptr(), t["chunk_begin"].data_ptr(),
+                                  rows.numel(), t["partial"].data_ptr())
+    return t
 
 
 def _aggregate_pairs(indptr, targets, weights, parent, n_coarse):
@@ -236,7 +264,7 @@ def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float
         # sectors by 12% on the mesh but cost 130 ms of segmented sort and no
         # kernel time (profiles/README.md), so it is off
         rec, V = pack_level(ip, tg, P, R, Wn, 1.0 / total, n_l, sort_rows=False)
-        out.append(LevelData(n_l, tg.numel(), ip, rec, V, alias))
+        out.append(LevelData(n_l, tg.numel(), ip, rec, V, alias, heavy_split(ip)))
     return out
 
 
@@ -331,7 +359,9 @@ class LayoutPlan:
                   _lib.ptr(L.alias), L.n, row_lo, row_hi, _lib.ptr(y_in), _lib.ptr(y_out),
                   t0, n_iter, o.iters, float(o.lr0), float(gamma), float(o.eps),
                   float(o.grad_clip), o.b, o.neg_samples, seed, level, _lib.ptr(neg_idx),
-                  _lib.ptr(self.nonfinite), flags, _lib.stream_ptr(stream))
+                  _lib.ptr(self.nonfinite),
+                  _lib.byref(L.heavy["struct"]) if L.heavy else None, flags,
+                  _lib.stream_ptr(stream))
 
     def check_finite(self, level: int) -> None:
         if self.nonfinite is None:

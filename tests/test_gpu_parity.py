@@ -541,3 +541,32 @@ def test_gpu_np_hubs_and_sample():
     nd = O.all_k_neighborhoods(g, 2)
     assert 0.0 <= got <= 1.0
     del full, nd
+
+
+def test_single_step_parity_heavy_rows():
+    """Rows longer than HEAVY_ROW are streamed in chunks by several warps; the step
+    still equals the oracle iteration (hub of degree 30 000)."""
+    from paper_2008_07799_b200.optimizer import HEAVY_ROW
+    rng = np.random.default_rng(11)
+    n = 30_001
+    hub = np.column_stack([np.zeros(n - 1, dtype=np.int64), np.arange(1, n)])
+    g = O.from_edges(np.concatenate([hub, rng.integers(1, n, size=(20_000, 2))]), n)
+    assert np.diff(g.indptr).max() > HEAVY_ROW
+    prep = _prepared(as_gpu_graph(g), k=1, M=5, levels=1, min_size=n)
+    plan = prep.plan
+    L = plan.levels[0]
+    assert L.heavy is not None
+    y = rng.normal(0, 1.0, size=(L.n, 2)).astype(np.float32)
+    neg = rng.integers(-1, L.n, size=(L.n, 5)).astype(np.int32)
+    neg[neg == np.arange(L.n)[:, None]] = -1
+    out = torch.empty((L.n, 2), dtype=torch.float32, device="cuda")
+    plan.kernel_step(0, torch.from_numpy(y).cuda(), out, 0, L.n, 2, 1,
+                     neg_idx=torch.from_numpy(neg).cuda())
+    got = out.cpu().numpy().astype(np.float64)
+    rec = L.rec.cpu().numpy().view(np.uint32).reshape(-1, 2)
+    lr = 1.0 * (1 - 2 / 10)
+    want = O.node_parallel_iteration(L.indptr.cpu().numpy(), rec[:, 0].astype(np.int64),
+                                     rec[:, 1].view(np.float32), L.V.cpu().numpy(), y, neg, lr,
+                                     plan.opt.gamma_coarsest, 1e-3, 5.0, 2)
+    g_got, g_want = (got - y) / lr, (want - y) / lr
+    assert np.all(np.abs(g_got - g_want) <= 1e-5 * np.maximum(1.0, np.abs(g_want)))
