@@ -72,6 +72,7 @@ def parse():
     ap.add_argument("--iters", type=int, default=None, help="override iterations per level")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the other update modes")
     ap.add_argument("--update", default="jacobi", choices=["jacobi", "inplace", "sampled"])
     return ap.parse_args()
 
@@ -331,6 +332,36 @@ def run_ours(args):
     value = iters * args.steps / (total_ms / 1e3)
     inter = plan.interactions() * args.steps / (total_ms / 1e3)
 
+    # the other update modes on the same prepared level data (same graph, P,
+    # hierarchy): device-resident iters/s, for comparison in the same JSON line
+    alt = {}
+    if not args.no_alt and group is None:
+        from paper_2008_07799_b200.optimizer import LayoutPlan, build_sampled_data
+        for mode in ("jacobi", "inplace", "sampled"):
+            if mode == opt.update:
+                continue
+            o2 = B.OptimizerParams(**{**opt.__dict__, "update": mode})
+            p2 = LayoutPlan(plan.levels, plan.maps, o2)
+            if mode == "sampled":
+                p2.sampled = build_sampled_data(prep.similarity, prep.hierarchy,
+                                                plan.levels[0].alias)
+            p2.run()
+            torch.cuda.synchronize()
+            ms = []
+            for _ in range(max(1, min(args.steps, 2))):
+                flush.zero_()
+                torch.cuda.synchronize()
+                s0, e0 = (torch.cuda.Event(enable_timing=True),
+                          torch.cuda.Event(enable_timing=True))
+                s0.record()
+                p2.run()
+                e0.record()
+                torch.cuda.synchronize()
+                ms.append(s0.elapsed_time(e0))
+            alt[mode] = {"value": iters / (sum(ms) / len(ms) / 1e3), "unit": UNIT,
+                         "ms_per_step": sum(ms) / len(ms)}
+            del p2
+
     # roofline of the dominant kernel: K7 at level 0
     peak, peak_kind = measured_peaks()
     T = opt.iters
@@ -407,6 +438,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps,
             "roofline": roofline,
+            "other_update_modes": alt,
             "clocks": clocks,
             "e2e": e2e,
             "cpu_baseline": cpu,
