@@ -274,12 +274,12 @@ StepFn = Callable[[torch.Tensor, torch.Tensor, int, int, int], None]
 @dataclass
 class SampledData:
     """Level-0 sampling tables of the reference-faithful mode (update="sampled"):
-    P^0 CSR with per-row cumulative weights, a Vose table over the row masses
-    (sources), the level-0 negative table, and the flat level maps."""
+    P^0 CSR with a Vose table per row, a Vose table over the row masses (sources),
+    the level-0 negative table, and the flat level maps."""
 
     indptr0: torch.Tensor
     targets0: torch.Tensor
-    cum0: torch.Tensor
+    row_alias: torch.Tensor
     src_alias: torch.Tensor
     neg_alias: torch.Tensor
     flat_maps: list   # flat_maps[l]: level-0 id -> level-l id (None at level 0)
@@ -288,9 +288,9 @@ class SampledData:
 def build_sampled_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_alias: torch.Tensor
                        ) -> SampledData:
     n0 = ds.node_count
-    cum = torch.empty(max(ds.entry_count, 1), dtype=torch.float32, device=ds.weights.device)
-    _lib.call("drg_row_cumulative", _lib.ptr(ds.indptr), _lib.ptr(ds.weights), n0,
-              _lib.ptr(cum), _lib.stream_ptr())
+    rows = torch.empty(max(ds.entry_count, 1), dtype=torch.int64, device=ds.weights.device)
+    _lib.call("drg_row_alias", _lib.ptr(ds.indptr), _lib.ptr(ds.targets), _lib.ptr(ds.weights),
+              n0, ds.entry_count, _lib.ptr(rows), _lib.stream_ptr())
     src_alias, _ = _alias_device(ds.row_mass)
     flat = [None]
     cur = None
@@ -303,7 +303,7 @@ def build_sampled_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_alias: tor
                       _lib.ptr(nxt), _lib.stream_ptr())
         flat.append(nxt)
         cur = nxt
-    return SampledData(ds.indptr, ds.targets, cum, src_alias, neg_alias, flat)
+    return SampledData(ds.indptr, ds.targets, rows, src_alias, neg_alias, flat)
 
 
 @dataclass
@@ -412,7 +412,7 @@ class LayoutPlan:
         fm = S.flat_maps[level]
         n0 = S.indptr0.numel() - 1
         _lib.call("drg_layout_sampled", _lib.ptr(S.indptr0), _lib.ptr(S.targets0),
-                  _lib.ptr(S.cum0), _lib.ptr(S.src_alias), _lib.ptr(S.neg_alias), n0,
+                  _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), _lib.ptr(S.neg_alias), n0,
                   _lib.ptr(fm), _lib.ptr(y), L.n, L.n, t0, n_iter, o.iters, float(o.lr0),
                   float(gamma), float(o.eps), float(o.grad_clip), o.b, o.neg_samples, seed,
                   level, max(256, L.n // max(1, o.sampled_concurrency)), _lib.stream_ptr())

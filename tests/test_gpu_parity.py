@@ -570,3 +570,27 @@ def test_single_step_parity_heavy_rows():
                                      plan.opt.gamma_coarsest, 1e-3, 5.0, 2)
     g_got, g_want = (got - y) / lr, (want - y) / lr
     assert np.all(np.abs(g_got - g_want) <= 1e-5 * np.maximum(1.0, np.abs(g_want)))
+
+
+def test_row_alias_tables_reproduce_row_laws(golden):
+    """drg_row_alias: every row's Vose table implies exactly P_ij / sum_j P_ij."""
+    from paper_2008_07799_b200.graph import DeviceGraph
+    from paper_2008_07799_b200.optimizer import build_sampled_data
+    g = golden_graph(golden, "dense80")
+    prep = _prepared(as_gpu_graph(g), k=2, M=5)
+    ds = prep.similarity
+    S = build_sampled_data(ds, prep.hierarchy, prep.plan.levels[0].alias)
+    rec = S.row_alias.cpu().numpy().view(np.uint32).reshape(-1, 2)
+    ip, tg, w = ds.indptr.cpu().numpy(), ds.targets.cpu().numpy(), ds.weights.cpu().numpy()
+    for i in range(len(ip) - 1):
+        lo, hi = ip[i], ip[i + 1]
+        if hi == lo:
+            continue
+        prob = rec[lo:hi, 0].view(np.float32).astype(np.float64)
+        mass = {int(t): p / (hi - lo) for t, p in zip(tg[lo:hi], prob)}
+        for q in range(hi - lo):
+            mass[int(rec[lo + q, 1])] += (1 - prob[q]) / (hi - lo)
+        want = w[lo:hi] / w[lo:hi].sum()
+        got = np.array([mass[int(t)] for t in tg[lo:hi]])
+        np.testing.assert_allclose(got, want, rtol=2e-6, atol=1e-7)
+    del DeviceGraph
