@@ -20,7 +20,7 @@
 namespace drg {
 namespace {
 
-constexpr int kMaxNeg = 8;  // negatives whose first draw is issued early
+constexpr int kMaxNeg = 6;  // negatives whose first draw is issued early
 
 struct SArgs {
     const int64_t *indptr0;
@@ -67,7 +67,7 @@ __device__ __forceinline__ void add_y(float2 *y, int64_t i, float dx, float dy) 
     atomicAdd(y + i, make_float2(dx, dy));
 }
 
-__global__ void __launch_bounds__(256) sampled_kernel(SArgs A, float2 *y) {
+__global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const float two_b = 2.0f * (float)A.b;
     const int Me = min(A.M, kMaxNeg);
@@ -79,14 +79,14 @@ __global__ void __launch_bounds__(256) sampled_kernel(SArgs A, float2 *y) {
                                    A.key0, A.key1);
         const int64_t sb = bucket(A.n0, r.x, r.y);
         const uint2 srec = __ldg(A.src_alias + sb);
-        int64_t nbk[kMaxNeg];
+        int32_t nbk[kMaxNeg];   // level-0 ids < 2^31
         uint2 nrec[kMaxNeg];
         uint32_t ncoin[kMaxNeg];
 #pragma unroll
         for (int m = 0; m < kMaxNeg; ++m) {
             if (m < Me) {
                 const u32x4 q = neg_draw(A, s, c1, m, 0);
-                nbk[m] = bucket(A.n0, q.x, q.y);
+                nbk[m] = (int32_t)bucket(A.n0, q.x, q.y);
                 ncoin[m] = q.z;
                 nrec[m] = __ldg(A.neg_alias + nbk[m]);
             }
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) sampled_kernel(SArgs A, float2 *y) {
             for (int attempt = 0; attempt < 9; ++attempt) {
                 int64_t c0;
                 if (attempt == 0 && m < Me) {
-                    int64_t bk = 0;
+                    int32_t bk = 0;
                     uint2 rc = make_uint2(0, 0);
                     uint32_t cn = 0;
 #pragma unroll

@@ -75,7 +75,7 @@ class OptimizerParams:
     init: str = "normal"
     update: str = "jacobi"
     shard_min_nodes: int = 65536
-    sampled_concurrency: int = 4   # update="sampled": n_l / this many steps in flight
+    sampled_concurrency: int = 16  # update="sampled": n_l / this many steps in flight
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
