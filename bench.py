@@ -336,15 +336,13 @@ def run_ours(args):
     # hierarchy): device-resident iters/s, for comparison in the same JSON line
     alt = {}
     if not args.no_alt and group is None:
-        from paper_2008_07799_b200.optimizer import LayoutPlan, build_sampled_data
+        from paper_2008_07799_b200.optimizer import LayoutPlan, build_plan
         for mode in ("jacobi", "inplace", "sampled"):
             if mode == opt.update:
                 continue
             o2 = B.OptimizerParams(**{**opt.__dict__, "update": mode})
-            p2 = LayoutPlan(plan.levels, plan.maps, o2)
-            if mode == "sampled":
-                p2.sampled = build_sampled_data(prep.similarity, prep.hierarchy,
-                                                plan.levels[0].alias)
+            p2 = (build_plan(prep.similarity, prep.hierarchy, o2) if mode == "sampled"
+                  else LayoutPlan(plan.levels, plan.maps, o2))
             p2.run()
             torch.cuda.synchronize()
             ms = []

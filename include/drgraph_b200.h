@@ -177,24 +177,25 @@ int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, const float *V,
  * Per-row Vose tables over P (optimizer.py:111-139 applied to each row):
  * out_rec[e] = {fp32 threshold of bucket e, int32 target of its alias entry}; a
  * row sample is e = lo + bucket, then target[e] if coin < threshold else the
- * alias target.  Together with a Vose table over the row masses this draws a
- * directed pair with probability P_ij, the law of the reference's canonical-pair
- * table plus direction coin (optimizer.py:206-240). */
+ * alias target.  out_rowsum[n] (optional) = row sums of P.  With a Vose table over
+ * the row masses this draws a directed pair with probability P_ij, the law of the
+ * reference's canonical-pair table plus direction coin (optimizer.py:206-240). */
 int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P, int64_t n,
-                  int64_t nnz, uint64_t *out_rec, void *stream);
+                  int64_t nnz, uint64_t *out_rec, double *out_rowsum, void *stream);
 /* n_iter epochs t = t0.. of n_steps steps each, every step being the reference
- * step (_kernels.py:65-140) on level-l positions y (in place, Hogwild): pair
- * (i0, j0) ~ P at level 0 (src_alias over row masses, then row_alias), mapped by
- * `map` (level-0 -> level-l flat map, NULL at level 0), clipped attraction on both
- * ends if i != j, M negatives ~ Q at level 0 (neg_alias) mapped and redrawn (<= 9)
- * while they hit i or j, both ends moved (float2 atomics).  At most max_threads
- * steps run concurrently. */
-int drg_layout_sampled(const int64_t *indptr0, const int32_t *targets0,
-                       const uint64_t *row_alias, const uint64_t *src_alias,
-                       const uint64_t *neg_alias, int64_t n0, const int32_t *map, float *y,
-                       int64_t n_l, int64_t n_steps, int t0, int n_iter, int iters, double lr0,
-                       double gamma, double eps, double clip, int b, int M, uint64_t seed,
-                       int level, int64_t max_threads, void *stream);
+ * step (_kernels.py:65-140) on the level's positions y (in place, Hogwild):
+ * source a ~ src_alias (R^l), collapsed pair (a, a) with probability collapse[a]
+ * (pairs inside a coarse node, which the reference draws at level 0 and maps),
+ * else b from the row's alias table (targets from rec = the level's {target, W}
+ * records); clipped attraction on both ends if i != j; M negatives ~ neg_alias
+ * (Q^l) redrawn (<= 9) while they hit i or j, both ends moved (float2 atomics).
+ * At most max_threads steps run concurrently. */
+int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,
+                       const uint64_t *src_alias, const float *collapse,
+                       const uint64_t *neg_alias, int64_t n, float *y, int64_t n_steps, int t0,
+                       int n_iter, int iters, double lr0, double gamma, double eps, double clip,
+                       int b, int M, uint64_t seed, int level, int64_t max_threads,
+                       void *stream);
 
 /* --- K6: prolongation ---------------------------------------------------------------
  * _layout_radius (optimizer.py:356-358): max distance to the centroid (host). */

@@ -3,18 +3,19 @@
 // K7 (layout.cu) applies one epoch's EXPECTED displacement with a CSR gather.  This
 // kernel instead replays the reference step itself (_kernels.py:65-140), Hogwild
 // style like sgd_epoch with threads > 1 (optimizer.py:325-345): every thread runs
-// steps s of the epoch; a step draws a directed pair (i0, j0) ~ P at level 0 (the
-// source by a Vose table over the row masses, then the target by the row's own Vose
-// table -- the same law as the reference's canonical-pair table plus direction
-// coin, optimizer.py:206-229), maps both ends to the current level, applies the
-// clipped attractive update to both ends if they differ, then M negatives ~ Q at
-// level 0, mapped and redrawn (<= 9 attempts) while they hit i or j, each moving
-// both ends.  Updates are float2 atomic adds on y; the source position is tracked
-// locally through the step as in the sequential kernel.
+// steps s of the epoch.  The reference draws a level-0 pair (i0, j0) ~ P and maps it
+// to level l; that law equals "source a ~ R^l, then with probability c_a the
+// collapsed pair (a, a), else the target b ~ P^l_a." (c_a = mass of pairs inside
+// a / R^l_a), which this kernel samples from level-l tables (a Vose table over R^l,
+// one Vose table per row of P^l) so coarse levels stay L2-resident.  Attraction is
+// clipped and applied to both ends if i != j; M negatives ~ Q^l are redrawn (<= 9
+// attempts) while they hit i or j, each moving both ends.  Updates are float2
+// atomic adds on y; the source position is tracked locally through the step as in
+// the sequential kernel.
 //
 // Latency: all first-attempt draws (pair + M negatives) are made up front and
 // their table loads issued together; the dependent chain of a step is then
-// source alias -> row bounds -> row alias record + target -> (map) -> y.
+// source alias -> row bounds / c_a -> row alias record + target -> y.
 #include "common.cuh"
 
 namespace drg {
@@ -23,13 +24,13 @@ namespace {
 constexpr int kMaxNeg = 6;  // negatives whose first draw is issued early
 
 struct SArgs {
-    const int64_t *indptr0;
-    const int32_t *targets0;
+    const int64_t *indptr;
+    const uint2 *rec;        // level CSR records {target, W}
     const uint2 *row_alias;  // per entry {fp32 threshold, int32 alias target}
-    const uint2 *src_alias;
-    const uint2 *neg_alias;
-    int64_t n0;
-    const int32_t *map;
+    const uint2 *src_alias;  // Vose over R^l
+    const float *collapse;   // probability that the drawn pair collapses into the source
+    const uint2 *neg_alias;  // Vose over Q^l
+    int64_t n;
     int64_t n_steps;
     float lr, gamma, eps, clip;
     int b, M;
@@ -77,33 +78,34 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
         // ---- all first-attempt draws, table loads in flight together
         const u32x4 r = philox4x32(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xff00u, 0x5a3d1e55u},
                                    A.key0, A.key1);
-        const int64_t sb = bucket(A.n0, r.x, r.y);
+        const int64_t sb = bucket(A.n, r.x, r.y);
         const uint2 srec = __ldg(A.src_alias + sb);
-        int32_t nbk[kMaxNeg];   // level-0 ids < 2^31
+        int32_t nbk[kMaxNeg];   // node ids < 2^31
         uint2 nrec[kMaxNeg];
         uint32_t ncoin[kMaxNeg];
 #pragma unroll
         for (int m = 0; m < kMaxNeg; ++m) {
             if (m < Me) {
                 const u32x4 q = neg_draw(A, s, c1, m, 0);
-                nbk[m] = (int32_t)bucket(A.n0, q.x, q.y);
+                nbk[m] = (int32_t)bucket(A.n, q.x, q.y);
                 ncoin[m] = q.z;
                 nrec[m] = __ldg(A.neg_alias + nbk[m]);
             }
         }
-        // ---- directed pair ~ P at level 0: source alias, then the row's alias
-        const int64_t i0 = accept(srec, sb, r.z);
-        const int64_t lo = __ldg(A.indptr0 + i0), hi = __ldg(A.indptr0 + i0 + 1);
-        if (hi <= lo) continue;
+        // ---- directed pair: source a ~ R^l; collapsed (a, a) with prob collapse[a],
+        // else target ~ P^l_a. by the row's alias table
+        const int64_t i = accept(srec, sb, r.z);
+        const int64_t lo = __ldg(A.indptr + i), hi = __ldg(A.indptr + i + 1);
+        const float cprob = __ldg(A.collapse + i);
         const u32x4 r2 = philox4x32(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xfe00u, 0x3c6ef372u},
                                     A.key0, A.key1);
-        const int64_t e = lo + bucket(hi - lo, r2.x, r2.y);
-        const uint2 rrec = __ldg(A.row_alias + e);
-        const int32_t tj = __ldg(A.targets0 + e);
-        const int64_t j0 = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)tj
-                                                                          : (int64_t)rrec.y;
-        const int64_t i = A.map ? (int64_t)__ldg(A.map + i0) : i0;
-        const int64_t j = A.map ? (int64_t)__ldg(A.map + j0) : j0;
+        int64_t j = i;
+        if (hi > lo && !(u32_to_unit(r.w) < cprob)) {
+            const int64_t e = lo + bucket(hi - lo, r2.x, r2.y);
+            const uint2 rrec = __ldg(A.row_alias + e);
+            const uint32_t tj = __ldg(A.rec + e).x;
+            j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)tj : (int64_t)rrec.y;
+        }
         float2 yi = ld_y(y, i);
         if (i != j) {  // _kernels.py:82-105
             const float2 yj = ld_y(y, j);
@@ -138,10 +140,10 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
                     c0 = accept(rc, bk, cn);
                 } else {
                     const u32x4 q = neg_draw(A, s, c1, m, attempt);
-                    const int64_t bk = bucket(A.n0, q.x, q.y);
+                    const int64_t bk = bucket(A.n, q.x, q.y);
                     c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
                 }
-                const int64_t cm = A.map ? (int64_t)__ldg(A.map + c0) : c0;
+                const int64_t cm = c0;
                 if (cm != i && cm != j) {
                     target = cm;
                     break;
@@ -173,14 +175,18 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
 __global__ void row_alias_kernel(const int64_t *__restrict__ indptr,
                                  const int32_t *__restrict__ targets,
                                  const double *__restrict__ P, int64_t n, int32_t *stack,
-                                 double *w, uint2 *rec) {
+                                 double *w, uint2 *rec, double *rowsum) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t lo = indptr[i], hi = indptr[i + 1];
         const int64_t len = hi - lo;
-        if (len <= 0) continue;
+        if (len <= 0) {
+            if (rowsum) rowsum[i] = 0.0;
+            continue;
+        }
         double total = 0.0;
         for (int64_t e = lo; e < hi; ++e) total += P[e];
+        if (rowsum) rowsum[i] = total;
         for (int64_t e = lo; e < hi; ++e) rec[e] = make_uint2(__float_as_uint(1.0f), targets[e]);
         if (!(total > 0.0)) continue;  // massless row: uniform
         const double f = (double)len / total;
@@ -208,37 +214,39 @@ __global__ void row_alias_kernel(const int64_t *__restrict__ indptr,
 using namespace drg;
 
 extern "C" int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P,
-                             int64_t n, int64_t nnz, uint64_t *out_rec, void *stream) {
-    if (n <= 0 || nnz <= 0) return DRG_OK;
+                             int64_t n, int64_t nnz, uint64_t *out_rec, double *out_rowsum,
+                             void *stream) {
+    if (n <= 0) return DRG_OK;
     cudaStream_t st = as_stream(stream);
     Scratch stack(st), w(st);
-    DRG_CUDA(stack.alloc(sizeof(int32_t) * (size_t)nnz));
-    DRG_CUDA(w.alloc(sizeof(double) * (size_t)nnz));
+    DRG_CUDA(stack.alloc(sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1)));
+    DRG_CUDA(w.alloc(sizeof(double) * (size_t)std::max<int64_t>(nnz, 1)));
     const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 128), kSMs * 64);
     row_alias_kernel<<<g, 128, 0, st>>>(indptr, targets, P, n, stack.as<int32_t>(),
-                                        w.as<double>(), reinterpret_cast<uint2 *>(out_rec));
+                                        w.as<double>(), reinterpret_cast<uint2 *>(out_rec),
+                                        out_rowsum);
     DRG_LAUNCHED("row_alias_kernel");
     return DRG_OK;
 }
 
-extern "C" int drg_layout_sampled(const int64_t *indptr0, const int32_t *targets0,
+extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                                   const uint64_t *row_alias, const uint64_t *src_alias,
-                                  const uint64_t *neg_alias, int64_t n0, const int32_t *map,
-                                  float *y, int64_t n_l, int64_t n_steps, int t0, int n_iter,
-                                  int iters, double lr0, double gamma, double eps, double clip,
-                                  int b, int M, uint64_t seed, int level, int64_t max_threads,
-                                  void *stream) {
-    if (n0 <= 0 || n_l <= 0 || n_steps < 0 || n_iter < 0) return DRG_OK;
+                                  const float *collapse, const uint64_t *neg_alias, int64_t n,
+                                  float *y, int64_t n_steps, int t0, int n_iter, int iters,
+                                  double lr0, double gamma, double eps, double clip, int b, int M,
+                                  uint64_t seed, int level, int64_t max_threads, void *stream) {
+    if (n <= 0 || n_steps < 0 || n_iter < 0) return DRG_OK;
+    if (n >= 0x7fffffffLL) return fail(DRG_ERR_INVALID, "level exceeds 2^31 - 1 nodes");
     if (b < 1 || M < 0 || iters < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
     cudaStream_t st = as_stream(stream);
     SArgs A;
-    A.indptr0 = indptr0;
-    A.targets0 = targets0;
+    A.indptr = indptr;
+    A.rec = reinterpret_cast<const uint2 *>(rec);
     A.row_alias = reinterpret_cast<const uint2 *>(row_alias);
     A.src_alias = reinterpret_cast<const uint2 *>(src_alias);
+    A.collapse = collapse;
     A.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
-    A.n0 = n0;
-    A.map = map;
+    A.n = n;
     A.n_steps = n_steps;
     A.gamma = (float)gamma;
     A.eps = (float)eps;

@@ -175,6 +175,7 @@ class LevelData:
     V: torch.Tensor        # fp32 [n]
     alias: torch.Tensor    # int64 [n]    (fp32 prob | int32 alias << 32)
     heavy: dict | None = None   # heavy-row split tensors (rows > HEAVY_ROW entries)
+    sampled: "SampledTables | None" = None   # update="sampled" tables of this level
 
     def algorithmic_bytes(self, M: int) -> int:
         """16 B per P entry + (24 + 16 M) B per node (level 0) --
@@ -243,11 +244,39 @@ def pack_level(indptr, targets, P, R, Wn, q_scale, n, sort_rows=False
     return rec[:nnz], V[:n]
 
 
-def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float = 0.75
-                     ) -> list[LevelData]:
+@dataclass
+class SampledTables:
+    """update="sampled" tables of one level l: drawing a level-0 pair ~ P and
+    mapping it to level l (the reference, _kernels.py:66-81) has exactly the law
+    "source a ~ R^l, then with probability c_a the collapsed pair (a, a), else b ~
+    P^l_a." with c_a = 1 - sum_b P^l_ab / R^l_a (mass of pairs inside a); negatives
+    drawn at level 0 and mapped follow Q^l (the level's negative table)."""
+
+    src_alias: torch.Tensor   # int64 [n]  Vose over R^l
+    row_alias: torch.Tensor   # int64 [nnz] per-row Vose over P^l (threshold, alias target)
+    collapse: torch.Tensor    # fp32 [n]   c_a
+
+
+def build_sampled_tables(ip, tg, P, R) -> SampledTables:
+    n = ip.numel() - 1
+    nnz = tg.numel()
+    rows = torch.empty(max(nnz, 1), dtype=torch.int64, device=R.device)
+    rowsum = torch.empty(max(n, 1), dtype=torch.float64, device=R.device)
+    _lib.call("drg_row_alias", _lib.ptr(ip), _lib.ptr(tg), _lib.ptr(P), n, nnz, _lib.ptr(rows),
+              _lib.ptr(rowsum), _lib.stream_ptr())
+    src, _ = _alias_device(R)
+    with torch.no_grad():
+        c = torch.where(R > 0, 1.0 - rowsum[:n] / torch.clamp(R, min=1e-300),
+                        torch.zeros_like(R)).clamp_(0.0, 1.0).to(torch.float32)
+    return SampledTables(src, rows[:nnz], c)
+
+
+def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float = 0.75,
+                     sampled: bool = False) -> list[LevelData]:
     """P^l, R^l, Q^l for every level, pulled up level by level through the parent
     maps (drg_aggregate_pairs / drg_aggregate_nodes), then packed (drg_level_pack)
-    with a Vose table per level (drg_alias_build)."""
+    with a Vose table per level (drg_alias_build); ``sampled`` also builds the
+    level's sampled-mode tables."""
     ip, tg, P = ds.indptr, ds.targets, ds.weights
     R = ds.row_mass
     Wn = device_negative_weights(R, neg_power)
@@ -264,46 +293,14 @@ def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float
         # sectors by 12% on the mesh but cost 130 ms of segmented sort and no
         # kernel time (profiles/README.md), so it is off
         rec, V = pack_level(ip, tg, P, R, Wn, 1.0 / total, n_l, sort_rows=False)
-        out.append(LevelData(n_l, tg.numel(), ip, rec, V, alias, heavy_split(ip)))
+        L = LevelData(n_l, tg.numel(), ip, rec, V, alias, heavy_split(ip))
+        if sampled and R.numel() > 0 and float(R.sum()) > 0:
+            L.sampled = build_sampled_tables(ip, tg, P, R)
+        out.append(L)
     return out
 
 
 StepFn = Callable[[torch.Tensor, torch.Tensor, int, int, int], None]
-
-
-@dataclass
-class SampledData:
-    """Level-0 sampling tables of the reference-faithful mode (update="sampled"):
-    P^0 CSR with a Vose table per row, a Vose table over the row masses (sources),
-    the level-0 negative table, and the flat level maps."""
-
-    indptr0: torch.Tensor
-    targets0: torch.Tensor
-    row_alias: torch.Tensor
-    src_alias: torch.Tensor
-    neg_alias: torch.Tensor
-    flat_maps: list   # flat_maps[l]: level-0 id -> level-l id (None at level 0)
-
-
-def build_sampled_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_alias: torch.Tensor
-                       ) -> SampledData:
-    n0 = ds.node_count
-    rows = torch.empty(max(ds.entry_count, 1), dtype=torch.int64, device=ds.weights.device)
-    _lib.call("drg_row_alias", _lib.ptr(ds.indptr), _lib.ptr(ds.targets), _lib.ptr(ds.weights),
-              n0, ds.entry_count, _lib.ptr(rows), _lib.stream_ptr())
-    src_alias, _ = _alias_device(ds.row_mass)
-    flat = [None]
-    cur = None
-    for level in range(1, dh.depth + 1):
-        nxt = torch.empty(n0, dtype=torch.int32, device=ds.weights.device)
-        if cur is None:
-            nxt.copy_(dh.maps[0])
-        else:
-            _lib.call("drg_compose_maps", _lib.ptr(cur), _lib.ptr(dh.maps[level - 1]), n0,
-                      _lib.ptr(nxt), _lib.stream_ptr())
-        flat.append(nxt)
-        cur = nxt
-    return SampledData(ds.indptr, ds.targets, rows, src_alias, neg_alias, flat)
 
 
 @dataclass
@@ -314,7 +311,6 @@ class LayoutPlan:
     maps: list
     opt: OptimizerParams
     nonfinite: torch.Tensor = None
-    sampled: SampledData | None = None
 
     @property
     def depth(self) -> int:
@@ -404,16 +400,14 @@ class LayoutPlan:
 
     def _run_level_sampled(self, level, y, t0, n_iter):
         """Reference-faithful epochs: n_l sampled steps each, Hogwild on y."""
-        S = self.sampled
+        L, gamma, seed = self._level_args(level)
+        S = L.sampled
         if S is None:
             raise RuntimeError("plan was built without sampled-mode tables")
-        L, gamma, seed = self._level_args(level)
         o = self.opt
-        fm = S.flat_maps[level]
-        n0 = S.indptr0.numel() - 1
-        _lib.call("drg_layout_sampled", _lib.ptr(S.indptr0), _lib.ptr(S.targets0),
-                  _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), _lib.ptr(S.neg_alias), n0,
-                  _lib.ptr(fm), _lib.ptr(y), L.n, L.n, t0, n_iter, o.iters, float(o.lr0),
+        _lib.call("drg_layout_sampled", _lib.ptr(L.indptr), _lib.ptr(L.rec),
+                  _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), _lib.ptr(S.collapse),
+                  _lib.ptr(L.alias), L.n, _lib.ptr(y), L.n, t0, n_iter, o.iters, float(o.lr0),
                   float(gamma), float(o.eps), float(o.grad_clip), o.b, o.neg_samples, seed,
                   level, max(256, L.n // max(1, o.sampled_concurrency)), _lib.stream_ptr())
         if not bool(torch.isfinite(y).all()):
@@ -473,10 +467,8 @@ def device_radius(y: torch.Tensor) -> float:
 
 
 def build_plan(ds: DeviceSimilarity, dh: DeviceHierarchy, opt: OptimizerParams) -> LayoutPlan:
-    plan = LayoutPlan(build_level_data(ds, dh, opt.neg_power), list(dh.maps), opt)
-    if opt.update == "sampled":
-        plan.sampled = build_sampled_data(ds, dh, plan.levels[0].alias)
-    return plan
+    return LayoutPlan(build_level_data(ds, dh, opt.neg_power, opt.update == "sampled"),
+                      list(dh.maps), opt)
 
 
 @dataclass
@@ -620,7 +612,7 @@ class Samplers:
                 torch.from_numpy(np.ascontiguousarray(ns.sigma)).cuda(),
                 torch.from_numpy(np.ascontiguousarray(ns.row_masses())).cuda(),
                 ns.total_mass, int((np.diff(ns.indptr) > 0).sum()), ns.k)
-            self._plans[key] = (h, LayoutPlan(build_level_data(ds, dh, self.neg_power),
+            self._plans[key] = (h, LayoutPlan(build_level_data(ds, dh, self.neg_power, True),
                                               list(dh.maps), params))
         plan = self._plans[key][1]
         plan.opt = params

@@ -575,11 +575,12 @@ def test_single_step_parity_heavy_rows():
 def test_row_alias_tables_reproduce_row_laws(golden):
     """drg_row_alias: every row's Vose table implies exactly P_ij / sum_j P_ij."""
     from paper_2008_07799_b200.graph import DeviceGraph
-    from paper_2008_07799_b200.optimizer import build_sampled_data
+    from paper_2008_07799_b200.optimizer import build_sampled_tables
     g = golden_graph(golden, "dense80")
     prep = _prepared(as_gpu_graph(g), k=2, M=5)
     ds = prep.similarity
-    S = build_sampled_data(ds, prep.hierarchy, prep.plan.levels[0].alias)
+    S = build_sampled_tables(ds.indptr, ds.targets, ds.weights, ds.row_mass)
+    assert float(S.collapse.abs().max()) < 1e-6      # level 0: no collapsed pairs
     rec = S.row_alias.cpu().numpy().view(np.uint32).reshape(-1, 2)
     ip, tg, w = ds.indptr.cpu().numpy(), ds.targets.cpu().numpy(), ds.weights.cpu().numpy()
     for i in range(len(ip) - 1):
