@@ -74,6 +74,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the other update modes")
     ap.add_argument("--update", default="jacobi", choices=["jacobi", "inplace", "sampled"])
+    ap.add_argument("--sampled-concurrency", type=int, default=16)
     return ap.parse_args()
 
 
@@ -153,12 +154,12 @@ def build_workload(name):
     return getattr(synthetic, fn)(*args)
 
 
-def params_for(name, iters_override=None, update="jacobi"):
+def params_for(name, iters_override=None, update="jacobi", concurrency=16):
     import paper_2008_07799_b200 as B
     w = WORKLOADS[name]
     sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"], neighbor_cap=w.get("cap"))
     opt = B.OptimizerParams(neg_samples=w["M"], iters=iters_override or w["iters"], seed=0,
-                            init=w["init"], update=update)
+                            init=w["init"], update=update, sampled_concurrency=concurrency)
     return sim, opt, dict(w["hier"])
 
 
@@ -273,7 +274,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
     name = args.workload
-    sim, opt, hier = params_for(name, args.iters, args.update)
+    sim, opt, hier = params_for(name, args.iters, args.update, args.sampled_concurrency)
 
     dg = build_workload(name)
     torch.cuda.synchronize()
