@@ -99,11 +99,14 @@ def level_order(n: int, seed: int) -> np.ndarray:
 
 
 def device_build_hierarchy(dg: DeviceGraph, rho: float = 0.8, min_size: int = 16, seed: int = 0,
-                           max_levels: int | None = None, force_levels: int | None = None
-                           ) -> DeviceHierarchy:
+                           max_levels: int | None = None, force_levels: int | None = None,
+                           level0_relabel: torch.Tensor | None = None) -> DeviceHierarchy:
     """build_hierarchy (multilevel.py:95-113) on a resident graph.  Extensions for
     the BASELINE configs: ``max_levels`` caps the total level count; ``force_levels``
-    keeps coarsening past the rho test until that many levels exist."""
+    keeps coarsening past the rho test until that many levels exist.
+    ``level0_relabel`` (old id -> new id): ``dg`` is the input graph relabelled; the
+    reference's level-0 visiting order (drawn over the original ids) is translated,
+    so the coarse levels are exactly the reference's."""
     if not 0.0 < rho < 1.0:
         raise ValueError("rho must be in (0, 1)")
     if min_size < 1:
@@ -116,6 +119,8 @@ def device_build_hierarchy(dg: DeviceGraph, rho: float = 0.8, min_size: int = 16
         level_seed = int(rng.integers(0, 2**63 - 1))
         top = h.levels[-1]
         order = torch.from_numpy(level_order(top.node_count, level_seed)).to(top.indptr.device)
+        if level0_relabel is not None and len(h.levels) == 1:
+            order = level0_relabel.to(torch.int64)[order]
         coarse, parent, rounds = device_coarsen(top, order)
         forced = force_levels is not None and len(h.levels) < force_levels
         if not forced and coarse.node_count > rho * top.node_count:
@@ -199,3 +204,42 @@ def prolong(coarse_positions: np.ndarray, cmap: np.ndarray, jitter_scale: float,
     yc = torch.from_numpy(np.ascontiguousarray(coarse_positions, dtype=np.float32)).cuda()
     pm = torch.from_numpy(np.ascontiguousarray(cmap, dtype=np.int32)).cuda()
     return device_prolong(yc, pm, jitter_scale, seed).cpu().numpy().astype(np.float64)
+
+
+def isolated_last(dg: DeviceGraph, min_fraction: float = 0.01):
+    """Relabelling that moves isolated nodes behind all others (relative order kept).
+    Isolated nodes are never gathered as neighbours, so the gathered part of Y
+    becomes one dense prefix (L2-resident where the whole Y would not be, e.g.
+    R-MAT).  Returns (relabelled graph, old -> new id) or (dg, None)."""
+    deg = dg.indptr[1:] - dg.indptr[:-1]
+    iso = deg == 0
+    n = deg.numel()
+    if n == 0 or float(iso.float().mean()) < min_fraction:
+        return dg, None
+    order = torch.argsort(iso.to(torch.int8), stable=True)           # new -> old
+    rel = torch.empty_like(order)
+    rel[order] = torch.arange(n, device=order.device)
+    indptr = torch.zeros(n + 1, dtype=torch.int64, device=order.device)
+    indptr[1:] = torch.cumsum(deg[order], 0)
+    # neighbours are never isolated and keep their relative order: rows stay sorted
+    indices = rel.to(torch.int32)[dg.indices.to(torch.int64)]
+    return DeviceGraph(indptr, indices), rel.to(torch.int32)
+
+
+def relabel_coarse_levels(dh: DeviceHierarchy) -> list:
+    """Isolated-last relabelling of every coarse level of a built hierarchy (maps
+    and level graphs rewritten).  Returns the per-level old -> new maps (None =
+    identity); level 0 is left to the caller."""
+    rels = [None]
+    for l in range(1, dh.depth + 1):
+        g2, rel = isolated_last(dh.levels[l])
+        rels.append(rel)
+        if rel is None:
+            continue
+        dh.levels[l] = g2
+        dh.maps[l - 1] = rel[dh.maps[l - 1].to(torch.int64)]
+        if l < dh.depth:
+            m = torch.empty_like(dh.maps[l])
+            m[rel.to(torch.int64)] = dh.maps[l]
+            dh.maps[l] = m
+    return rels

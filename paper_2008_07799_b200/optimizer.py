@@ -31,7 +31,7 @@ import torch
 from . import _lib
 from .graph import DeviceGraph, Graph, device_components, device_k_neighborhoods
 from .multilevel import (DeviceHierarchy, Hierarchy, compose_maps, device_build_hierarchy,
-                         device_prolong)
+                         device_prolong, isolated_last, relabel_coarse_levels)
 from .similarity import (DeviceSimilarity, SimilarityParams, SparseSimilarity,
                          device_similarity)
 
@@ -480,6 +480,20 @@ class PreparedLayout:
     hierarchy: DeviceHierarchy
     stats: dict
     timings: dict
+    relabel: list = None   # per level old -> new id (None = identity); see isolated_last
+
+    def to_original(self, y0: torch.Tensor) -> torch.Tensor:
+        """Level-0 positions in the caller's node order."""
+        rel = self.relabel[0] if self.relabel else None
+        return y0 if rel is None else y0[rel.to(torch.int64)]
+
+    def from_original_coarsest(self, y: torch.Tensor) -> torch.Tensor:
+        rel = self.relabel[-1] if self.relabel else None
+        if rel is None:
+            return y
+        out = torch.empty_like(y)
+        out[rel.to(torch.int64)] = y
+        return out
 
 
 def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
@@ -498,6 +512,9 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
             ev.append((name, e))
 
     stamp("start")
+    # isolated nodes last (layout-internal ids; outputs are mapped back)
+    dg_in = dg
+    dg, rel0 = isolated_last(dg)
     n_comp = device_components(dg)
     if n_comp > 1:
         logger.warning("input has %d connected components; repulsion alone separates them",
@@ -509,7 +526,10 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
     del nd
     stamp("similarity")
     dh = device_build_hierarchy(dg, rho, min_size, _derive_seed(opt.seed, _HIERARCHY_TAG),
-                                max_levels, force_levels)
+                                max_levels, force_levels, level0_relabel=rel0)
+    relabel = relabel_coarse_levels(dh)
+    relabel[0] = rel0
+    del dg_in
     stamp("hierarchy")
     stats = {
         "components": n_comp,
@@ -527,7 +547,7 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
         torch.cuda.synchronize()
         for (a, ea), (b, eb) in zip(ev[:-1], ev[1:]):
             timings[b + "_ms"] = ea.elapsed_time(eb)
-    return PreparedLayout(plan, ds, dh, stats, timings)
+    return PreparedLayout(plan, ds, dh, stats, timings, relabel)
 
 
 def layout_device(dg: DeviceGraph, sim: SimilarityParams | None = None,
@@ -543,6 +563,7 @@ def layout_device(dg: DeviceGraph, sim: SimilarityParams | None = None,
     if init_positions is not None:
         y0 = torch.as_tensor(np.asarray(init_positions, dtype=np.float32)).cuda() \
             if not isinstance(init_positions, torch.Tensor) else init_positions.float().cuda()
+        y0 = prep.from_original_coarsest(y0)
     else:
         y0 = None
     if prep.plan is None:
@@ -554,8 +575,8 @@ def layout_device(dg: DeviceGraph, sim: SimilarityParams | None = None,
         y = tmp.init_positions() if y0 is None else y0
         for level in range(dh.depth, 0, -1):
             y = device_prolong(y, dh.maps[level - 1], 0.0, 0)
-        return y, stats, prep
-    y = prep.plan.run(y0, group=group)
+        return prep.to_original(y), stats, prep
+    y = prep.to_original(prep.plan.run(y0, group=group))
     M = opt.neg_samples
     stats["gradient_steps"] = opt.iters * sum(dh.sizes)
     # reference-equivalent interaction count: each iteration stands for n_l steps of

@@ -595,3 +595,39 @@ def test_row_alias_tables_reproduce_row_laws(golden):
         got = np.array([mass[int(t)] for t in tg[lo:hi]])
         np.testing.assert_allclose(got, want, rtol=2e-6, atol=1e-7)
     del DeviceGraph
+
+
+def test_isolated_last_relabelling_keeps_the_reference_hierarchy():
+    """Inside the layout pipeline isolated nodes are moved behind all others; the
+    translated visiting orders reproduce the reference hierarchy exactly, and
+    positions come back in the caller's node order."""
+    from paper_2008_07799_b200.graph import DeviceGraph
+    from paper_2008_07799_b200.optimizer import _HIERARCHY_TAG, _derive_seed, prepare_layout
+    rng = np.random.default_rng(21)
+    n = 3000
+    pairs = rng.integers(0, 2000, size=(5000, 2))        # nodes 2000..2999 isolated
+    pairs = pairs[(pairs % 7 != 3).all(axis=1)]           # plus scattered isolated ids
+    g = O.from_edges(pairs, n)
+    prep = prepare_layout(DeviceGraph.from_host(as_gpu_graph(g)), B.SimilarityParams(k=1),
+                          B.OptimizerParams(seed=4, iters=5), min_size=16)
+    assert prep.relabel[0] is not None
+    href = O.build_hierarchy(g, 0.8, 16, _derive_seed(4, _HIERARCHY_TAG))
+    dh = prep.hierarchy
+    assert dh.sizes == [lv.node_count for lv in href.levels]
+    rel0 = prep.relabel[0].cpu().numpy().astype(np.int64)
+    flat = np.arange(n)
+    for level in range(1, dh.depth + 1):
+        flat = dh.maps[level - 1].cpu().numpy()[flat] if level > 1 else \
+            dh.maps[0].cpu().numpy()[np.arange(n)]
+        rel = prep.relabel[level]
+        inv = np.arange(dh.sizes[level])
+        if rel is not None:
+            inv = np.empty(dh.sizes[level], dtype=np.int64)
+            inv[rel.cpu().numpy()] = np.arange(dh.sizes[level])
+        got = inv[flat[rel0]]                               # original ids -> original coarse ids
+        assert np.array_equal(got, O.compose_maps(href, level))
+    lay = B.layout_graph(as_gpu_graph(g), B.SimilarityParams(k=1),
+                         B.OptimizerParams(seed=4, iters=30))
+    assert np.isfinite(lay.positions).all()
+    iso = np.diff(g.indptr) == 0
+    assert np.abs(lay.positions[iso]).max() < 1.0         # isolated nodes barely move
