@@ -1,0 +1,22 @@
+#!/bin/bash
+# Profiling pass for a gpurun box (1 GPU).  Each ncu run follows the same command
+# run plainly (exit 0) first, per /opt/skills/guides/B200_PROFILING.md.
+#   bash scripts/profile.sh [workload] [update]
+set -u
+W=${1:-mesh}
+U=${2:-jacobi}
+OUT=gpurun_out
+CMD="python bench.py --workload $W --update $U --iters 20 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-alt"
+mkdir -p $OUT
+# 1) launch list: every launch of one reduced step with its device time
+$CMD > $OUT/plain_${W}_${U}.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file $OUT/launches_${W}_${U}.csv $CMD > $OUT/ncu_launches_${W}_${U}.log 2>&1
+echo "launch list rc=$?"
+# 2) full capture of the dominant kernel (first level-0 launch of the timed step)
+K=layout_iter
+[ "$U" = "sampled" ] && K=sampled_kernel
+$CMD > $OUT/plain2_${W}_${U}.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:$K -s 60 -c 1 -f \
+      -o $OUT/full_${W}_${U} $CMD > $OUT/ncu_full_${W}_${U}.log 2>&1
+echo "full capture rc=$?"
