@@ -73,7 +73,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the other update modes")
-    ap.add_argument("--update", default="jacobi", choices=["jacobi", "inplace", "sampled"])
+    ap.add_argument("--update", default="jacobi",
+                    choices=["jacobi", "inplace", "sampled", "sgather"])
     ap.add_argument("--sampled-concurrency", type=int, default=16)
     return ap.parse_args()
 
@@ -338,11 +339,12 @@ def run_ours(args):
     alt = {}
     if not args.no_alt and group is None:
         from paper_2008_07799_b200.optimizer import LayoutPlan, build_plan
-        for mode in ("jacobi", "inplace", "sampled"):
+        for mode in ("jacobi", "inplace", "sampled", "sgather"):
             if mode == opt.update:
                 continue
             o2 = B.OptimizerParams(**{**opt.__dict__, "update": mode})
-            p2 = (build_plan(prep.similarity, prep.hierarchy, o2) if mode == "sampled"
+            p2 = (build_plan(prep.similarity, prep.hierarchy, o2)
+                  if mode in ("sampled", "sgather") and plan.levels[0].sampled is None
                   else LayoutPlan(plan.levels, plan.maps, o2))
             p2.run()
             torch.cuda.synchronize()

@@ -197,6 +197,19 @@ int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_
                        int b, int M, uint64_t seed, int level, int64_t max_threads,
                        void *stream);
 
+/* Stochastic gather (update = "sgather"): drg_layout_iters with the attraction
+ * SAMPLED -- every node draws S partners b ~ W_a. from its row's alias table
+ * (row_alias, from drg_row_alias) and applies wsum[a]/S * clip(g_att) per draw
+ * (wsum[a] = sum_b W_ab), plus M negatives as in drg_layout_iters, redrawn if they
+ * hit the node or its first partner.  Same buffers, flags and determinism as
+ * drg_layout_iters; S + M <= 32. */
+int drg_layout_sgather(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,
+                       const float *wsum, const float *V, const uint64_t *alias, int64_t n,
+                       int64_t row_lo, int64_t row_hi, float *y_in, float *y_out, int t0,
+                       int n_iter, int iters, double lr0, double gamma, double eps, double clip,
+                       int b, int M, int S, uint64_t seed, int level, const int32_t *neg_idx,
+                       int32_t *nonfinite, unsigned flags, void *stream);
+
 /* --- K6: prolongation ---------------------------------------------------------------
  * _layout_radius (optimizer.py:356-358): max distance to the centroid (host). */
 int drg_layout_radius(const float *y, int64_t n, double *out_radius, void *stream);

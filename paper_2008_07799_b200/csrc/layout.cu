@@ -394,6 +394,128 @@ __global__ void __launch_bounds__(kWpb * 32)
     if (lane == 0) A.hpart[c] = make_float2(ax, ay);
 }
 
+// ---------------------------------------------------------------------------------
+// Stochastic gather (update="sgather"): the node-parallel Jacobi iteration with the
+// attraction SAMPLED instead of summed over the whole row -- each node draws S
+// partners b ~ W_a. from its row's Vose table and applies (sum_b W_ab / S) clip(g_att)
+// per draw (unbiased for the A12 expectation, with the reference's per-epoch
+// sampling noise: a node takes part in ~2 attractive interactions per epoch), plus
+// the M negatives of K7 (redrawn if they hit the node or its first partner, like
+// _kernels.py:108-117).  Deterministic (Philox per node), gather-only (no atomics),
+// node-range shardable like K7.  A warp owns npw = 32 / (S + M) nodes; each lane
+// makes one draw and one y gather, then a segmented shuffle sum per node.
+struct SGArgs {
+    const uint2 *row_alias;  // per entry {threshold, alias target}
+    const float *wsum;       // per node sum_b W_ab
+    int S;
+};
+
+template <bool INPLACE, int B, bool CLAMP_ATT>
+__global__ void __launch_bounds__(kWpb * 32)
+    sgather_kernel(IterArgs A, SGArgs G, int npw, const float2 *y_in, float2 *y_out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t a0 = A.row_lo + ((int64_t)blockIdx.x * kWpb + warp) * npw;
+    if (a0 >= A.row_hi) return;
+    const int nodes = (int)min((int64_t)npw, A.row_hi - a0);
+    const int b = B > 0 ? B : A.b;
+    const float two_b = 2.0f * (float)b;
+    const int K = G.S + A.M;
+    const int my = K > 0 ? lane / K : 0;
+    const int r = lane - my * K;
+    const bool active = lane < nodes * K;
+    const bool att = active && r < G.S;
+    const int64_t a = a0 + min(my, nodes - 1);
+    // 1. attraction draws
+    int64_t pb = -1;
+    if (att) {
+        const int64_t lo = __ldg(A.indptr + a), hi = __ldg(A.indptr + a + 1);
+        if (hi > lo) {
+            const u32x4 q = philox4x32(u32x4{(uint32_t)a, (uint32_t)(a >> 32) ^ ((uint32_t)A.t << 1),
+                                             (A.level << 24) | 0xA00000u | (uint32_t)r, 0x71d3a5c1u},
+                                       A.key0, A.key1);
+            const int64_t e = lo + (int64_t)__umul64hi(((uint64_t)q.x << 32) | q.y,
+                                                        (uint64_t)(hi - lo));
+            const uint2 rr = __ldg(G.row_alias + e);
+            const uint32_t tj = __ldg(A.rec + e).x;
+            pb = (u32_to_unit(q.z) < __uint_as_float(rr.x)) ? (int64_t)tj : (int64_t)rr.y;
+        }
+    }
+    // 2. the node's first partner, for the negatives' rejection
+    const int64_t partner = __shfl_sync(kFull, pb, min(my * K, 31));
+    // 3. negatives
+    int64_t c = -1;
+    if (active && !att) {
+        const int m = r - G.S;
+        if (A.neg_idx) {
+            c = A.neg_idx[a * A.M + m];
+        } else {
+            for (int attempt = 0; attempt < 9; ++attempt) {
+                const u32x4 nb = neg_bits(A, a, m, attempt);
+                const int64_t idx = alias_index(A, nb);
+                c = resolve_draw(A, nb, __ldg(A.alias + idx), idx);
+                if (c != a && c != partner) break;
+                c = -1;
+            }
+        }
+    }
+    // 4. one interaction per lane
+    float gx = 0.f, gy = 0.f;
+    const int64_t other = att ? pb : c;
+    if (active && other >= 0) {
+        const float2 ya = load_y<INPLACE>(y_in, a);
+        const float2 yo = load_y<INPLACE>(y_in, other);
+        const float dx = ya.x - yo.x, dy = ya.y - yo.y;
+        const float ld2 = fmaf(dx, dx, dy * dy);
+        const float pw = powbm1<B>(ld2, b);
+        if (att) {
+            const float wS = __ldg(G.wsum + a) / (float)G.S;
+            const float coef = -two_b * pw * rcp_approx(fmaf(pw, ld2, 1.0f));
+            gx = wS * (CLAMP_ATT ? clampf(coef * dx, A.clip) : coef * dx);
+            gy = wS * (CLAMP_ATT ? clampf(coef * dy, A.clip) : coef * dy);
+        } else if (ld2 + A.eps > 0.f) {
+            const float Va = __ldg(A.V + a);
+            const float den = fmaxf((ld2 + A.eps) * fmaf(pw, ld2, 1.0f), 1.17549435e-38f);
+            const float coef = A.gamma * two_b * rcp_approx(den);
+            gx = Va * clampf(coef * dx, A.clip);
+            gy = Va * clampf(coef * dy, A.clip);
+        }
+    }
+    // 5. segmented sum over the K lanes of each node; lane i writes node i
+    for (int o = 1; o < K; o <<= 1) {
+        const float tx = __shfl_down_sync(kFull, gx, o);
+        const float ty = __shfl_down_sync(kFull, gy, o);
+        if (r + o < K && lane + o < 32) {
+            gx += tx;
+            gy += ty;
+        }
+    }
+    const int src = min(lane * K, 31);
+    gx = __shfl_sync(kFull, gx, src);
+    gy = __shfl_sync(kFull, gy, src);
+    if (lane < nodes) {
+        const int64_t an = a0 + lane;
+        const float2 ya = load_y<INPLACE>(y_in, an);
+        const float2 out = make_float2(fmaf(A.lr, gx, ya.x), fmaf(A.lr, gy, ya.y));
+        if (!isfinite(out.x) || !isfinite(out.y)) {
+            if (A.nonfinite) atomicMin(A.nonfinite, A.t);
+        }
+        y_out[an] = out;
+    }
+}
+
+template <bool INPLACE>
+void launch_sgather(unsigned grid, cudaStream_t st, const IterArgs &A, const SGArgs &G, int npw,
+                    bool clamp, const float2 *src, float2 *dst) {
+#define DRG_SG(BB, CC) sgather_kernel<INPLACE, BB, CC><<<grid, kWpb * 32, 0, st>>>(A, G, npw, src, dst)
+    switch (A.b) {
+        case 1: if (clamp) DRG_SG(1, true); else DRG_SG(1, false); break;
+        case 2: if (clamp) DRG_SG(2, true); else DRG_SG(2, false); break;
+        case 3: if (clamp) DRG_SG(3, true); else DRG_SG(3, false); break;
+        default: if (clamp) DRG_SG(0, true); else DRG_SG(0, false); break;
+    }
+#undef DRG_SG
+}
+
 template <bool INPLACE, int B>
 void launch_iter_b(unsigned grid, cudaStream_t st, const IterArgs &A, int npw, bool clamp,
                    bool partner, const float2 *src, float2 *dst) {
@@ -773,5 +895,69 @@ extern "C" int drg_alias_build(const double *weights, int64_t n, uint64_t *out_t
     DRG_CUDA(cudaMemcpyAsync(out_table, packed.data(), sizeof(uint64_t) * (size_t)n,
                              cudaMemcpyHostToDevice, st));
     DRG_CUDA(cudaStreamSynchronize(st));
+    return DRG_OK;
+}
+
+extern "C" int drg_layout_sgather(const int64_t *indptr, const uint64_t *rec,
+                                  const uint64_t *row_alias, const float *wsum, const float *V,
+                                  const uint64_t *alias, int64_t n, int64_t row_lo,
+                                  int64_t row_hi, float *y_in, float *y_out, int t0, int n_iter,
+                                  int iters, double lr0, double gamma, double eps, double clip,
+                                  int b, int M, int S, uint64_t seed, int level,
+                                  const int32_t *neg_idx, int32_t *nonfinite, unsigned flags,
+                                  void *stream) {
+    if (n <= 0 || n_iter < 0) return DRG_OK;
+    if (n >= 0x7fffffffLL) return fail(DRG_ERR_INVALID, "level exceeds 2^31 - 1 nodes");
+    if (row_lo < 0 || row_hi > n || row_lo > row_hi) return fail(DRG_ERR_INVALID, "bad row range");
+    if (b < 1 || M < 0 || S < 1 || S + M > 32 || iters < 1)
+        return fail(DRG_ERR_INVALID, "need b >= 1, S >= 1, S + M <= 32");
+    if (neg_idx && n_iter != 1) return fail(DRG_ERR_INVALID, "neg_idx needs n_iter == 1");
+    const bool inplace = (flags & DRG_FLAG_INPLACE) != 0;
+    if (inplace != (y_in == y_out)) return fail(DRG_ERR_INVALID, "buffer / flag mismatch");
+    if (n_iter > 1 && (row_lo != 0 || row_hi != n))
+        return fail(DRG_ERR_INVALID, "n_iter > 1 needs the full row range");
+    cudaStream_t st = as_stream(stream);
+    IterArgs A = {};
+    A.indptr = indptr;
+    A.rec = reinterpret_cast<const uint2 *>(rec);
+    A.V = V;
+    A.alias = reinterpret_cast<const uint2 *>(alias);
+    A.n = n;
+    A.row_lo = row_lo;
+    A.row_hi = row_hi;
+    A.gamma = (float)gamma;
+    A.eps = (float)eps;
+    A.clip = (float)clip;
+    A.b = b;
+    A.M = M;
+    A.key0 = (uint32_t)seed;
+    A.key1 = (uint32_t)(seed >> 32);
+    A.level = (uint32_t)level;
+    A.neg_idx = neg_idx;
+    A.nonfinite = nonfinite;
+    SGArgs G{reinterpret_cast<const uint2 *>(row_alias), wsum, S};
+    const int64_t rows = row_hi - row_lo;
+    if (rows == 0) return DRG_OK;
+    const int npw = std::max(1, 32 / (S + M));
+    const unsigned grid = (unsigned)ceil_div(ceil_div(rows, npw), kWpb);
+    const bool clamp = attractive_clip_active(b, clip);
+    float2 *src = reinterpret_cast<float2 *>(y_in);
+    float2 *dst = reinterpret_cast<float2 *>(y_out);
+    if (!inplace && n_iter > 1 && n_iter % 2 == 0) {
+        DRG_CUDA(cudaMemcpyAsync(dst, src, sizeof(float2) * (size_t)n, cudaMemcpyDeviceToDevice,
+                                 st));
+        std::swap(src, dst);
+    }
+    for (int j = 0; j < n_iter; ++j) {
+        A.t = t0 + j;
+        A.lr = (float)std::max(lr0 * (1.0 - (double)A.t / (double)iters), 0.0);
+        if (inplace) {
+            launch_sgather<true>(grid, st, A, G, npw, clamp, src, src);
+        } else {
+            launch_sgather<false>(grid, st, A, G, npw, clamp, src, dst);
+            std::swap(src, dst);
+        }
+        DRG_LAUNCHED("sgather_kernel");
+    }
     return DRG_OK;
 }

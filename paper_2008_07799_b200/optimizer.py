@@ -76,6 +76,7 @@ class OptimizerParams:
     update: str = "jacobi"
     shard_min_nodes: int = 65536
     sampled_concurrency: int = 16  # update="sampled": n_l / this many steps in flight
+    att_samples: int = 2           # update="sgather": attraction partners drawn per node
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
@@ -94,8 +95,11 @@ class OptimizerParams:
             raise ValueError("seed must be non-negative")
         if self.init not in ("normal", "uniform"):
             raise ValueError("init must be 'normal' or 'uniform'")
-        if self.update not in ("jacobi", "inplace", "sampled"):
-            raise ValueError("update must be 'jacobi', 'inplace' or 'sampled'")
+        if self.update not in ("jacobi", "inplace", "sampled", "sgather"):
+            raise ValueError("update must be 'jacobi', 'inplace', 'sampled' or 'sgather'")
+        if self.att_samples < 1 or self.att_samples + self.neg_samples > 32 and \
+                self.update == "sgather":
+            raise ValueError("sgather needs att_samples >= 1 and att_samples + neg_samples <= 32")
 
 
 @dataclass
@@ -255,6 +259,7 @@ class SampledTables:
     src_alias: torch.Tensor   # int64 [n]  Vose over R^l
     row_alias: torch.Tensor   # int64 [nnz] per-row Vose over P^l (threshold, alias target)
     collapse: torch.Tensor    # fp32 [n]   c_a
+    wsum: torch.Tensor        # fp32 [n]   sum_b W_ab = 2 n_l sum_b P^l_ab (sgather)
 
 
 def build_sampled_tables(ip, tg, P, R) -> SampledTables:
@@ -268,7 +273,8 @@ def build_sampled_tables(ip, tg, P, R) -> SampledTables:
     with torch.no_grad():
         c = torch.where(R > 0, 1.0 - rowsum[:n] / torch.clamp(R, min=1e-300),
                         torch.zeros_like(R)).clamp_(0.0, 1.0).to(torch.float32)
-    return SampledTables(src, rows[:nnz], c)
+        wsum = (2.0 * n * rowsum[:n]).to(torch.float32)
+    return SampledTables(src, rows[:nnz], c, wsum)
 
 
 def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float = 0.75,
@@ -351,6 +357,15 @@ class LayoutPlan:
         flags = _lib.DRG_FLAG_INPLACE if y_in.data_ptr() == y_out.data_ptr() else 0
         if self.nonfinite is None:
             self.nonfinite = torch.full((1,), _INT_MAX, dtype=torch.int32, device=y_in.device)
+        if o.update == "sgather" and L.sampled is not None:
+            S = L.sampled
+            _lib.call("drg_layout_sgather", _lib.ptr(L.indptr), _lib.ptr(L.rec),
+                      _lib.ptr(S.row_alias), _lib.ptr(S.wsum), _lib.ptr(L.V), _lib.ptr(L.alias),
+                      L.n, row_lo, row_hi, _lib.ptr(y_in), _lib.ptr(y_out), t0, n_iter, o.iters,
+                      float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
+                      o.neg_samples, o.att_samples, seed, level, _lib.ptr(neg_idx),
+                      _lib.ptr(self.nonfinite), flags, _lib.stream_ptr(stream))
+            return
         _lib.call("drg_layout_iters", _lib.ptr(L.indptr), _lib.ptr(L.rec), _lib.ptr(L.V),
                   _lib.ptr(L.alias), L.n, row_lo, row_hi, _lib.ptr(y_in), _lib.ptr(y_out),
                   t0, n_iter, o.iters, float(o.lr0), float(gamma), float(o.eps),
@@ -467,7 +482,8 @@ def device_radius(y: torch.Tensor) -> float:
 
 
 def build_plan(ds: DeviceSimilarity, dh: DeviceHierarchy, opt: OptimizerParams) -> LayoutPlan:
-    return LayoutPlan(build_level_data(ds, dh, opt.neg_power, opt.update == "sampled"),
+    return LayoutPlan(build_level_data(ds, dh, opt.neg_power,
+                                       opt.update in ("sampled", "sgather")),
                       list(dh.maps), opt)
 
 

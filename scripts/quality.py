@@ -81,7 +81,11 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
         for m in modes:
             t0 = time.perf_counter()
             upd, _, div = m.partition(":")
-            extra = {"sampled_concurrency": int(div)} if div else {}
+            extra = {}
+            if div and upd == "sampled":
+                extra = {"sampled_concurrency": int(div)}
+            elif div and upd == "sgather":
+                extra = {"att_samples": int(div)}
             lay = B.layout_graph(bg, B.SimilarityParams(k=cfg["k"], perplexity=cfg["perplexity"]),
                                  B.OptimizerParams(iters=cfg["iters"], seed=seed, update=upd,
                                                    init=cfg["init"], **extra),

@@ -631,3 +631,29 @@ def test_isolated_last_relabelling_keeps_the_reference_hierarchy():
     assert np.isfinite(lay.positions).all()
     iso = np.diff(g.indptr) == 0
     assert np.abs(lay.positions[iso]).max() < 1.0         # isolated nodes barely move
+
+
+def test_sgather_attraction_is_unbiased(golden):
+    """update="sgather": the sampled attraction (S partners ~ W_a., weight wsum/S)
+    averages to the full CSR gather of K7 (attraction only, M = 0)."""
+    g = golden_graph(golden, "r500")
+    prep = _prepared(as_gpu_graph(g), k=2, M=0)
+    from paper_2008_07799_b200.optimizer import build_plan
+    o_full = B.OptimizerParams(neg_samples=0, iters=10**6, seed=0)
+    o_sg = B.OptimizerParams(neg_samples=0, iters=10**6, seed=0, update="sgather", att_samples=2)
+    p_full = prep.plan
+    p_full.opt = o_full
+    p_sg = build_plan(prep.similarity, prep.hierarchy, o_sg)
+    L = p_full.levels[0]
+    y = torch.randn(L.n, 2, device="cuda")
+    out = torch.empty_like(y)
+    p_full.kernel_step(0, y, out, 0, L.n, 0, 1)
+    want = (out - y).double()
+    acc = torch.zeros_like(want)
+    T = 4000
+    for t in range(T):
+        p_sg.kernel_step(0, y, out, 0, L.n, t, 1)
+        acc += (out - y).double()
+    got = acc / T
+    rel = float((got - want).norm() / want.norm())
+    assert rel < 0.05, rel
