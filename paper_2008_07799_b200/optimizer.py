@@ -75,7 +75,8 @@ class OptimizerParams:
     init: str = "normal"
     update: str = "jacobi"
     shard_min_nodes: int = 65536
-    sampled_concurrency: int = 16  # update="sampled": n_l / this many steps in flight
+    sampled_concurrency: int = 16  # update="sampled": n_0 / this many steps in flight (level 0)
+    sampled_concurrency_coarse: int = 4   # ... and n_l / this many on coarser levels
     att_samples: int = 2           # update="sgather": attraction partners drawn per node
 
     def __post_init__(self) -> None:
@@ -424,7 +425,9 @@ class LayoutPlan:
                   _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), _lib.ptr(S.collapse),
                   _lib.ptr(L.alias), L.n, _lib.ptr(y), L.n, t0, n_iter, o.iters, float(o.lr0),
                   float(gamma), float(o.eps), float(o.grad_clip), o.b, o.neg_samples, seed,
-                  level, max(256, L.n // max(1, o.sampled_concurrency)), _lib.stream_ptr())
+                  level, max(256, L.n // max(1, o.sampled_concurrency if level == 0
+                                             else o.sampled_concurrency_coarse)),
+                  _lib.stream_ptr())
         if not bool(torch.isfinite(y).all()):
             raise FloatingPointError(f"non-finite coordinate in epochs {t0}..{t0 + n_iter - 1} "
                                      f"at level {level}")
