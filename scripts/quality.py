@@ -54,7 +54,8 @@ def init_for(cfg, n, seed):
     return rng.normal(0.0, 1e-4, size=(n, 2)).astype(np.float32).astype(np.float64)
 
 
-def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evaluator="gpu"):
+def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evaluator="gpu",
+         seed0=0):
     import paper_2008_07799_b200 as B
     from paper_2008_07799_b200 import quality as Q
     cfg = CONFIGS[name]
@@ -68,7 +69,7 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
         sample = np.random.default_rng(7).choice(og.node_count, cfg["np_sample"], replace=False)
     results = {"reference": [], **{m: [] for m in modes}}
     threads = os.cpu_count() if og.node_count > 50_000 else 1
-    for seed in range(n_seeds):
+    for seed in range(seed0, seed0 + n_seeds):
         h = O.build_hierarchy(og, 0.8, 16, O.derive_seed(seed, O.HIERARCHY_TAG),
                               max_levels=cfg["max_levels"])
         y0 = init_for(cfg, h.levels[-1].node_count, seed)
@@ -105,11 +106,16 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
         line = {"workload": name, "impl": key, "seeds": len(rs),
                 "kl_median": statistics.median(kls), "kl_min": min(kls), "kl_max": max(kls),
                 "np_median": statistics.median(nps), "np_min": min(nps), "np_max": max(nps),
+                "kl_mean": statistics.fmean(kls), "np_mean": statistics.fmean(nps),
+                "kl_sem": statistics.stdev(kls) / len(kls) ** 0.5 if len(kls) > 1 else None,
+                "np_sem": statistics.stdev(nps) / len(nps) ** 0.5 if len(nps) > 1 else None,
                 "seconds_median": statistics.median(r["s"] for r in rs)}
         if key != "reference":
             ref = results["reference"]
             line["kl_rel_vs_ref"] = line["kl_median"] / statistics.median(r["kl"] for r in ref) - 1
             line["np_rel_vs_ref"] = line["np_median"] / statistics.median(r["np"] for r in ref) - 1
+            line["kl_mean_rel_vs_ref"] = line["kl_mean"] / statistics.fmean(r["kl"] for r in ref) - 1
+            line["np_mean_rel_vs_ref"] = line["np_mean"] / statistics.fmean(r["np"] for r in ref) - 1
         print(json.dumps(line), flush=True)
 
 
@@ -117,4 +123,4 @@ if __name__ == "__main__":
     a = sys.argv[1:]
     main(a[0] if a else "grid", int(a[1]) if len(a) > 1 else 10,
          tuple(a[2].split(",")) if len(a) > 2 else ("jacobi", "inplace", "sampled"),
-         a[3] if len(a) > 3 else "gpu")
+         a[3] if len(a) > 3 else "gpu", int(a[4]) if len(a) > 4 else 0)
