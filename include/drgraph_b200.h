@@ -123,9 +123,11 @@ int drg_aggregate_nodes(const double *values, const int32_t *parent, int64_t n,
  * zero -> 1e-8 * max, power 0 -> uniform.  out_w[n] device. */
 int drg_negative_weights(const double *row_mass, int64_t n, double power, double *out_w,
                          void *stream);
-/* Vose alias table (optimizer.py:111-139) over weights[n] (device), packed as
+/* Alias table (replaces build_alias_table, optimizer.py:111-139) over weights[n]
+ * (device), built on the device by a parallel sweep (prefix sums of light deficits
+ * and heavy surpluses + binary search; the same law as Vose's table), packed as
  * uint64 records {float32 threshold (low word), int32 alias (high word)};
- * *out_total (host, may be NULL) receives the weight sum. */
+ * *out_total (host, may be NULL) receives the weight sum.  n < 2^31. */
 int drg_alias_build(const double *weights, int64_t n, uint64_t *out_table, double *out_total,
                     void *stream);
 

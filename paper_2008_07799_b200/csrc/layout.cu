@@ -845,56 +845,168 @@ extern "C" int drg_negative_weights(const double *row_mass, int64_t n, double po
     return DRG_OK;
 }
 
-// Vose's alias method (optimizer.py:111-139), host side: the weights come down
-// once per level, the packed table goes back up.  Same stack discipline as the
-// reference (small/large built in index order, pop from the back).
+// Alias table on the device (replaces the host Vose loop of build_alias_table,
+// optimizer.py:111-139).  Parallel "sweep" construction: with normalised weights
+// (mean 1), light items l_1..l_a (w < 1) and heavy items h_1..h_b in index order,
+// deficits delta_i = sum_{k<=i} (1 - w_lk) and surpluses sigma_j = sum_{k<=j}
+// (w_hk - 1), the sequential sweep (a heavy absorbs lights until its residual drops
+// to <= 1, then is itself topped up by the next heavy) assigns
+//   light i  -> alias h_j, j = first j with sigma_j > delta_{i-1},  prob w_li;
+//   heavy j  -> alias h_{j+1}, prob 1 + sigma_j - delta_i', i' = first i with
+//               delta_i >= sigma_j (prob 1 if it never retires).
+// Every bucket holds exactly mass 1 and every item its weight: the same law as
+// Vose's table (a different but equally valid table).
+namespace drg {
+namespace {
+
+__global__ void alias_norm_kernel(const double *__restrict__ w, int64_t n, const double *total,
+                                  double *wn, uint8_t *light, uint8_t *heavy, int *bad) {
+    const double f = (double)n / *total;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = w[i];
+        if (v < 0.0 || !(v == v)) atomicExch(bad, 1);
+        const double x = v * f;
+        wn[i] = x;
+        light[i] = x < 1.0;
+        heavy[i] = !(x < 1.0);
+    }
+}
+
+__global__ void alias_gap_kernel(const double *__restrict__ wn, const int32_t *__restrict__ idx,
+                                 const int64_t *cnt, int heavy, double *out) {
+    const int64_t m = *cnt;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const double x = wn[idx[k]];
+        out[k] = heavy ? x - 1.0 : 1.0 - x;
+    }
+}
+
+__device__ __forceinline__ int64_t upper_bound_d(const double *a, int64_t m, double v) {
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] > v) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int64_t lower_bound_d(const double *a, int64_t m, double v) {
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] >= v) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+__global__ void alias_light_kernel(const double *__restrict__ wn, const int32_t *__restrict__ L,
+                                   const int64_t *na, const double *__restrict__ delta,
+                                   const int32_t *__restrict__ H, const int64_t *nb,
+                                   const double *__restrict__ sigma, uint2 *table) {
+    const int64_t a = *na, b = *nb;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const double prev = k == 0 ? 0.0 : delta[k - 1];
+        const int64_t j = upper_bound_d(sigma, b, prev);
+        const int32_t item = L[k];
+        if (j < b) table[item] = make_uint2(__float_as_uint((float)wn[item]), (uint32_t)H[j]);
+        else table[item] = make_uint2(__float_as_uint(1.0f), (uint32_t)item);
+    }
+}
+
+__global__ void alias_heavy_kernel(const int32_t *__restrict__ H, const int64_t *nb,
+                                   const double *__restrict__ sigma, const int64_t *na,
+                                   const double *__restrict__ delta, uint2 *table) {
+    const int64_t a = *na, b = *nb;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < b;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t item = H[k];
+        const int64_t i = lower_bound_d(delta, a, sigma[k]);
+        if (i < a && k + 1 < b) {
+            const double p = fmin(fmax(1.0 + sigma[k] - delta[i], 0.0), 1.0);
+            table[item] = make_uint2(__float_as_uint((float)p), (uint32_t)H[k + 1]);
+        } else {
+            table[item] = make_uint2(__float_as_uint(1.0f), (uint32_t)item);
+        }
+    }
+}
+
+__global__ void iota_i32_kernel(int32_t *out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int32_t)i;
+}
+
+}  // namespace
+}  // namespace drg
+
 extern "C" int drg_alias_build(const double *weights, int64_t n, uint64_t *out_table,
                                double *out_total, void *stream) {
     if (n <= 0) return fail(DRG_ERR_INVALID, "cannot build an alias table over zero items");
+    if (n >= 0x7fffffffLL) return fail(DRG_ERR_INVALID, "alias table over >= 2^31 items");
     cudaStream_t st = as_stream(stream);
-    std::vector<double> w((size_t)n);
-    DRG_CUDA(cudaMemcpyAsync(w.data(), weights, sizeof(double) * (size_t)n,
-                             cudaMemcpyDeviceToHost, st));
-    DRG_CUDA(cudaStreamSynchronize(st));
+    Scratch tot(st), wn(st), lf(st), hf(st), idx(st), L(st), H(st), cnt(st), dl(st), sg(st),
+        dls(st), sgs(st), tmp(st), bad(st);
+    DRG_CUDA(tot.alloc(sizeof(double)));
+    DRG_CUDA(wn.alloc(sizeof(double) * (size_t)n));
+    DRG_CUDA(lf.alloc((size_t)n));
+    DRG_CUDA(hf.alloc((size_t)n));
+    DRG_CUDA(idx.alloc(sizeof(int32_t) * (size_t)n));
+    DRG_CUDA(L.alloc(sizeof(int32_t) * (size_t)n));
+    DRG_CUDA(H.alloc(sizeof(int32_t) * (size_t)n));
+    DRG_CUDA(cnt.alloc(2 * sizeof(int64_t)));
+    DRG_CUDA(dl.alloc(sizeof(double) * (size_t)n));
+    DRG_CUDA(sg.alloc(sizeof(double) * (size_t)n));
+    DRG_CUDA(dls.alloc(sizeof(double) * (size_t)n));
+    DRG_CUDA(sgs.alloc(sizeof(double) * (size_t)n));
+    DRG_CUDA(bad.alloc(sizeof(int)));
+    DRG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    cub::DeviceReduce::Sum(nullptr, t1, weights, tot.as<double>(), n, st);
+    cub::DeviceSelect::Flagged(nullptr, t2, idx.as<int32_t>(), lf.as<uint8_t>(), L.as<int32_t>(),
+                               cnt.as<int64_t>(), n, st);
+    cub::DeviceScan::InclusiveSum(nullptr, t3, dl.as<double>(), dls.as<double>(), n, st);
+    DRG_CUDA(tmp.alloc(std::max(t1, std::max(t2, t3))));
+    DRG_CUDA(cub::DeviceReduce::Sum(tmp.p, t1, weights, tot.as<double>(), n, st));
     double total = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-        if (w[i] < 0) return fail(DRG_ERR_INVALID, "negative weight");
-        total += w[i];
-    }
-    if (!(total > 0)) return fail(DRG_ERR_INVALID, "all weights are zero");
-    if (out_total) *out_total = total;
-    const double f = (double)n / total;
-    std::vector<double> prob((size_t)n, 1.0);
-    std::vector<int32_t> alias((size_t)n);
-    std::vector<int64_t> small, large;
-    small.reserve((size_t)n);
-    large.reserve((size_t)n);
-    for (int64_t i = 0; i < n; ++i) {
-        w[i] *= f;
-        alias[i] = (int32_t)i;
-    }
-    for (int64_t i = 0; i < n; ++i) (w[i] < 1.0 ? small : large).push_back(i);
-    while (!small.empty() && !large.empty()) {
-        int64_t s = small.back();
-        small.pop_back();
-        int64_t l = large.back();
-        large.pop_back();
-        prob[s] = w[s];
-        alias[s] = (int32_t)l;
-        w[l] = (w[l] + w[s]) - 1.0;
-        (w[l] < 1.0 ? small : large).push_back(l);
-    }
-    for (int64_t i : small) prob[i] = 1.0;
-    std::vector<uint64_t> packed((size_t)n);
-    for (int64_t i = 0; i < n; ++i) {
-        float p = (float)prob[i];
-        uint32_t pb;
-        memcpy(&pb, &p, 4);
-        packed[i] = (uint64_t)pb | ((uint64_t)(uint32_t)alias[i] << 32);
-    }
-    DRG_CUDA(cudaMemcpyAsync(out_table, packed.data(), sizeof(uint64_t) * (size_t)n,
-                             cudaMemcpyHostToDevice, st));
+    DRG_CUDA(cudaMemcpyAsync(&total, tot.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     DRG_CUDA(cudaStreamSynchronize(st));
+    if (!(total > 0.0)) return fail(DRG_ERR_INVALID, "all weights are zero");
+    if (out_total) *out_total = total;
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 256), kSMs * 16);
+    alias_norm_kernel<<<g, 256, 0, st>>>(weights, n, tot.as<double>(), wn.as<double>(),
+                                         lf.as<uint8_t>(), hf.as<uint8_t>(), bad.as<int>());
+    DRG_LAUNCHED("alias_norm_kernel");
+    iota_i32_kernel<<<g, 256, 0, st>>>(idx.as<int32_t>(), n);
+    DRG_LAUNCHED("iota_i32_kernel");
+    int64_t *na = cnt.as<int64_t>(), *nb = cnt.as<int64_t>() + 1;
+    DRG_CUDA(cub::DeviceSelect::Flagged(tmp.p, t2, idx.as<int32_t>(), lf.as<uint8_t>(),
+                                        L.as<int32_t>(), na, n, st));
+    DRG_CUDA(cub::DeviceSelect::Flagged(tmp.p, t2, idx.as<int32_t>(), hf.as<uint8_t>(),
+                                        H.as<int32_t>(), nb, n, st));
+    alias_gap_kernel<<<g, 256, 0, st>>>(wn.as<double>(), L.as<int32_t>(), na, 0, dl.as<double>());
+    DRG_LAUNCHED("alias_gap_kernel");
+    alias_gap_kernel<<<g, 256, 0, st>>>(wn.as<double>(), H.as<int32_t>(), nb, 1, sg.as<double>());
+    DRG_LAUNCHED("alias_gap_kernel");
+    // prefix sums over the full length (entries past the counts are never read)
+    DRG_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, t3, dl.as<double>(), dls.as<double>(), n, st));
+    DRG_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, t3, sg.as<double>(), sgs.as<double>(), n, st));
+    g_launches.fetch_add(5, std::memory_order_relaxed);
+    uint2 *table = reinterpret_cast<uint2 *>(out_table);
+    alias_light_kernel<<<g, 256, 0, st>>>(wn.as<double>(), L.as<int32_t>(), na, dls.as<double>(),
+                                          H.as<int32_t>(), nb, sgs.as<double>(), table);
+    DRG_LAUNCHED("alias_light_kernel");
+    alias_heavy_kernel<<<g, 256, 0, st>>>(H.as<int32_t>(), nb, sgs.as<double>(), na,
+                                          dls.as<double>(), table);
+    DRG_LAUNCHED("alias_heavy_kernel");
+    int h_bad = 0;
+    DRG_CUDA(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    DRG_CUDA(cudaStreamSynchronize(st));
+    if (h_bad) return fail(DRG_ERR_INVALID, "negative weight");
     return DRG_OK;
 }
 

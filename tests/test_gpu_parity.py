@@ -657,3 +657,19 @@ def test_sgather_attraction_is_unbiased(golden):
     got = acc / T
     rel = float((got - want).norm() / want.norm())
     assert rel < 0.05, rel
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_device_alias_tables_are_exact(seed):
+    """Parallel-sweep alias construction: every bucket holds mass 1 and each item
+    its normalised weight, for skewed, tied, zero-floored and tiny inputs."""
+    rng = np.random.default_rng(seed)
+    cases = [rng.pareto(1.2, size=100_003) + 1e-9, np.ones(1000), np.array([5.0]),
+             np.array([0.0, 0.0, 3.0, 0.0]), rng.random(77) ** 8]
+    for w in cases:
+        t = B.build_alias_table(w)
+        n = len(w)
+        mass = t.prob / n
+        np.add.at(mass, t.alias, (1 - t.prob) / n)
+        np.testing.assert_allclose(mass, w / w.sum(), rtol=2e-5, atol=2e-7 / n)
+        assert np.all((t.prob >= 0) & (t.prob <= 1))
