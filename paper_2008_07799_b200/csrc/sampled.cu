@@ -31,6 +31,7 @@ struct SArgs {
     const float *collapse;   // probability that the drawn pair collapses into the source
     const uint2 *neg_alias;  // Vose over Q^l
     int64_t n;
+    int64_t step_lo;
     int64_t n_steps;
     float lr, gamma, eps, clip;
     int b, M;
@@ -72,8 +73,9 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const float two_b = 2.0f * (float)A.b;
     const int Me = min(A.M, kMaxNeg);
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < A.n_steps;
-         s += nthreads) {
+    for (int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sl < A.n_steps;
+         sl += nthreads) {
+        const int64_t s = A.step_lo + sl;
         const uint32_t c1 = (uint32_t)(s >> 32) ^ ((uint32_t)A.t << 1);
         // ---- all first-attempt draws, table loads in flight together
         const u32x4 r = philox4x32(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xff00u, 0x5a3d1e55u},
@@ -232,7 +234,8 @@ extern "C" int drg_row_alias(const int64_t *indptr, const int32_t *targets, cons
 extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                                   const uint64_t *row_alias, const uint64_t *src_alias,
                                   const float *collapse, const uint64_t *neg_alias, int64_t n,
-                                  float *y, int64_t n_steps, int t0, int n_iter, int iters,
+                                  float *y, int64_t step_lo, int64_t n_steps, int t0, int n_iter,
+                                  int iters,
                                   double lr0, double gamma, double eps, double clip, int b, int M,
                                   uint64_t seed, int level, int64_t max_threads, void *stream) {
     if (n <= 0 || n_steps < 0 || n_iter < 0) return DRG_OK;
@@ -247,6 +250,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     A.collapse = collapse;
     A.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
     A.n = n;
+    A.step_lo = step_lo;
     A.n_steps = n_steps;
     A.gamma = (float)gamma;
     A.eps = (float)eps;

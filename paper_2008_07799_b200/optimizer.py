@@ -395,7 +395,8 @@ class LayoutPlan:
             import torch.distributed as dist
             world = dist.get_world_size(group)
         if self.opt.update == "sampled":
-            return self._run_level_sampled(level, y, t0, n_iter)
+            return self._run_level_sampled(level, y, t0, n_iter, group if world > 1 else None,
+                                           step_fn)
         inplace = self.opt.update == "inplace"
         if world > 1 and L.n >= self.opt.shard_min_nodes:
             return self._run_level_sharded(level, y, t0, n_iter, group, step_fn)
@@ -414,20 +415,48 @@ class LayoutPlan:
         self.kernel_step(level, y, out, 0, L.n, t0, n_iter)
         return out
 
-    def _run_level_sampled(self, level, y, t0, n_iter):
-        """Reference-faithful epochs: n_l sampled steps each, Hogwild on y."""
+    def sampled_steps(self, level: int, y: torch.Tensor, step_lo: int, n_steps: int, t0: int,
+                      n_iter: int = 1) -> None:
+        """drg_layout_sampled: steps [step_lo, step_lo + n_steps) of epochs t0.. in place."""
         L, gamma, seed = self._level_args(level)
         S = L.sampled
         if S is None:
             raise RuntimeError("plan was built without sampled-mode tables")
         o = self.opt
+        div = o.sampled_concurrency if level == 0 else o.sampled_concurrency_coarse
         _lib.call("drg_layout_sampled", _lib.ptr(L.indptr), _lib.ptr(L.rec),
                   _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), _lib.ptr(S.collapse),
-                  _lib.ptr(L.alias), L.n, _lib.ptr(y), L.n, t0, n_iter, o.iters, float(o.lr0),
-                  float(gamma), float(o.eps), float(o.grad_clip), o.b, o.neg_samples, seed,
-                  level, max(256, L.n // max(1, o.sampled_concurrency if level == 0
-                                             else o.sampled_concurrency_coarse)),
-                  _lib.stream_ptr())
+                  _lib.ptr(L.alias), L.n, _lib.ptr(y), step_lo, n_steps, t0, n_iter, o.iters,
+                  float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
+                  o.neg_samples, seed, level, max(256, L.n // max(1, div)), _lib.stream_ptr())
+
+    def _run_level_sampled(self, level, y, t0, n_iter, group=None, step_fn=None):
+        """Reference-faithful epochs: n_l sampled steps each, Hogwild on y.  With a
+        process group the epoch's steps are split across ranks, each applies its
+        share to its replica, and the per-rank displacements are summed with one
+        all-reduce per epoch (Hogwild with a per-epoch exchange)."""
+        L = self.levels[level]
+        if group is None:
+            if step_fn is not None:
+                for j in range(n_iter):
+                    step_fn(y, 0, L.n, t0 + j)
+            else:
+                self.sampled_steps(level, y, 0, L.n, t0, n_iter)
+        else:
+            import torch.distributed as dist
+            world = dist.get_world_size(group)
+            rank = dist.get_rank(group)
+            chunk = -(-L.n // world)
+            lo, hi = min(rank * chunk, L.n), min(rank * chunk + chunk, L.n)
+            for j in range(n_iter):
+                base = y.clone()
+                if step_fn is not None:
+                    step_fn(y, lo, hi, t0 + j)
+                elif hi > lo:
+                    self.sampled_steps(level, y, lo, hi - lo, t0 + j, 1)
+                y.sub_(base)
+                dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
+                y.add_(base)
         if not bool(torch.isfinite(y).all()):
             raise FloatingPointError(f"non-finite coordinate in epochs {t0}..{t0 + n_iter - 1} "
                                      f"at level {level}")

@@ -105,3 +105,46 @@ def test_partition_covers_rows():
                 lo, hi = r * chunk, min(r * chunk + chunk, n)
                 owned[lo:hi] += 1
             assert (owned == 1).all()
+
+
+def _sampled_step(n):
+    def step(y, lo, hi, t):
+        for s in range(lo, hi):
+            r = np.random.default_rng(t * 100_003 + s)
+            i, c = r.integers(0, n, size=2)
+            y[i] += 0.05 * (y[c] - y[i])
+    return step
+
+
+def _sampled_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 97
+    plan = _plan(n, 5, "sampled")
+    y0 = torch.from_numpy(np.random.default_rng(3).normal(size=(n, 2)).astype(np.float32))
+    y = plan.run_level(0, y0.clone(), group=dist.group.WORLD, step_fn=_sampled_step(n))
+    if rank == 0:
+        np.save(out_path, y.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sampled_mode_epoch_exchange(tmp_path):
+    """update="sampled" on 2 ranks: each rank runs its share of the epoch's steps on
+    its replica; displacements are summed by one all-reduce per epoch."""
+    out = str(tmp_path / "ys.npy")
+    mp.spawn(_sampled_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    n, world = 97, 2
+    step = _sampled_step(n)
+    y = torch.from_numpy(np.random.default_rng(3).normal(size=(n, 2)).astype(np.float32))
+    chunk = -(-n // world)
+    for t in range(5):
+        base = y.clone()
+        delta = torch.zeros_like(y)
+        for r in range(world):
+            yr = base.clone()
+            step(yr, r * chunk, min(n, r * chunk + chunk), t)
+            delta += yr - base
+        y = base + delta
+    assert np.array_equal(got, y.numpy())
