@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
             j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)tj : (int64_t)rrec.y;
         }
         float2 yi = ld_y(y, i);
+        const float2 yi0 = yi;
         if (i != j) {  // _kernels.py:82-105
             const float2 yj = ld_y(y, j);
             const float dx = yi.x - yj.x, dy = yi.y - yj.y;
@@ -118,7 +119,6 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
                 const float coef = -two_b * pw / (1.0f + pw * ld2);
                 const float gx = A.lr * clampf(coef * dx, A.clip);
                 const float gy = A.lr * clampf(coef * dy, A.clip);
-                add_y(y, i, gx, gy);
                 add_y(y, j, -gx, -gy);
                 yi.x += gx;
                 yi.y += gy;
@@ -160,12 +160,14 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
                 const float coef = A.gamma * two_b / ((ld2 + A.eps) * (1.0f + pw * ld2));
                 const float gx = A.lr * clampf(coef * dx, A.clip);
                 const float gy = A.lr * clampf(coef * dy, A.clip);
-                add_y(y, i, gx, gy);
                 add_y(y, target, -gx, -gy);
                 yi.x += gx;
                 yi.y += gy;
             }
         }
+        // the source's own increments of the step, published once (the step sees
+        // them locally in sequence, as the reference kernel does)
+        if (yi.x != yi0.x || yi.y != yi0.y) add_y(y, i, yi.x - yi0.x, yi.y - yi0.y);
     }
 }
 
