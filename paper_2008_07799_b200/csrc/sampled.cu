@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
             j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)tj : (int64_t)rrec.y;
         }
         float2 yi = ld_y(y, i);
-        const float2 yi0 = yi;
+        float gix = 0.f, giy = 0.f;   // the source's own increments of this step
         if (i != j) {  // _kernels.py:82-105
             const float2 yj = ld_y(y, j);
             const float dx = yi.x - yj.x, dy = yi.y - yj.y;
@@ -122,6 +122,8 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
                 add_y(y, j, -gx, -gy);
                 yi.x += gx;
                 yi.y += gy;
+                gix += gx;
+                giy += gy;
             }
         }
         for (int m = 0; m < A.M; ++m) {  // _kernels.py:106-140
@@ -163,11 +165,13 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
                 add_y(y, target, -gx, -gy);
                 yi.x += gx;
                 yi.y += gy;
+                gix += gx;
+                giy += gy;
             }
         }
         // the source's own increments of the step, published once (the step sees
         // them locally in sequence, as the reference kernel does)
-        if (yi.x != yi0.x || yi.y != yi0.y) add_y(y, i, yi.x - yi0.x, yi.y - yi0.y);
+        if (gix != 0.f || giy != 0.f) add_y(y, i, gix, giy);
     }
 }
 
