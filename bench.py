@@ -73,7 +73,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the other update modes")
-    ap.add_argument("--update", default="jacobi",
+    ap.add_argument("--update", default="sampled",
                     choices=["jacobi", "inplace", "sampled", "sgather"])
     ap.add_argument("--sampled-concurrency", type=int, default=16)
     return ap.parse_args()
@@ -155,7 +155,7 @@ def build_workload(name):
     return getattr(synthetic, fn)(*args)
 
 
-def params_for(name, iters_override=None, update="jacobi", concurrency=16):
+def params_for(name, iters_override=None, update="sampled", concurrency=16):
     import paper_2008_07799_b200 as B
     w = WORKLOADS[name]
     sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"], neighbor_cap=w.get("cap"))
@@ -334,6 +334,8 @@ def run_ours(args):
     value = iters * args.steps / (total_ms / 1e3)
     inter = plan.interactions() * args.steps / (total_ms / 1e3)
 
+    peak, peak_kind = measured_peaks()
+    T = opt.iters
     # the other update modes on the same prepared level data (same graph, P,
     # hierarchy): device-resident iters/s, for comparison in the same JSON line
     alt = {}
@@ -348,34 +350,39 @@ def run_ours(args):
                   else LayoutPlan(plan.levels, plan.maps, o2))
             p2.run()
             torch.cuda.synchronize()
-            ms = []
+            ms, l0 = [], []
             for _ in range(max(1, min(args.steps, 2))):
                 flush.zero_()
                 torch.cuda.synchronize()
                 s0, e0 = (torch.cuda.Event(enable_timing=True),
                           torch.cuda.Event(enable_timing=True))
                 s0.record()
-                p2.run()
+                p2.run(on_level=on_level)
                 e0.record()
                 torch.cuda.synchronize()
                 ms.append(s0.elapsed_time(e0))
+                l0.append(lvl_events[(0, "start")].elapsed_time(lvl_events[(0, "end")]))
+            k2, b2 = p2.launch_bytes(0)
+            us = sum(l0) / len(l0) / T * 1e3
             alt[mode] = {"value": iters / (sum(ms) / len(ms) / 1e3), "unit": UNIT,
-                         "ms_per_step": sum(ms) / len(ms)}
+                         "ms_per_step": sum(ms) / len(ms),
+                         "roofline": {"kernel": f"{k2} (level 0)", "launch_us": us,
+                                      "alg_bytes_per_launch": b2,
+                                      "achieved": b2 / us / 1e3,
+                                      "frac": b2 / us / 1e3 / peak}}
             del p2
 
-    # roofline of the dominant kernel: K7 at level 0
-    peak, peak_kind = measured_peaks()
-    T = opt.iters
+    # roofline of the dominant kernel: the level-0 iteration kernel
     l0_launch_s = (l0_total / args.steps / T) / 1e3
-    alg_bytes = L0.algorithmic_bytes(opt.neg_samples)
+    kname, alg_bytes = plan.launch_bytes(0)
     if group is not None:
-        alg_bytes = alg_bytes // world   # rows per rank
+        alg_bytes = alg_bytes // world   # rows / steps per rank
     achieved = alg_bytes / l0_launch_s / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "kernel": "layout_iter_kernel (level 0)",
+                "frac": achieved / peak, "traffic": None, "kernel": f"{kname} (level 0)",
                 "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes,
                 "launch_us": l0_launch_s * 1e6}
-    prof = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
+    prof = os.path.join(ROOT, "profiles", f"traffic_{name}_{opt.update}.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:

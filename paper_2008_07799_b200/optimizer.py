@@ -53,10 +53,17 @@ def _derive_seed(seed: int, *tags: int) -> int:
 class OptimizerParams:
     """optimizer.py:37-74 (same fields, defaults and validation) plus B200
     extensions: ``init`` ("normal" = reference N(0, init_scale); "uniform" =
-    U[-init_scale, init_scale], BASELINE config C1), ``update`` ("jacobi" =
-    deterministic double buffer; "inplace" = Hogwild-style in-place gather, closer
-    to the reference's sequential order; "sampled" = the reference's own sampled
-    steps, Hogwild with atomics), ``shard_min_nodes`` (multi-GPU).
+    U[-init_scale, init_scale], BASELINE config C1) and ``update``:
+
+    * "sampled" (default): the reference's own step (_kernels.py:65-140) run
+      Hogwild-style on the GPU -- KL/NP parity with the reference, fastest on one
+      GPU; run-to-run nondeterministic like the reference's threads > 1 mode.
+    * "jacobi": the node-parallel expected-gradient iteration (SURVEY §8(a) A12,
+      CSR gather + M negatives per node) -- bitwise deterministic and node-range
+      shardable across GPUs; matches KL, lower NP on multilevel RGG.
+    * "inplace": the gather with in-place (Hogwild) updates.
+    * "sgather": the gather with S sampled attraction partners (fast, lower NP).
+
     ``threads`` is accepted and ignored (the GPU replaces the Hogwild threads)."""
 
     neg_samples: int = 5
@@ -73,7 +80,7 @@ class OptimizerParams:
     seed: int = 0
     threads: int = 1
     init: str = "normal"
-    update: str = "jacobi"
+    update: str = "sampled"
     shard_min_nodes: int = 65536
     sampled_concurrency: int = 16  # update="sampled": n_0 / this many steps in flight (level 0)
     sampled_concurrency_coarse: int = 4   # ... and n_l / this many on coarser levels
@@ -325,6 +332,23 @@ class LayoutPlan:
 
     def iterations(self) -> int:
         return self.opt.iters * len(self.levels)
+
+    def launch_bytes(self, level: int = 0) -> tuple[str, int]:
+        """(kernel, algorithmic bytes of one iteration launch) at ``level`` for the
+        plan's update mode (the gather's 16 B per P entry + (24 + 16 M)
+        B per node of SURVEY §8(d); the sampled step's 92 + 32 M B: source alias 8,
+        row bounds 16, collapse 4, row alias 8, target record 8, y_i and y_j 16, per
+        negative alias 8 + y_c 8, and 16 B per float2 atomic on j, each negative and
+        the source)."""
+        L = self.levels[level]
+        M = self.opt.neg_samples
+        u = self.opt.update
+        if u == "sampled":
+            return "sampled_kernel", L.n * (92 + 32 * M)
+        if u == "sgather":
+            S = self.opt.att_samples
+            return "sgather_kernel", L.n * (32 + 24 * S + 16 * M)
+        return "layout_iter_kernel", L.algorithmic_bytes(M)
 
     def interactions(self) -> int:
         """(P entries + M negatives) updated over the whole layout stage."""

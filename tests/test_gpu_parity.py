@@ -322,11 +322,15 @@ def test_sampled_negatives_follow_q(golden):
 
 # ------------------------------------------------------------------ whole layouts
 def test_layout_graph_deterministic_and_stats(golden):
+    """update="jacobi" is bitwise deterministic (acceptance 8's contract); the
+    default sampled mode is Hogwild (like the reference with threads > 1)."""
     g = as_gpu_graph(golden_graph(golden, "r500"))
-    p = B.OptimizerParams(seed=5, iters=30)
+    p = B.OptimizerParams(seed=5, iters=30, update="jacobi")
     a = B.layout_graph(g, opt_params=p)
     b_ = B.layout_graph(g, opt_params=p)
     assert np.array_equal(a.positions, b_.positions)
+    d = B.layout_graph(g, opt_params=B.OptimizerParams(seed=5, iters=30))
+    assert np.isfinite(d.positions).all() and d.stats["levels"] == a.stats["levels"]
     assert a.positions.shape == (500, 2) and np.isfinite(a.positions).all()
     st = a.stats
     for key in ("components", "levels", "similarity_nbytes", "hierarchy_nbytes",
@@ -334,7 +338,7 @@ def test_layout_graph_deterministic_and_stats(golden):
         assert key in st
     assert st["gradient_steps"] == 30 * sum(st["levels"])
     assert st["distance_evals"] <= st["gradient_steps"] * 6
-    c = B.layout_graph(g, opt_params=B.OptimizerParams(seed=6, iters=30))
+    c = B.layout_graph(g, opt_params=B.OptimizerParams(seed=6, iters=30, update="jacobi"))
     assert not np.array_equal(a.positions, c.positions)
 
 
