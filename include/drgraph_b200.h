@@ -192,14 +192,16 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * records); clipped attraction on both ends if i != j; M negatives ~ neg_alias
  * (Q^l) redrawn (<= 9) while they hit i or j, both ends moved (float2 atomics).
  * Steps step_lo .. step_lo + n_steps - 1 of each epoch run here (a rank's share of
- * the epoch in the multi-GPU mode); at most max_threads steps run concurrently. */
+ * the epoch in the multi-GPU mode); at most max_threads steps run concurrently.
+ * aggregate != 0 combines the updates of a warp's lanes that hit the same node
+ * before the atomic (hub-heavy levels). */
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,
                        const uint64_t *src_alias, const float *collapse,
                        const uint64_t *neg_alias, int64_t n, float *y, int64_t step_lo,
                        int64_t n_steps, int t0,
                        int n_iter, int iters, double lr0, double gamma, double eps, double clip,
                        int b, int M, uint64_t seed, int level, int64_t max_threads,
-                       void *stream);
+                       int aggregate, void *stream);
 
 /* Stochastic gather (update = "sgather"): drg_layout_iters with the attraction
  * SAMPLED -- every node draws S partners b ~ W_a. from its row's alias table

@@ -69,6 +69,33 @@ __device__ __forceinline__ void add_y(float2 *y, int64_t i, float dx, float dy) 
     atomicAdd(y + i, make_float2(dx, dy));
 }
 
+// Warp-aggregated update: lanes of the warp that target the same node combine their
+// increments and one of them issues the atomic (same-address atomics serialise in
+// L2; on hub-heavy levels -- R-MAT coarse levels -- most of a warp hits the same
+// few nodes).  Called by all active lanes together; i < 0 = no update.
+template <bool AGG>
+__device__ __forceinline__ void add_y_w(float2 *y, int64_t i, float dx, float dy) {
+    if (!AGG) {
+        if (i >= 0) add_y(y, i, dx, dy);
+        return;
+    }
+    const unsigned active = __activemask();
+    const unsigned peers = __match_any_sync(active, (unsigned long long)i);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    for (unsigned rest = peers & ~(1u << leader); rest; rest &= rest - 1) {
+        const int src = __ffs(rest) - 1;
+        const float tx = __shfl_sync(peers, dx, src);
+        const float ty = __shfl_sync(peers, dy, src);
+        if (lane == leader) {
+            dx += tx;
+            dy += ty;
+        }
+    }
+    if (lane == leader && i >= 0) add_y(y, i, dx, dy);
+}
+
+template <bool AGG>
 __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const float two_b = 2.0f * (float)A.b;
@@ -110,6 +137,8 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
         }
         float2 yi = ld_y(y, i);
         float gix = 0.f, giy = 0.f;   // the source's own increments of this step
+        int64_t upd = -1;
+        float ux = 0.f, uy = 0.f;
         if (i != j) {  // _kernels.py:82-105
             const float2 yj = ld_y(y, j);
             const float dx = yi.x - yj.x, dy = yi.y - yj.y;
@@ -119,13 +148,16 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
                 const float coef = -two_b * pw / (1.0f + pw * ld2);
                 const float gx = A.lr * clampf(coef * dx, A.clip);
                 const float gy = A.lr * clampf(coef * dy, A.clip);
-                add_y(y, j, -gx, -gy);
+                upd = j;
+                ux = -gx;
+                uy = -gy;
                 yi.x += gx;
                 yi.y += gy;
                 gix += gx;
                 giy += gy;
             }
         }
+        add_y_w<AGG>(y, upd, ux, uy);
         for (int m = 0; m < A.M; ++m) {  // _kernels.py:106-140
             int64_t target = -1;
             for (int attempt = 0; attempt < 9; ++attempt) {
@@ -153,25 +185,31 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
                     break;
                 }
             }
-            if (target < 0) continue;
-            const float2 yc = ld_y(y, target);
-            const float dx = yi.x - yc.x, dy = yi.y - yc.y;
-            const float ld2 = dx * dx + dy * dy;
-            if (ld2 + A.eps > 0.f) {
-                const float pw = ipowf(ld2, A.b - 1);
-                const float coef = A.gamma * two_b / ((ld2 + A.eps) * (1.0f + pw * ld2));
-                const float gx = A.lr * clampf(coef * dx, A.clip);
-                const float gy = A.lr * clampf(coef * dy, A.clip);
-                add_y(y, target, -gx, -gy);
-                yi.x += gx;
-                yi.y += gy;
-                gix += gx;
-                giy += gy;
+            int64_t tu = -1;
+            float tx = 0.f, ty = 0.f;
+            if (target >= 0) {
+                const float2 yc = ld_y(y, target);
+                const float dx = yi.x - yc.x, dy = yi.y - yc.y;
+                const float ld2 = dx * dx + dy * dy;
+                if (ld2 + A.eps > 0.f) {
+                    const float pw = ipowf(ld2, A.b - 1);
+                    const float coef = A.gamma * two_b / ((ld2 + A.eps) * (1.0f + pw * ld2));
+                    const float gx = A.lr * clampf(coef * dx, A.clip);
+                    const float gy = A.lr * clampf(coef * dy, A.clip);
+                    tu = target;
+                    tx = -gx;
+                    ty = -gy;
+                    yi.x += gx;
+                    yi.y += gy;
+                    gix += gx;
+                    giy += gy;
+                }
             }
+            add_y_w<AGG>(y, tu, tx, ty);
         }
         // the source's own increments of the step, published once (the step sees
         // them locally in sequence, as the reference kernel does)
-        if (gix != 0.f || giy != 0.f) add_y(y, i, gix, giy);
+        add_y_w<AGG>(y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy);
     }
 }
 
@@ -243,7 +281,8 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                                   float *y, int64_t step_lo, int64_t n_steps, int t0, int n_iter,
                                   int iters,
                                   double lr0, double gamma, double eps, double clip, int b, int M,
-                                  uint64_t seed, int level, int64_t max_threads, void *stream) {
+                                  uint64_t seed, int level, int64_t max_threads, int aggregate,
+                                  void *stream) {
     if (n <= 0 || n_steps < 0 || n_iter < 0) return DRG_OK;
     if (n >= 0x7fffffffLL) return fail(DRG_ERR_INVALID, "level exceeds 2^31 - 1 nodes");
     if (b < 1 || M < 0 || iters < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
@@ -271,7 +310,8 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     for (int j = 0; j < n_iter; ++j) {
         A.t = t0 + j;
         A.lr = (float)std::max(lr0 * (1.0 - (double)A.t / (double)iters), 0.0);
-        sampled_kernel<<<grid, 256, 0, st>>>(A, reinterpret_cast<float2 *>(y));
+        if (aggregate) sampled_kernel<true><<<grid, 256, 0, st>>>(A, reinterpret_cast<float2 *>(y));
+        else sampled_kernel<false><<<grid, 256, 0, st>>>(A, reinterpret_cast<float2 *>(y));
         DRG_LAUNCHED("sampled_kernel");
     }
     return DRG_OK;

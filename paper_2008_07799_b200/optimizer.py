@@ -268,6 +268,10 @@ class SampledTables:
     row_alias: torch.Tensor   # int64 [nnz] per-row Vose over P^l (threshold, alias target)
     collapse: torch.Tensor    # fp32 [n]   c_a
     wsum: torch.Tensor        # fp32 [n]   sum_b W_ab = 2 n_l sum_b P^l_ab (sgather)
+    hubs: bool = False        # some node takes part in > HUB_STEPS steps per epoch
+
+
+HUB_STEPS = 512   # warp-aggregate the sampled updates above this per-node rate
 
 
 def build_sampled_tables(ip, tg, P, R) -> SampledTables:
@@ -282,7 +286,9 @@ def build_sampled_tables(ip, tg, P, R) -> SampledTables:
         c = torch.where(R > 0, 1.0 - rowsum[:n] / torch.clamp(R, min=1e-300),
                         torch.zeros_like(R)).clamp_(0.0, 1.0).to(torch.float32)
         wsum = (2.0 * n * rowsum[:n]).to(torch.float32)
-    return SampledTables(src, rows[:nnz], c, wsum)
+        # expected steps per epoch in which the busiest node is the source
+        hubs = bool(float(R.max()) / max(float(R.sum()), 1e-300) * n > HUB_STEPS)
+    return SampledTables(src, rows[:nnz], c, wsum, hubs)
 
 
 def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float = 0.75,
@@ -452,7 +458,8 @@ class LayoutPlan:
                   _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), _lib.ptr(S.collapse),
                   _lib.ptr(L.alias), L.n, _lib.ptr(y), step_lo, n_steps, t0, n_iter, o.iters,
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
-                  o.neg_samples, seed, level, max(256, L.n // max(1, div)), _lib.stream_ptr())
+                  o.neg_samples, seed, level, max(256, L.n // max(1, div)), int(S.hubs),
+                  _lib.stream_ptr())
 
     def _run_level_sampled(self, level, y, t0, n_iter, group=None, step_fn=None):
         """Reference-faithful epochs: n_l sampled steps each, Hogwild on y.  With a

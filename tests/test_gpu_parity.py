@@ -677,3 +677,18 @@ def test_device_alias_tables_are_exact(seed):
         np.add.at(mass, t.alias, (1 - t.prob) / n)
         np.testing.assert_allclose(mass, w / w.sum(), rtol=2e-5, atol=2e-7 / n)
         assert np.all((t.prob >= 0) & (t.prob <= 1))
+
+
+def test_sampled_mode_hub_aggregation():
+    """Hub-heavy levels switch the sampled kernel to warp-aggregated atomics."""
+    from paper_2008_07799_b200.graph import DeviceGraph
+    from paper_2008_07799_b200.optimizer import prepare_layout
+    rng = np.random.default_rng(8)
+    n = 20_001
+    hub = np.column_stack([np.zeros(n - 1, dtype=np.int64), np.arange(1, n)])
+    g = O.from_edges(np.concatenate([hub, rng.integers(1, n, size=(4000, 2))]), n)
+    prep = prepare_layout(DeviceGraph.from_host(as_gpu_graph(g)), B.SimilarityParams(k=1),
+                          B.OptimizerParams(seed=1, iters=20), min_size=16)
+    assert any(L.sampled is not None and L.sampled.hubs for L in prep.plan.levels)
+    lay = B.layout_graph(as_gpu_graph(g), B.SimilarityParams(k=1), B.OptimizerParams(seed=1, iters=20))
+    assert np.isfinite(lay.positions).all()
