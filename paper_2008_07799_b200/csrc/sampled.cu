@@ -218,6 +218,109 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
 // fp64 scaled weights in scratch, stacks in the caller's int32 scratch (the small
 // stack grows up from the row start, the large one down from the row end).
 // rec[e] = {fp32 threshold of bucket e, target of its alias entry}.
+constexpr int kRowWarpMax = 512;   // rows up to this length: warp-parallel sweep
+constexpr int kRowWarps = 4;
+
+// Warp per row (len <= kRowWarpMax): the parallel sweep of drg_alias_build
+// (layout.cu) inside one row, in shared memory -- lights / heavies compacted in index
+// order by ballots, deficit / surplus prefix sums by warp scans, then each lane
+// resolves its items by binary search.
+__global__ void __launch_bounds__(kRowWarps * 32)
+    row_alias_warp_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ targets,
+                          const double *__restrict__ P, int64_t n, uint2 *rec, double *rowsum) {
+    __shared__ double s_w[kRowWarps][kRowWarpMax];
+    __shared__ double s_ds[kRowWarps][kRowWarpMax];   // delta (lights) | sigma (heavies)
+    __shared__ int16_t s_idx[kRowWarps][kRowWarpMax]; // lights from the front, heavies after
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    double *w = s_w[wp], *ds = s_ds[wp];
+    int16_t *idx = s_idx[wp];
+    for (int64_t i = (int64_t)blockIdx.x * kRowWarps + wp; i < n; i += (int64_t)gridDim.x * kRowWarps) {
+        const int64_t lo = indptr[i], hi = indptr[i + 1];
+        const int len = (int)(hi - lo);
+        if (len > kRowWarpMax) continue;   // the thread tier takes it
+        if (len == 0) {
+            if (lane == 0 && rowsum) rowsum[i] = 0.0;
+            continue;
+        }
+        double tot = 0.0;
+        for (int e = lane; e < len; e += 32) tot += P[lo + e];
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
+        if (lane == 0 && rowsum) rowsum[i] = tot;
+        if (!(tot > 0.0)) {
+            for (int e = lane; e < len; e += 32)
+                rec[lo + e] = make_uint2(__float_as_uint(1.0f), targets[lo + e]);
+            continue;
+        }
+        const double f = (double)len / tot;
+        // compaction: lights [0, na), heavies [na, len) in index order
+        int na = 0;
+        for (int base = 0; base < len; base += 32) {
+            const int e = base + lane;
+            const double x = e < len ? P[lo + e] * f : 2.0;
+            if (e < len) w[e] = x;
+            const unsigned bl = __ballot_sync(kFull, e < len && x < 1.0);
+            if (e < len && x < 1.0) idx[na + __popc(bl & ((1u << lane) - 1u))] = (int16_t)e;
+            na += __popc(bl);
+        }
+        int nh = 0;
+        for (int base = 0; base < len; base += 32) {
+            const int e = base + lane;
+            const bool h = e < len && !(w[e] < 1.0);
+            const unsigned bh = __ballot_sync(kFull, h);
+            if (h) idx[na + nh + __popc(bh & ((1u << lane) - 1u))] = (int16_t)e;
+            nh += __popc(bh);
+        }
+        __syncwarp();
+        // inclusive prefix sums: delta over lights, sigma over heavies
+        for (int part = 0; part < 2; ++part) {
+            const int off = part ? na : 0, cnt = part ? nh : na;
+            double carry = 0.0;
+            for (int base = 0; base < cnt; base += 32) {
+                const int k = base + lane;
+                double v = 0.0;
+                if (k < cnt) v = part ? w[idx[off + k]] - 1.0 : 1.0 - w[idx[off + k]];
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double t = __shfl_up_sync(kFull, v, o);
+                    if (lane >= o) v += t;
+                }
+                if (k < cnt) ds[off + k] = carry + v;
+                carry += __shfl_sync(kFull, v, 31);
+            }
+        }
+        __syncwarp();
+        const double *delta = ds, *sigma = ds + na;
+        for (int k = lane; k < na; k += 32) {   // lights
+            const double prev = k ? delta[k - 1] : 0.0;
+            int a = 0, b = nh;
+            while (a < b) {
+                const int m = (a + b) >> 1;
+                if (sigma[m] > prev) b = m;
+                else a = m + 1;
+            }
+            const int item = idx[k];
+            rec[lo + item] = a < nh ? make_uint2(__float_as_uint((float)w[item]),
+                                                 targets[lo + idx[na + a]])
+                                    : make_uint2(__float_as_uint(1.0f), targets[lo + item]);
+        }
+        for (int k = lane; k < nh; k += 32) {   // heavies
+            int a = 0, b = na;
+            while (a < b) {
+                const int m = (a + b) >> 1;
+                if (delta[m] >= sigma[k]) b = m;
+                else a = m + 1;
+            }
+            const int item = idx[na + k];
+            if (a < na && k + 1 < nh) {
+                const double p = fmin(fmax(1.0 + sigma[k] - delta[a], 0.0), 1.0);
+                rec[lo + item] = make_uint2(__float_as_uint((float)p), targets[lo + idx[na + k + 1]]);
+            } else {
+                rec[lo + item] = make_uint2(__float_as_uint(1.0f), targets[lo + item]);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 __global__ void row_alias_kernel(const int64_t *__restrict__ indptr,
                                  const int32_t *__restrict__ targets,
                                  const double *__restrict__ P, int64_t n, int32_t *stack,
@@ -226,6 +329,7 @@ __global__ void row_alias_kernel(const int64_t *__restrict__ indptr,
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t lo = indptr[i], hi = indptr[i + 1];
         const int64_t len = hi - lo;
+        if (len <= kRowWarpMax) continue;   // the warp tier takes it
         if (len <= 0) {
             if (rowsum) rowsum[i] = 0.0;
             continue;
@@ -267,6 +371,11 @@ extern "C" int drg_row_alias(const int64_t *indptr, const int32_t *targets, cons
     Scratch stack(st), w(st);
     DRG_CUDA(stack.alloc(sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1)));
     DRG_CUDA(w.alloc(sizeof(double) * (size_t)std::max<int64_t>(nnz, 1)));
+    const unsigned gw = (unsigned)std::min<int64_t>(ceil_div(n, kRowWarps), kSMs * 64);
+    row_alias_warp_kernel<<<gw, kRowWarps * 32, 0, st>>>(indptr, targets, P, n,
+                                                         reinterpret_cast<uint2 *>(out_rec),
+                                                         out_rowsum);
+    DRG_LAUNCHED("row_alias_warp_kernel");
     const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 128), kSMs * 64);
     row_alias_kernel<<<g, 128, 0, st>>>(indptr, targets, P, n, stack.as<int32_t>(),
                                         w.as<double>(), reinterpret_cast<uint2 *>(out_rec),
