@@ -58,6 +58,8 @@ class OptimizerParams:
     * "sampled" (default): the reference's own step (_kernels.py:65-140) run
       Hogwild-style on the GPU -- KL/NP parity with the reference, fastest on one
       GPU; run-to-run nondeterministic like the reference's threads > 1 mode.
+      Levels whose busiest node is the source of > HUB_STEPS steps per epoch
+      (R-MAT hubs) run the "jacobi" gather instead (``hub_levels``).
     * "jacobi": the node-parallel expected-gradient iteration (SURVEY §8(a) A12,
       CSR gather + M negatives per node) -- bitwise deterministic and node-range
       shardable across GPUs; matches KL, lower NP on multilevel RGG.
@@ -85,6 +87,7 @@ class OptimizerParams:
     sampled_concurrency: int = 16  # update="sampled": n_0 / this many steps in flight (level 0)
     sampled_concurrency_coarse: int = 4   # ... and n_l / this many on coarser levels
     att_samples: int = 2           # update="sgather": attraction partners drawn per node
+    hub_levels: str = "jacobi"     # update="sampled": hub-heavy levels run this update
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
@@ -349,6 +352,9 @@ class LayoutPlan:
         L = self.levels[level]
         M = self.opt.neg_samples
         u = self.opt.update
+        if u == "sampled" and L.sampled is not None and L.sampled.hubs and \
+                self.opt.hub_levels == "jacobi":
+            u = "jacobi"
         if u == "sampled":
             return "sampled_kernel", L.n * (92 + 32 * M)
         if u == "sgather":
@@ -425,8 +431,12 @@ class LayoutPlan:
             import torch.distributed as dist
             world = dist.get_world_size(group)
         if self.opt.update == "sampled":
-            return self._run_level_sampled(level, y, t0, n_iter, group if world > 1 else None,
-                                           step_fn)
+            hub = L.sampled is not None and L.sampled.hubs and self.opt.hub_levels == "jacobi"
+            if not hub:
+                return self._run_level_sampled(level, y, t0, n_iter,
+                                               group if world > 1 else None, step_fn)
+            # hub-heavy level (R-MAT-like): same-address atomics would serialise the
+            # sampled steps; the gather (K7 + heavy-row split) has no contention
         inplace = self.opt.update == "inplace"
         if world > 1 and L.n >= self.opt.shard_min_nodes:
             return self._run_level_sharded(level, y, t0, n_iter, group, step_fn)
