@@ -697,5 +697,7 @@ def test_sampled_mode_hub_aggregation():
     prep = prepare_layout(DeviceGraph.from_host(as_gpu_graph(g)), B.SimilarityParams(k=1),
                           B.OptimizerParams(seed=1, iters=20), min_size=16)
     assert any(L.sampled is not None and L.sampled.hubs for L in prep.plan.levels)
-    lay = B.layout_graph(as_gpu_graph(g), B.SimilarityParams(k=1), B.OptimizerParams(seed=1, iters=20))
-    assert np.isfinite(lay.positions).all()
+    for hub_levels in ("jacobi", "sampled"):   # gather fallback / aggregated atomics
+        lay = B.layout_graph(as_gpu_graph(g), B.SimilarityParams(k=1),
+                             B.OptimizerParams(seed=1, iters=20, hub_levels=hub_levels))
+        assert np.isfinite(lay.positions).all()
