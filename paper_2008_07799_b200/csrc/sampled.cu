@@ -96,7 +96,7 @@ __device__ __forceinline__ void add_y_w(float2 *y, int64_t i, float dx, float dy
 }
 
 template <bool AGG>
-__global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
+__global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const float two_b = 2.0f * (float)A.b;
     const int Me = min(A.M, kMaxNeg);
@@ -104,30 +104,33 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
          sl += nthreads) {
         const int64_t s = A.step_lo + sl;
         const uint32_t c1 = (uint32_t)(s >> 32) ^ ((uint32_t)A.t << 1);
-        // ---- all first-attempt draws, table loads in flight together
+        // ---- every first-attempt draw up front; table loads in flight together
         const u32x4 r = philox4x32(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xff00u, 0x5a3d1e55u},
                                    A.key0, A.key1);
+        const u32x4 r2 = philox4x32(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xfe00u, 0x3c6ef372u},
+                                    A.key0, A.key1);
         const int64_t sb = bucket(A.n, r.x, r.y);
         const uint2 srec = __ldg(A.src_alias + sb);
-        int32_t nbk[kMaxNeg];   // node ids < 2^31
-        uint2 nrec[kMaxNeg];
-        uint32_t ncoin[kMaxNeg];
+        int32_t cand[kMaxNeg];   // first-attempt negatives (node ids < 2^31)
+        float2 ycand[kMaxNeg];
 #pragma unroll
         for (int m = 0; m < kMaxNeg; ++m) {
             if (m < Me) {
                 const u32x4 q = neg_draw(A, s, c1, m, 0);
-                nbk[m] = (int32_t)bucket(A.n, q.x, q.y);
-                ncoin[m] = q.z;
-                nrec[m] = __ldg(A.neg_alias + nbk[m]);
+                const int32_t bk = (int32_t)bucket(A.n, q.x, q.y);
+                cand[m] = (int32_t)accept(__ldg(A.neg_alias + bk), bk, q.z);
             }
         }
+        // speculative gathers of the candidates (redrawn below only if they hit i/j)
+#pragma unroll
+        for (int m = 0; m < kMaxNeg; ++m)
+            if (m < Me) ycand[m] = ld_y(y, cand[m]);
         // ---- directed pair: source a ~ R^l; collapsed (a, a) with prob collapse[a],
         // else target ~ P^l_a. by the row's alias table
         const int64_t i = accept(srec, sb, r.z);
         const int64_t lo = __ldg(A.indptr + i), hi = __ldg(A.indptr + i + 1);
         const float cprob = __ldg(A.collapse + i);
-        const u32x4 r2 = philox4x32(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xfe00u, 0x3c6ef372u},
-                                    A.key0, A.key1);
+        float2 yi = ld_y(y, i);
         int64_t j = i;
         if (hi > lo && !(u32_to_unit(r.w) < cprob)) {
             const int64_t e = lo + bucket(hi - lo, r2.x, r2.y);
@@ -135,7 +138,6 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
             const uint32_t tj = __ldg(A.rec + e).x;
             j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)tj : (int64_t)rrec.y;
         }
-        float2 yi = ld_y(y, i);
         float gix = 0.f, giy = 0.f;   // the source's own increments of this step
         int64_t upd = -1;
         float ux = 0.f, uy = 0.f;
@@ -160,35 +162,35 @@ __global__ void __launch_bounds__(256, 4) sampled_kernel(SArgs A, float2 *y) {
         add_y_w<AGG>(y, upd, ux, uy);
         for (int m = 0; m < A.M; ++m) {  // _kernels.py:106-140
             int64_t target = -1;
-            for (int attempt = 0; attempt < 9; ++attempt) {
-                int64_t c0;
-                if (attempt == 0 && m < Me) {
-                    int32_t bk = 0;
-                    uint2 rc = make_uint2(0, 0);
-                    uint32_t cn = 0;
+            float2 yc = make_float2(0.f, 0.f);
+            int first = 0;
+            if (m < Me) {
+                int32_t c0 = 0;
+                float2 y0 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int q = 0; q < kMaxNeg; ++q)
-                        if (q == m) {
-                            bk = nbk[q];
-                            rc = nrec[q];
-                            cn = ncoin[q];
-                        }
-                    c0 = accept(rc, bk, cn);
-                } else {
-                    const u32x4 q = neg_draw(A, s, c1, m, attempt);
-                    const int64_t bk = bucket(A.n, q.x, q.y);
-                    c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
+                for (int q = 0; q < kMaxNeg; ++q)
+                    if (q == m) {
+                        c0 = cand[q];
+                        y0 = ycand[q];
+                    }
+                if (c0 != i && c0 != j) {
+                    target = c0;
+                    yc = y0;
                 }
-                const int64_t cm = c0;
-                if (cm != i && cm != j) {
-                    target = cm;
-                    break;
+                first = 1;
+            }
+            for (int attempt = first; target < 0 && attempt < 9; ++attempt) {
+                const u32x4 q = neg_draw(A, s, c1, m, attempt);
+                const int64_t bk = bucket(A.n, q.x, q.y);
+                const int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
+                if (c0 != i && c0 != j) {
+                    target = c0;
+                    yc = ld_y(y, c0);
                 }
             }
             int64_t tu = -1;
             float tx = 0.f, ty = 0.f;
             if (target >= 0) {
-                const float2 yc = ld_y(y, target);
                 const float dx = yi.x - yc.x, dy = yi.y - yc.y;
                 const float ld2 = dx * dx + dy * dy;
                 if (ld2 + A.eps > 0.f) {
