@@ -16,6 +16,8 @@
 // Latency: all first-attempt draws (pair + M negatives) are made up front and
 // their table loads issued together; the dependent chain of a step is then
 // source alias -> row bounds / c_a -> row alias record + target -> y.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace drg {
@@ -37,6 +39,7 @@ struct SArgs {
     int b, M;
     uint32_t key0, key1, level;
     int t;
+    int probe;   // latency probe (DRG_SAMPLED_PROBE, tests only): 1 = no atomics, 2 = no row draw
 };
 
 __device__ __forceinline__ float clampf(float g, float c) { return fminf(fmaxf(g, -c), c); }
@@ -74,7 +77,11 @@ __device__ __forceinline__ void add_y(float2 *y, int64_t i, float dx, float dy) 
 // L2; on hub-heavy levels -- R-MAT coarse levels -- most of a warp hits the same
 // few nodes).  Called by all active lanes together; i < 0 = no update.
 template <bool AGG>
-__device__ __forceinline__ void add_y_w(float2 *y, int64_t i, float dx, float dy) {
+__device__ __forceinline__ void add_y_w(float2 *y, int64_t i, float dx, float dy, int probe = 0) {
+    if (probe & 1) {   // latency probe: keep the value live, skip the memory update
+        if (i >= 0 && dx == 1234.5f) y[0].x = dy;
+        return;
+    }
     if (!AGG) {
         if (i >= 0) add_y(y, i, dx, dy);
         return;
@@ -132,7 +139,9 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
         const float cprob = __ldg(A.collapse + i);
         float2 yi = ld_y(y, i);
         int64_t j = i;
-        if (hi > lo && !(u32_to_unit(r.w) < cprob)) {
+        if ((A.probe & 2) && hi > lo) {
+            j = (int64_t)bucket(A.n, r2.x, r2.y);
+        } else if (hi > lo && !(u32_to_unit(r.w) < cprob)) {
             const int64_t e = lo + bucket(hi - lo, r2.x, r2.y);
             const uint2 rrec = __ldg(A.row_alias + e);
             const uint32_t tj = __ldg(A.rec + e).x;
@@ -159,7 +168,7 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
                 giy += gy;
             }
         }
-        add_y_w<AGG>(y, upd, ux, uy);
+        add_y_w<AGG>(y, upd, ux, uy, A.probe);
         for (int m = 0; m < A.M; ++m) {  // _kernels.py:106-140
             int64_t target = -1;
             float2 yc = make_float2(0.f, 0.f);
@@ -207,11 +216,11 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
                     giy += gy;
                 }
             }
-            add_y_w<AGG>(y, tu, tx, ty);
+            add_y_w<AGG>(y, tu, tx, ty, A.probe);
         }
         // the source's own increments of the step, published once (the step sees
         // them locally in sequence, as the reference kernel does)
-        add_y_w<AGG>(y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy);
+        add_y_w<AGG>(y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy, A.probe);
     }
 }
 
@@ -416,6 +425,8 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     A.key0 = (uint32_t)seed;
     A.key1 = (uint32_t)(seed >> 32);
     A.level = (uint32_t)level;
+    const char *probe = getenv("DRG_SAMPLED_PROBE");
+    A.probe = probe ? atoi(probe) : 0;
     int64_t threads = std::max<int64_t>(256, std::min<int64_t>(n_steps, max_threads));
     const unsigned grid = (unsigned)ceil_div(threads, 256);
     for (int j = 0; j < n_iter; ++j) {
