@@ -84,7 +84,10 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
             upd, _, div = m.partition(":")
             extra = {}
             if div and upd == "sampled":
-                extra = {"sampled_concurrency": int(div)}
+                fine, _, coarse = div.partition(":")
+                extra = {"sampled_concurrency": int(fine)}
+                if coarse:
+                    extra["sampled_concurrency_coarse"] = int(coarse)
             elif div and upd == "sgather":
                 extra = {"att_samples": int(div)}
             lay = B.layout_graph(bg, B.SimilarityParams(k=cfg["k"], perplexity=cfg["perplexity"]),
