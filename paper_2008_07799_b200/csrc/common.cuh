@@ -68,9 +68,12 @@ struct u32x4 {
     uint32_t x, y, z, w;
 };
 
+// Philox4x32-R (Salmon et al., SC'11); R = 10 is the standard safety margin, R = 7
+// already passes BigCrush (used where the draw count per step is high).
+template <int ROUNDS = 10>
 __device__ __forceinline__ u32x4 philox4x32(u32x4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
-    for (int r = 0; r < 10; ++r) {
+    for (int r = 0; r < ROUNDS; ++r) {
         uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
         uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
         c = u32x4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};

@@ -60,7 +60,7 @@ __device__ __forceinline__ int64_t accept(const uint2 rec, int64_t idx, uint32_t
 
 __device__ __forceinline__ u32x4 neg_draw(const SArgs &A, int64_t s, uint32_t c1, int m,
                                           int attempt) {
-    return philox4x32(
+    return philox4x32<7>(
         u32x4{(uint32_t)s, c1, (A.level << 24) | ((uint32_t)m << 8) | (uint32_t)attempt,
               0x9e6a7e11u},
         A.key0, A.key1);
@@ -112,9 +112,9 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
         const int64_t s = A.step_lo + sl;
         const uint32_t c1 = (uint32_t)(s >> 32) ^ ((uint32_t)A.t << 1);
         // ---- every first-attempt draw up front; table loads in flight together
-        const u32x4 r = philox4x32(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xff00u, 0x5a3d1e55u},
+        const u32x4 r = philox4x32<7>(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xff00u, 0x5a3d1e55u},
                                    A.key0, A.key1);
-        const u32x4 r2 = philox4x32(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xfe00u, 0x3c6ef372u},
+        const u32x4 r2 = philox4x32<7>(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xfe00u, 0x3c6ef372u},
                                     A.key0, A.key1);
         const int64_t sb = bucket(A.n, r.x, r.y);
         const uint2 srec = __ldg(A.src_alias + sb);
