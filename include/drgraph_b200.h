@@ -176,10 +176,10 @@ int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, const float *V,
                      const drg_heavy_split *heavy, unsigned flags, void *stream);
 
 /* --- reference-faithful sampled epochs (update = "sampled") ----------------------
- * Per-row Vose tables over P (optimizer.py:111-139 applied to each row):
- * out_rec[e] = {fp32 threshold of bucket e, int32 target of its alias entry}; a
- * row sample is e = lo + bucket, then target[e] if coin < threshold else the
- * alias target.  out_rowsum[n] (optional) = row sums of P.  With a Vose table over
+ * Per-row alias tables over P (optimizer.py:111-139 applied to each row):
+ * out_rec[e] = 16-byte {fp32 threshold of bucket e, int32 target of its alias
+ * entry, int32 target[e], 0} (out_rec holds 2*nnz uint64); a row sample is
+ * e = lo + bucket, then target[e] if coin < threshold else the alias target.  out_rowsum[n] (optional) = row sums of P.  With a Vose table over
  * the row masses this draws a directed pair with probability P_ij, the law of the
  * reference's canonical-pair table plus direction coin (optimizer.py:206-240). */
 int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P, int64_t n,

@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kWpb * 32)
 // node-range shardable like K7.  A warp owns npw = 32 / (S + M) nodes; each lane
 // makes one draw and one y gather, then a segmented shuffle sum per node.
 struct SGArgs {
-    const uint2 *row_alias;  // per entry {threshold, alias target}
+    const uint4 *row_alias;  // per entry {threshold, alias target, own target, 0}
     const float *wsum;       // per node sum_b W_ab
     int S;
 };
@@ -435,9 +435,8 @@ __global__ void __launch_bounds__(kWpb * 32)
                                        A.key0, A.key1);
             const int64_t e = lo + (int64_t)__umul64hi(((uint64_t)q.x << 32) | q.y,
                                                         (uint64_t)(hi - lo));
-            const uint2 rr = __ldg(G.row_alias + e);
-            const uint32_t tj = __ldg(A.rec + e).x;
-            pb = (u32_to_unit(q.z) < __uint_as_float(rr.x)) ? (int64_t)tj : (int64_t)rr.y;
+            const uint4 rr = __ldg(G.row_alias + e);
+            pb = (u32_to_unit(q.z) < __uint_as_float(rr.x)) ? (int64_t)rr.z : (int64_t)rr.y;
         }
     }
     // 2. the node's first partner, for the negatives' rejection
@@ -1047,7 +1046,7 @@ extern "C" int drg_layout_sgather(const int64_t *indptr, const uint64_t *rec,
     A.level = (uint32_t)level;
     A.neg_idx = neg_idx;
     A.nonfinite = nonfinite;
-    SGArgs G{reinterpret_cast<const uint2 *>(row_alias), wsum, S};
+    SGArgs G{reinterpret_cast<const uint4 *>(row_alias), wsum, S};
     const int64_t rows = row_hi - row_lo;
     if (rows == 0) return DRG_OK;
     const int npw = std::max(1, 32 / (S + M));

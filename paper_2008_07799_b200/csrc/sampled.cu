@@ -28,7 +28,7 @@ constexpr int kMaxNeg = 6;  // negatives whose first draw is issued early
 struct SArgs {
     const int64_t *indptr;
     const uint2 *rec;        // level CSR records {target, W}
-    const uint2 *row_alias;  // per entry {fp32 threshold, int32 alias target}
+    const uint4 *row_alias;  // per entry {fp32 threshold, alias target, own target, 0}
     const uint2 *src_alias;  // Vose over R^l
     const float *collapse;   // probability that the drawn pair collapses into the source
     const uint2 *neg_alias;  // Vose over Q^l
@@ -143,9 +143,8 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
             j = (int64_t)bucket(A.n, r2.x, r2.y);
         } else if (hi > lo && !(u32_to_unit(r.w) < cprob)) {
             const int64_t e = lo + bucket(hi - lo, r2.x, r2.y);
-            const uint2 rrec = __ldg(A.row_alias + e);
-            const uint32_t tj = __ldg(A.rec + e).x;
-            j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)tj : (int64_t)rrec.y;
+            const uint4 rrec = __ldg(A.row_alias + e);   // one 16-byte record per entry
+            j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)rrec.z : (int64_t)rrec.y;
         }
         float gix = 0.f, giy = 0.f;   // the source's own increments of this step
         int64_t upd = -1;
@@ -238,7 +237,7 @@ constexpr int kRowWarps = 4;
 // resolves its items by binary search.
 __global__ void __launch_bounds__(kRowWarps * 32)
     row_alias_warp_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ targets,
-                          const double *__restrict__ P, int64_t n, uint2 *rec, double *rowsum) {
+                          const double *__restrict__ P, int64_t n, uint4 *rec, double *rowsum) {
     __shared__ double s_w[kRowWarps][kRowWarpMax];
     __shared__ double s_ds[kRowWarps][kRowWarpMax];   // delta (lights) | sigma (heavies)
     __shared__ int16_t s_idx[kRowWarps][kRowWarpMax]; // lights from the front, heavies after
@@ -259,7 +258,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
         if (lane == 0 && rowsum) rowsum[i] = tot;
         if (!(tot > 0.0)) {
             for (int e = lane; e < len; e += 32)
-                rec[lo + e] = make_uint2(__float_as_uint(1.0f), targets[lo + e]);
+                rec[lo + e] = make_uint4(__float_as_uint(1.0f), targets[lo + e], targets[lo + e], 0u);
             continue;
         }
         const double f = (double)len / tot;
@@ -309,9 +308,10 @@ __global__ void __launch_bounds__(kRowWarps * 32)
                 else a = m + 1;
             }
             const int item = idx[k];
-            rec[lo + item] = a < nh ? make_uint2(__float_as_uint((float)w[item]),
-                                                 targets[lo + idx[na + a]])
-                                    : make_uint2(__float_as_uint(1.0f), targets[lo + item]);
+            const uint32_t own = (uint32_t)targets[lo + item];
+            rec[lo + item] = a < nh ? make_uint4(__float_as_uint((float)w[item]),
+                                                 (uint32_t)targets[lo + idx[na + a]], own, 0u)
+                                    : make_uint4(__float_as_uint(1.0f), own, own, 0u);
         }
         for (int k = lane; k < nh; k += 32) {   // heavies
             int a = 0, b = na;
@@ -321,11 +321,13 @@ __global__ void __launch_bounds__(kRowWarps * 32)
                 else a = m + 1;
             }
             const int item = idx[na + k];
+            const uint32_t own = (uint32_t)targets[lo + item];
             if (a < na && k + 1 < nh) {
                 const double p = fmin(fmax(1.0 + sigma[k] - delta[a], 0.0), 1.0);
-                rec[lo + item] = make_uint2(__float_as_uint((float)p), targets[lo + idx[na + k + 1]]);
+                rec[lo + item] = make_uint4(__float_as_uint((float)p),
+                                            (uint32_t)targets[lo + idx[na + k + 1]], own, 0u);
             } else {
-                rec[lo + item] = make_uint2(__float_as_uint(1.0f), targets[lo + item]);
+                rec[lo + item] = make_uint4(__float_as_uint(1.0f), own, own, 0u);
             }
         }
         __syncwarp();
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(kRowWarps * 32)
 __global__ void row_alias_kernel(const int64_t *__restrict__ indptr,
                                  const int32_t *__restrict__ targets,
                                  const double *__restrict__ P, int64_t n, int32_t *stack,
-                                 double *w, uint2 *rec, double *rowsum) {
+                                 double *w, uint4 *rec, double *rowsum) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t lo = indptr[i], hi = indptr[i + 1];
@@ -348,7 +350,8 @@ __global__ void row_alias_kernel(const int64_t *__restrict__ indptr,
         double total = 0.0;
         for (int64_t e = lo; e < hi; ++e) total += P[e];
         if (rowsum) rowsum[i] = total;
-        for (int64_t e = lo; e < hi; ++e) rec[e] = make_uint2(__float_as_uint(1.0f), targets[e]);
+        for (int64_t e = lo; e < hi; ++e)
+            rec[e] = make_uint4(__float_as_uint(1.0f), targets[e], targets[e], 0u);
         if (!(total > 0.0)) continue;  // massless row: uniform
         const double f = (double)len / total;
         int64_t ns = 0, nl = 0;
@@ -360,7 +363,7 @@ __global__ void row_alias_kernel(const int64_t *__restrict__ indptr,
         while (ns > 0 && nl > 0) {
             const int64_t sm = lo + stack[lo + --ns];
             const int64_t lg = lo + stack[hi - 1 - --nl];
-            rec[sm] = make_uint2(__float_as_uint((float)w[sm]), targets[lg]);
+            rec[sm] = make_uint4(__float_as_uint((float)w[sm]), targets[lg], targets[sm], 0u);
             w[lg] = (w[lg] + w[sm]) - 1.0;
             if (w[lg] < 1.0) stack[lo + ns++] = (int32_t)(lg - lo);
             else stack[hi - 1 - nl++] = (int32_t)(lg - lo);
@@ -384,12 +387,12 @@ extern "C" int drg_row_alias(const int64_t *indptr, const int32_t *targets, cons
     DRG_CUDA(w.alloc(sizeof(double) * (size_t)std::max<int64_t>(nnz, 1)));
     const unsigned gw = (unsigned)std::min<int64_t>(ceil_div(n, kRowWarps), kSMs * 64);
     row_alias_warp_kernel<<<gw, kRowWarps * 32, 0, st>>>(indptr, targets, P, n,
-                                                         reinterpret_cast<uint2 *>(out_rec),
+                                                         reinterpret_cast<uint4 *>(out_rec),
                                                          out_rowsum);
     DRG_LAUNCHED("row_alias_warp_kernel");
     const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 128), kSMs * 64);
     row_alias_kernel<<<g, 128, 0, st>>>(indptr, targets, P, n, stack.as<int32_t>(),
-                                        w.as<double>(), reinterpret_cast<uint2 *>(out_rec),
+                                        w.as<double>(), reinterpret_cast<uint4 *>(out_rec),
                                         out_rowsum);
     DRG_LAUNCHED("row_alias_kernel");
     return DRG_OK;
@@ -410,7 +413,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     SArgs A;
     A.indptr = indptr;
     A.rec = reinterpret_cast<const uint2 *>(rec);
-    A.row_alias = reinterpret_cast<const uint2 *>(row_alias);
+    A.row_alias = reinterpret_cast<const uint4 *>(row_alias);
     A.src_alias = reinterpret_cast<const uint2 *>(src_alias);
     A.collapse = collapse;
     A.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);

@@ -268,7 +268,8 @@ class SampledTables:
     drawn at level 0 and mapped follow Q^l (the level's negative table)."""
 
     src_alias: torch.Tensor   # int64 [n]  Vose over R^l
-    row_alias: torch.Tensor   # int64 [nnz] per-row Vose over P^l (threshold, alias target)
+    row_alias: torch.Tensor   # int64 [nnz, 2] per-row Vose over P^l: {threshold, alias target,
+                              # own target, 0} -- one 16-byte record per entry
     collapse: torch.Tensor    # fp32 [n]   c_a
     wsum: torch.Tensor        # fp32 [n]   sum_b W_ab = 2 n_l sum_b P^l_ab (sgather)
     hubs: bool = False        # some node takes part in > HUB_STEPS steps per epoch
@@ -280,7 +281,7 @@ HUB_STEPS = 512   # warp-aggregate the sampled updates above this per-node rate
 def build_sampled_tables(ip, tg, P, R) -> SampledTables:
     n = ip.numel() - 1
     nnz = tg.numel()
-    rows = torch.empty(max(nnz, 1), dtype=torch.int64, device=R.device)
+    rows = torch.empty((max(nnz, 1), 2), dtype=torch.int64, device=R.device)   # 16 B per entry
     rowsum = torch.empty(max(n, 1), dtype=torch.float64, device=R.device)
     _lib.call("drg_row_alias", _lib.ptr(ip), _lib.ptr(tg), _lib.ptr(P), n, nnz, _lib.ptr(rows),
               _lib.ptr(rowsum), _lib.stream_ptr())

@@ -592,12 +592,13 @@ def test_row_alias_tables_reproduce_row_laws(golden, which):
     ds = prep.similarity
     S = build_sampled_tables(ds.indptr, ds.targets, ds.weights, ds.row_mass)
     assert float(S.collapse.abs().max()) < 1e-6      # level 0: no collapsed pairs
-    rec = S.row_alias.cpu().numpy().view(np.uint32).reshape(-1, 2)
+    rec = S.row_alias.cpu().numpy().view(np.uint32).reshape(-1, 4)   # thr, alias, own, 0
     ip, tg, w = ds.indptr.cpu().numpy(), ds.targets.cpu().numpy(), ds.weights.cpu().numpy()
     for i in range(len(ip) - 1):
         lo, hi = ip[i], ip[i + 1]
         if hi == lo:
             continue
+        assert np.array_equal(rec[lo:hi, 2], tg[lo:hi].astype(np.uint32))
         prob = rec[lo:hi, 0].view(np.float32).astype(np.float64)
         mass = {int(t): p / (hi - lo) for t, p in zip(tg[lo:hi], prob)}
         for q in range(hi - lo):
