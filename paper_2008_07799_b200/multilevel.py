@@ -100,13 +100,16 @@ def level_order(n: int, seed: int) -> np.ndarray:
 
 def device_build_hierarchy(dg: DeviceGraph, rho: float = 0.8, min_size: int = 16, seed: int = 0,
                            max_levels: int | None = None, force_levels: int | None = None,
-                           level0_relabel: torch.Tensor | None = None) -> DeviceHierarchy:
+                           level0_relabel: torch.Tensor | None = None,
+                           first_order=None) -> DeviceHierarchy:
     """build_hierarchy (multilevel.py:95-113) on a resident graph.  Extensions for
     the BASELINE configs: ``max_levels`` caps the total level count; ``force_levels``
     keeps coarsening past the rho test until that many levels exist.
     ``level0_relabel`` (old id -> new id): ``dg`` is the input graph relabelled; the
     reference's level-0 visiting order (drawn over the original ids) is translated,
-    so the coarse levels are exactly the reference's."""
+    so the coarse levels are exactly the reference's.  ``first_order``: a
+    concurrent.futures.Future of that level-0 order, drawn ahead (see
+    first_level_order) so the host permutation overlaps device work."""
     if not 0.0 < rho < 1.0:
         raise ValueError("rho must be in (0, 1)")
     if min_size < 1:
@@ -118,7 +121,11 @@ def device_build_hierarchy(dg: DeviceGraph, rho: float = 0.8, min_size: int = 16
             break
         level_seed = int(rng.integers(0, 2**63 - 1))
         top = h.levels[-1]
-        order = torch.from_numpy(level_order(top.node_count, level_seed)).to(top.indptr.device)
+        if first_order is not None and len(h.levels) == 1:
+            host_order = first_order.result()
+        else:
+            host_order = level_order(top.node_count, level_seed)
+        order = torch.from_numpy(host_order).to(top.indptr.device)
         if level0_relabel is not None and len(h.levels) == 1:
             order = level0_relabel.to(torch.int64)[order]
         coarse, parent, rounds = device_coarsen(top, order)
@@ -243,3 +250,13 @@ def relabel_coarse_levels(dh: DeviceHierarchy) -> list:
             m[rel.to(torch.int64)] = dh.maps[l]
             dh.maps[l] = m
     return rels
+
+
+def first_level_order(n: int, seed: int, executor):
+    """Future of the reference's level-0 visiting order (multilevel.py:91 with the
+    first seed of build_hierarchy's stream, multilevel.py:104-107), computed on a
+    host thread while the device runs the k-hop / similarity kernels."""
+    def draw():
+        level_seed = int(np.random.default_rng(seed).integers(0, 2**63 - 1))
+        return level_order(n, level_seed)
+    return executor.submit(draw)

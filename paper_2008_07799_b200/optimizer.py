@@ -21,6 +21,7 @@ smaller levels run replicated (identical on every rank, no traffic).
 
 from __future__ import annotations
 
+import concurrent.futures
 import logging
 from dataclasses import dataclass, field
 from typing import Callable
@@ -31,7 +32,8 @@ import torch
 from . import _lib
 from .graph import DeviceGraph, Graph, device_components, device_k_neighborhoods
 from .multilevel import (DeviceHierarchy, Hierarchy, compose_maps, device_build_hierarchy,
-                         device_prolong, isolated_last, relabel_coarse_levels)
+                         device_prolong, first_level_order, isolated_last,
+                         relabel_coarse_levels)
 from .similarity import (DeviceSimilarity, SimilarityParams, SparseSimilarity,
                          device_similarity)
 
@@ -602,6 +604,13 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
             ev.append((name, e))
 
     stamp("start")
+    # the level-0 visiting permutation (host numpy, the reference's stream) is drawn
+    # on a host thread while the device runs the stages below
+    pool = concurrent.futures.ThreadPoolExecutor(1)
+    hseed = _derive_seed(opt.seed, _HIERARCHY_TAG)
+    first_order = (first_level_order(dg.node_count, hseed, pool)
+                   if dg.node_count > min_size and (max_levels is None or max_levels > 1)
+                   else None)
     # isolated nodes last (layout-internal ids; outputs are mapped back)
     dg_in = dg
     dg, rel0 = isolated_last(dg)
@@ -615,8 +624,9 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
     ds = device_similarity(nd, sim)
     del nd
     stamp("similarity")
-    dh = device_build_hierarchy(dg, rho, min_size, _derive_seed(opt.seed, _HIERARCHY_TAG),
-                                max_levels, force_levels, level0_relabel=rel0)
+    dh = device_build_hierarchy(dg, rho, min_size, hseed, max_levels, force_levels,
+                                level0_relabel=rel0, first_order=first_order)
+    pool.shutdown(wait=False)
     relabel = relabel_coarse_levels(dh)
     relabel[0] = rel0
     del dg_in
