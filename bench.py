@@ -341,10 +341,15 @@ def run_ours(args):
     alt = {}
     if not args.no_alt and group is None:
         from paper_2008_07799_b200.optimizer import LayoutPlan, build_plan
-        for mode in ("jacobi", "inplace", "sampled", "sgather"):
-            if mode == opt.update:
+        variants = {"jacobi": {}, "inplace": {}, "sampled": {"sampled_fused": False},
+                    "sampled_fused": {"update": "sampled", "sampled_fused": True},
+                    "sgather": {}}
+        for label, extra in variants.items():
+            kw2 = {"update": label, **extra}
+            if all(getattr(opt, k) == v for k, v in kw2.items()):
                 continue
-            o2 = B.OptimizerParams(**{**opt.__dict__, "update": mode})
+            o2 = B.OptimizerParams(**{**opt.__dict__, **kw2})
+            mode = kw2["update"]
             p2 = (build_plan(prep.similarity, prep.hierarchy, o2)
                   if mode in ("sampled", "sgather") and plan.levels[0].sampled is None
                   else LayoutPlan(plan.levels, plan.maps, o2))
@@ -364,7 +369,7 @@ def run_ours(args):
                 l0.append(lvl_events[(0, "start")].elapsed_time(lvl_events[(0, "end")]))
             k2, b2 = p2.launch_bytes(0)
             us = sum(l0) / len(l0) / T * 1e3
-            alt[mode] = {"value": iters / (sum(ms) / len(ms) / 1e3), "unit": UNIT,
+            alt[label] = {"value": iters / (sum(ms) / len(ms) / 1e3), "unit": UNIT,
                          "ms_per_step": sum(ms) / len(ms),
                          "roofline": {"kernel": f"{k2} (level 0)", "launch_us": us,
                                       "alg_bytes_per_launch": b2,

@@ -193,15 +193,38 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * (Q^l) redrawn (<= 9) while they hit i or j, both ends moved (float2 atomics).
  * Steps step_lo .. step_lo + n_steps - 1 of each epoch run here (a rank's share of
  * the epoch in the multi-GPU mode); at most max_threads steps run concurrently.
- * aggregate != 0 combines the updates of a warp's lanes that hit the same node
- * before the atomic (hub-heavy levels). */
+ * flags: DRG_SAMPLED_AGGREGATE combines the updates of a warp's lanes that hit the
+ * same node before the atomic (hub-heavy levels); DRG_SAMPLED_FUSED draws inline in
+ * the update kernel (one launch per epoch) instead of the default split -- every
+ * draw of whole epochs resolved first by a full-occupancy pass on an internal
+ * low-priority stream, the updates then replaying them on a high-priority stream,
+ * double-buffered so the next epochs' draws overlap the current updates; the work
+ * is joined back into `stream`.  Both forms draw identical steps. */
+#define DRG_SAMPLED_AGGREGATE 1
+#define DRG_SAMPLED_FUSED 2
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,
                        const uint64_t *src_alias, const float *collapse,
                        const uint64_t *neg_alias, int64_t n, float *y, int64_t step_lo,
                        int64_t n_steps, int t0,
                        int n_iter, int iters, double lr0, double gamma, double eps, double clip,
                        int b, int M, uint64_t seed, int level, int64_t max_threads,
-                       int aggregate, void *stream);
+                       int flags, void *stream);
+
+/* The two halves of the split form, exposed for callers that keep the draws (and
+ * for the parity tests).  drg_sampled_draws: out[(e * (2 + M) + f) * n_steps + s]
+ * for epochs t0 + e (e < n_epochs) and steps step_lo + s: f = 0 the source i, f = 1
+ * the target j (j == i: collapsed pair), f = 2 + m negative m (-1 when all 9
+ * attempts hit i or j) -- exactly the steps drg_layout_sampled runs.
+ * drg_sampled_apply: one epoch of those steps on y, at most max_threads steps in
+ * flight (max_threads = 1: sequential, the reference kernel's order). */
+int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alias,
+                      const uint64_t *src_alias, const float *collapse,
+                      const uint64_t *neg_alias, int64_t n, int64_t step_lo, int64_t n_steps,
+                      int t0, int n_epochs, int M, uint64_t seed, int level, int32_t *out,
+                      void *stream);
+int drg_sampled_apply(const int32_t *draws, int64_t n_steps, float *y, double lr, double gamma,
+                      double eps, double clip, int b, int M, int64_t max_threads, int flags,
+                      void *stream);
 
 /* Stochastic gather (update = "sgather"): drg_layout_iters with the attraction
  * SAMPLED -- every node draws S partners b ~ W_a. from its row's alias table

@@ -634,6 +634,42 @@ def clipped_repulsive(d, b, gamma, eps, clip):
     return np.clip(coef[:, None] * d, -clip, clip)
 
 
+def drawn_steps(pos, draws, lr, gamma, eps, clip, b):
+    """The reference step loop (_kernels.py:82-140) on steps whose draws are given:
+    draws[f, s] = source i (f = 0), target j (f = 1; j == i: collapsed pair, no
+    attraction), negative m (f = 2 + m; -1 = every attempt hit i or j, skipped as
+    at _kernels.py:118-119).  Sequential, fp64, updates ``pos`` in place."""
+    bf = float(b)
+    for s in range(draws.shape[1]):
+        i, j = int(draws[0, s]), int(draws[1, s])
+        if i != j:                                   # _kernels.py:82-105
+            dx = pos[i, 0] - pos[j, 0]
+            dy = pos[i, 1] - pos[j, 1]
+            ld2 = dx * dx + dy * dy
+            if ld2 > 0.0:
+                pw = ld2 ** (b - 1)
+                coef = -2.0 * bf * pw / (1.0 + pw * ld2)
+                gx = min(max(coef * dx, -clip), clip)
+                gy = min(max(coef * dy, -clip), clip)
+                pos[i] += (lr * gx, lr * gy)
+                pos[j] -= (lr * gx, lr * gy)
+        for m in range(2, draws.shape[0]):           # _kernels.py:106-140
+            t = int(draws[m, s])
+            if t < 0:
+                continue
+            dx = pos[i, 0] - pos[t, 0]
+            dy = pos[i, 1] - pos[t, 1]
+            ld2 = dx * dx + dy * dy
+            if ld2 + eps > 0.0:
+                pw = ld2 ** (b - 1)
+                coef = gamma * 2.0 * bf / ((ld2 + eps) * (1.0 + pw * ld2))
+                gx = min(max(coef * dx, -clip), clip)
+                gy = min(max(coef * dy, -clip), clip)
+                pos[i] += (lr * gx, lr * gy)
+                pos[t] -= (lr * gx, lr * gy)
+    return pos
+
+
 def node_parallel_iteration(indptr, targets, W, V, y, neg_idx, lr, gamma, eps, clip, b):
     """One Jacobi iteration of K7 in fp64:
     y_a' = y_a + lr * (sum_b W_ab clip(g_att(y_a, y_b)) + V_a sum_m clip(g_rep(y_a, y_cm)))

@@ -18,6 +18,9 @@
 // source alias -> row bounds / c_a -> row alias record + target -> y.
 #include <stdlib.h>
 
+#include <algorithm>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace drg {
@@ -223,6 +226,202 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
     }
 }
 
+// ---- split formulation: draws, then updates -----------------------------------
+// Everything a step draws -- the directed pair (i, j) and its M negatives, including
+// the redraws (they are rejected only against i and j) -- depends on the static
+// level tables and the counters, never on y.  draw_kernel resolves all of it for
+// one or more whole epochs at full occupancy (a throughput-bound pass over the
+// alias tables); apply_kernel then runs the Hogwild updates with the draws as a
+// coalesced stream, so a step's dependent chain is just "gather y_i, y_j, y_c ->
+// math -> atomics".  The same counters are used as in sampled_kernel, so the drawn
+// steps are identical; only the interleaving of concurrent steps differs.
+// Draw records: [epoch][field][step] int32, field 0 = i, 1 = j (j == i: collapsed
+// pair, no attraction), 2 + m = negative m (-1: all 9 attempts hit i or j).
+struct DArgs {
+    const int64_t *indptr;
+    const uint4 *row_alias;
+    const uint2 *src_alias;
+    const float *collapse;
+    const uint2 *neg_alias;
+    int64_t n;
+    int64_t step_lo;
+    int64_t n_steps;
+    int64_t n_epochs;
+    int M;
+    uint32_t key0, key1, level;
+    int t_first;
+    int probe;
+    int32_t *out;
+};
+
+__global__ void __launch_bounds__(256) draw_kernel(DArgs A) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= A.n_steps * A.n_epochs) return;
+    const int64_t ep = g / A.n_steps, sl = g - ep * A.n_steps;
+    const int64_t s = A.step_lo + sl;
+    const uint32_t c1 = (uint32_t)(s >> 32) ^ ((uint32_t)(A.t_first + (int)ep) << 1);
+    SArgs K;   // the counter layout of sampled_kernel
+    K.key0 = A.key0;
+    K.key1 = A.key1;
+    K.level = A.level;
+    const u32x4 r = philox4x32<7>(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xff00u, 0x5a3d1e55u},
+                                  A.key0, A.key1);
+    const u32x4 r2 = philox4x32<7>(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xfe00u, 0x3c6ef372u},
+                                   A.key0, A.key1);
+    const int64_t sb = bucket(A.n, r.x, r.y);
+    const uint2 srec = __ldg(A.src_alias + sb);
+    const int Me = min(A.M, kMaxNeg);
+    int32_t cand[kMaxNeg];
+#pragma unroll
+    for (int m = 0; m < kMaxNeg; ++m) {
+        if (m < Me) {
+            const u32x4 q = neg_draw(K, s, c1, m, 0);
+            const int32_t bk = (int32_t)bucket(A.n, q.x, q.y);
+            cand[m] = (int32_t)accept(__ldg(A.neg_alias + bk), bk, q.z);
+        }
+    }
+    const int64_t i = accept(srec, sb, r.z);
+    const int64_t lo = __ldg(A.indptr + i), hi = __ldg(A.indptr + i + 1);
+    const float cprob = __ldg(A.collapse + i);
+    int64_t j = i;
+    if ((A.probe & 2) && hi > lo) {
+        j = (int64_t)bucket(A.n, r2.x, r2.y);
+    } else if (hi > lo && !(u32_to_unit(r.w) < cprob)) {
+        const uint4 rrec = __ldg(A.row_alias + lo + bucket(hi - lo, r2.x, r2.y));
+        j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)rrec.z : (int64_t)rrec.y;
+    }
+    int32_t *o = A.out + ep * (int64_t)(2 + A.M) * A.n_steps + sl;
+    o[0] = (int32_t)i;
+    o[A.n_steps] = (int32_t)j;
+    for (int m = 0; m < A.M; ++m) {
+        int64_t target = -1;
+        int first = 0;
+        if (m < Me) {
+            int32_t c0 = 0;
+#pragma unroll
+            for (int q = 0; q < kMaxNeg; ++q)
+                if (q == m) c0 = cand[q];
+            if (c0 != i && c0 != j) target = c0;
+            first = 1;
+        }
+        for (int attempt = first; target < 0 && attempt < 9; ++attempt) {
+            const u32x4 q = neg_draw(K, s, c1, m, attempt);
+            const int64_t bk = bucket(A.n, q.x, q.y);
+            const int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
+            if (c0 != i && c0 != j) target = c0;
+        }
+        o[(int64_t)(2 + m) * A.n_steps] = (int32_t)target;
+    }
+}
+
+struct PArgs {
+    const int32_t *draws;   // one epoch of draw records
+    int64_t n_steps;
+    float lr, gamma, eps, clip;
+    int b, M;
+    int probe;
+};
+
+// The reference step (_kernels.py:82-140) on drawn (i, j, negatives): the source's
+// position is carried through the step, attraction and each repulsion move the
+// other end by the opposite clipped increment; the source's own total is published
+// once.  The next step's draw record is prefetched while this step runs.
+template <bool AGG>
+__global__ void __launch_bounds__(256) apply_kernel(PArgs A, float2 *y) {
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const float two_b = 2.0f * (float)A.b;
+    const int Me = min(A.M, kMaxNeg);
+    const int64_t ns = A.n_steps;
+    int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (sl >= ns) return;
+    int32_t ci = __ldcs(A.draws + sl), cj = __ldcs(A.draws + ns + sl);
+    int32_t cc[kMaxNeg];
+#pragma unroll
+    for (int m = 0; m < kMaxNeg; ++m) cc[m] = m < Me ? __ldcs(A.draws + (2 + m) * ns + sl) : -1;
+    for (; sl < ns; sl += nthreads) {
+        const int64_t i = ci, j = cj;
+        int32_t cand[kMaxNeg];
+#pragma unroll
+        for (int m = 0; m < kMaxNeg; ++m) cand[m] = cc[m];
+        // prefetch the next step's record
+        const int64_t nx = sl + nthreads;
+        if (nx < ns) {
+            ci = __ldcs(A.draws + nx);
+            cj = __ldcs(A.draws + ns + nx);
+#pragma unroll
+            for (int m = 0; m < kMaxNeg; ++m)
+                if (m < Me) cc[m] = __ldcs(A.draws + (2 + m) * ns + nx);
+        }
+        float2 yi = ld_y(y, i);
+        const float2 yj = ld_y(y, j);
+        float2 ycand[kMaxNeg];
+#pragma unroll
+        for (int m = 0; m < kMaxNeg; ++m)
+            ycand[m] = (m < Me && cand[m] >= 0) ? ld_y(y, cand[m]) : make_float2(0.f, 0.f);
+        float gix = 0.f, giy = 0.f;
+        int64_t upd = -1;
+        float ux = 0.f, uy = 0.f;
+        if (i != j) {  // _kernels.py:82-105
+            const float dx = yi.x - yj.x, dy = yi.y - yj.y;
+            const float ld2 = dx * dx + dy * dy;
+            if (ld2 > 0.f) {
+                const float pw = ipowf(ld2, A.b - 1);
+                const float coef = -two_b * pw / (1.0f + pw * ld2);
+                const float gx = A.lr * clampf(coef * dx, A.clip);
+                const float gy = A.lr * clampf(coef * dy, A.clip);
+                upd = j;
+                ux = -gx;
+                uy = -gy;
+                yi.x += gx;
+                yi.y += gy;
+                gix += gx;
+                giy += gy;
+            }
+        }
+        add_y_w<AGG>(y, upd, ux, uy, A.probe);
+        for (int m = 0; m < A.M; ++m) {  // _kernels.py:106-140
+            int64_t target;
+            float2 yc;
+            if (m < Me) {
+                int32_t c0 = -1;
+                float2 y0 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < kMaxNeg; ++q)
+                    if (q == m) {
+                        c0 = cand[q];
+                        y0 = ycand[q];
+                    }
+                target = c0;
+                yc = y0;
+            } else {
+                target = __ldcs(A.draws + (2 + m) * ns + sl);
+                yc = target >= 0 ? ld_y(y, target) : make_float2(0.f, 0.f);
+            }
+            int64_t tu = -1;
+            float tx = 0.f, ty = 0.f;
+            if (target >= 0) {
+                const float dx = yi.x - yc.x, dy = yi.y - yc.y;
+                const float ld2 = dx * dx + dy * dy;
+                if (ld2 + A.eps > 0.f) {
+                    const float pw = ipowf(ld2, A.b - 1);
+                    const float coef = A.gamma * two_b / ((ld2 + A.eps) * (1.0f + pw * ld2));
+                    const float gx = A.lr * clampf(coef * dx, A.clip);
+                    const float gy = A.lr * clampf(coef * dy, A.clip);
+                    tu = target;
+                    tx = -gx;
+                    ty = -gy;
+                    yi.x += gx;
+                    yi.y += gy;
+                    gix += gx;
+                    giy += gy;
+                }
+            }
+            add_y_w<AGG>(y, tu, tx, ty, A.probe);
+        }
+        add_y_w<AGG>(y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy, A.probe);
+    }
+}
+
 // Thread per row: Vose's construction over the row's entries (optimizer.py:111-139,
 // same stack discipline: small / large lists in index order, popped from the back),
 // fp64 scaled weights in scratch, stacks in the caller's int32 scratch (the small
@@ -398,46 +597,228 @@ extern "C" int drg_row_alias(const int64_t *indptr, const int32_t *targets, cons
     return DRG_OK;
 }
 
+namespace {
+
+// Internal streams of the split formulation, per device: the updates run on the
+// highest-priority stream (their blocks are placed first whenever an SM frees up),
+// the draws of the next epochs on the lowest, so the throughput-bound draw pass
+// fills what the latency-bound, concurrency-capped update pass leaves idle.
+struct SideStreams {
+    cudaStream_t hi = nullptr, lo = nullptr;
+};
+
+cudaError_t side_streams(SideStreams *out) {
+    static std::mutex mu;
+    static SideStreams per_dev[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> g(mu);
+    SideStreams &ss = per_dev[dev];
+    if (!ss.hi) {
+        int least = 0, greatest = 0;
+        if ((e = cudaDeviceGetStreamPriorityRange(&least, &greatest)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithPriority(&ss.hi, cudaStreamNonBlocking, greatest)) != cudaSuccess)
+            return e;
+        if ((e = cudaStreamCreateWithPriority(&ss.lo, cudaStreamNonBlocking, least)) != cudaSuccess)
+            return e;
+    }
+    *out = ss;
+    return cudaSuccess;
+}
+
+struct Events {
+    cudaEvent_t e[6] = {};
+    ~Events() {
+        for (cudaEvent_t x : e)
+            if (x) cudaEventDestroy(x);
+    }
+    cudaError_t create() {
+        for (cudaEvent_t &x : e) {
+            cudaError_t r = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+            if (r != cudaSuccess) return r;
+        }
+        return cudaSuccess;
+    }
+};
+
+constexpr size_t kDrawBudget = size_t(64) << 20;   // bytes per draw buffer (two buffers)
+
+}  // namespace
+
+extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alias,
+                                 const uint64_t *src_alias, const float *collapse,
+                                 const uint64_t *neg_alias, int64_t n, int64_t step_lo,
+                                 int64_t n_steps, int t0, int n_epochs, int M, uint64_t seed,
+                                 int level, int32_t *out, void *stream) {
+    if (n <= 0 || n_steps <= 0 || n_epochs <= 0) return DRG_OK;
+    if (n >= 0x7fffffffLL) return fail(DRG_ERR_INVALID, "level exceeds 2^31 - 1 nodes");
+    if (M < 0) return fail(DRG_ERR_INVALID, "M must be >= 0");
+    DArgs D;
+    D.indptr = indptr;
+    D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
+    D.src_alias = reinterpret_cast<const uint2 *>(src_alias);
+    D.collapse = collapse;
+    D.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+    D.n = n;
+    D.step_lo = step_lo;
+    D.n_steps = n_steps;
+    D.n_epochs = n_epochs;
+    D.M = M;
+    D.key0 = (uint32_t)seed;
+    D.key1 = (uint32_t)(seed >> 32);
+    D.level = (uint32_t)level;
+    D.t_first = t0;
+    D.probe = 0;
+    D.out = out;
+    draw_kernel<<<(unsigned)ceil_div(n_steps * (int64_t)n_epochs, 256), 256, 0, as_stream(stream)>>>(D);
+    DRG_LAUNCHED("draw_kernel");
+    return DRG_OK;
+}
+
+extern "C" int drg_sampled_apply(const int32_t *draws, int64_t n_steps, float *y, double lr,
+                                 double gamma, double eps, double clip, int b, int M,
+                                 int64_t max_threads, int flags, void *stream) {
+    if (n_steps <= 0) return DRG_OK;
+    if (b < 1 || M < 0 || max_threads < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
+    PArgs P;
+    P.draws = draws;
+    P.n_steps = n_steps;
+    P.lr = (float)lr;
+    P.gamma = (float)gamma;
+    P.eps = (float)eps;
+    P.clip = (float)clip;
+    P.b = b;
+    P.M = M;
+    P.probe = 0;
+    const int64_t threads = std::min<int64_t>(n_steps, max_threads);
+    const int block = (int)std::min<int64_t>(256, threads);
+    const unsigned grid = (unsigned)(threads / block);   // <= threads steps in flight
+    cudaStream_t st = as_stream(stream);
+    if (flags & DRG_SAMPLED_AGGREGATE)
+        apply_kernel<true><<<grid, block, 0, st>>>(P, reinterpret_cast<float2 *>(y));
+    else
+        apply_kernel<false><<<grid, block, 0, st>>>(P, reinterpret_cast<float2 *>(y));
+    DRG_LAUNCHED("apply_kernel");
+    return DRG_OK;
+}
+
 extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                                   const uint64_t *row_alias, const uint64_t *src_alias,
                                   const float *collapse, const uint64_t *neg_alias, int64_t n,
                                   float *y, int64_t step_lo, int64_t n_steps, int t0, int n_iter,
                                   int iters,
                                   double lr0, double gamma, double eps, double clip, int b, int M,
-                                  uint64_t seed, int level, int64_t max_threads, int aggregate,
+                                  uint64_t seed, int level, int64_t max_threads, int flags,
                                   void *stream) {
-    if (n <= 0 || n_steps < 0 || n_iter < 0) return DRG_OK;
+    if (n <= 0 || n_steps <= 0 || n_iter <= 0) return DRG_OK;
     if (n >= 0x7fffffffLL) return fail(DRG_ERR_INVALID, "level exceeds 2^31 - 1 nodes");
     if (b < 1 || M < 0 || iters < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
     cudaStream_t st = as_stream(stream);
-    SArgs A;
-    A.indptr = indptr;
-    A.rec = reinterpret_cast<const uint2 *>(rec);
-    A.row_alias = reinterpret_cast<const uint4 *>(row_alias);
-    A.src_alias = reinterpret_cast<const uint2 *>(src_alias);
-    A.collapse = collapse;
-    A.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
-    A.n = n;
-    A.step_lo = step_lo;
-    A.n_steps = n_steps;
-    A.gamma = (float)gamma;
-    A.eps = (float)eps;
-    A.clip = (float)clip;
-    A.b = b;
-    A.M = M;
-    A.key0 = (uint32_t)seed;
-    A.key1 = (uint32_t)(seed >> 32);
-    A.level = (uint32_t)level;
-    const char *probe = getenv("DRG_SAMPLED_PROBE");
-    A.probe = probe ? atoi(probe) : 0;
-    int64_t threads = std::max<int64_t>(256, std::min<int64_t>(n_steps, max_threads));
+    const bool agg = flags & DRG_SAMPLED_AGGREGATE;
+    const char *probe_env = getenv("DRG_SAMPLED_PROBE");
+    const int probe = probe_env ? atoi(probe_env) : 0;
+    const int64_t threads = std::max<int64_t>(256, std::min<int64_t>(n_steps, max_threads));
     const unsigned grid = (unsigned)ceil_div(threads, 256);
-    for (int j = 0; j < n_iter; ++j) {
-        A.t = t0 + j;
-        A.lr = (float)std::max(lr0 * (1.0 - (double)A.t / (double)iters), 0.0);
-        if (aggregate) sampled_kernel<true><<<grid, 256, 0, st>>>(A, reinterpret_cast<float2 *>(y));
-        else sampled_kernel<false><<<grid, 256, 0, st>>>(A, reinterpret_cast<float2 *>(y));
-        DRG_LAUNCHED("sampled_kernel");
+    auto lr_at = [&](int t) { return (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0); };
+    if (flags & DRG_SAMPLED_FUSED) {   // one kernel per epoch, draws inline
+        SArgs A;
+        A.indptr = indptr;
+        A.rec = reinterpret_cast<const uint2 *>(rec);
+        A.row_alias = reinterpret_cast<const uint4 *>(row_alias);
+        A.src_alias = reinterpret_cast<const uint2 *>(src_alias);
+        A.collapse = collapse;
+        A.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+        A.n = n;
+        A.step_lo = step_lo;
+        A.n_steps = n_steps;
+        A.gamma = (float)gamma;
+        A.eps = (float)eps;
+        A.clip = (float)clip;
+        A.b = b;
+        A.M = M;
+        A.key0 = (uint32_t)seed;
+        A.key1 = (uint32_t)(seed >> 32);
+        A.level = (uint32_t)level;
+        A.probe = probe;
+        for (int j = 0; j < n_iter; ++j) {
+            A.t = t0 + j;
+            A.lr = lr_at(A.t);
+            if (agg) sampled_kernel<true><<<grid, 256, 0, st>>>(A, reinterpret_cast<float2 *>(y));
+            else sampled_kernel<false><<<grid, 256, 0, st>>>(A, reinterpret_cast<float2 *>(y));
+            DRG_LAUNCHED("sampled_kernel");
+        }
+        return DRG_OK;
     }
+    // split: draw_kernel (K epochs per launch, double-buffered, low-priority stream)
+    // -> apply_kernel per epoch (high-priority stream); joined back into `stream`
+    const size_t rec_bytes = (size_t)(2 + M) * sizeof(int32_t) * (size_t)n_steps;
+    const int K = (int)std::max<int64_t>(1, std::min<int64_t>(n_iter, (int64_t)(kDrawBudget / rec_bytes)));
+    const int nchunks = (n_iter + K - 1) / K;
+    Scratch buf(st);
+    DRG_CUDA(buf.alloc(rec_bytes * (size_t)K * (nchunks > 1 ? 2 : 1)));
+    SideStreams ss;
+    DRG_CUDA(side_streams(&ss));
+    Events ev;   // 0 start, 1-2 drawn[2], 3-4 applied[2], 5 draws done
+    DRG_CUDA(ev.create());
+    DRG_CUDA(cudaEventRecord(ev.e[0], st));
+    DRG_CUDA(cudaStreamWaitEvent(ss.lo, ev.e[0], 0));
+    DRG_CUDA(cudaStreamWaitEvent(ss.hi, ev.e[0], 0));
+    DArgs D;
+    D.indptr = indptr;
+    D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
+    D.src_alias = reinterpret_cast<const uint2 *>(src_alias);
+    D.collapse = collapse;
+    D.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+    D.n = n;
+    D.step_lo = step_lo;
+    D.n_steps = n_steps;
+    D.M = M;
+    D.key0 = (uint32_t)seed;
+    D.key1 = (uint32_t)(seed >> 32);
+    D.level = (uint32_t)level;
+    D.probe = probe;
+    auto chunk_buf = [&](int c) { return buf.as<int32_t>() + (size_t)(c & 1) * K * (rec_bytes / 4); };
+    auto draw = [&](int c) -> int {
+        D.t_first = t0 + c * K;
+        D.n_epochs = std::min(K, n_iter - c * K);
+        D.out = chunk_buf(c);
+        draw_kernel<<<(unsigned)ceil_div(D.n_steps * D.n_epochs, 256), 256, 0, ss.lo>>>(D);
+        DRG_LAUNCHED("draw_kernel");
+        DRG_CUDA(cudaEventRecord(ev.e[1 + (c & 1)], ss.lo));
+        return DRG_OK;
+    };
+    int rc = draw(0);
+    if (rc) return rc;
+    PArgs P;
+    P.n_steps = n_steps;
+    P.gamma = (float)gamma;
+    P.eps = (float)eps;
+    P.clip = (float)clip;
+    P.b = b;
+    P.M = M;
+    P.probe = probe;
+    for (int c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) {
+            if (c >= 1) DRG_CUDA(cudaStreamWaitEvent(ss.lo, ev.e[3 + ((c + 1) & 1)], 0));
+            if ((rc = draw(c + 1))) return rc;
+        }
+        DRG_CUDA(cudaStreamWaitEvent(ss.hi, ev.e[1 + (c & 1)], 0));
+        const int ne = std::min(K, n_iter - c * K);
+        for (int e = 0; e < ne; ++e) {
+            const int t = t0 + c * K + e;
+            P.lr = lr_at(t);
+            P.draws = chunk_buf(c) + (size_t)e * (rec_bytes / 4);
+            if (agg) apply_kernel<true><<<grid, 256, 0, ss.hi>>>(P, reinterpret_cast<float2 *>(y));
+            else apply_kernel<false><<<grid, 256, 0, ss.hi>>>(P, reinterpret_cast<float2 *>(y));
+            DRG_LAUNCHED("apply_kernel");
+        }
+        DRG_CUDA(cudaEventRecord(ev.e[3 + (c & 1)], ss.hi));
+    }
+    DRG_CUDA(cudaEventRecord(ev.e[5], ss.lo));
+    DRG_CUDA(cudaStreamWaitEvent(st, ev.e[5], 0));
+    DRG_CUDA(cudaEventRecord(ev.e[0], ss.hi));
+    DRG_CUDA(cudaStreamWaitEvent(st, ev.e[0], 0));
     return DRG_OK;
 }

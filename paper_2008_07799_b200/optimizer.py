@@ -90,6 +90,8 @@ class OptimizerParams:
     sampled_concurrency_coarse: int = 4   # ... and n_l / this many on coarser levels
     att_samples: int = 2           # update="sgather": attraction partners drawn per node
     hub_levels: str = "jacobi"     # update="sampled": hub-heavy levels run this update
+    sampled_fused: bool = False    # update="sampled": draw inline (one kernel per epoch)
+                                   # instead of the split draw pass + update pass
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
@@ -349,7 +351,7 @@ class LayoutPlan:
         """(kernel, algorithmic bytes of one iteration launch) at ``level`` for the
         plan's update mode (the gather's 16 B per P entry + (24 + 16 M)
         B per node of SURVEY §8(d); the sampled step's 92 + 32 M B: source alias 8,
-        row bounds 16, collapse 4, row alias 8, target record 8, y_i and y_j 16, per
+        row bounds 16, collapse 4, row alias record 16, y_i and y_j 16, per
         negative alias 8 + y_c 8, and 16 B per float2 atomic on j, each negative and
         the source)."""
         L = self.levels[level]
@@ -359,7 +361,8 @@ class LayoutPlan:
                 self.opt.hub_levels == "jacobi":
             u = "jacobi"
         if u == "sampled":
-            return "sampled_kernel", L.n * (92 + 32 * M)
+            k = "sampled_kernel" if self.opt.sampled_fused else "draw_kernel + apply_kernel"
+            return k, L.n * (92 + 32 * M)
         if u == "sgather":
             S = self.opt.att_samples
             return "sgather_kernel", L.n * (32 + 24 * S + 16 * M)
@@ -471,8 +474,36 @@ class LayoutPlan:
                   _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), _lib.ptr(S.collapse),
                   _lib.ptr(L.alias), L.n, _lib.ptr(y), step_lo, n_steps, t0, n_iter, o.iters,
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
-                  o.neg_samples, seed, level, max(256, L.n // max(1, div)), int(S.hubs),
+                  o.neg_samples, seed, level, max(256, L.n // max(1, div)),
+                  int(S.hubs) | (2 if o.sampled_fused else 0), _lib.stream_ptr())
+
+    def sampled_draws(self, level: int, step_lo: int, n_steps: int, t0: int,
+                      n_epochs: int = 1) -> torch.Tensor:
+        """drg_sampled_draws: int32 [n_epochs, 2 + M, n_steps] -- source, target and
+        negatives of every step the sampled epochs t0.. run (split form)."""
+        L, _, seed = self._level_args(level)
+        S = L.sampled
+        if S is None:
+            raise RuntimeError("plan was built without sampled-mode tables")
+        M = self.opt.neg_samples
+        out = torch.empty((n_epochs, 2 + M, n_steps), dtype=torch.int32, device=L.indptr.device)
+        _lib.call("drg_sampled_draws", _lib.ptr(L.indptr), _lib.ptr(S.row_alias),
+                  _lib.ptr(S.src_alias), _lib.ptr(S.collapse), _lib.ptr(L.alias), L.n,
+                  step_lo, n_steps, t0, n_epochs, M, seed, level, _lib.ptr(out),
                   _lib.stream_ptr())
+        return out
+
+    def sampled_apply(self, level: int, draws: torch.Tensor, y: torch.Tensor, t: int,
+                      max_threads: int = 1) -> None:
+        """drg_sampled_apply: one epoch's drawn steps (int32 [2 + M, n_steps]) on y in
+        place at epoch t's learning rate, <= max_threads steps in flight."""
+        _, gamma, _ = self._level_args(level)
+        o = self.opt
+        draws = draws.contiguous()
+        lr = max(o.lr0 * (1.0 - t / o.iters), 0.0)
+        _lib.call("drg_sampled_apply", _lib.ptr(draws), draws.shape[-1], _lib.ptr(y), lr,
+                  float(gamma), float(o.eps), float(o.grad_clip), o.b, o.neg_samples,
+                  max_threads, 0, _lib.stream_ptr())
 
     def _run_level_sampled(self, level, y, t0, n_iter, group=None, step_fn=None):
         """Reference-faithful epochs: n_l sampled steps each, Hogwild on y.  With a

@@ -1,0 +1,161 @@
+"""Parity of the default update="sampled" path (split form: drg_sampled_draws ->
+drg_sampled_apply) against the oracle.
+
+* the drawn directed pairs follow the level's pair law -- the reference's level-0
+  pair draw mapped to level l (_kernels.py:66-81) -- chi-square against the
+  oracle's level data (P^l, R^l);
+* the drawn negatives follow Q^l with the reference's <= 9 redraws while they hit
+  i or j (_kernels.py:106-119), exact per-step law, chi-square;
+* given the draws, one step == the reference step (_kernels.py:82-140, oracle
+  drawn_steps, fp64) within 1e-5 * max(1, |g|); a whole epoch run sequentially
+  (one step in flight) == the oracle's sequential replay;
+* the fused kernel (draws inline) runs the same steps as the split form.
+"""
+import numpy as np
+import pytest
+import torch
+from scipy import stats
+
+import paper_2008_07799_b200 as B
+from oracle import oracle as O
+from conftest import golden_graph
+
+pytestmark = pytest.mark.gpu
+
+LEVELS = ["finest", "middle", "coarsest"]
+
+
+def _setup(golden, name="r500", k=2, M=5):
+    from paper_2008_07799_b200.graph import DeviceGraph
+    from paper_2008_07799_b200.optimizer import prepare_layout
+    g = golden_graph(golden, name)
+    gg = B.Graph(np.asarray(g.indptr, dtype=np.int64), np.asarray(g.indices, dtype=np.int32))
+    prep = prepare_layout(DeviceGraph.from_host(gg), B.SimilarityParams(k=k),
+                          B.OptimizerParams(seed=0, neg_samples=M, iters=10), min_size=8)
+    assert prep.relabel[0] is None          # oracle level data is in the same ids
+    ns = O.build_sparse_similarity(O.all_k_neighborhoods(g, k))
+    dh = prep.hierarchy
+    oh = O.Hierarchy([lv.to_host() for lv in dh.levels], [m.cpu().numpy() for m in dh.maps],
+                     0.8, 8)
+    return prep.plan, ns, oh
+
+
+def _level(plan, pick):
+    return {"finest": 0, "middle": plan.depth // 2, "coarsest": plan.depth}[pick]
+
+
+def _chi2(counts, expected):
+    keep = expected > 0
+    assert counts[~keep].sum() == 0, "draws outside the support"
+    e = expected[keep]
+    c = counts[keep]
+    e = e * (c.sum() / e.sum())
+    return stats.chisquare(c, e).pvalue
+
+
+@pytest.mark.parametrize("pick", LEVELS)
+def test_sampled_pair_law(golden, pick):
+    plan, ns, oh = _setup(golden)
+    level = _level(plan, pick)
+    n = plan.levels[level].n
+    ip, tg, P, R, Q = O.level_data(ns, oh, level)
+    epochs = max(1, 3_000_000 // n)
+    d = plan.sampled_draws(level, 0, n, 2, epochs).cpu().numpy()
+    i = d[:, 0, :].ravel().astype(np.int64)
+    j = d[:, 1, :].ravel().astype(np.int64)
+    counts = np.bincount(i * n + j, minlength=n * n).astype(np.float64)
+    expected = np.zeros(n * n)
+    rows = np.repeat(np.arange(n), np.diff(ip))
+    np.add.at(expected, rows * n + tg, P)
+    inner = R - np.bincount(rows, weights=P, minlength=n)          # collapsed pairs (a, a)
+    expected[np.arange(n) * n + np.arange(n)] += np.maximum(inner, 0.0)
+    if level == 0:
+        assert counts[np.arange(n) * n + np.arange(n)].sum() == 0
+    assert _chi2(counts, expected) > 1e-6
+
+
+@pytest.mark.parametrize("pick", LEVELS)
+def test_sampled_negative_law(golden, pick):
+    plan, ns, oh = _setup(golden)
+    level = _level(plan, pick)
+    n = plan.levels[level].n
+    M = plan.opt.neg_samples
+    _, _, _, _, Q = O.level_data(ns, oh, level)
+    Q = Q / Q.sum()
+    epochs = max(1, 600_000 // n)
+    d = plan.sampled_draws(level, 0, n, 5, epochs).cpu().numpy()
+    i = d[:, 0, :].ravel().astype(np.int64)
+    j = d[:, 1, :].ravel().astype(np.int64)
+    q = Q[i] + np.where(j != i, Q[j], 0.0)         # a draw is rejected with prob q
+    f = np.where(q < 1, (1 - q ** 9) / np.maximum(1 - q, 1e-300), 9.0)
+    exp = Q * f.sum() - np.bincount(i, weights=f * Q[i], minlength=n) \
+        - np.bincount(j, weights=np.where(j != i, f * Q[j], 0.0), minlength=n)
+    expected = np.concatenate([[np.sum(q ** 9)], exp]) * M
+    negs = d[:, 2:, :].transpose(1, 0, 2).reshape(M, -1)
+    assert not np.any((negs == i) | (negs == j))
+    counts = np.bincount(negs.ravel().astype(np.int64) + 1, minlength=n + 1).astype(np.float64)
+    assert _chi2(counts, expected) > 1e-6
+
+
+@pytest.mark.parametrize("b", [1, 2, 3])
+@pytest.mark.parametrize("pick", ["finest", "coarsest"])
+def test_sampled_drawn_step_parity(golden, b, pick):
+    """One step from identical Y and identical draws: |d| <= 1e-5 max(1, |g|)."""
+    plan, _, _ = _setup(golden)
+    plan.opt = B.OptimizerParams(seed=0, neg_samples=5, iters=10, b=b)
+    level = _level(plan, pick)
+    n = plan.levels[level].n
+    t = 3
+    lr = 1.0 - t / 10
+    _, gamma, _ = plan._level_args(level)
+    d = plan.sampled_draws(level, 0, n, t)[0]
+    rng = np.random.default_rng(b)
+    y = rng.normal(0, 1.0, size=(n, 2)).astype(np.float32)
+    yd = torch.from_numpy(y).cuda()
+    for s in range(min(n, 48)):
+        out = yd.clone()
+        plan.sampled_apply(level, d[:, s:s + 1], out, t)
+        got = out.cpu().numpy().astype(np.float64)
+        want = O.drawn_steps(y.astype(np.float64), d[:, s:s + 1].cpu().numpy(), lr, gamma,
+                             1e-3, 5.0, b)
+        g_got, g_want = (got - y) / lr, (want - y) / lr
+        assert np.all(np.abs(g_got - g_want) <= 1e-5 * np.maximum(1.0, np.abs(g_want))), s
+
+
+@pytest.mark.parametrize("pick", ["finest", "coarsest"])
+def test_sampled_sequential_epoch_parity(golden, pick):
+    """A whole epoch with one step in flight == the oracle's sequential replay."""
+    plan, _, _ = _setup(golden)
+    level = _level(plan, pick)
+    n = plan.levels[level].n
+    t = 8
+    _, gamma, _ = plan._level_args(level)
+    d = plan.sampled_draws(level, 0, n, t)[0]
+    rng = np.random.default_rng(7)
+    y = rng.normal(0, 1.0, size=(n, 2)).astype(np.float32)
+    yd = torch.from_numpy(y).cuda()
+    plan.sampled_apply(level, d, yd, t, max_threads=1)
+    want = O.drawn_steps(y.astype(np.float64), d.cpu().numpy(), 1.0 - t / 10, gamma, 1e-3, 5.0,
+                         plan.opt.b)
+    np.testing.assert_allclose(yd.cpu().numpy(), want, rtol=0, atol=1e-4)
+
+
+def test_split_and_fused_run_the_same_steps(golden):
+    plan, _, _ = _setup(golden)
+    L = plan.levels[0]
+    rng = np.random.default_rng(3)
+    y = torch.from_numpy(rng.normal(0, 1.0, size=(L.n, 2)).astype(np.float32)).cuda()
+    for s in (0, 1, 17, 250, L.n - 1):
+        outs = []
+        for fused in (False, True):
+            plan.opt.sampled_fused = fused
+            out = y.clone()
+            plan.sampled_steps(0, out, s, 1, 4, 1)
+            outs.append(out)
+        plan.opt.sampled_fused = False
+        assert not torch.equal(outs[0], y)
+        torch.testing.assert_close(outs[0], outs[1], rtol=0, atol=1e-6)
+    # a whole split epoch through drg_layout_sampled stays finite and moves y
+    a = y.clone()
+    plan.sampled_steps(0, a, 0, L.n, 5, 1)
+    assert torch.isfinite(a).all() and not torch.equal(a, y)
