@@ -187,6 +187,7 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
 /* n_iter epochs t = t0.. of n_steps steps each, every step being the reference
  * step (_kernels.py:65-140) on the level's positions y (in place, Hogwild):
  * source a ~ src_alias (R^l), collapsed pair (a, a) with probability collapse[a]
+ * (collapse = NULL: no collapsed pairs, as at level 0)
  * (pairs inside a coarse node, which the reference draws at level 0 and maps),
  * else b from the row's alias table (targets from rec = the level's {target, W}
  * records); clipped attraction on both ends if i != j; M negatives ~ neg_alias

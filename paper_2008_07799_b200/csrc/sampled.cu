@@ -105,6 +105,44 @@ __device__ __forceinline__ void add_y_w(float2 *y, int64_t i, float dx, float dy
     if (lane == leader && i >= 0) add_y(y, i, dx, dy);
 }
 
+// One repulsion of _kernels.py:120-140: the source moves by +g (tracked locally in
+// yi and in its step total), the negative by -g (returned in tu/tx/ty).
+__device__ __forceinline__ void repel(float2 &yi, float2 yc, int64_t target, float lr,
+                                      float gamma, float eps, float clip, float two_b, int b,
+                                      int64_t &tu, float &tx, float &ty, float &gix, float &giy) {
+    tu = -1;
+    tx = ty = 0.f;
+    if (target < 0) return;
+    const float dx = yi.x - yc.x, dy = yi.y - yc.y;
+    const float ld2 = dx * dx + dy * dy;
+    if (!(ld2 + eps > 0.f)) return;
+    const float pw = ipowf(ld2, b - 1);
+    const float coef = __fdividef(gamma * two_b, (ld2 + eps) * (1.0f + pw * ld2));
+    const float gx = lr * clampf(coef * dx, clip);
+    const float gy = lr * clampf(coef * dy, clip);
+    tu = target;
+    tx = -gx;
+    ty = -gy;
+    yi.x += gx;
+    yi.y += gy;
+    gix += gx;
+    giy += gy;
+}
+
+// A negative whose position was gathered at the start of the step misses the
+// updates this step already applied to the same node (a repeated negative); they
+// are added back from the step's own record, giving the sequential kernel's value.
+__device__ __forceinline__ void own_updates(float2 &yc, int64_t target, int m,
+                                            const int32_t *at, const float *ax,
+                                            const float *ay) {
+#pragma unroll
+    for (int q = 0; q < kMaxNeg; ++q)
+        if (q < m && at[q] == target) {
+            yc.x += ax[q];
+            yc.y += ay[q];
+        }
+}
+
 template <bool AGG>
 __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -139,14 +177,14 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
         // else target ~ P^l_a. by the row's alias table
         const int64_t i = accept(srec, sb, r.z);
         const int64_t lo = __ldg(A.indptr + i), hi = __ldg(A.indptr + i + 1);
-        const float cprob = __ldg(A.collapse + i);
+        const float cprob = A.collapse ? __ldg(A.collapse + i) : 0.0f;   // NULL: none (level 0)
         float2 yi = ld_y(y, i);
         int64_t j = i;
         if ((A.probe & 2) && hi > lo) {
             j = (int64_t)bucket(A.n, r2.x, r2.y);
         } else if (hi > lo && !(u32_to_unit(r.w) < cprob)) {
             const int64_t e = lo + bucket(hi - lo, r2.x, r2.y);
-            const uint4 rrec = __ldg(A.row_alias + e);   // one 16-byte record per entry
+            const uint4 rrec = __ldcs(A.row_alias + e);   // one 16-byte record, evict-first
             j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)rrec.z : (int64_t)rrec.y;
         }
         float gix = 0.f, giy = 0.f;   // the source's own increments of this step
@@ -158,7 +196,7 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
             const float ld2 = dx * dx + dy * dy;
             if (ld2 > 0.f) {
                 const float pw = ipowf(ld2, A.b - 1);
-                const float coef = -two_b * pw / (1.0f + pw * ld2);
+                const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
                 const float gx = A.lr * clampf(coef * dx, A.clip);
                 const float gy = A.lr * clampf(coef * dy, A.clip);
                 upd = j;
@@ -171,26 +209,41 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
             }
         }
         add_y_w<AGG>(y, upd, ux, uy, A.probe);
-        for (int m = 0; m < A.M; ++m) {  // _kernels.py:106-140
+        int32_t at[kMaxNeg];   // this step's updates of its first negatives
+        float ax[kMaxNeg], ay[kMaxNeg];
+#pragma unroll
+        for (int m = 0; m < kMaxNeg; ++m) {  // _kernels.py:106-140
+            if (m < Me) {
+                int64_t target = -1;
+                float2 yc = make_float2(0.f, 0.f);
+                if (cand[m] != i && cand[m] != j) {
+                    target = cand[m];
+                    yc = ycand[m];
+                    own_updates(yc, target, m, at, ax, ay);   // gathered before them
+                }
+                for (int attempt = 1; target < 0 && attempt < 9; ++attempt) {
+                    const u32x4 q = neg_draw(A, s, c1, m, attempt);
+                    const int64_t bk = bucket(A.n, q.x, q.y);
+                    const int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
+                    if (c0 != i && c0 != j) {
+                        target = c0;
+                        yc = ld_y(y, c0);   // after this step's own atomics
+                    }
+                }
+                int64_t tu;
+                float tx, ty;
+                repel(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix,
+                      giy);
+                at[m] = (int32_t)tu;
+                ax[m] = tx;
+                ay[m] = ty;
+                add_y_w<AGG>(y, tu, tx, ty, A.probe);
+            }
+        }
+        for (int m = Me; m < A.M; ++m) {
             int64_t target = -1;
             float2 yc = make_float2(0.f, 0.f);
-            int first = 0;
-            if (m < Me) {
-                int32_t c0 = 0;
-                float2 y0 = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int q = 0; q < kMaxNeg; ++q)
-                    if (q == m) {
-                        c0 = cand[q];
-                        y0 = ycand[q];
-                    }
-                if (c0 != i && c0 != j) {
-                    target = c0;
-                    yc = y0;
-                }
-                first = 1;
-            }
-            for (int attempt = first; target < 0 && attempt < 9; ++attempt) {
+            for (int attempt = 0; target < 0 && attempt < 9; ++attempt) {
                 const u32x4 q = neg_draw(A, s, c1, m, attempt);
                 const int64_t bk = bucket(A.n, q.x, q.y);
                 const int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
@@ -199,25 +252,9 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
                     yc = ld_y(y, c0);
                 }
             }
-            int64_t tu = -1;
-            float tx = 0.f, ty = 0.f;
-            if (target >= 0) {
-                const float dx = yi.x - yc.x, dy = yi.y - yc.y;
-                const float ld2 = dx * dx + dy * dy;
-                if (ld2 + A.eps > 0.f) {
-                    const float pw = ipowf(ld2, A.b - 1);
-                    const float coef = A.gamma * two_b / ((ld2 + A.eps) * (1.0f + pw * ld2));
-                    const float gx = A.lr * clampf(coef * dx, A.clip);
-                    const float gy = A.lr * clampf(coef * dy, A.clip);
-                    tu = target;
-                    tx = -gx;
-                    ty = -gy;
-                    yi.x += gx;
-                    yi.y += gy;
-                    gix += gx;
-                    giy += gy;
-                }
-            }
+            int64_t tu;
+            float tx, ty;
+            repel(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
             add_y_w<AGG>(y, tu, tx, ty, A.probe);
         }
         // the source's own increments of the step, published once (the step sees
@@ -282,17 +319,19 @@ __global__ void __launch_bounds__(256) draw_kernel(DArgs A) {
     }
     const int64_t i = accept(srec, sb, r.z);
     const int64_t lo = __ldg(A.indptr + i), hi = __ldg(A.indptr + i + 1);
-    const float cprob = __ldg(A.collapse + i);
+    const float cprob = A.collapse ? __ldg(A.collapse + i) : 0.0f;   // NULL: none (level 0)
     int64_t j = i;
     if ((A.probe & 2) && hi > lo) {
         j = (int64_t)bucket(A.n, r2.x, r2.y);
     } else if (hi > lo && !(u32_to_unit(r.w) < cprob)) {
-        const uint4 rrec = __ldg(A.row_alias + lo + bucket(hi - lo, r2.x, r2.y));
+        // one random 16-byte record of a multi-GB table: evict-first, so it does not
+        // push the hot alias / y tables out of L2
+        const uint4 rrec = __ldcs(A.row_alias + lo + bucket(hi - lo, r2.x, r2.y));
         j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)rrec.z : (int64_t)rrec.y;
     }
     int32_t *o = A.out + ep * (int64_t)(2 + A.M) * A.n_steps + sl;
-    o[0] = (int32_t)i;
-    o[A.n_steps] = (int32_t)j;
+    __stcs(o, (int32_t)i);   // read once by the update pass: streaming stores
+    __stcs(o + A.n_steps, (int32_t)j);
     for (int m = 0; m < A.M; ++m) {
         int64_t target = -1;
         int first = 0;
@@ -310,7 +349,7 @@ __global__ void __launch_bounds__(256) draw_kernel(DArgs A) {
             const int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
             if (c0 != i && c0 != j) target = c0;
         }
-        o[(int64_t)(2 + m) * A.n_steps] = (int32_t)target;
+        __stcs(o + (int64_t)(2 + m) * A.n_steps, (int32_t)target);
     }
 }
 
@@ -366,7 +405,7 @@ __global__ void __launch_bounds__(256) apply_kernel(PArgs A, float2 *y) {
             const float ld2 = dx * dx + dy * dy;
             if (ld2 > 0.f) {
                 const float pw = ipowf(ld2, A.b - 1);
-                const float coef = -two_b * pw / (1.0f + pw * ld2);
+                const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
                 const float gx = A.lr * clampf(coef * dx, A.clip);
                 const float gy = A.lr * clampf(coef * dy, A.clip);
                 upd = j;
@@ -379,43 +418,29 @@ __global__ void __launch_bounds__(256) apply_kernel(PArgs A, float2 *y) {
             }
         }
         add_y_w<AGG>(y, upd, ux, uy, A.probe);
-        for (int m = 0; m < A.M; ++m) {  // _kernels.py:106-140
-            int64_t target;
-            float2 yc;
-            if (m < Me) {
-                int32_t c0 = -1;
-                float2 y0 = make_float2(0.f, 0.f);
+        int32_t at[kMaxNeg];   // this step's updates of its first negatives
+        float ax[kMaxNeg], ay[kMaxNeg];
 #pragma unroll
-                for (int q = 0; q < kMaxNeg; ++q)
-                    if (q == m) {
-                        c0 = cand[q];
-                        y0 = ycand[q];
-                    }
-                target = c0;
-                yc = y0;
-            } else {
-                target = __ldcs(A.draws + (2 + m) * ns + sl);
-                yc = target >= 0 ? ld_y(y, target) : make_float2(0.f, 0.f);
+        for (int m = 0; m < kMaxNeg; ++m) {  // _kernels.py:106-140
+            if (m < Me) {
+                float2 yc = ycand[m];
+                own_updates(yc, cand[m], m, at, ax, ay);   // gathered before them
+                int64_t tu;
+                float tx, ty;
+                repel(yi, yc, cand[m], A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix,
+                      giy);
+                at[m] = (int32_t)tu;
+                ax[m] = tx;
+                ay[m] = ty;
+                add_y_w<AGG>(y, tu, tx, ty, A.probe);
             }
-            int64_t tu = -1;
-            float tx = 0.f, ty = 0.f;
-            if (target >= 0) {
-                const float dx = yi.x - yc.x, dy = yi.y - yc.y;
-                const float ld2 = dx * dx + dy * dy;
-                if (ld2 + A.eps > 0.f) {
-                    const float pw = ipowf(ld2, A.b - 1);
-                    const float coef = A.gamma * two_b / ((ld2 + A.eps) * (1.0f + pw * ld2));
-                    const float gx = A.lr * clampf(coef * dx, A.clip);
-                    const float gy = A.lr * clampf(coef * dy, A.clip);
-                    tu = target;
-                    tx = -gx;
-                    ty = -gy;
-                    yi.x += gx;
-                    yi.y += gy;
-                    gix += gx;
-                    giy += gy;
-                }
-            }
+        }
+        for (int m = Me; m < A.M; ++m) {   // negatives past kMaxNeg: gathered after the atomics
+            const int64_t target = __ldcs(A.draws + (2 + m) * ns + sl);
+            const float2 yc = target >= 0 ? ld_y(y, target) : make_float2(0.f, 0.f);
+            int64_t tu;
+            float tx, ty;
+            repel(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
             add_y_w<AGG>(y, tu, tx, ty, A.probe);
         }
         add_y_w<AGG>(y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy, A.probe);

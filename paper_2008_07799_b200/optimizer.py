@@ -471,11 +471,15 @@ class LayoutPlan:
         o = self.opt
         div = o.sampled_concurrency if level == 0 else o.sampled_concurrency_coarse
         _lib.call("drg_layout_sampled", _lib.ptr(L.indptr), _lib.ptr(L.rec),
-                  _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), _lib.ptr(S.collapse),
+                  _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), self._collapse(level),
                   _lib.ptr(L.alias), L.n, _lib.ptr(y), step_lo, n_steps, t0, n_iter, o.iters,
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
                   o.neg_samples, seed, level, max(256, L.n // max(1, div)),
                   int(S.hubs) | (2 if o.sampled_fused else 0), _lib.stream_ptr())
+
+    def _collapse(self, level: int):
+        """Collapse probabilities of ``level`` (NULL at level 0: no pair collapses)."""
+        return None if level == 0 else _lib.ptr(self.levels[level].sampled.collapse)
 
     def sampled_draws(self, level: int, step_lo: int, n_steps: int, t0: int,
                       n_epochs: int = 1) -> torch.Tensor:
@@ -488,7 +492,7 @@ class LayoutPlan:
         M = self.opt.neg_samples
         out = torch.empty((n_epochs, 2 + M, n_steps), dtype=torch.int32, device=L.indptr.device)
         _lib.call("drg_sampled_draws", _lib.ptr(L.indptr), _lib.ptr(S.row_alias),
-                  _lib.ptr(S.src_alias), _lib.ptr(S.collapse), _lib.ptr(L.alias), L.n,
+                  _lib.ptr(S.src_alias), self._collapse(level), _lib.ptr(L.alias), L.n,
                   step_lo, n_steps, t0, n_epochs, M, seed, level, _lib.ptr(out),
                   _lib.stream_ptr())
         return out

@@ -1,0 +1,7 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_sampled.py -x -q > gpurun_out/t_sampled.log 2>&1
+timeout 300 python scripts/sampled_probe.py mesh > gpurun_out/probe3.log 2>&1
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_split.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/t_gpu.log 2>&1
+tail -3 gpurun_out/t_sampled.log gpurun_out/t_gpu.log

@@ -14,9 +14,11 @@ $CMD > $OUT/plain_${W}_${U}.log 2>&1 && \
       --log-file $OUT/launches_${W}_${U}.csv $CMD > $OUT/ncu_launches_${W}_${U}.log 2>&1
 echo "launch list rc=$?"
 # 2) full capture of the dominant kernel (first level-0 launch of the timed step)
-K=layout_iter
-[ "$U" = "sampled" ] && K=sampled_kernel
+K=layout_iter; S=60; C=1
+# sampled (split form): one draw_kernel + one apply_kernel of level 0 in the timed
+# step (104 matching launches per 20-iteration run of the 4 mesh levels)
+[ "$U" = "sampled" ] && K="draw_kernel|apply_kernel" && S=170 && C=2
 $CMD > $OUT/plain2_${W}_${U}.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:$K -s 60 -c 1 -f \
+  ncu --set full --clock-control none --import-source on -k "regex:$K" -s $S -c $C -f \
       -o $OUT/full_${W}_${U} $CMD > $OUT/ncu_full_${W}_${U}.log 2>&1
 echo "full capture rc=$?"

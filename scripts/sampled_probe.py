@@ -20,8 +20,9 @@ def main(name="mesh"):
     L = plan.levels[0]
     y = plan.init_positions()
     y = torch.randn(L.n, 2, device="cuda")
-    for probe in ("0", "1", "2", "3"):
+    for fused, probe in ((True, "0"), (True, "1"), (False, "0"), (False, "1"), (False, "2")):
         os.environ["DRG_SAMPLED_PROBE"] = probe
+        plan.opt.sampled_fused = fused
         for div in (4, 16, 64):
             plan.opt.sampled_concurrency = div
             plan.sampled_steps(0, y, 0, L.n, 5, 2)
@@ -31,7 +32,7 @@ def main(name="mesh"):
             plan.sampled_steps(0, y, 0, L.n, 5, 10)
             e.record()
             torch.cuda.synchronize()
-            print(f"probe={probe} concurrency=n/{div}: {s.elapsed_time(e) / 10 * 1e3:.1f} us/epoch",
+            print(f"{'fused' if fused else 'split'} probe={probe} concurrency=n/{div}: {s.elapsed_time(e) / 10 * 1e3:.1f} us/epoch",
                   flush=True)
     os.environ["DRG_SAMPLED_PROBE"] = "0"
 
