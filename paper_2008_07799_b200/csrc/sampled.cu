@@ -131,7 +131,8 @@ __device__ __forceinline__ void repel(float2 &yi, float2 yc, int64_t target, flo
 
 // A negative whose position was gathered at the start of the step misses the
 // updates this step already applied to the same node (a repeated negative); they
-// are added back from the step's own record, giving the sequential kernel's value.
+// are added back from the step's own record (ax/ay = 0 where nothing was applied),
+// giving the sequential kernel's value.
 __device__ __forceinline__ void own_updates(float2 &yc, int64_t target, int m,
                                             const int32_t *at, const float *ax,
                                             const float *ay) {
@@ -291,7 +292,10 @@ struct DArgs {
     int32_t *out;
 };
 
-__global__ void __launch_bounds__(256) draw_kernel(DArgs A) {
+// small blocks: they fit beside the update pass's resident blocks
+constexpr int kDrawBlock = 128;
+
+__global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= A.n_steps * A.n_epochs) return;
     const int64_t ep = g / A.n_steps, sl = g - ep * A.n_steps;
@@ -366,12 +370,11 @@ struct PArgs {
 // other end by the opposite clipped increment; the source's own total is published
 // once.  The next step's draw record is prefetched while this step runs.
 template <bool AGG>
-__global__ void __launch_bounds__(256) apply_kernel(PArgs A, float2 *y) {
-    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+__device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t sl,
+                                            const int64_t nthreads) {
     const float two_b = 2.0f * (float)A.b;
     const int Me = min(A.M, kMaxNeg);
     const int64_t ns = A.n_steps;
-    int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (sl >= ns) return;
     int32_t ci = __ldcs(A.draws + sl), cj = __ldcs(A.draws + ns + sl);
     int32_t cc[kMaxNeg];
@@ -418,18 +421,16 @@ __global__ void __launch_bounds__(256) apply_kernel(PArgs A, float2 *y) {
             }
         }
         add_y_w<AGG>(y, upd, ux, uy, A.probe);
-        int32_t at[kMaxNeg];   // this step's updates of its first negatives
-        float ax[kMaxNeg], ay[kMaxNeg];
+        float ax[kMaxNeg], ay[kMaxNeg];   // this step's updates of its first negatives
 #pragma unroll
         for (int m = 0; m < kMaxNeg; ++m) {  // _kernels.py:106-140
             if (m < Me) {
                 float2 yc = ycand[m];
-                own_updates(yc, cand[m], m, at, ax, ay);   // gathered before them
+                own_updates(yc, cand[m], m, cand, ax, ay);   // gathered before them
                 int64_t tu;
                 float tx, ty;
                 repel(yi, yc, cand[m], A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix,
                       giy);
-                at[m] = (int32_t)tu;
                 ax[m] = tx;
                 ay[m] = ty;
                 add_y_w<AGG>(y, tu, tx, ty, A.probe);
@@ -444,6 +445,50 @@ __global__ void __launch_bounds__(256) apply_kernel(PArgs A, float2 *y) {
             add_y_w<AGG>(y, tu, tx, ty, A.probe);
         }
         add_y_w<AGG>(y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy, A.probe);
+    }
+}
+
+template <bool AGG>
+__global__ void __launch_bounds__(256, 4) apply_kernel(PArgs A, float2 *y) {
+    apply_epoch<AGG>(A, y, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                     (int64_t)gridDim.x * blockDim.x);
+}
+
+// Grid-wide barrier of a cooperative launch: `count` starts at 0; after barrier e
+// it holds (e + 1) * gridDim.x.  The fences order this epoch's atomics on y before
+// the next epoch's gathers.
+__device__ __forceinline__ void grid_barrier(unsigned *count, unsigned e) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned target = (e + 1) * gridDim.x;
+        __threadfence();
+        atomicAdd(count, 1u);
+        while (*(volatile unsigned *)count < target) __nanosleep(20);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+struct EArgs {
+    int t0, n_epochs, iters;
+    double lr0;
+    unsigned *bar;
+};
+
+// Several consecutive epochs in one persistent cooperative launch (small levels:
+// an epoch is a few steps per thread, so per-epoch launch gaps would dominate).
+// A.draws = the first epoch's records; epoch e's follow at e * (2 + M) * n_steps.
+template <bool AGG>
+__global__ void __launch_bounds__(256, 4) apply_epochs_kernel(PArgs A, float2 *y, EArgs E) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    const int32_t *base = A.draws;
+    for (int e = 0; e < E.n_epochs; ++e) {
+        PArgs P = A;
+        P.draws = base + (size_t)e * (size_t)(2 + A.M) * (size_t)A.n_steps;
+        P.lr = (float)fmax(E.lr0 * (1.0 - (double)(E.t0 + e) / (double)E.iters), 0.0);
+        apply_epoch<AGG>(P, y, tid, nth);
+        if (e + 1 < E.n_epochs) grid_barrier(E.bar, (unsigned)e);
     }
 }
 
@@ -697,7 +742,7 @@ extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alia
     D.t_first = t0;
     D.probe = 0;
     D.out = out;
-    draw_kernel<<<(unsigned)ceil_div(n_steps * (int64_t)n_epochs, 256), 256, 0, as_stream(stream)>>>(D);
+    draw_kernel<<<(unsigned)ceil_div(n_steps * (int64_t)n_epochs, kDrawBlock), kDrawBlock, 0, as_stream(stream)>>>(D);
     DRG_LAUNCHED("draw_kernel");
     return DRG_OK;
 }
@@ -781,8 +826,9 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     const size_t rec_bytes = (size_t)(2 + M) * sizeof(int32_t) * (size_t)n_steps;
     const int K = (int)std::max<int64_t>(1, std::min<int64_t>(n_iter, (int64_t)(kDrawBudget / rec_bytes)));
     const int nchunks = (n_iter + K - 1) / K;
-    Scratch buf(st);
+    Scratch buf(st), bar(st);
     DRG_CUDA(buf.alloc(rec_bytes * (size_t)K * (nchunks > 1 ? 2 : 1)));
+    DRG_CUDA(bar.alloc(sizeof(unsigned)));
     SideStreams ss;
     DRG_CUDA(side_streams(&ss));
     Events ev;   // 0 start, 1-2 drawn[2], 3-4 applied[2], 5 draws done
@@ -809,7 +855,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
         D.t_first = t0 + c * K;
         D.n_epochs = std::min(K, n_iter - c * K);
         D.out = chunk_buf(c);
-        draw_kernel<<<(unsigned)ceil_div(D.n_steps * D.n_epochs, 256), 256, 0, ss.lo>>>(D);
+        draw_kernel<<<(unsigned)ceil_div(D.n_steps * D.n_epochs, kDrawBlock), kDrawBlock, 0, ss.lo>>>(D);
         DRG_LAUNCHED("draw_kernel");
         DRG_CUDA(cudaEventRecord(ev.e[1 + (c & 1)], ss.lo));
         return DRG_OK;
@@ -831,6 +877,20 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
         }
         DRG_CUDA(cudaStreamWaitEvent(ss.hi, ev.e[1 + (c & 1)], 0));
         const int ne = std::min(K, n_iter - c * K);
+        if (ne > 1 && grid <= (unsigned)kSMs) {   // small level: one persistent launch
+            DRG_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(unsigned), ss.hi));
+            P.draws = chunk_buf(c);
+            P.lr = 0.f;
+            EArgs E{t0 + c * K, ne, iters, lr0, bar.as<unsigned>()};
+            float2 *yy = reinterpret_cast<float2 *>(y);
+            void *args[] = {&P, &yy, &E};
+            DRG_CUDA(cudaLaunchCooperativeKernel(
+                agg ? (const void *)apply_epochs_kernel<true> : (const void *)apply_epochs_kernel<false>,
+                dim3(grid), dim3(256), args, 0, ss.hi));
+            DRG_LAUNCHED("apply_epochs_kernel");
+            DRG_CUDA(cudaEventRecord(ev.e[3 + (c & 1)], ss.hi));
+            continue;
+        }
         for (int e = 0; e < ne; ++e) {
             const int t = t0 + c * K + e;
             P.lr = lr_at(t);

@@ -1,0 +1,12 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_sampled.py -q -x > gpurun_out/t_sampled.log 2>&1
+timeout 300 python scripts/split_probe.py mesh > gpurun_out/split_probe3.log 2>&1
+timeout 900 python bench.py --no-cpu-baseline --no-alt > gpurun_out/bench_split3.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/t_gpu.log 2>&1
+tail -2 gpurun_out/t_sampled.log gpurun_out/t_gpu.log; grep level gpurun_out/split_probe3.log
+python -c "
+import json
+for l in open('gpurun_out/bench_split3.log'):
+    if l.startswith('{'):
+        d=json.loads(l); print(d['value'], d['ms_per_step'], d['level_ms_last_step'], d['roofline']['launch_us'], d['roofline']['frac'], d['e2e']['value'])
+"
