@@ -454,44 +454,6 @@ __global__ void __launch_bounds__(256, 4) apply_kernel(PArgs A, float2 *y) {
                      (int64_t)gridDim.x * blockDim.x);
 }
 
-// Grid-wide barrier of a cooperative launch: `count` starts at 0; after barrier e
-// it holds (e + 1) * gridDim.x.  The fences order this epoch's atomics on y before
-// the next epoch's gathers.
-__device__ __forceinline__ void grid_barrier(unsigned *count, unsigned e) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned target = (e + 1) * gridDim.x;
-        __threadfence();
-        atomicAdd(count, 1u);
-        while (*(volatile unsigned *)count < target) __nanosleep(20);
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-struct EArgs {
-    int t0, n_epochs, iters;
-    double lr0;
-    unsigned *bar;
-};
-
-// Several consecutive epochs in one persistent cooperative launch (small levels:
-// an epoch is a few steps per thread, so per-epoch launch gaps would dominate).
-// A.draws = the first epoch's records; epoch e's follow at e * (2 + M) * n_steps.
-template <bool AGG>
-__global__ void __launch_bounds__(256, 4) apply_epochs_kernel(PArgs A, float2 *y, EArgs E) {
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    const int32_t *base = A.draws;
-    for (int e = 0; e < E.n_epochs; ++e) {
-        PArgs P = A;
-        P.draws = base + (size_t)e * (size_t)(2 + A.M) * (size_t)A.n_steps;
-        P.lr = (float)fmax(E.lr0 * (1.0 - (double)(E.t0 + e) / (double)E.iters), 0.0);
-        apply_epoch<AGG>(P, y, tid, nth);
-        if (e + 1 < E.n_epochs) grid_barrier(E.bar, (unsigned)e);
-    }
-}
-
 // Thread per row: Vose's construction over the row's entries (optimizer.py:111-139,
 // same stack discipline: small / large lists in index order, popped from the back),
 // fp64 scaled weights in scratch, stacks in the caller's int32 scratch (the small
@@ -826,9 +788,8 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     const size_t rec_bytes = (size_t)(2 + M) * sizeof(int32_t) * (size_t)n_steps;
     const int K = (int)std::max<int64_t>(1, std::min<int64_t>(n_iter, (int64_t)(kDrawBudget / rec_bytes)));
     const int nchunks = (n_iter + K - 1) / K;
-    Scratch buf(st), bar(st);
+    Scratch buf(st);
     DRG_CUDA(buf.alloc(rec_bytes * (size_t)K * (nchunks > 1 ? 2 : 1)));
-    DRG_CUDA(bar.alloc(sizeof(unsigned)));
     SideStreams ss;
     DRG_CUDA(side_streams(&ss));
     Events ev;   // 0 start, 1-2 drawn[2], 3-4 applied[2], 5 draws done
@@ -877,20 +838,6 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
         }
         DRG_CUDA(cudaStreamWaitEvent(ss.hi, ev.e[1 + (c & 1)], 0));
         const int ne = std::min(K, n_iter - c * K);
-        if (ne > 1 && grid <= (unsigned)kSMs) {   // small level: one persistent launch
-            DRG_CUDA(cudaMemsetAsync(bar.p, 0, sizeof(unsigned), ss.hi));
-            P.draws = chunk_buf(c);
-            P.lr = 0.f;
-            EArgs E{t0 + c * K, ne, iters, lr0, bar.as<unsigned>()};
-            float2 *yy = reinterpret_cast<float2 *>(y);
-            void *args[] = {&P, &yy, &E};
-            DRG_CUDA(cudaLaunchCooperativeKernel(
-                agg ? (const void *)apply_epochs_kernel<true> : (const void *)apply_epochs_kernel<false>,
-                dim3(grid), dim3(256), args, 0, ss.hi));
-            DRG_LAUNCHED("apply_epochs_kernel");
-            DRG_CUDA(cudaEventRecord(ev.e[3 + (c & 1)], ss.hi));
-            continue;
-        }
         for (int e = 0; e < ne; ++e) {
             const int t = t0 + c * K + e;
             P.lr = lr_at(t);
