@@ -275,6 +275,36 @@ int drg_neighborhood_preservation(const float *y, int64_t n, const int64_t *hop_
  * lie in [0, n). */
 int drg_from_edges(const int64_t *pairs, int64_t m, int64_t n, int64_t *out_indptr,
                    int32_t *out_indices, int64_t *out_nnz, void *stream);
+/* --- text ingestion (graph.py:128-243) -----------------------------
+ * drg_text_lines: line starts of UTF-8 text (device bytes).  mode 0 = str.splitlines
+ * (graph.py:128-131 on the text cli.py:194 reads: \n, \r, \r\n, \v, \f, \x1c-\x1e,
+ * U+0085, U+2028, U+2029), mode 1 = "\n" only (text-stream iteration).  *out_count
+ * (host) = number of lines (a final break opens no line); out_starts (device int64
+ * [*out_count], NULL: count only).  out_bad_byte (host, NULL: no check) = offset of
+ * the first byte that is not strict UTF-8 (-1: valid; else nothing else is done). */
+int drg_text_lines(const uint8_t *text, int64_t nbytes, int mode, int64_t *out_starts,
+                   int64_t *out_count, int64_t *out_bad_byte, void *stream);
+/* drg_parse_lines: lines [starts[l], starts[l+1]) (the last ends at nbytes) parsed as
+ * kind 0 = edge list (graph.py:134-167: blank and '#'/'%' lines skipped, exactly two
+ * int() ids, none negative) or kind 1 = MatrixMarket entry lines (graph.py:218-241:
+ * blank and '%' lines skipped, >= 2 parts, 1 <= i, j <= rows, at most `declared`).
+ * int() = Python's grammar over Unicode decimal digits with single underscores.
+ * out_pairs (device int64 [n_lines][2]) receives the accepted ids in line order
+ * (0-based for kind 1), *out_m (host) their count.  The first failing line (index,
+ * host *out_err_line, -1 if none) and its status (*out_err_status: 2 token count,
+ * 3 malformed integer, 4 negative id, 5 index out of range, 6 beyond the declared
+ * entries) let the caller raise the reference's ParseError; *out_overflow (host) = an
+ * accepted edge-list id exceeds 2^63 - 1. */
+int drg_parse_lines(const uint8_t *text, int64_t nbytes, const int64_t *starts, int64_t n_lines,
+                    int kind, int64_t rows, int64_t declared, int64_t *out_pairs, int64_t *out_m,
+                    int64_t *out_err_line, int32_t *out_err_status, int32_t *out_overflow,
+                    void *stream);
+/* drg_id_remap: node count of from_edges without an explicit count (graph.py:90-103)
+ * for m device pairs: *out_n (host) = max id + 1, or -- remap_sparse != 0 and max id
+ * > 2 * distinct ids -- the distinct count, the ids then compacted in place to their
+ * rank among the distinct ids.  A negative id returns DRG_ERR_INVALID. */
+int drg_id_remap(int64_t *pairs, int64_t m, int remap_sparse, int64_t *out_n, void *stream);
+
 /* connected_components (graph.py:369-388): out_labels[n] (device, may be NULL)
  * numbered 0..C-1 in first-seen order (component of the smallest unlabelled id),
  * *out_count (host) = C.  layout_graph uses it for a warning and

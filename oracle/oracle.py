@@ -133,6 +133,123 @@ def from_edges(pairs, node_count: int | None = None) -> Graph:
     return Graph(indptr=indptr, indices=dst.astype(np.int32))
 
 
+# ---------------------------------------------------------------------------
+# Text parsers (graph.py:128-243), restated for the parse parity tests
+# ---------------------------------------------------------------------------
+
+class OracleParseError(ValueError):
+    """graph.py:17-24: message prefixed with 'line N: ' when the line is known."""
+
+    def __init__(self, message, line=None):
+        self.line = line
+        super().__init__(message if line is None else f"line {line}: {message}")
+
+
+def _source_lines(source):
+    """graph.py:128-131: a str splits by str.splitlines, anything else iterates."""
+    return source.splitlines() if isinstance(source, str) else list(source)
+
+
+def _as_int(tok):
+    try:
+        return int(tok)
+    except ValueError:
+        return None
+
+
+def remap_node_count(pairs):
+    """Node count and (possibly compacted) pairs of from_edges(remap_sparse_ids=True)
+    (graph.py:90-103)."""
+    if pairs.size == 0:
+        return 0, pairs
+    ids = np.unique(pairs)
+    if ids[-1] > 2 * len(ids):
+        if ids[-1] == np.iinfo(np.int64).max:   # numpy cannot size the lookup table
+            raise ValueError("Maximum allowed dimension exceeded")
+        return len(ids), np.searchsorted(ids, pairs)
+    return int(ids[-1]) + 1, pairs
+
+
+def parse_edge_list(source) -> Graph:
+    """graph.py:134-167."""
+    ids = []
+    for k, raw in enumerate(_source_lines(source)):
+        body = raw.strip()
+        if body == "" or body[0] == "#" or body[0] == "%":
+            continue
+        toks = body.split()
+        if len(toks) != 2:
+            raise OracleParseError(f"expected two ids, got {len(toks)} tokens", k + 1)
+        a, b = _as_int(toks[0]), _as_int(toks[1])
+        if a is None or b is None:
+            raise OracleParseError(f"malformed integer in {toks!r}", k + 1)
+        if min(a, b) < 0:
+            raise OracleParseError(f"negative node id in {toks!r}", k + 1)
+        ids += (a, b)
+    if not ids:
+        return Graph(np.zeros(1, dtype=np.int64), np.empty(0, dtype=np.int32))
+    pairs = np.array(ids, dtype=np.int64).reshape(-1, 2)
+    n, pairs = remap_node_count(pairs)
+    return from_edges(pairs, n)
+
+
+def parse_matrix_market(source) -> Graph:
+    """graph.py:170-243."""
+    lines = _source_lines(source)
+    if not lines:
+        raise OracleParseError("empty file, missing MatrixMarket header")
+    head = lines[0].strip().split()
+    if len(head) < 5 or head[0] != "%%MatrixMarket":
+        raise OracleParseError("missing '%%MatrixMarket' header", 1)
+    obj, fmt, fld, sym = (t.lower() for t in head[1:5])
+    if (obj, fmt) != ("matrix", "coordinate"):
+        raise OracleParseError(f"unsupported MatrixMarket type '{obj} {fmt}'"
+                               " (need 'matrix coordinate')", 1)
+    if fld not in ("pattern", "real", "integer", "complex"):
+        raise OracleParseError(f"unsupported field '{fld}'", 1)
+    if sym not in ("general", "symmetric", "skew-symmetric", "hermitian"):
+        raise OracleParseError(f"unsupported symmetry '{sym}'", 1)
+    k, size = 1, None
+    while k < len(lines):
+        body = lines[k].strip()
+        k += 1
+        if body == "" or body.startswith("%"):
+            continue
+        parts = body.split()
+        if len(parts) != 3:
+            raise OracleParseError("size line must be 'rows cols nnz'", k)
+        size = [_as_int(p) for p in parts]
+        if None in size:
+            raise OracleParseError(f"malformed size line {body!r}", k)
+        break
+    if size is None:
+        raise OracleParseError("missing size line")
+    rows, cols, declared = size
+    if rows != cols:
+        raise OracleParseError(f"adjacency matrix must be square, got {rows}x{cols}", k)
+    if rows < 0 or declared < 0:
+        raise OracleParseError("negative dimension in size line", k)
+    ids = []
+    for j in range(k, len(lines)):
+        body = lines[j].strip()
+        if body == "" or body.startswith("%"):
+            continue
+        if len(ids) // 2 >= declared:
+            raise OracleParseError(f"more than the declared {declared} entries", j + 1)
+        parts = body.split()
+        if len(parts) < 2:
+            raise OracleParseError("coordinate entry needs at least 'i j'", j + 1)
+        a, b = _as_int(parts[0]), _as_int(parts[1])
+        if a is None or b is None:
+            raise OracleParseError(f"malformed coordinate entry {body!r}", j + 1)
+        if not (1 <= a <= rows and 1 <= b <= cols):
+            raise OracleParseError(f"index ({a}, {b}) outside declared {rows}x{cols}", j + 1)
+        ids += (a - 1, b - 1)
+    if len(ids) // 2 != declared:
+        raise OracleParseError(f"declared {declared} entries but found {len(ids) // 2}")
+    return from_edges(np.array(ids, dtype=np.int64).reshape(-1, 2), rows)
+
+
 def connected_components(g: Graph) -> int:
     """Component count (graph.py:369-388), via scipy's C implementation."""
     from scipy.sparse import csr_matrix

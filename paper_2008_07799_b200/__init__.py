@@ -7,7 +7,8 @@ kernels in ``libdrgraph_b200.so`` (C ABI: include/drgraph_b200.h) -- no CPU path
 
 from .graph import (DeviceGraph, DeviceNeighborDistances, Graph, NeighborDistances, ParseError,
                     all_k_neighborhoods, connected_components, device_from_edges,
-                    device_k_neighborhoods, from_edges)
+                    device_k_neighborhoods, from_edges, parse_edge_list, parse_matrix_market,
+                    read_graph)
 from .multilevel import (DeviceHierarchy, Hierarchy, build_hierarchy, coarsen_once,
                          coarsen_with_order, compose_maps, device_build_hierarchy, prolong)
 from .optimizer import (AliasTable, Layout, LayoutPlan, OptimizerParams, Samplers,
@@ -19,7 +20,8 @@ from .similarity import (DeviceSimilarity, SimilarityParams, SparseSimilarity,
 __version__ = "0.1.0"
 
 __all__ = [
-    "Graph", "NeighborDistances", "ParseError", "from_edges", "all_k_neighborhoods",
+    "Graph", "NeighborDistances", "ParseError", "from_edges", "parse_edge_list",
+    "parse_matrix_market", "read_graph", "all_k_neighborhoods",
     "connected_components", "SimilarityParams", "SparseSimilarity", "build_sparse_similarity",
     "Hierarchy", "coarsen_once", "coarsen_with_order", "build_hierarchy", "compose_maps",
     "prolong", "OptimizerParams", "Layout", "AliasTable", "build_alias_table",

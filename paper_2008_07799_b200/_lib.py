@@ -60,6 +60,9 @@ SIGNATURES = {
     "drg_sampled_draws": [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _U64, _I32, _P,
                           _P],
     "drg_sampled_apply": [_P, _I64, _P, _F64, _F64, _F64, _F64, _I32, _I32, _I64, _I32, _P],
+    "drg_text_lines": [_P, _I64, _I32, _P, _P, _P, _P],
+    "drg_parse_lines": [_P, _I64, _P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P],
+    "drg_id_remap": [_P, _I64, _I32, _P, _P],
     "drg_layout_sgather": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _I32, _I32, _I32,
                            _F64, _F64, _F64, _F64, _I32, _I32, _I32, _U64, _I32, _P, _P, _U32,
                            _P],
@@ -152,6 +155,10 @@ def launch_count() -> int:
 
 class HostInt64(ctypes.c_int64):
     pass
+
+
+def out_i32() -> ctypes.c_int32:
+    return ctypes.c_int32(0)
 
 
 def out_i64() -> ctypes.c_int64:

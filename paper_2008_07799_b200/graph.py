@@ -119,6 +119,24 @@ def device_from_edges(pairs: torch.Tensor, node_count: int) -> DeviceGraph:
     return DeviceGraph(indptr, out[:nnz.value].clone())
 
 
+def device_remap_ids(pairs: torch.Tensor, remap_sparse_ids: bool) -> int:
+    """node_count of from_edges without an explicit count (graph.py:90-103), on the
+    device: distinct ids by radix sort + unique; with ``remap_sparse_ids`` and
+    max id > 2 * distinct the ids are compacted in place (lower bound in the
+    distinct ids == the reference's lookup table).  Raises on a negative id."""
+    n = _lib.out_i64()
+    try:
+        _lib.call("drg_id_remap", _lib.ptr(pairs), pairs.numel() // 2, int(remap_sparse_ids),
+                  _lib.byref(n), _lib.stream_ptr())
+    except ValueError as e:
+        if "negative node id" in str(e):
+            raise ParseError("negative node id") from None
+        if "Maximum allowed dimension exceeded" in str(e):
+            raise ValueError("Maximum allowed dimension exceeded") from None
+        raise
+    return n.value
+
+
 def from_edges(pairs, node_count: int | None = None, remap_sparse_ids: bool = False) -> Graph:
     """Canonical CSR from (u, v) pairs (graph.py:80-125), built on the GPU.
 
@@ -126,24 +144,210 @@ def from_edges(pairs, node_count: int | None = None, remap_sparse_ids: bool = Fa
     ``remap_sparse_ids`` ids are compacted when the max id exceeds twice the
     distinct-id count (graph.py:94-100)."""
     pairs = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
-    if pairs.size and pairs.min() < 0:
-        raise ParseError("negative node id")
-    if node_count is None:
-        if pairs.size == 0:
-            node_count = 0
-        else:
-            distinct = np.unique(pairs)
-            max_id = int(distinct[-1])
-            if remap_sparse_ids and max_id > 2 * len(distinct):
-                lookup = np.full(max_id + 1, -1, dtype=np.int64)
-                lookup[distinct] = np.arange(len(distinct))
-                pairs = lookup[pairs]
-                node_count = len(distinct)
-            else:
-                node_count = max_id + 1
+    if pairs.size == 0:
+        n = 0 if node_count is None else node_count
+        return Graph(np.zeros(n + 1, dtype=np.int64), np.empty(0, dtype=np.int32))
     _lib.load()
-    dg = device_from_edges(torch.from_numpy(np.ascontiguousarray(pairs)).cuda(), node_count)
-    return dg.to_host()
+    dp = torch.from_numpy(np.ascontiguousarray(pairs)).cuda()
+    if node_count is None:
+        node_count = device_remap_ids(dp, remap_sparse_ids)
+    elif pairs.min() < 0:
+        raise ParseError("negative node id")
+    return device_from_edges(dp, node_count).to_host()
+
+
+# ------------------------------------------------------------------ text ingestion
+# graph.py:128-243 on the device (ingest.cu): the bytes go to HBM once, line
+# splitting, tokenising and int() run there; the host only formats the message of
+# the first failing line, and (MatrixMarket) reads the header and size lines.
+
+_MM_FIELDS = {"pattern", "real", "integer", "complex"}
+_MM_SYMMETRIES = {"general", "symmetric", "skew-symmetric", "hermitian"}
+_SPLITLINES, _NEWLINE_ONLY = 0, 1
+_SPLITLINES_CHECKED = 2   # raw file bytes: strict UTF-8 first, as open(encoding="utf-8")
+
+
+def _text_source(source):
+    """(UTF-8 bytes, line mode, explicit line starts or None) for the reference's
+    source kinds (graph.py:128-131): a str is split by str.splitlines, a text stream
+    by its "\n" line iteration, any other iterable element-wise.  ``bytes`` (the
+    raw contents of a UTF-8 file, as cli.py:194 reads them) split like the str."""
+    if isinstance(source, (bytes, bytearray, memoryview)):
+        return np.frombuffer(bytes(source), dtype=np.uint8), _SPLITLINES_CHECKED, None
+    if isinstance(source, np.ndarray) and source.dtype == np.uint8:
+        return np.ascontiguousarray(source).reshape(-1), _SPLITLINES_CHECKED, None
+    if isinstance(source, str):
+        return np.frombuffer(source.encode("utf-8", "surrogatepass"), np.uint8), _SPLITLINES, None
+    if hasattr(source, "read"):
+        text = source.read()
+        return np.frombuffer(text.encode("utf-8", "surrogatepass"), np.uint8), _NEWLINE_ONLY, None
+    parts = [str(x).encode("utf-8", "surrogatepass") for x in source]
+    starts = np.zeros(len(parts), dtype=np.int64)
+    if parts:
+        np.cumsum(np.fromiter(map(len, parts[:-1]), dtype=np.int64, count=len(parts) - 1),
+                  out=starts[1:])
+    return np.frombuffer(b"".join(parts), dtype=np.uint8), None, starts
+
+
+class _DeviceText:
+    """Text bytes in HBM with their line starts (drg_text_lines)."""
+
+    def __init__(self, data: np.ndarray, mode, starts):
+        _lib.load()
+        self.host = data
+        self.n = int(data.size)
+        host = torch.from_numpy(data) if data.size else torch.empty(0, dtype=torch.uint8)
+        if data.size:
+            host = host.pin_memory() if torch.cuda.is_available() else host
+        self.dev = host.to("cuda", non_blocking=True) if data.size else \
+            torch.empty(1, dtype=torch.uint8, device="cuda")
+        if starts is not None:
+            self.starts = torch.from_numpy(starts).cuda()
+            return
+        count, bad = _lib.out_i64(), _lib.out_i64()
+        check = mode == _SPLITLINES_CHECKED
+        mode = _SPLITLINES if check else mode
+        _lib.call("drg_text_lines", _lib.ptr(self.dev), self.n, mode, None, _lib.byref(count),
+                  _lib.byref(bad) if check else None, _lib.stream_ptr())
+        if bad.value >= 0:
+            p = bad.value
+            try:   # the codec's own message for the first invalid byte
+                bytes(data[p:p + 4]).decode("utf-8")
+                reason = "invalid continuation byte"
+            except UnicodeDecodeError as e:
+                reason = e.reason
+            raise UnicodeDecodeError("utf-8", bytes(data), p, p + 1, reason)
+        self.starts = torch.empty(max(count.value, 1), dtype=torch.int64, device="cuda")
+        if count.value:
+            _lib.call("drg_text_lines", _lib.ptr(self.dev), self.n, mode, _lib.ptr(self.starts),
+                      _lib.byref(count), None, _lib.stream_ptr())
+        self.starts = self.starts[:count.value]
+
+    @property
+    def n_lines(self) -> int:
+        return int(self.starts.numel())
+
+    def lines(self, lo: int, hi: int) -> list[str]:
+        """Decoded text of lines lo..hi-1 (host, for headers and messages)."""
+        hi = min(hi, self.n_lines)
+        if hi <= lo:
+            return []
+        st = self.starts[lo:min(hi + 1, self.n_lines)].cpu().numpy().tolist()
+        if len(st) == hi - lo:
+            st.append(self.n)
+        return [bytes(self.host[a:b]).decode("utf-8", "surrogatepass") for a, b in zip(st[:-1], st[1:])]
+
+    def parse(self, first: int, kind: int, rows: int = 0, declared: int = 0):
+        """drg_parse_lines over lines first..: (device pairs [m, 2], error line index or
+        -1, status, overflow)."""
+        n_lines = self.n_lines - first
+        pairs = torch.empty((max(n_lines, 1), 2), dtype=torch.int64, device="cuda")
+        m, err, status, over = _lib.out_i64(), _lib.out_i64(), _lib.out_i32(), _lib.out_i32()
+        starts = self.starts[first:] if n_lines > 0 else self.starts
+        _lib.call("drg_parse_lines", _lib.ptr(self.dev), self.n, _lib.ptr(starts), max(n_lines, 0),
+                  kind, rows, declared, _lib.ptr(pairs), _lib.byref(m), _lib.byref(err),
+                  _lib.byref(status), _lib.byref(over), _lib.stream_ptr())
+        e = err.value
+        return pairs[:m.value], (first + e if e >= 0 else -1), status.value, over.value
+
+
+def _graph_from_device_pairs(pairs: torch.Tensor, node_count: int | None,
+                             remap_sparse_ids: bool) -> Graph:
+    if pairs.numel() == 0:
+        n = 0 if node_count is None else node_count
+        return Graph(np.zeros(n + 1, dtype=np.int64), np.empty(0, dtype=np.int32))
+    pairs = pairs.contiguous()
+    if node_count is None:
+        node_count = device_remap_ids(pairs, remap_sparse_ids)
+    return device_from_edges(pairs, node_count).to_host()
+
+
+def parse_edge_list(source) -> Graph:
+    """Whitespace-separated "u v" edge list (graph.py:134-167): '#'/'%' comments and
+    blank lines skipped, exactly two non-negative int() ids per line, sparse id
+    spaces remapped.  Same ParseError messages and line numbers."""
+    text = _DeviceText(*_text_source(source))
+    pairs, err, status, overflow = text.parse(0, 0)
+    if err >= 0:
+        line = text.lines(err, err + 1)[0].strip()
+        tokens = line.split()
+        if status == 2:
+            raise ParseError(f"expected two ids, got {len(tokens)} tokens", err + 1)
+        if status == 3:
+            raise ParseError(f"malformed integer in {tokens!r}", err + 1)
+        raise ParseError(f"negative node id in {tokens!r}", err + 1)
+    if overflow:   # np.asarray(us, dtype=np.int64) on an id >= 2**63 (graph.py:162-163)
+        raise OverflowError("Python int too large to convert to C long")
+    return _graph_from_device_pairs(pairs, None, True)
+
+
+def parse_matrix_market(source) -> Graph:
+    """MatrixMarket coordinate file as an undirected graph (graph.py:170-243): the
+    header and size lines are read on the host, the entry lines on the device."""
+    text = _DeviceText(*_text_source(source))
+    if text.n_lines == 0:
+        raise ParseError("empty file, missing MatrixMarket header")
+    header = text.lines(0, 1)[0]
+    tokens = header.strip().split()
+    if len(tokens) < 5 or tokens[0] != "%%MatrixMarket":
+        raise ParseError("missing '%%MatrixMarket' header", 1)
+    obj, fmt, fld, sym = (t.lower() for t in tokens[1:5])
+    if obj != "matrix" or fmt != "coordinate":
+        raise ParseError(f"unsupported MatrixMarket type '{obj} {fmt}' (need 'matrix coordinate')", 1)
+    if fld not in _MM_FIELDS:
+        raise ParseError(f"unsupported field '{fld}'", 1)
+    if sym not in _MM_SYMMETRIES:
+        raise ParseError(f"unsupported symmetry '{sym}'", 1)
+    rows = cols = declared = None
+    idx, chunk = 1, 64
+    while rows is None and idx < text.n_lines:
+        for raw in text.lines(idx, idx + chunk):
+            idx += 1
+            line = raw.strip()
+            if not line or line.startswith("%"):
+                continue
+            parts = line.split()
+            if len(parts) != 3:
+                raise ParseError("size line must be 'rows cols nnz'", idx)
+            try:
+                rows, cols, declared = (int(p) for p in parts)
+            except ValueError:
+                raise ParseError(f"malformed size line {line!r}", idx) from None
+            break
+        chunk *= 2
+    if rows is None:
+        raise ParseError("missing size line")
+    if rows != cols:
+        raise ParseError(f"adjacency matrix must be square, got {rows}x{cols}", idx)
+    if rows < 0 or declared < 0:
+        raise ParseError("negative dimension in size line", idx)
+    pairs, err, status, _ = text.parse(idx, 1, rows, declared)
+    if err >= 0:
+        lineno = err + 1
+        if status == 6:
+            raise ParseError(f"more than the declared {declared} entries", lineno)
+        line = text.lines(err, err + 1)[0].strip()
+        parts = line.split()
+        if status == 2:
+            raise ParseError("coordinate entry needs at least 'i j'", lineno)
+        if status == 3:
+            raise ParseError(f"malformed coordinate entry {line!r}", lineno)
+        i, j = int(parts[0]), int(parts[1])
+        raise ParseError(f"index ({i}, {j}) outside declared {rows}x{cols}", lineno)
+    if pairs.shape[0] != declared:
+        raise ParseError(f"declared {declared} entries but found {pairs.shape[0]}")
+    return _graph_from_device_pairs(pairs, rows, False)
+
+
+def read_graph(path: str, fmt: str = "auto") -> Graph:
+    """cli.load_graph (cli.py:185-203) from the file's bytes: format sniffed from the
+    extension or a '%%MatrixMarket' head, then the device parser."""
+    data = np.fromfile(path, dtype=np.uint8)
+    if fmt == "auto":
+        head = bytes(data[:1024]).decode("utf-8", "ignore").replace("\r\n", "\n").replace("\r", "\n")
+        fmt = "mtx" if path.endswith(".mtx") or head[:128].lstrip().startswith("%%MatrixMarket") \
+            else "edgelist"
+    return parse_matrix_market(data) if fmt == "mtx" else parse_edge_list(data)
 
 
 @dataclass(frozen=True)
