@@ -8,6 +8,7 @@ the HBM-resident forms the pipeline passes between kernels without host trips.
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass
 from typing import Iterator
 
@@ -196,7 +197,9 @@ class _DeviceText:
         _lib.load()
         self.host = data
         self.n = int(data.size)
-        host = torch.from_numpy(data) if data.size else torch.empty(0, dtype=torch.uint8)
+        with warnings.catch_warnings():   # read-only bytes: only copied from, never written
+            warnings.simplefilter("ignore", UserWarning)
+            host = torch.from_numpy(data) if data.size else torch.empty(0, dtype=torch.uint8)
         if data.size:
             host = host.pin_memory() if torch.cuda.is_available() else host
         self.dev = host.to("cuda", non_blocking=True) if data.size else \
@@ -209,14 +212,14 @@ class _DeviceText:
         mode = _SPLITLINES if check else mode
         _lib.call("drg_text_lines", _lib.ptr(self.dev), self.n, mode, None, _lib.byref(count),
                   _lib.byref(bad) if check else None, _lib.stream_ptr())
-        if bad.value >= 0:
+        if check and bad.value >= 0:
             p = bad.value
-            try:   # the codec's own message for the first invalid byte
+            try:   # the codec's own verdict on the sequence at the first invalid byte
                 bytes(data[p:p + 4]).decode("utf-8")
-                reason = "invalid continuation byte"
+                start, end, reason = 0, 1, "invalid continuation byte"
             except UnicodeDecodeError as e:
-                reason = e.reason
-            raise UnicodeDecodeError("utf-8", bytes(data), p, p + 1, reason)
+                start, end, reason = e.start, e.end, e.reason
+            raise UnicodeDecodeError("utf-8", bytes(data), p + start, p + end, reason)
         self.starts = torch.empty(max(count.value, 1), dtype=torch.int64, device="cuda")
         if count.value:
             _lib.call("drg_text_lines", _lib.ptr(self.dev), self.n, mode, _lib.ptr(self.starts),

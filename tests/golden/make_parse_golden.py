@@ -45,10 +45,10 @@ EDGE_TEXTS = {
     "vt_ff_breaks": "0 1\x0b1 2\x0c2 3",
     "sep_breaks": "0 1\x1c1 2\x1d2 3\x1e3 4",
     "unit_sep_space": "0\x1f1\n",
-    "unicode_spaces": "0 1\n1　2\n2 3\n3 4\n",
-    "unicode_breaks": "0 1 1 2 2 33 4",
-    "fullwidth_digits": "１ ２\n２ ３\n",
-    "arabic_digits": "٣ ٤\n١٢ 3\n",
+    "unicode_spaces": "0\u00a01\n1\u30002\n2\u20093\n3\u202f4\n",
+    "unicode_breaks": "0 1\u20281 2\u20292 3\u00853 4",
+    "fullwidth_digits": "\uff11 \uff12\n\uff12 \uff13\n",
+    "arabic_digits": "\u0663 \u0664\n\u0661\u0662 3\n",
     "underscores": "1_0 2_0\n1_000 10\n",
     "double_underscore": "1__0 2\n",
     "leading_underscore": "_1 2\n",
@@ -60,12 +60,12 @@ EDGE_TEXTS = {
     "empty": "",
     "only_comments": "# nothing\n% here\n",
     "only_blank": "\n\n   \n",
-    "bom": "﻿0 1\n1 2\n",
+    "bom": "\ufeff0 1\n1 2\n",
     "hash_inside": "0 1 # trailing comment\n",
     "error_after_blanks": "0 1\n\n\n2 x\n",
     "leading_zeros": "007 010\n",
     "first_error_wins": "0 1 2\n1 x\n",
-    "non_ascii_token": "0 1\né 2\n",
+    "non_ascii_token": "0 1\n\u00e9 2\n",
     "hex": "0x1 2\n",
     "float": "1.0 2\n",
     "trailing_break_pair": "0 1\n\r\n",
@@ -99,14 +99,14 @@ MM_TEXTS = {
     "header_only": "%%MatrixMarket matrix coordinate pattern general\n% c\n",
     "comments_between": ("%%MatrixMarket matrix coordinate pattern general\r\n% a\r\n\r\n"
                          "3 3 2\r\n% b\r\n1 2\r\n\r\n2 3\r\n"),
-    "unicode_digits": "%%MatrixMarket matrix coordinate pattern general\n3 3 2\n１ ２\n2_0 3\n",
+    "unicode_digits": "%%MatrixMarket matrix coordinate pattern general\n3 3 2\n\uff11 \uff12\n2_0 3\n",
     "empty_matrix": "%%MatrixMarket matrix coordinate pattern general\n0 0 0\n",
     "underscore_size": "%%MatrixMarket matrix coordinate pattern general\n1_0 1_0 1\n10 1\n",
 }
 
 RAW_FILES = {   # bytes of a file, read as cli.py:194 reads it
     "el_crlf_file": ("el", b"0 1\r\n1 2\r\n# c\r\n2 3"),
-    "el_utf8_file": ("el", "0 1\n２ ３\n".encode()),
+    "el_utf8_file": ("el", "0 1\n\uff12 \uff13\n\u0663\u3000\u0661\u2028".encode()),
     "el_invalid_utf8": ("el", b"0 1\n1 \xff2\n"),
     "el_truncated_utf8": ("el", b"0 1\n1 2\xe2\x80"),
     "el_overlong": ("el", b"0 1\n\xc0\xb1 2\n"),
@@ -127,7 +127,7 @@ def run(fn, src):
 
 def random_edge_text(seed, lines=3000):
     rng = np.random.default_rng(seed)
-    ws = [" ", "\t", "  ", " ", "　", " \t"]
+    ws = [" ", "\t", "  ", "\u2009", "\u3000", " \t", "\xa0"]
     out = []
     for _ in range(lines):
         r = rng.random()

@@ -66,8 +66,8 @@ def test_device_parsers_match_reference(case):
 
 
 def _random_edge_text(rng, lines, id_max, unicode=True):
-    ws = [" ", "\t", "  ", " \t "] + ([" ", "　", "\x1f"] if unicode else [])
-    brk = ["\n", "\r\n", "\r"] + (["\x0b", " "] if unicode else [])
+    ws = [" ", "\t", "  ", " \t "] + (["\u2009", "\u3000", "\x1f"] if unicode else [])
+    brk = ["\n", "\r\n", "\r"] + (["\x0b", "\u2028", "\x85"] if unicode else [])
     out = []
     for _ in range(lines):
         r = rng.random()
