@@ -119,7 +119,7 @@ def test_read_graph_files(tmp_path):
     got = B.read_graph(str(el))
     assert np.array_equal(got.indptr, want.indptr) and np.array_equal(got.indices, want.indices)
     mm = tmp_path / "g.mtx"
-    mm.write_text("%%MatrixMarket matrix coordinate pattern general\n5000 5000 %d\n" % len(pairs)
+    mm.write_text("%%MatrixMarket matrix coordinate pattern general\n" + f"5000 5000 {len(pairs)}\n"
                   + "\n".join(f"{u + 1} {v + 1}" for u, v in pairs) + "\n")
     want = O.parse_matrix_market(mm.read_text())
     got = B.read_graph(str(mm))
