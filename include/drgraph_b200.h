@@ -305,6 +305,33 @@ int drg_parse_lines(const uint8_t *text, int64_t nbytes, const int64_t *starts, 
  * rank among the distinct ids.  A negative id returns DRG_ERR_INVALID. */
 int drg_id_remap(int64_t *pairs, int64_t m, int remap_sparse, int64_t *out_n, void *stream);
 
+/* --- output formats (output.py:12-108, graph.py:246-250) -------
+ * Each entry is called twice: out == NULL returns the byte count in *out_len (host),
+ * then out (device, *out_len bytes) receives the text.  Numbers are formatted as
+ * Python formats them (f"{x:.6f}" / f"{x:.2f}": exact round-half-even; nan, inf).
+ * drg_format_coords: "x y\n" per node of pos (device fp64 [n][2]) -- write_coords
+ * without its "#nodes N" header line.  *out_bad_row (host): first row with a
+ * coordinate >= 2^50 / 10^6 in magnitude (not formatted exactly), -1 if none. */
+int drg_format_coords(const double *pos, int64_t n, char *out, int64_t *out_len,
+                      int64_t *out_bad_row, void *stream);
+/* drg_format_edge_list: "u v\n" for every CSR entry with u < v, in CSR order. */
+int drg_format_edge_list(const int64_t *indptr, const int32_t *indices, int64_t n, int64_t nnz,
+                         char *out, int64_t *out_len, void *stream);
+/* drg_bbox2: out_bbox (host) = {min x, min y, max x, max y} of pos (device fp64 [n][2]). */
+int drg_bbox2(const double *pos, int64_t n, double *out_bbox, void *stream);
+/* drg_format_svg: the <line> records of the m edges (device int32 [m][2], the drawn
+ * sample) and the <circle> records of the n nodes of write_svg (output.py:56-108),
+ * node positions fitted with the host-computed min / offset / scale / canvas size
+ * exactly as output.py:70-80 does; edge colours from the edge length range.
+ * line_tail / circle_tail (host strings < 64 bytes): the text after the colour /
+ * after cy (the style's formatted widths).  Two outputs as above; *out_bad (host)
+ * = first record with an out-of-range number, -1 if none. */
+int drg_format_svg(const double *pos, int64_t n, const int32_t *edges, int64_t m, double min_x,
+                   double min_y, double off_x, double off_y, double scale, double size,
+                   const char *line_tail, const char *circle_tail, char *out_lines,
+                   int64_t *out_lines_len, char *out_circles, int64_t *out_circles_len,
+                   int64_t *out_bad, void *stream);
+
 /* connected_components (graph.py:369-388): out_labels[n] (device, may be NULL)
  * numbered 0..C-1 in first-seen order (component of the smallest unlabelled id),
  * *out_count (host) = C.  layout_graph uses it for a warning and

@@ -250,6 +250,73 @@ def parse_matrix_market(source) -> Graph:
     return from_edges(np.array(ids, dtype=np.int64).reshape(-1, 2), rows)
 
 
+# ---------------------------------------------------------------------------
+# Output formats (output.py:12-108, graph.py:246-250), restated for the tests
+# ---------------------------------------------------------------------------
+
+def write_coords(positions) -> str:
+    """output.py:12-17."""
+    pos = np.asarray(positions, dtype=np.float64).reshape(-1, 2)
+    return "".join([f"#nodes {len(pos)}\n"] + [f"{x:.6f} {y:.6f}\n" for x, y in pos])
+
+
+def format_edge_list(g: Graph) -> str:
+    """graph.py:246-250 (edges u < v in CSR order)."""
+    src = np.repeat(np.arange(g.node_count), np.diff(g.indptr))
+    keep = src < g.indices
+    return "".join(f"{u} {v}\n" for u, v in zip(src[keep].tolist(), g.indices[keep].tolist()))
+
+
+def _svg_color(t: float) -> str:
+    """_edge_color (output.py:44-51)."""
+    if t <= 0.5:
+        u = 2.0 * t
+        rgb = (1.0 - u, u, 0.0)
+    else:
+        u = 2.0 * t - 1.0
+        rgb = (0.0, 1.0 - u, u)
+    return "#" + "".join(f"{int(round(255 * c)):02x}" for c in rgb)
+
+
+def write_svg(g: Graph, positions, canvas=1000, margin=20.0, node_radius=2.0, edge_width=1.0,
+              edge_cap=600_000, seed=0) -> str:
+    """output.py:56-108."""
+    pos = np.asarray(positions, dtype=np.float64).reshape(-1, 2)
+    size = float(canvas)
+    inner = size - 2.0 * margin
+    xs = ys = np.empty(0)
+    if len(pos):
+        lo = pos.min(axis=0)
+        spans = pos.max(axis=0) - lo
+        span = float(spans.max())
+        scale = inner / span if span > 0 else 0.0
+        off = margin + (inner - spans * scale) / 2.0
+        xs = off[0] + (pos[:, 0] - lo[0]) * scale
+        ys = size - (off[1] + (pos[:, 1] - lo[1]) * scale)
+    src = np.repeat(np.arange(g.node_count), np.diff(g.indptr))
+    keep = src < g.indices
+    edges = np.column_stack([src[keep], g.indices[keep]])
+    if len(edges) > edge_cap:
+        pick = np.sort(np.random.default_rng(seed).choice(len(edges), size=edge_cap,
+                                                          replace=False))
+        edges = edges[pick]
+    out = [f'<svg xmlns="http://www.w3.org/2000/svg" width="{canvas}" height="{canvas}" '
+           f'viewBox="0 0 {canvas} {canvas}">', f'<rect width="{canvas}" height="{canvas}" fill="white"/>']
+    if len(edges):
+        a, b = edges[:, 0], edges[:, 1]
+        du, dv = xs[a] - xs[b], ys[a] - ys[b]
+        ln = np.sqrt(du * du + dv * dv)
+        lmin, lrange = float(ln.min()), float(ln.max()) - float(ln.min())
+        for (u, v), L in zip(edges.tolist(), ln):
+            t = (L - lmin) / lrange if lrange > 0 else 0.0
+            out.append(f'<line x1="{xs[u]:.2f}" y1="{ys[u]:.2f}" x2="{xs[v]:.2f}" '
+                       f'y2="{ys[v]:.2f}" stroke="{_svg_color(t)}" stroke-width="{edge_width}"/>')
+    out += [f'<circle cx="{x:.2f}" cy="{y:.2f}" r="{node_radius}" fill="black"/>'
+            for x, y in zip(xs, ys)]
+    out.append("</svg>")
+    return "\n".join(out) + "\n"
+
+
 def connected_components(g: Graph) -> int:
     """Component count (graph.py:369-388), via scipy's C implementation."""
     from scipy.sparse import csr_matrix

@@ -11,6 +11,7 @@ from .graph import (DeviceGraph, DeviceNeighborDistances, Graph, NeighborDistanc
                     read_graph)
 from .multilevel import (DeviceHierarchy, Hierarchy, build_hierarchy, coarsen_once,
                          coarsen_with_order, compose_maps, device_build_hierarchy, prolong)
+from .output import SvgStyle, format_edge_list, read_coords, write_coords, write_svg
 from .optimizer import (AliasTable, Layout, LayoutPlan, OptimizerParams, Samplers,
                         build_alias_table, build_negative_sampler, build_samplers,
                         layout_device, layout_graph, prepare_layout, sgd_epoch)
@@ -21,7 +22,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Graph", "NeighborDistances", "ParseError", "from_edges", "parse_edge_list",
-    "parse_matrix_market", "read_graph", "all_k_neighborhoods",
+    "parse_matrix_market", "read_graph", "format_edge_list", "write_coords", "read_coords",
+    "write_svg", "SvgStyle", "all_k_neighborhoods",
     "connected_components", "SimilarityParams", "SparseSimilarity", "build_sparse_similarity",
     "Hierarchy", "coarsen_once", "coarsen_with_order", "build_hierarchy", "compose_maps",
     "prolong", "OptimizerParams", "Layout", "AliasTable", "build_alias_table",

@@ -63,6 +63,11 @@ SIGNATURES = {
     "drg_text_lines": [_P, _I64, _I32, _P, _P, _P, _P],
     "drg_parse_lines": [_P, _I64, _P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P],
     "drg_id_remap": [_P, _I64, _I32, _P, _P],
+    "drg_format_coords": [_P, _I64, _P, _P, _P, _P],
+    "drg_format_edge_list": [_P, _P, _I64, _I64, _P, _P, _P],
+    "drg_bbox2": [_P, _I64, _P, _P],
+    "drg_format_svg": [_P, _I64, _P, _I64, _F64, _F64, _F64, _F64, _F64, _F64, ctypes.c_char_p,
+                       ctypes.c_char_p, _P, _P, _P, _P, _P, _P],
     "drg_layout_sgather": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _I32, _I32, _I32,
                            _F64, _F64, _F64, _F64, _I32, _I32, _I32, _U64, _I32, _P, _P, _U32,
                            _P],
