@@ -1,0 +1,84 @@
+// Random-access ceiling of the B200 memory system for the sampled update pass's
+// access pattern: 8-byte gathers and float2 reductions at uniformly random indices
+// of an L2-resident array (the C4 level-0 positions: 1.728 M float2 = 13.8 MB), at
+// full occupancy with many independent accesses in flight per thread.  Reports
+// accesses per second; apply_kernel's rate (14 such accesses per step) is compared
+// against it in DESIGN.md.  Diagnostics only:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/l2peak scripts/l2_random_peak.cu
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+__device__ __forceinline__ uint32_t hash(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+
+template <int MODE>   // 0 gather, 1 red, 2 gather + red (1:1)
+__global__ void __launch_bounds__(256) probe(float2 *y, uint32_t n, int per_thread, float *sink) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    float acc = 0.f;
+    for (int k = 0; k < per_thread; k += 8) {
+        uint32_t idx[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) idx[u] = hash(tid * 0x9e3779b9u + (uint32_t)(k + u)) % n;
+        if (MODE == 0 || MODE == 2) {
+            float2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(y + idx[u]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y;
+        }
+        if (MODE == 1 || MODE == 2) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) atomicAdd(y + idx[(u + 3) & 7], make_float2(1e-9f, acc * 1e-30f));
+        }
+    }
+    if (acc == 123.456f) *sink = acc;
+}
+
+int main() {
+    const uint32_t n = 1728000;
+    float2 *y;
+    float *sink;
+    cudaMalloc(&y, sizeof(float2) * n);
+    cudaMalloc(&sink, 4);
+    cudaMemset(y, 0, sizeof(float2) * n);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int per_thread = 256;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const char *names[3] = {"gather 8B", "float2 red", "gather+red 1:1"};
+    for (int blocks_per_sm : {2, 4, 8}) {
+        const int grid = sms * blocks_per_sm;
+        for (int mode = 0; mode < 3; ++mode) {
+            for (int rep = 0; rep < 2; ++rep) {
+                cudaEventRecord(a);
+                if (mode == 0) probe<0><<<grid, 256>>>(y, n, per_thread, sink);
+                if (mode == 1) probe<1><<<grid, 256>>>(y, n, per_thread, sink);
+                if (mode == 2) probe<2><<<grid, 256>>>(y, n, per_thread, sink);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, a, b);
+                const double accesses = (double)grid * 256 * per_thread * (mode == 2 ? 2 : 1);
+                if (rep == 1)
+                    printf("{\"mode\": \"%s\", \"threads_per_sm\": %d, \"ms\": %.3f, "
+                           "\"G_accesses_per_s\": %.1f}\n",
+                           names[mode], blocks_per_sm * 256, ms, accesses / (ms * 1e-3) / 1e9);
+            }
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        printf("error %s\n", cudaGetErrorString(e));
+        return 1;
+    }
+    return 0;
+}

@@ -83,9 +83,11 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
             t0 = time.perf_counter()
             upd, _, div = m.partition(":")
             extra = {}
+            if upd == "sampledf":   # the fused one-kernel form of "sampled"
+                upd, extra = "sampled", {"sampled_fused": True}
             if div and upd == "sampled":
                 fine, _, coarse = div.partition(":")
-                extra = {"sampled_concurrency": int(fine)}
+                extra = {**extra, "sampled_concurrency": int(fine)}
                 if coarse:
                     extra["sampled_concurrency_coarse"] = int(coarse)
             elif div and upd == "sgather":
