@@ -203,10 +203,7 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * is joined back into `stream`.  Both forms draw identical steps. */
 #define DRG_SAMPLED_AGGREGATE 1
 #define DRG_SAMPLED_FUSED 2
-/* Levels of <= 262144 nodes run their update pass cluster-resident (positions in the
- * distributed shared memory of one thread-block cluster, a chunk of epochs per
- * launch); DRG_SAMPLED_GLOBAL keeps them on the global-memory update pass. */
-#define DRG_SAMPLED_GLOBAL 4
+
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,
                        const uint64_t *src_alias, const float *collapse,
                        const uint64_t *neg_alias, int64_t n, float *y, int64_t step_lo,

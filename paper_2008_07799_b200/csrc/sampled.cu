@@ -21,8 +21,6 @@
 #include <algorithm>
 #include <mutex>
 
-#include <cooperative_groups.h>
-
 #include "common.cuh"
 
 namespace drg {
@@ -509,153 +507,6 @@ __global__ void __launch_bounds__(256, 4) apply_kernel(PArgs A, float2 *y) {
                      (int64_t)gridDim.x * blockDim.x);
 }
 
-// ---- cluster-resident small levels ----------------------------------------------------
-// A level of n <= 16 * 16384 nodes keeps its positions in the distributed shared memory
-// of one thread-block cluster (node v in CTA v >> 14, slot v & 16383): a chunk of
-// epochs runs in ONE launch, the steps' gathers and float atomics go to DSMEM
-// (~200 cycles instead of an L2 round trip under load) and consecutive epochs are
-// separated by cluster barriers instead of kernel boundaries.  Same draws, same step
-// arithmetic as apply_kernel; at most C * blockDim steps in flight.
-namespace cg = cooperative_groups;
-constexpr int kClusterShift = 14;                    // 16384 nodes (128 KiB) per CTA
-constexpr int kClusterMax = 16;                      // non-portable cluster size
-
-struct CArgs {
-    const int32_t *draws;   // the chunk's first epoch; epoch e at e * (2 + M) * n_steps
-    int64_t n_steps;
-    int64_t n;
-    int t0, n_epochs, iters;
-    double lr0;
-    float gamma, eps, clip;
-    int b, M;
-};
-
-__global__ void __launch_bounds__(1024) cluster_apply_kernel(CArgs A, float2 *y) {
-    extern __shared__ float2 ys[];
-    cg::cluster_group cl = cg::this_cluster();
-    const unsigned rank = cl.block_rank();
-    constexpr int64_t chunk = 1LL << kClusterShift, mask = chunk - 1;
-    const int64_t base = (int64_t)rank * chunk;
-    const int64_t own = A.n - base < chunk ? (A.n - base > 0 ? A.n - base : 0) : chunk;
-    for (int64_t k = threadIdx.x; k < own; k += blockDim.x) ys[k] = y[base + k];
-    cl.sync();
-    auto at = [&](int64_t v) -> float2 * {
-        return cl.map_shared_rank(ys, (unsigned)(v >> kClusterShift)) + (v & mask);
-    };
-    const int64_t tid = (int64_t)rank * blockDim.x + threadIdx.x;
-    const int64_t nth = (int64_t)cl.num_blocks() * blockDim.x;
-    const float two_b = 2.0f * (float)A.b;
-    const int Me = min(A.M, kMaxNeg);
-    const int64_t ns = A.n_steps;
-    for (int e = 0; e < A.n_epochs; ++e) {
-        const int32_t *d = A.draws + (size_t)e * (size_t)(2 + A.M) * (size_t)ns;
-        const float lr = (float)fmax(A.lr0 * (1.0 - (double)(A.t0 + e) / (double)A.iters), 0.0);
-        for (int64_t sl = tid; sl < ns; sl += nth) {
-            const int64_t i = __ldcs(d + sl), j = __ldcs(d + ns + sl);
-            int32_t cand[kMaxNeg];
-            float2 ycand[kMaxNeg];
-#pragma unroll
-            for (int m = 0; m < kMaxNeg; ++m)
-                cand[m] = m < Me ? __ldcs(d + (2 + m) * ns + sl) : -1;
-            float2 *pi = at(i);
-            float2 yi = *pi;
-            const float2 yj = *at(j);
-#pragma unroll
-            for (int m = 0; m < kMaxNeg; ++m)
-                ycand[m] = cand[m] >= 0 ? *at(cand[m]) : make_float2(0.f, 0.f);
-            float gix = 0.f, giy = 0.f;
-            if (i != j) {   // _kernels.py:82-105
-                const float dx = yi.x - yj.x, dy = yi.y - yj.y;
-                const float ld2 = dx * dx + dy * dy;
-                if (ld2 > 0.f) {
-                    const float pw = ipowf(ld2, A.b - 1);
-                    const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
-                    const float gx = lr * clampf(coef * dx, A.clip);
-                    const float gy = lr * clampf(coef * dy, A.clip);
-                    float2 *pj = at(j);
-                    atomicAdd(&pj->x, -gx);
-                    atomicAdd(&pj->y, -gy);
-                    yi.x += gx;
-                    yi.y += gy;
-                    gix += gx;
-                    giy += gy;
-                }
-            }
-            float ax[kMaxNeg], ay[kMaxNeg];
-#pragma unroll
-            for (int m = 0; m < kMaxNeg; ++m) {   // _kernels.py:106-140
-                if (m < Me) {
-                    float2 yc = ycand[m];
-                    own_updates(yc, cand[m], m, cand, ax, ay);
-                    int64_t tu;
-                    float tx, ty;
-                    repel(yi, yc, cand[m], lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty,
-                          gix, giy);
-                    ax[m] = tx;
-                    ay[m] = ty;
-                    if (tu >= 0) {
-                        float2 *pc = at(tu);
-                        atomicAdd(&pc->x, tx);
-                        atomicAdd(&pc->y, ty);
-                    }
-                }
-            }
-            for (int m = Me; m < A.M; ++m) {
-                const int64_t target = __ldcs(d + (2 + m) * ns + sl);
-                const float2 yc = target >= 0 ? *at(target) : make_float2(0.f, 0.f);
-                int64_t tu;
-                float tx, ty;
-                repel(yi, yc, target, lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
-                if (tu >= 0) {
-                    float2 *pc = at(tu);
-                    atomicAdd(&pc->x, tx);
-                    atomicAdd(&pc->y, ty);
-                }
-            }
-            if (gix != 0.f || giy != 0.f) {
-                atomicAdd(&pi->x, gix);
-                atomicAdd(&pi->y, giy);
-            }
-        }
-        cl.sync();
-    }
-    for (int64_t k = threadIdx.x; k < own; k += blockDim.x) y[base + k] = ys[k];
-}
-
-// Cluster size for a level of n nodes (0: not cluster-resident)
-int cluster_size_for(int64_t n) {
-    const int64_t c = (n + (1LL << kClusterShift) - 1) >> kClusterShift;
-    return (n > 0 && c <= kClusterMax) ? (int)std::max<int64_t>(c, 1) : 0;
-}
-
-int launch_cluster_apply(const CArgs &A, float2 *y, int C, int threads_per_cta,
-                         cudaStream_t st) {
-    static bool configured = false;
-    const size_t smem = sizeof(float2) << kClusterShift;
-    if (!configured) {
-        DRG_CUDA(cudaFuncSetAttribute(cluster_apply_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        DRG_CUDA(cudaFuncSetAttribute(cluster_apply_kernel,
-                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        configured = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)C);
-    cfg.blockDim = dim3((unsigned)threads_per_cta);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    DRG_CUDA(cudaLaunchKernelEx(&cfg, cluster_apply_kernel, A, y));
-    DRG_LAUNCHED("cluster_apply_kernel");
-    return DRG_OK;
-}
-
 // Thread per row: Vose's construction over the row's entries (optimizer.py:111-139,
 // same stack discipline: small / large lists in index order, popped from the back),
 // fp64 scaled weights in scratch, stacks in the caller's int32 scratch (the small
@@ -984,13 +835,6 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
         }
         return DRG_OK;
     }
-    // small levels: positions resident in one cluster's distributed shared memory
-    const int cluster = (!agg && !(flags & DRG_SAMPLED_GLOBAL)) ? cluster_size_for(n) : 0;
-    int cluster_threads = 0;
-    if (cluster) {   // <= max_threads steps in flight, whole warps, <= 1024 per CTA
-        const int64_t per = (threads + cluster - 1) / cluster;
-        cluster_threads = (int)std::min<int64_t>(1024, std::max<int64_t>(32, (per + 31) / 32 * 32));
-    }
     // split: draw_kernel (K epochs per launch, double-buffered, low-priority stream)
     // -> apply_kernel per epoch (high-priority stream); joined back into `stream`
     const size_t rec_bytes = (size_t)(2 + M) * sizeof(int32_t) * (size_t)n_steps;
@@ -1045,14 +889,6 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
         }
         DRG_CUDA(cudaStreamWaitEvent(ss.hi, ev.e[1 + (c & 1)], 0));
         const int ne = std::min(K, n_iter - c * K);
-        if (cluster) {   // the whole chunk in one cluster-resident launch
-            CArgs C{chunk_buf(c), n_steps, n, t0 + c * K, ne, iters, lr0, (float)gamma,
-                    (float)eps, (float)clip, b, M};
-            DRG_TRY(launch_cluster_apply(C, reinterpret_cast<float2 *>(y), cluster, cluster_threads,
-                                         ss.hi));
-            DRG_CUDA(cudaEventRecord(ev.e[3 + (c & 1)], ss.hi));
-            continue;
-        }
         for (int e = 0; e < ne; ++e) {
             const int t = t0 + c * K + e;
             P.lr = lr_at(t);

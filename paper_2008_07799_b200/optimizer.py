@@ -92,8 +92,6 @@ class OptimizerParams:
     hub_levels: str = "jacobi"     # update="sampled": hub-heavy levels run this update
     sampled_fused: bool = False    # update="sampled": draw inline (one kernel per epoch)
                                    # instead of the split draw pass + update pass
-    sampled_cluster: bool = True   # update="sampled": levels <= 262144 nodes keep Y in
-                                   # one thread-block cluster's shared memory
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
@@ -477,8 +475,7 @@ class LayoutPlan:
                   _lib.ptr(L.alias), L.n, _lib.ptr(y), step_lo, n_steps, t0, n_iter, o.iters,
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
                   o.neg_samples, seed, level, max(256, L.n // max(1, div)),
-                  int(S.hubs) | (2 if o.sampled_fused else 0) | (0 if o.sampled_cluster else 4),
-                  _lib.stream_ptr())
+                  int(S.hubs) | (2 if o.sampled_fused else 0), _lib.stream_ptr())
 
     def _collapse(self, level: int):
         """Collapse probabilities of ``level`` (NULL at level 0: no pair collapses)."""

@@ -160,39 +160,3 @@ def test_split_and_fused_run_the_same_steps(golden):
     plan.sampled_steps(0, a, 0, L.n, 5, 1)
     assert torch.isfinite(a).all() and not torch.equal(a, y)
 
-
-def test_cluster_resident_level_runs_the_same_steps():
-    """Levels of <= 262144 nodes keep Y in a cluster's distributed shared memory
-    (node v in CTA v >> 14): a 40k-node level spans 3 CTAs.  Steps applied one at a
-    time (sequential) give the global-memory update pass's result."""
-    from paper_2008_07799_b200.graph import DeviceGraph
-    from paper_2008_07799_b200.optimizer import prepare_layout
-    side = 200
-    idx = np.arange(side * side).reshape(side, side)
-    e = np.concatenate([np.column_stack([idx[:, :-1].ravel(), idx[:, 1:].ravel()]),
-                        np.column_stack([idx[:-1, :].ravel(), idx[1:, :].ravel()])])
-    g = B.from_edges(e, side * side)
-    prep = prepare_layout(DeviceGraph.from_host(g), B.SimilarityParams(k=1),
-                          B.OptimizerParams(seed=2, iters=10), max_levels=1)
-    plan = prep.plan
-    L = plan.levels[0]
-    assert L.n == 40000
-    rng = np.random.default_rng(8)
-    y0 = torch.from_numpy(rng.normal(0, 5.0, size=(L.n, 2)).astype(np.float32)).cuda()
-    outs = []
-    for cluster in (True, False):
-        plan.opt.sampled_cluster = cluster
-        y = y0.clone()
-        for s in range(0, 40000, 397):        # steps touching all three CTAs' slices
-            plan.sampled_steps(0, y, s, 1, 1, 1)
-        outs.append(y)
-    plan.opt.sampled_cluster = True
-    assert not torch.equal(outs[0], y0)
-    torch.testing.assert_close(outs[0], outs[1], rtol=0, atol=1e-5)
-    # whole epochs on the cluster path: finite, and every slice moved
-    y = y0.clone()
-    plan.sampled_steps(0, y, 0, L.n, 0, 3)
-    assert torch.isfinite(y).all()
-    for c in range(3):
-        sl = slice(c * 16384, min((c + 1) * 16384, L.n))
-        assert not torch.equal(y[sl], y0[sl])
