@@ -400,6 +400,30 @@ def run_ours(args):
         except (OSError, ValueError):
             pass
 
+    # the sampled form's second roofline: random accesses against the measured
+    # random-access ceiling of this GPU (scripts/l2_random_peak.cu): per step the
+    # update pass issues M + 2 gathers + M + 2 float2 reductions (1:1 mix ceiling),
+    # the draw pass 4 + M random table loads (gather ceiling)
+    random_access = None
+    ceil_path = os.path.join(ROOT, "profiles", "r01_l2_random_peak.txt")
+    if kname.startswith("draw_kernel") and os.path.exists(ceil_path):
+        ceil = {}
+        for ln in open(ceil_path):
+            if ln.startswith("{"):
+                r = json.loads(ln)
+                ceil[r["mode"]] = max(ceil.get(r["mode"], 0.0), r["G_accesses_per_s"])
+        M = opt.neg_samples
+        n0 = L0.n // (world if group is not None else 1)
+        # update: y_i, y_j, M y_c gathers + the same M + 2 reductions; draws: source
+        # alias, the two row bounds, the row-alias record and M negative alias loads
+        upd, drw = n0 * 2 * (M + 2), n0 * (4 + M)
+        t_min = upd / (ceil["gather+red 1:1"] * 1e9) + drw / (ceil["gather 8B"] * 1e9)
+        random_access = {"accesses_per_launch": upd + drw,
+                         "achieved_G_per_s": (upd + drw) / l0_launch_s / 1e9,
+                         "ceiling_G_per_s": ceil, "t_min_us": t_min * 1e6,
+                         "frac": t_min / l0_launch_s,
+                         "source": "profiles/r01_l2_random_peak.txt"}
+
     # e2e through the public API: pinned host CSR in, host positions out
     e2e = None
     if not args.no_e2e:
@@ -456,6 +480,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps,
             "roofline": roofline,
+            "random_access_roofline": random_access,
             "other_update_modes": alt,
             "clocks": clocks,
             "e2e": e2e,
