@@ -345,7 +345,7 @@ def run_ours(args):
     # hierarchy): device-resident iters/s, for comparison in the same JSON line
     alt = {}
     if not args.no_alt and group is None:
-        from paper_2008_07799_b200.optimizer import LayoutPlan, build_plan
+        from paper_2008_07799_b200.optimizer import build_plan
         variants = {"jacobi": {}, "inplace": {}, "sampled": {"sampled_fused": False},
                     "sampled_fused": {"update": "sampled", "sampled_fused": True},
                     "sgather": {}}
@@ -355,9 +355,7 @@ def run_ours(args):
                 continue
             o2 = B.OptimizerParams(**{**opt.__dict__, **kw2})
             mode = kw2["update"]
-            p2 = (build_plan(prep.similarity, prep.hierarchy, o2)
-                  if mode in ("sampled", "sgather") and plan.levels[0].sampled is None
-                  else LayoutPlan(plan.levels, plan.maps, o2))
+            p2 = build_plan(prep.similarity, prep.hierarchy, o2)
             p2.run()
             torch.cuda.synchronize()
             ms, l0 = [], []

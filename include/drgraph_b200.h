@@ -194,6 +194,10 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * (Q^l) redrawn (<= 9) while they hit i or j, both ends moved (float2 atomics).
  * Steps step_lo .. step_lo + n_steps - 1 of each epoch run here (a rank's share of
  * the epoch in the multi-GPU mode); at most max_threads steps run concurrently.
+ * map (device int32 [n], may be NULL): the tables are level 0's over n nodes and
+ * every drawn node -- source, target, negatives before their rejection test -- is
+ * mapped to level l through map (composed parent maps), the reference's own
+ * draw-then-map (_kernels.py:76-81, 115); y then holds the level's nodes.
  * flags: DRG_SAMPLED_AGGREGATE combines the updates of a warp's lanes that hit the
  * same node before the atomic (hub-heavy levels); DRG_SAMPLED_FUSED draws inline in
  * the update kernel (one launch per epoch) instead of the default split -- every
@@ -206,7 +210,8 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
 
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,
                        const uint64_t *src_alias, const float *collapse,
-                       const uint64_t *neg_alias, int64_t n, float *y, int64_t step_lo,
+                       const uint64_t *neg_alias, const int32_t *map, int64_t n, float *y,
+                       int64_t step_lo,
                        int64_t n_steps, int t0,
                        int n_iter, int iters, double lr0, double gamma, double eps, double clip,
                        int b, int M, uint64_t seed, int level, int64_t max_threads,
@@ -221,7 +226,8 @@ int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_
  * flight (max_threads = 1: sequential, the reference kernel's order). */
 int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alias,
                       const uint64_t *src_alias, const float *collapse,
-                      const uint64_t *neg_alias, int64_t n, int64_t step_lo, int64_t n_steps,
+                      const uint64_t *neg_alias, const int32_t *map, int64_t n, int64_t step_lo,
+                      int64_t n_steps,
                       int t0, int n_epochs, int M, uint64_t seed, int level, int32_t *out,
                       void *stream);
 int drg_sampled_apply(const int32_t *draws, int64_t n_steps, float *y, double lr, double gamma,

@@ -281,7 +281,8 @@ struct DArgs {
     const uint2 *src_alias;
     const float *collapse;
     const uint2 *neg_alias;
-    int64_t n;
+    const int32_t *map;   // non-NULL: level-0 tables, drawn nodes mapped to level l
+    int64_t n;            // nodes of the tables
     int64_t step_lo;
     int64_t n_steps;
     int64_t n_epochs;
@@ -295,117 +296,78 @@ struct DArgs {
 // small blocks: they fit beside the update pass's resident blocks
 constexpr int kDrawBlock = 128;
 
-// kDrawIlp independent steps per thread, their load chains interleaved stage by stage
-template <int kDrawIlp>
 __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
-    const int64_t total = A.n_steps * A.n_epochs;
-    const int64_t half = (total + kDrawIlp - 1) / kDrawIlp;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid >= half) return;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= A.n_steps * A.n_epochs) return;
+    const int64_t ep = g / A.n_steps, sl = g - ep * A.n_steps;
+    const int64_t s = A.step_lo + sl;
+    const uint32_t c1 = (uint32_t)(s >> 32) ^ ((uint32_t)(A.t_first + (int)ep) << 1);
     SArgs K;   // the counter layout of sampled_kernel
     K.key0 = A.key0;
     K.key1 = A.key1;
     K.level = A.level;
+    const u32x4 r = philox4x32<7>(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xff00u, 0x5a3d1e55u},
+                                  A.key0, A.key1);
+    const u32x4 r2 = philox4x32<7>(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xfe00u, 0x3c6ef372u},
+                                   A.key0, A.key1);
+    const int64_t sb = bucket(A.n, r.x, r.y);
+    const uint2 srec = __ldg(A.src_alias + sb);
     const int Me = min(A.M, kMaxNeg);
-    bool live[kDrawIlp];
-    int64_t ep[kDrawIlp], sl[kDrawIlp], s[kDrawIlp], sb[kDrawIlp], i[kDrawIlp], j[kDrawIlp];
-    uint32_t c1[kDrawIlp];
-    u32x4 r[kDrawIlp], r2[kDrawIlp];
-    uint2 srec[kDrawIlp];
-    int32_t cand[kDrawIlp][kMaxNeg];
-    // stage 1: counters, the source-alias and first-attempt negative loads of both steps
+    int32_t cand[kMaxNeg];
 #pragma unroll
-    for (int u = 0; u < kDrawIlp; ++u) {
-        const int64_t g = tid + u * half;
-        live[u] = g < total;
-        const int64_t gg = live[u] ? g : tid;
-        ep[u] = gg / A.n_steps;
-        sl[u] = gg - ep[u] * A.n_steps;
-        s[u] = A.step_lo + sl[u];
-        c1[u] = (uint32_t)(s[u] >> 32) ^ ((uint32_t)(A.t_first + (int)ep[u]) << 1);
-        r[u] = philox4x32<7>(u32x4{(uint32_t)s[u], c1[u], (A.level << 24) | 0xff00u, 0x5a3d1e55u},
-                             A.key0, A.key1);
-        r2[u] = philox4x32<7>(u32x4{(uint32_t)s[u], c1[u], (A.level << 24) | 0xfe00u, 0x3c6ef372u},
-                              A.key0, A.key1);
-        sb[u] = bucket(A.n, r[u].x, r[u].y);
-        srec[u] = __ldg(A.src_alias + sb[u]);
-#pragma unroll
-        for (int m = 0; m < kMaxNeg; ++m) {
-            if (m < Me) {
-                const u32x4 q = neg_draw(K, s[u], c1[u], m, 0);
-                const int32_t bk = (int32_t)bucket(A.n, q.x, q.y);
-                cand[u][m] = (int32_t)accept(__ldg(A.neg_alias + bk), bk, q.z);
-            }
+    for (int m = 0; m < kMaxNeg; ++m) {
+        if (m < Me) {
+            const u32x4 q = neg_draw(K, s, c1, m, 0);
+            const int32_t bk = (int32_t)bucket(A.n, q.x, q.y);
+            cand[m] = (int32_t)accept(__ldg(A.neg_alias + bk), bk, q.z);
         }
     }
-    // stage 2: sources, their row bounds and collapse probabilities
-    int64_t lo[kDrawIlp], hi[kDrawIlp];
-    float cprob[kDrawIlp];
-#pragma unroll
-    for (int u = 0; u < kDrawIlp; ++u) {
-        i[u] = accept(srec[u], sb[u], r[u].z);
-        lo[u] = __ldg(A.indptr + i[u]);
-        hi[u] = __ldg(A.indptr + i[u] + 1);
-        cprob[u] = A.collapse ? __ldg(A.collapse + i[u]) : 0.0f;   // NULL: none (level 0)
+    int64_t i = accept(srec, sb, r.z);
+    const int64_t lo = __ldg(A.indptr + i), hi = __ldg(A.indptr + i + 1);
+    const float cprob = A.collapse ? __ldg(A.collapse + i) : 0.0f;   // NULL: none
+    int64_t j = i;
+    if ((A.probe & 2) && hi > lo) {
+        j = (int64_t)bucket(A.n, r2.x, r2.y);
+    } else if (hi > lo && !(u32_to_unit(r.w) < cprob)) {
+        // one random 16-byte record of a multi-GB table: evict-first, so it does not
+        // push the hot alias / y tables out of L2
+        const uint4 rrec = __ldcs(A.row_alias + lo + bucket(hi - lo, r2.x, r2.y));
+        j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)rrec.z : (int64_t)rrec.y;
     }
-    // stage 3: targets through the row's alias table
+    if (A.map) {   // the level-0 pair and negatives as seen at level l (_kernels.py:76-81, 115)
+        i = __ldg(A.map + i);
+        j = __ldg(A.map + j);
 #pragma unroll
-    for (int u = 0; u < kDrawIlp; ++u) {
-        j[u] = i[u];
-        if ((A.probe & 2) && hi[u] > lo[u]) {
-            j[u] = (int64_t)bucket(A.n, r2[u].x, r2[u].y);
-        } else if (hi[u] > lo[u] && !(u32_to_unit(r[u].w) < cprob[u])) {
-            // one random 16-byte record of a multi-GB table: evict-first, so it does not
-            // push the hot alias / y tables out of L2
-            const uint4 rrec = __ldcs(A.row_alias + lo[u] + bucket(hi[u] - lo[u], r2[u].x, r2[u].y));
-            j[u] = (u32_to_unit(r2[u].z) < __uint_as_float(rrec.x)) ? (int64_t)rrec.z
-                                                                    : (int64_t)rrec.y;
-        }
+        for (int m = 0; m < kMaxNeg; ++m)
+            if (m < Me) cand[m] = __ldg(A.map + cand[m]);
     }
-    // stage 4: negatives (redrawn while they hit i or j) and the streaming stores
+    int32_t *o = A.out + ep * (int64_t)(2 + A.M) * A.n_steps + sl;
+    __stcs(o, (int32_t)i);   // read once by the update pass: streaming stores
+    __stcs(o + A.n_steps, (int32_t)j);
+    for (int m = 0; m < A.M; ++m) {
+        int64_t target = -1;
+        int first = 0;
+        if (m < Me) {
+            int32_t c0 = 0;
 #pragma unroll
-    for (int u = 0; u < kDrawIlp; ++u) {
-        if (!live[u]) continue;
-        int32_t *o = A.out + ep[u] * (int64_t)(2 + A.M) * A.n_steps + sl[u];
-        __stcs(o, (int32_t)i[u]);   // read once by the update pass
-        __stcs(o + A.n_steps, (int32_t)j[u]);
-#pragma unroll
-        for (int m = 0; m < kMaxNeg; ++m) {
-            if (m < Me) {
-                int64_t target = (cand[u][m] != i[u] && cand[u][m] != j[u]) ? cand[u][m] : -1;
-                for (int attempt = 1; target < 0 && attempt < 9; ++attempt) {
-                    const u32x4 q = neg_draw(K, s[u], c1[u], m, attempt);
-                    const int64_t bk = bucket(A.n, q.x, q.y);
-                    const int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
-                    if (c0 != i[u] && c0 != j[u]) target = c0;
-                }
-                __stcs(o + (int64_t)(2 + m) * A.n_steps, (int32_t)target);
-            }
+            for (int q = 0; q < kMaxNeg; ++q)
+                if (q == m) c0 = cand[q];
+            if (c0 != i && c0 != j) target = c0;
+            first = 1;
         }
-        for (int m = Me; m < A.M; ++m) {
-            int64_t target = -1;
-            for (int attempt = 0; target < 0 && attempt < 9; ++attempt) {
-                const u32x4 q = neg_draw(K, s[u], c1[u], m, attempt);
-                const int64_t bk = bucket(A.n, q.x, q.y);
-                const int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
-                if (c0 != i[u] && c0 != j[u]) target = c0;
-            }
-            __stcs(o + (int64_t)(2 + m) * A.n_steps, (int32_t)target);
+        for (int attempt = first; target < 0 && attempt < 9; ++attempt) {
+            const u32x4 q = neg_draw(K, s, c1, m, attempt);
+            const int64_t bk = bucket(A.n, q.x, q.y);
+            int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
+            if (A.map) c0 = __ldg(A.map + c0);
+            if (c0 != i && c0 != j) target = c0;
         }
+        __stcs(o + (int64_t)(2 + m) * A.n_steps, (int32_t)target);
     }
 }
 
-// ILP 1 or 2 (DRG_DRAW_ILP, default 1)
 int launch_draws(const DArgs &D, cudaStream_t st) {
-    static const int ilp = [] {
-        const char *e = getenv("DRG_DRAW_ILP");
-        return e && atoi(e) == 2 ? 2 : 1;
-    }();
-    const int64_t total = D.n_steps * D.n_epochs;
-    if (ilp == 2)
-        draw_kernel<2><<<(unsigned)ceil_div(ceil_div(total, 2), kDrawBlock), kDrawBlock, 0, st>>>(D);
-    else
-        draw_kernel<1><<<(unsigned)ceil_div(total, kDrawBlock), kDrawBlock, 0, st>>>(D);
+    draw_kernel<<<(unsigned)ceil_div(D.n_steps * D.n_epochs, kDrawBlock), kDrawBlock, 0, st>>>(D);
     DRG_LAUNCHED("draw_kernel");
     return DRG_OK;
 }
@@ -734,7 +696,8 @@ constexpr size_t kDrawBudget = size_t(64) << 20;   // bytes per draw buffer (two
 
 extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alias,
                                  const uint64_t *src_alias, const float *collapse,
-                                 const uint64_t *neg_alias, int64_t n, int64_t step_lo,
+                                 const uint64_t *neg_alias, const int32_t *map, int64_t n,
+                                 int64_t step_lo,
                                  int64_t n_steps, int t0, int n_epochs, int M, uint64_t seed,
                                  int level, int32_t *out, void *stream) {
     if (n <= 0 || n_steps <= 0 || n_epochs <= 0) return DRG_OK;
@@ -746,6 +709,7 @@ extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alia
     D.src_alias = reinterpret_cast<const uint2 *>(src_alias);
     D.collapse = collapse;
     D.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+    D.map = map;
     D.n = n;
     D.step_lo = step_lo;
     D.n_steps = n_steps;
@@ -790,7 +754,8 @@ extern "C" int drg_sampled_apply(const int32_t *draws, int64_t n_steps, float *y
 
 extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                                   const uint64_t *row_alias, const uint64_t *src_alias,
-                                  const float *collapse, const uint64_t *neg_alias, int64_t n,
+                                  const float *collapse, const uint64_t *neg_alias,
+                                  const int32_t *map, int64_t n,
                                   float *y, int64_t step_lo, int64_t n_steps, int t0, int n_iter,
                                   int iters,
                                   double lr0, double gamma, double eps, double clip, int b, int M,
@@ -806,6 +771,8 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     const int64_t threads = std::max<int64_t>(256, std::min<int64_t>(n_steps, max_threads));
     const unsigned grid = (unsigned)ceil_div(threads, 256);
     auto lr_at = [&](int t) { return (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0); };
+    if ((flags & DRG_SAMPLED_FUSED) && map)
+        return fail(DRG_ERR_UNSUPPORTED, "the fused form draws from level tables (map == NULL)");
     if (flags & DRG_SAMPLED_FUSED) {   // one kernel per epoch, draws inline
         SArgs A;
         A.indptr = indptr;
@@ -855,6 +822,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     D.src_alias = reinterpret_cast<const uint2 *>(src_alias);
     D.collapse = collapse;
     D.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+    D.map = map;
     D.n = n;
     D.step_lo = step_lo;
     D.n_steps = n_steps;

@@ -274,9 +274,14 @@ class SampledTables:
     src_alias: torch.Tensor   # int64 [n]  Vose over R^l
     row_alias: torch.Tensor   # int64 [nnz, 2] per-row Vose over P^l: {threshold, alias target,
                               # own target, 0} -- one 16-byte record per entry
-    collapse: torch.Tensor    # fp32 [n]   c_a
-    wsum: torch.Tensor        # fp32 [n]   sum_b W_ab = 2 n_l sum_b P^l_ab (sgather)
+    collapse: torch.Tensor | None   # fp32 [n]   c_a (None: no collapsed pairs)
+    wsum: torch.Tensor | None       # fp32 [n]   sum_b W_ab = 2 n_l sum_b P^l_ab (sgather)
     hubs: bool = False        # some node takes part in > HUB_STEPS steps per epoch
+    # draw-then-map form (coarse levels of a "sampled" plan): the tables above are
+    # level 0's, ``map`` (int32 [n_0]) the composed parent map to this level
+    map: torch.Tensor | None = None
+    indptr: torch.Tensor | None = None      # level-0 row offsets of row_alias
+    neg_alias: torch.Tensor | None = None   # level-0 Vose table over Q^0
 
 
 HUB_STEPS = 512   # warp-aggregate the sampled updates above this per-node rate
@@ -297,6 +302,39 @@ def build_sampled_tables(ip, tg, P, R) -> SampledTables:
         # expected steps per epoch in which the busiest node is the source
         hubs = bool(float(R.max()) / max(float(R.sum()), 1e-300) * n > HUB_STEPS)
     return SampledTables(src, rows[:nnz], c, wsum, hubs)
+
+
+def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
+                            neg_power: float = 0.75) -> list[LevelData]:
+    """update="sampled" without level aggregation: the reference draws every pair
+    and negative at level 0 and maps it to the current level (_kernels.py:76-81,
+    115), so the level-0 tables (per-row Vose over P, Vose over R and Q) serve all
+    levels through the composed parent maps (drg_compose_maps).  Only R^l is pulled
+    up (drg_aggregate_nodes) to detect hub-heavy levels.  No P^l, no packed
+    records: the gather modes build them with build_level_data."""
+    ip, tg, P, R = ds.indptr, ds.targets, ds.weights, ds.row_mass
+    Wn = device_negative_weights(R, neg_power)
+    alias0, _ = _alias_device(Wn)
+    S0 = build_sampled_tables(ip, tg, P, R)
+    S0.collapse = None   # no pair collapses at level 0
+    n0 = dh.levels[0].node_count
+    out = [LevelData(n0, tg.numel(), ip, None, None, alias0, None, S0)]
+    flat = None
+    st = _lib.stream_ptr()
+    for level in range(1, dh.depth + 1):
+        n_l = dh.levels[level].node_count
+        parent = dh.maps[level - 1]
+        nxt = torch.empty(n0, dtype=torch.int32, device=ip.device)
+        _lib.call("drg_compose_maps", _lib.ptr(flat) if flat is not None else None,
+                  _lib.ptr(parent), n0, _lib.ptr(nxt), st)
+        flat = nxt
+        R = _aggregate_nodes(R, parent, n_l)
+        hubs = bool(float(R.max()) / max(float(R.sum()), 1e-300) * n_l > HUB_STEPS) \
+            if n_l > 0 else False
+        S = SampledTables(S0.src_alias, S0.row_alias, None, None, hubs, map=flat, indptr=ip,
+                          neg_alias=alias0)
+        out.append(LevelData(n_l, 0, None, None, None, None, None, S))
+    return out
 
 
 def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float = 0.75,
@@ -369,8 +407,12 @@ class LayoutPlan:
         return "layout_iter_kernel", L.algorithmic_bytes(M)
 
     def interactions(self) -> int:
-        """(P entries + M negatives) updated over the whole layout stage."""
+        """Interactions applied over the whole layout stage: per gather iteration every
+        P entry + M negatives per node; per sampled epoch n_l steps of one pair + M
+        negatives (the reference's count)."""
         M = self.opt.neg_samples
+        if self.opt.update == "sampled":
+            return self.opt.iters * sum((1 + M) * L.n for L in self.levels)
         return self.opt.iters * sum(L.nnz + M * L.n for L in self.levels)
 
     def init_positions(self) -> torch.Tensor:
@@ -470,16 +512,28 @@ class LayoutPlan:
             raise RuntimeError("plan was built without sampled-mode tables")
         o = self.opt
         div = o.sampled_concurrency if level == 0 else o.sampled_concurrency_coarse
-        _lib.call("drg_layout_sampled", _lib.ptr(L.indptr), _lib.ptr(L.rec),
+        ip, neg, n_tab, mp = self._tables(level)
+        _lib.call("drg_layout_sampled", _lib.ptr(ip), None,
                   _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), self._collapse(level),
-                  _lib.ptr(L.alias), L.n, _lib.ptr(y), step_lo, n_steps, t0, n_iter, o.iters,
+                  _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(y), step_lo, n_steps, t0, n_iter,
+                  o.iters,
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
                   o.neg_samples, seed, level, max(256, L.n // max(1, div)),
                   int(S.hubs) | (2 if o.sampled_fused else 0), _lib.stream_ptr())
 
     def _collapse(self, level: int):
-        """Collapse probabilities of ``level`` (NULL at level 0: no pair collapses)."""
-        return None if level == 0 else _lib.ptr(self.levels[level].sampled.collapse)
+        """Collapse probabilities of ``level`` (NULL at level 0 and for mapped draws)."""
+        c = self.levels[level].sampled.collapse
+        return None if level == 0 or c is None else _lib.ptr(c)
+
+    def _tables(self, level: int):
+        """(row offsets, negative table, table size, map) the draws of ``level`` use:
+        the level's own, or level 0's with the composed map (draw-then-map)."""
+        L = self.levels[level]
+        S = L.sampled
+        if S.map is None:
+            return L.indptr, L.alias, L.n, None
+        return S.indptr, S.neg_alias, S.map.numel(), S.map
 
     def sampled_draws(self, level: int, step_lo: int, n_steps: int, t0: int,
                       n_epochs: int = 1) -> torch.Tensor:
@@ -490,10 +544,11 @@ class LayoutPlan:
         if S is None:
             raise RuntimeError("plan was built without sampled-mode tables")
         M = self.opt.neg_samples
-        out = torch.empty((n_epochs, 2 + M, n_steps), dtype=torch.int32, device=L.indptr.device)
-        _lib.call("drg_sampled_draws", _lib.ptr(L.indptr), _lib.ptr(S.row_alias),
-                  _lib.ptr(S.src_alias), self._collapse(level), _lib.ptr(L.alias), L.n,
-                  step_lo, n_steps, t0, n_epochs, M, seed, level, _lib.ptr(out),
+        ip, neg, n_tab, mp = self._tables(level)
+        out = torch.empty((n_epochs, 2 + M, n_steps), dtype=torch.int32, device=ip.device)
+        _lib.call("drg_sampled_draws", _lib.ptr(ip), _lib.ptr(S.row_alias),
+                  _lib.ptr(S.src_alias), self._collapse(level), _lib.ptr(neg), _lib.ptr(mp),
+                  n_tab, step_lo, n_steps, t0, n_epochs, M, seed, level, _lib.ptr(out),
                   _lib.stream_ptr())
         return out
 
@@ -593,6 +648,15 @@ def device_radius(y: torch.Tensor) -> float:
 
 
 def build_plan(ds: DeviceSimilarity, dh: DeviceHierarchy, opt: OptimizerParams) -> LayoutPlan:
+    """Level data for the plan's update mode: "sampled" draws from the level-0 tables
+    through the composed maps (build_mapped_level_data) unless a hub-heavy level
+    needs the gather (hub_levels="jacobi") or the fused form is asked for; the other
+    modes (and those cases) aggregate P^l per level."""
+    if opt.update == "sampled" and not opt.sampled_fused:
+        levels = build_mapped_level_data(ds, dh, opt.neg_power)
+        if not (opt.hub_levels == "jacobi" and any(L.sampled.hubs for L in levels)):
+            return LayoutPlan(levels, list(dh.maps), opt)
+        del levels
     return LayoutPlan(build_level_data(ds, dh, opt.neg_power,
                                        opt.update in ("sampled", "sgather")),
                       list(dh.maps), opt)

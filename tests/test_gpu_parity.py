@@ -246,8 +246,9 @@ def _prepared(g, k=2, perp="auto", levels=None, seed=0, M=5, min_size=8):
     from paper_2008_07799_b200.graph import DeviceGraph
     from paper_2008_07799_b200.optimizer import prepare_layout
     dg = DeviceGraph.from_host(g)
+    # the gather's level data (P^l, packed records): update="jacobi"
     return prepare_layout(dg, B.SimilarityParams(k=k, perplexity=perp),
-                          B.OptimizerParams(seed=seed, neg_samples=M, iters=10),
+                          B.OptimizerParams(seed=seed, neg_samples=M, iters=10, update="jacobi"),
                           min_size=min_size, max_levels=levels)
 
 
