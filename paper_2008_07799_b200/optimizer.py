@@ -324,10 +324,12 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
     for level in range(1, dh.depth + 1):
         n_l = dh.levels[level].node_count
         parent = dh.maps[level - 1]
-        nxt = torch.empty(n0, dtype=torch.int32, device=ip.device)
-        _lib.call("drg_compose_maps", _lib.ptr(flat) if flat is not None else None,
-                  _lib.ptr(parent), n0, _lib.ptr(nxt), st)
-        flat = nxt
+        if flat is None:   # level 1: the parent map itself
+            flat = parent.to(torch.int32).contiguous()
+        else:              # out[i] = parent[flat[i]]
+            nxt = torch.empty(n0, dtype=torch.int32, device=ip.device)
+            _lib.call("drg_compose_maps", _lib.ptr(flat), _lib.ptr(parent), n0, _lib.ptr(nxt), st)
+            flat = nxt
         R = _aggregate_nodes(R, parent, n_l)
         hubs = bool(float(R.max()) / max(float(R.sum()), 1e-300) * n_l > HUB_STEPS) \
             if n_l > 0 else False
