@@ -689,10 +689,25 @@ class PreparedLayout:
         return out
 
 
+def start_first_order(n: int, opt: OptimizerParams, min_size: int = 16,
+                      max_levels: int | None = None, pool=None):
+    """Future of the level-0 visiting order of build_hierarchy for an n-node graph
+    (None when no coarsening will happen), drawn on a host thread."""
+    if n <= min_size or (max_levels is not None and max_levels <= 1):
+        return None
+    pool = pool or _ORDER_POOL
+    return first_level_order(n, _derive_seed(opt.seed, _HIERARCHY_TAG), pool)
+
+
+_ORDER_POOL = concurrent.futures.ThreadPoolExecutor(1)
+
+
 def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
                    rho: float = 0.8, min_size: int = 16, max_levels: int | None = None,
-                   force_levels: int | None = None, timed: bool = False) -> PreparedLayout:
-    """Preprocessing stages of layout_graph (optimizer.py:372-391) on device."""
+                   force_levels: int | None = None, timed: bool = False,
+                   first_order=None) -> PreparedLayout:
+    """Preprocessing stages of layout_graph (optimizer.py:372-391) on device.
+    ``first_order``: start_first_order's future, if the caller started it early."""
     if dg.node_count < 1:
         raise ValueError("cannot lay out an empty graph")
     timings = {}
@@ -706,12 +721,13 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
 
     stamp("start")
     # the level-0 visiting permutation (host numpy, the reference's stream) is drawn
-    # on a host thread while the device runs the stages below
-    pool = concurrent.futures.ThreadPoolExecutor(1)
+    # on a host thread while the device runs the stages below (layout_graph starts it
+    # before the graph's host-to-device copy)
     hseed = _derive_seed(opt.seed, _HIERARCHY_TAG)
-    first_order = (first_level_order(dg.node_count, hseed, pool)
-                   if dg.node_count > min_size and (max_levels is None or max_levels > 1)
-                   else None)
+    pool = None
+    if first_order is None:
+        pool = concurrent.futures.ThreadPoolExecutor(1)
+        first_order = start_first_order(dg.node_count, opt, min_size, max_levels, pool)
     # isolated nodes last (layout-internal ids; outputs are mapped back)
     dg_in = dg
     dg, rel0 = isolated_last(dg)
@@ -727,7 +743,8 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
     stamp("similarity")
     dh = device_build_hierarchy(dg, rho, min_size, hseed, max_levels, force_levels,
                                 level0_relabel=rel0, first_order=first_order)
-    pool.shutdown(wait=False)
+    if pool is not None:
+        pool.shutdown(wait=False)
     relabel = relabel_coarse_levels(dh)
     relabel[0] = rel0
     del dg_in
@@ -754,12 +771,13 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
 def layout_device(dg: DeviceGraph, sim: SimilarityParams | None = None,
                   opt: OptimizerParams | None = None, rho: float = 0.8, min_size: int = 16,
                   max_levels: int | None = None, force_levels: int | None = None,
-                  init_positions: np.ndarray | torch.Tensor | None = None, group=None
-                  ) -> tuple[torch.Tensor, dict, PreparedLayout]:
+                  init_positions: np.ndarray | torch.Tensor | None = None, group=None,
+                  first_order=None) -> tuple[torch.Tensor, dict, PreparedLayout]:
     """layout_graph on a resident graph; returns (Y on device, stats, prepared)."""
     sim = sim or SimilarityParams()
     opt = opt or OptimizerParams()
-    prep = prepare_layout(dg, sim, opt, rho, min_size, max_levels, force_levels)
+    prep = prepare_layout(dg, sim, opt, rho, min_size, max_levels, force_levels,
+                          first_order=first_order)
     stats, dh = prep.stats, prep.hierarchy
     if init_positions is not None:
         y0 = torch.as_tensor(np.asarray(init_positions, dtype=np.float32)).cuda() \
@@ -792,14 +810,17 @@ def layout_graph(g: Graph, sim_params: SimilarityParams | None = None,
                  min_size: int = 16, *, max_levels: int | None = None,
                  force_levels: int | None = None, init_positions=None, group=None) -> Layout:
     """Full pipeline (optimizer.py:361-413) on the GPU.  Graph in (host CSR),
-    positions out (host float64 [n, 2]).  Deterministic for a fixed seed with the
-    default Jacobi update."""
+    positions out (host float64 [n, 2]).  Bitwise deterministic for a fixed seed with
+    update="jacobi"; the default "sampled" update is Hogwild, like the reference's
+    threads > 1."""
     if g.node_count < 1:
         raise ValueError("cannot lay out an empty graph")
     _lib.load()
+    # the host permutation of the first coarsening overlaps the copy and the kernels
+    order = start_first_order(g.node_count, opt_params or OptimizerParams(), min_size, max_levels)
     dg = DeviceGraph.from_host(g)
     y, stats, _ = layout_device(dg, sim_params, opt_params, rho, min_size, max_levels,
-                                force_levels, init_positions, group)
+                                force_levels, init_positions, group, first_order=order)
     return Layout(positions=y.cpu().numpy().astype(np.float64), stats=stats)
 
 
