@@ -299,8 +299,7 @@ def build_sampled_tables(ip, tg, P, R) -> SampledTables:
         c = torch.where(R > 0, 1.0 - rowsum[:n] / torch.clamp(R, min=1e-300),
                         torch.zeros_like(R)).clamp_(0.0, 1.0).to(torch.float32)
         wsum = (2.0 * n * rowsum[:n]).to(torch.float32)
-        # expected steps per epoch in which the busiest node is the source
-        hubs = bool(float(R.max()) / max(float(R.sum()), 1e-300) * n > HUB_STEPS)
+        hubs = _is_hub_level(R)
     return SampledTables(src, rows[:nnz], c, wsum, hubs)
 
 
@@ -331,20 +330,27 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
             _lib.call("drg_compose_maps", _lib.ptr(flat), _lib.ptr(parent), n0, _lib.ptr(nxt), st)
             flat = nxt
         R = _aggregate_nodes(R, parent, n_l)
-        hubs = bool(float(R.max()) / max(float(R.sum()), 1e-300) * n_l > HUB_STEPS) \
-            if n_l > 0 else False
+        hubs = _is_hub_level(R)
         S = SampledTables(S0.src_alias, S0.row_alias, None, None, hubs, map=flat, indptr=ip,
                           neg_alias=alias0)
         out.append(LevelData(n_l, 0, None, None, None, None, None, S))
     return out
 
 
+def _is_hub_level(R: torch.Tensor) -> bool:
+    """Expected steps per epoch in which the busiest node is the source > HUB_STEPS."""
+    n = R.numel()
+    return n > 0 and float(R.max()) / max(float(R.sum()), 1e-300) * n > HUB_STEPS
+
+
 def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float = 0.75,
-                     sampled: bool = False) -> list[LevelData]:
+                     sampled: bool = False, skip_hub_tables: bool = False) -> list[LevelData]:
     """P^l, R^l, Q^l for every level, pulled up level by level through the parent
     maps (drg_aggregate_pairs / drg_aggregate_nodes), then packed (drg_level_pack)
     with a Vose table per level (drg_alias_build); ``sampled`` also builds the
-    level's sampled-mode tables."""
+    level's sampled-mode tables -- except, with ``skip_hub_tables``, on hub-heavy
+    levels, which then run the gather and never draw (their per-row tables over
+    million-entry hub rows would be the most expensive part of the build)."""
     ip, tg, P = ds.indptr, ds.targets, ds.weights
     R = ds.row_mass
     Wn = device_negative_weights(R, neg_power)
@@ -363,7 +369,10 @@ def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float
         rec, V = pack_level(ip, tg, P, R, Wn, 1.0 / total, n_l, sort_rows=False)
         L = LevelData(n_l, tg.numel(), ip, rec, V, alias, heavy_split(ip))
         if sampled and R.numel() > 0 and float(R.sum()) > 0:
-            L.sampled = build_sampled_tables(ip, tg, P, R)
+            if skip_hub_tables and _is_hub_level(R):
+                L.sampled = SampledTables(None, None, None, None, hubs=True)
+            else:
+                L.sampled = build_sampled_tables(ip, tg, P, R)
         out.append(L)
     return out
 
@@ -654,13 +663,21 @@ def build_plan(ds: DeviceSimilarity, dh: DeviceHierarchy, opt: OptimizerParams) 
     through the composed maps (build_mapped_level_data) unless a hub-heavy level
     needs the gather (hub_levels="jacobi") or the fused form is asked for; the other
     modes (and those cases) aggregate P^l per level."""
+    gather_hubs = opt.update == "sampled" and opt.hub_levels == "jacobi"
     if opt.update == "sampled" and not opt.sampled_fused:
-        levels = build_mapped_level_data(ds, dh, opt.neg_power)
-        if not (opt.hub_levels == "jacobi" and any(L.sampled.hubs for L in levels)):
-            return LayoutPlan(levels, list(dh.maps), opt)
-        del levels
+        # hub-heavy levels (decided on R^l alone) need the gather's level data
+        R = ds.row_mass
+        hub = _is_hub_level(R)
+        for level in range(1, dh.depth + 1):
+            if hub:
+                break
+            R = _aggregate_nodes(R, dh.maps[level - 1], dh.levels[level].node_count)
+            hub = _is_hub_level(R)
+        if not (gather_hubs and hub):
+            return LayoutPlan(build_mapped_level_data(ds, dh, opt.neg_power), list(dh.maps), opt)
     return LayoutPlan(build_level_data(ds, dh, opt.neg_power,
-                                       opt.update in ("sampled", "sgather")),
+                                       opt.update in ("sampled", "sgather"),
+                                       skip_hub_tables=gather_hubs),
                       list(dh.maps), opt)
 
 
