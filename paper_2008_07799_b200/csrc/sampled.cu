@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <mutex>
 
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 
 namespace drg {
@@ -469,11 +471,9 @@ __global__ void __launch_bounds__(256, 4) apply_kernel(PArgs A, float2 *y) {
                      (int64_t)gridDim.x * blockDim.x);
 }
 
-// Thread per row: Vose's construction over the row's entries (optimizer.py:111-139,
-// same stack discipline: small / large lists in index order, popped from the back),
-// fp64 scaled weights in scratch, stacks in the caller's int32 scratch (the small
-// stack grows up from the row start, the large one down from the row end).
-// rec[e] = {fp32 threshold of bucket e, target of its alias entry}.
+// Per-row alias tables (build_alias_table, optimizer.py:111-139, applied to every
+// row of P) by the parallel sweep: the law of Vose's construction without its
+// sequential stack.  rec[e] = {fp32 threshold of bucket e, alias target, own target}.
 constexpr int kRowWarpMax = 512;   // rows up to this length: warp-parallel sweep
 constexpr int kRowWarps = 4;
 
@@ -580,41 +580,115 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     }
 }
 
-__global__ void row_alias_kernel(const int64_t *__restrict__ indptr,
-                                 const int32_t *__restrict__ targets,
-                                 const double *__restrict__ P, int64_t n, int32_t *stack,
-                                 double *w, uint4 *rec, double *rowsum) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+// Block per long row (> kRowWarpMax entries): the same parallel sweep as the warp
+// tier, chunked over the row with block scans, the per-entry arrays (scaled weight,
+// deficit / surplus prefix sums, light / heavy index lists) in global scratch at the
+// row's own entry range -- rows of any length, O(len / blockDim) steps per thread.
+constexpr int kRowBlock = 512;
+
+__global__ void __launch_bounds__(kRowBlock)
+    row_alias_block_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ targets,
+                           const double *__restrict__ P, int64_t n, double *w, double *ds,
+                           int32_t *idx, uint4 *rec, double *rowsum) {
+    using BR = cub::BlockReduce<double, kRowBlock>;
+    using BSI = cub::BlockScan<int, kRowBlock>;
+    using BSD = cub::BlockScan<double, kRowBlock>;
+    __shared__ union {
+        typename BR::TempStorage r;
+        typename BSI::TempStorage si;
+        typename BSD::TempStorage sd;
+    } tmp;
+    __shared__ double s_bcast;
+    const int tid = threadIdx.x;
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
         const int64_t lo = indptr[i], hi = indptr[i + 1];
         const int64_t len = hi - lo;
         if (len <= kRowWarpMax) continue;   // the warp tier takes it
-        if (len <= 0) {
-            if (rowsum) rowsum[i] = 0.0;
+        double part = 0.0;
+        for (int64_t e = tid; e < len; e += kRowBlock) part += P[lo + e];
+        const double tot_r = BR(tmp.r).Sum(part);
+        if (tid == 0) s_bcast = tot_r;
+        __syncthreads();
+        const double tot = s_bcast;
+        if (tid == 0 && rowsum) rowsum[i] = tot;
+        if (!(tot > 0.0)) {
+            for (int64_t e = tid; e < len; e += kRowBlock)
+                rec[lo + e] = make_uint4(__float_as_uint(1.0f), targets[lo + e], targets[lo + e], 0u);
+            __syncthreads();
             continue;
         }
-        double total = 0.0;
-        for (int64_t e = lo; e < hi; ++e) total += P[e];
-        if (rowsum) rowsum[i] = total;
-        for (int64_t e = lo; e < hi; ++e)
-            rec[e] = make_uint4(__float_as_uint(1.0f), targets[e], targets[e], 0u);
-        if (!(total > 0.0)) continue;  // massless row: uniform
-        const double f = (double)len / total;
-        int64_t ns = 0, nl = 0;
-        for (int64_t e = lo; e < hi; ++e) {
-            w[e] = P[e] * f;
-            if (w[e] < 1.0) stack[lo + ns++] = (int32_t)(e - lo);
-            else stack[hi - 1 - nl++] = (int32_t)(e - lo);
+        const double f = (double)len / tot;
+        // stable compaction: lights [0, na), heavies [na, len) in index order
+        int64_t count[2] = {0, 0};
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int64_t base = 0; base < len; base += kRowBlock) {
+                const int64_t e = base + tid;
+                bool take = false;
+                if (e < len) {
+                    const double x = pass == 0 ? P[lo + e] * f : w[lo + e];
+                    if (pass == 0) w[lo + e] = x;
+                    take = pass == 0 ? x < 1.0 : !(x < 1.0);
+                }
+                int pos, tot_take;
+                BSI(tmp.si).ExclusiveSum(take ? 1 : 0, pos, tot_take);
+                if (take) idx[lo + (pass ? count[0] : 0) + count[pass] + pos] = (int32_t)e;
+                count[pass] += tot_take;
+                __syncthreads();
+            }
         }
-        while (ns > 0 && nl > 0) {
-            const int64_t sm = lo + stack[lo + --ns];
-            const int64_t lg = lo + stack[hi - 1 - --nl];
-            rec[sm] = make_uint4(__float_as_uint((float)w[sm]), targets[lg], targets[sm], 0u);
-            w[lg] = (w[lg] + w[sm]) - 1.0;
-            if (w[lg] < 1.0) stack[lo + ns++] = (int32_t)(lg - lo);
-            else stack[hi - 1 - nl++] = (int32_t)(lg - lo);
+        const int64_t na = count[0], nh = count[1];
+        // inclusive prefix sums: delta over lights, sigma over heavies
+        for (int part2 = 0; part2 < 2; ++part2) {
+            const int64_t off = part2 ? na : 0, cnt = part2 ? nh : na;
+            double carry = 0.0;
+            for (int64_t base = 0; base < cnt; base += kRowBlock) {
+                const int64_t k = base + tid;
+                double v = 0.0;
+                if (k < cnt) {
+                    const double x = w[lo + idx[lo + off + k]];
+                    v = part2 ? x - 1.0 : 1.0 - x;
+                }
+                double incl, agg;
+                BSD(tmp.sd).InclusiveSum(v, incl, agg);
+                if (k < cnt) ds[lo + off + k] = carry + incl;
+                carry += agg;
+                __syncthreads();
+            }
         }
-        // leftovers keep threshold 1 (optimizer.py:137-138)
+        const double *delta = ds + lo, *sigma = ds + lo + na;
+        const int32_t *id = idx + lo;
+        for (int64_t k = tid; k < na; k += kRowBlock) {   // lights
+            const double prev = k ? delta[k - 1] : 0.0;
+            int64_t a = 0, b = nh;
+            while (a < b) {
+                const int64_t m = (a + b) >> 1;
+                if (sigma[m] > prev) b = m;
+                else a = m + 1;
+            }
+            const int64_t item = id[k];
+            const uint32_t own = (uint32_t)targets[lo + item];
+            rec[lo + item] = a < nh ? make_uint4(__float_as_uint((float)w[lo + item]),
+                                                 (uint32_t)targets[lo + id[na + a]], own, 0u)
+                                    : make_uint4(__float_as_uint(1.0f), own, own, 0u);
+        }
+        for (int64_t k = tid; k < nh; k += kRowBlock) {   // heavies
+            int64_t a = 0, b = na;
+            while (a < b) {
+                const int64_t m = (a + b) >> 1;
+                if (delta[m] >= sigma[k]) b = m;
+                else a = m + 1;
+            }
+            const int64_t item = id[na + k];
+            const uint32_t own = (uint32_t)targets[lo + item];
+            if (a < na && k + 1 < nh) {
+                const double p = fmin(fmax(1.0 + sigma[k] - delta[a], 0.0), 1.0);
+                rec[lo + item] = make_uint4(__float_as_uint((float)p),
+                                            (uint32_t)targets[lo + id[na + k + 1]], own, 0u);
+            } else {
+                rec[lo + item] = make_uint4(__float_as_uint(1.0f), own, own, 0u);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -628,19 +702,21 @@ extern "C" int drg_row_alias(const int64_t *indptr, const int32_t *targets, cons
                              void *stream) {
     if (n <= 0) return DRG_OK;
     cudaStream_t st = as_stream(stream);
-    Scratch stack(st), w(st);
-    DRG_CUDA(stack.alloc(sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1)));
+    Scratch idx(st), w(st), ds(st);
+    DRG_CUDA(idx.alloc(sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1)));
     DRG_CUDA(w.alloc(sizeof(double) * (size_t)std::max<int64_t>(nnz, 1)));
+    DRG_CUDA(ds.alloc(sizeof(double) * (size_t)std::max<int64_t>(nnz, 1)));
     const unsigned gw = (unsigned)std::min<int64_t>(ceil_div(n, kRowWarps), kSMs * 64);
     row_alias_warp_kernel<<<gw, kRowWarps * 32, 0, st>>>(indptr, targets, P, n,
                                                          reinterpret_cast<uint4 *>(out_rec),
                                                          out_rowsum);
     DRG_LAUNCHED("row_alias_warp_kernel");
-    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 128), kSMs * 64);
-    row_alias_kernel<<<g, 128, 0, st>>>(indptr, targets, P, n, stack.as<int32_t>(),
-                                        w.as<double>(), reinterpret_cast<uint4 *>(out_rec),
-                                        out_rowsum);
-    DRG_LAUNCHED("row_alias_kernel");
+    const unsigned g = (unsigned)std::min<int64_t>(n, kSMs * 4);
+    row_alias_block_kernel<<<g, kRowBlock, 0, st>>>(indptr, targets, P, n, w.as<double>(),
+                                                    ds.as<double>(), idx.as<int32_t>(),
+                                                    reinterpret_cast<uint4 *>(out_rec),
+                                                    out_rowsum);
+    DRG_LAUNCHED("row_alias_block_kernel");
     return DRG_OK;
 }
 

@@ -577,19 +577,23 @@ def test_single_step_parity_heavy_rows():
     assert np.all(np.abs(g_got - g_want) <= 1e-5 * np.maximum(1.0, np.abs(g_want)))
 
 
-@pytest.mark.parametrize("which", ["dense80", "hub"])
+@pytest.mark.parametrize("which", ["dense80", "hub", "bighub"])
 def test_row_alias_tables_reproduce_row_laws(golden, which):
-    """drg_row_alias: every row's table (warp tier <= 512 entries, thread tier
-    above) implies exactly P_ij / sum_j P_ij."""
+    """drg_row_alias: every row's table (warp tier <= 512 entries, block tier
+    above, here up to a 70 000-entry hub row) implies exactly P_ij / sum_j P_ij."""
     from paper_2008_07799_b200.graph import DeviceGraph
     from paper_2008_07799_b200.optimizer import build_sampled_tables
     if which == "dense80":
         g = golden_graph(golden, "dense80")
+    elif which == "bighub":
+        rng = np.random.default_rng(3)
+        hub = np.column_stack([np.zeros(70_000, dtype=np.int64), np.arange(1, 70_001)])
+        g = O.from_edges(np.concatenate([hub, rng.integers(1, 70_001, size=(20_000, 2))]), 70_001)
     else:
         rng = np.random.default_rng(2)
         hub = np.column_stack([np.zeros(1500, dtype=np.int64), np.arange(1, 1501)])
         g = O.from_edges(np.concatenate([hub, rng.integers(1, 1501, size=(3000, 2))]), 1501)
-    prep = _prepared(as_gpu_graph(g), k=2, M=5)
+    prep = _prepared(as_gpu_graph(g), k=1 if which == "bighub" else 2, M=5)
     ds = prep.similarity
     S = build_sampled_tables(ds.indptr, ds.targets, ds.weights, ds.row_mass)
     assert float(S.collapse.abs().max()) < 1e-6      # level 0: no collapsed pairs
