@@ -213,65 +213,33 @@ def prolong(coarse_positions: np.ndarray, cmap: np.ndarray, jitter_scale: float,
     return device_prolong(yc, pm, jitter_scale, seed).cpu().numpy().astype(np.float64)
 
 
-def isolated_last(dg: DeviceGraph, min_fraction: float = 0.01, by_degree: bool = False):
+def isolated_last(dg: DeviceGraph, min_fraction: float = 0.01):
     """Relabelling that moves isolated nodes behind all others (relative order kept).
     Isolated nodes are never gathered as neighbours, so the gathered part of Y
     becomes one dense prefix (L2-resident where the whole Y would not be, e.g.
-    R-MAT).  ``by_degree`` also orders the others by descending degree (stable):
-    on power-law graphs most gathers then hit the hubs' compact prefix of Y.  The
-    hierarchy is unaffected (coarsening depends on the visiting ranks only, which
-    callers translate).  Returns (relabelled graph, old -> new id) or (dg, None)."""
+    R-MAT).  Returns (relabelled graph, old -> new id) or (dg, None)."""
     deg = dg.indptr[1:] - dg.indptr[:-1]
     iso = deg == 0
     n = deg.numel()
-    if n == 0 or (not by_degree and float(iso.float().mean()) < min_fraction):
+    if n == 0 or float(iso.float().mean()) < min_fraction:
         return dg, None
-    if by_degree:
-        order = torch.argsort(-deg, stable=True)                      # isolated last
-    else:
-        order = torch.argsort(iso.to(torch.int8), stable=True)       # new -> old
+    order = torch.argsort(iso.to(torch.int8), stable=True)           # new -> old
     rel = torch.empty_like(order)
     rel[order] = torch.arange(n, device=order.device)
-    cnt = deg[order]
     indptr = torch.zeros(n + 1, dtype=torch.int64, device=order.device)
-    indptr[1:] = torch.cumsum(cnt, 0)
-    if not by_degree:
-        # only empty rows move: the entries keep their order, rows stay sorted
-        return DeviceGraph(indptr, rel.to(torch.int32)[dg.indices.to(torch.int64)]), \
-            rel.to(torch.int32)
-    # rows move: gather each new row's entries from its old position
-    new_row = torch.repeat_interleave(torch.arange(n, device=order.device), cnt)
-    src = dg.indptr[:-1][order][new_row] + (torch.arange(new_row.numel(), device=order.device)
-                                            - indptr[:-1][new_row])
-    del new_row
-    indices = rel.to(torch.int32)[dg.indices[src].to(torch.int64)]
-    del src
-    return DeviceGraph(indptr, _sort_rows(indptr, indices)), rel.to(torch.int32)
+    indptr[1:] = torch.cumsum(deg[order], 0)
+    # neighbours are never isolated and keep their relative order: rows stay sorted
+    indices = rel.to(torch.int32)[dg.indices.to(torch.int64)]
+    return DeviceGraph(indptr, indices), rel.to(torch.int32)
 
 
-def _sort_rows(indptr: torch.Tensor, indices: torch.Tensor) -> torch.Tensor:
-    """Rows sorted by id: one stable sort of (row, id) keys."""
-    n = indptr.numel() - 1
-    rows = torch.repeat_interleave(torch.arange(n, device=indptr.device),
-                                   indptr[1:] - indptr[:-1])
-    key = rows * (n + 1) + indices.to(torch.int64)
-    return (torch.sort(key).values % (n + 1)).to(torch.int32)
-
-
-def skewed_degrees(dg: DeviceGraph, ratio: float = 64.0) -> bool:
-    """Power-law-like degree distribution: max degree > ratio * mean degree."""
-    deg = dg.indptr[1:] - dg.indptr[:-1]
-    n = deg.numel()
-    return n > 0 and float(deg.max()) > ratio * max(float(deg.sum()) / n, 1.0)
-
-
-def relabel_coarse_levels(dh: DeviceHierarchy, by_degree: bool = False) -> list:
-    """Isolated-last (``by_degree``: degree-ordered) relabelling of every coarse level
-    of a built hierarchy (maps and level graphs rewritten).  Returns the per-level
-    old -> new maps (None = identity); level 0 is left to the caller."""
+def relabel_coarse_levels(dh: DeviceHierarchy) -> list:
+    """Isolated-last relabelling of every coarse level of a built hierarchy (maps
+    and level graphs rewritten).  Returns the per-level old -> new maps (None =
+    identity); level 0 is left to the caller."""
     rels = [None]
     for l in range(1, dh.depth + 1):
-        g2, rel = isolated_last(dh.levels[l], by_degree=by_degree)
+        g2, rel = isolated_last(dh.levels[l])
         rels.append(rel)
         if rel is None:
             continue

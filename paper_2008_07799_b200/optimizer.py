@@ -33,7 +33,7 @@ from . import _lib
 from .graph import DeviceGraph, Graph, device_components, device_k_neighborhoods
 from .multilevel import (DeviceHierarchy, Hierarchy, compose_maps, device_build_hierarchy,
                          device_prolong, first_level_order, isolated_last,
-                         relabel_coarse_levels, skewed_degrees)
+                         relabel_coarse_levels)
 from .similarity import (DeviceSimilarity, SimilarityParams, SparseSimilarity,
                          device_similarity)
 
@@ -745,12 +745,9 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
     if first_order is None:
         pool = concurrent.futures.ThreadPoolExecutor(1)
         first_order = start_first_order(dg.node_count, opt, min_size, max_levels, pool)
-    # isolated nodes last (layout-internal ids; outputs are mapped back); on
-    # power-law graphs without a neighbour cap the others are ordered by degree (a
-    # cap keeps the first entries by (distance, id), so ids must keep their order)
+    # isolated nodes last (layout-internal ids; outputs are mapped back)
     dg_in = dg
-    by_degree = sim.neighbor_cap is None and skewed_degrees(dg)
-    dg, rel0 = isolated_last(dg, by_degree=by_degree)
+    dg, rel0 = isolated_last(dg)
     n_comp = device_components(dg)
     if n_comp > 1:
         logger.warning("input has %d connected components; repulsion alone separates them",
@@ -765,7 +762,7 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
                                 level0_relabel=rel0, first_order=first_order)
     if pool is not None:
         pool.shutdown(wait=False)
-    relabel = relabel_coarse_levels(dh, by_degree=by_degree)
+    relabel = relabel_coarse_levels(dh)
     relabel[0] = rel0
     del dg_in
     stamp("hierarchy")

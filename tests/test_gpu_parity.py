@@ -650,59 +650,6 @@ def test_isolated_last_relabelling_keeps_the_reference_hierarchy():
     assert np.abs(lay.positions[iso]).max() < 1.0         # isolated nodes barely move
 
 
-def test_degree_relabelling_keeps_the_reference_hierarchy():
-    """On a power-law graph without a neighbour cap the layout pipeline orders nodes
-    by degree (isolated last); the translated visiting orders still give exactly the
-    reference hierarchy, P is the same relation, and positions come back in the
-    caller's order."""
-    from paper_2008_07799_b200.graph import DeviceGraph
-    from paper_2008_07799_b200.multilevel import skewed_degrees
-    from paper_2008_07799_b200.optimizer import _HIERARCHY_TAG, _derive_seed, prepare_layout
-    rng = np.random.default_rng(5)
-    n = 4000
-    hubs = rng.integers(0, 20, size=6000)                 # a few hubs ...
-    leaves = rng.integers(20, 3600, size=6000)           # ... many leaves, 3600.. isolated
-    pairs = np.concatenate([np.column_stack([hubs, leaves]),
-                            rng.integers(20, 3600, size=(1500, 2))])
-    g = O.from_edges(pairs, n)
-    dg = DeviceGraph.from_host(as_gpu_graph(g))
-    assert skewed_degrees(dg)
-    prep = prepare_layout(dg, B.SimilarityParams(k=1), B.OptimizerParams(seed=6, iters=5),
-                          min_size=16)
-    rel0 = prep.relabel[0].cpu().numpy().astype(np.int64)
-    deg = np.diff(g.indptr)
-    inv = np.empty(n, dtype=np.int64)
-    inv[rel0] = np.arange(n)
-    assert np.all(np.diff(deg[inv]) <= 0)                 # descending degree, isolated last
-    href = O.build_hierarchy(g, 0.8, 16, _derive_seed(6, _HIERARCHY_TAG))
-    dh = prep.hierarchy
-    assert dh.sizes == [lv.node_count for lv in href.levels]
-    flat = np.arange(n)
-    for level in range(1, dh.depth + 1):
-        flat = dh.maps[level - 1].cpu().numpy()[flat] if level > 1 else \
-            dh.maps[0].cpu().numpy()[np.arange(n)]
-        rel = prep.relabel[level]
-        inv_l = np.arange(dh.sizes[level])
-        if rel is not None:
-            inv_l = np.empty(dh.sizes[level], dtype=np.int64)
-            inv_l[rel.cpu().numpy()] = np.arange(dh.sizes[level])
-        assert np.array_equal(inv_l[flat[rel0]], O.compose_maps(href, level))
-    # P: the same pairs and values as the reference's, in relabelled ids
-    ns = O.build_sparse_similarity(O.all_k_neighborhoods(g, 1))
-    ds = prep.similarity
-    ip, tg, w = ds.indptr.cpu().numpy(), ds.targets.cpu().numpy(), ds.weights.cpu().numpy()
-    rows = np.repeat(np.arange(n), np.diff(ip))
-    got = dict(zip(zip(inv[rows].tolist(), inv[tg].tolist()), w.tolist()))
-    want_rows = np.repeat(np.arange(n), np.diff(ns.indptr))
-    want = dict(zip(zip(want_rows.tolist(), ns.targets.tolist()), ns.weights.tolist()))
-    assert got.keys() == want.keys()
-    np.testing.assert_allclose([got[k] for k in want], list(want.values()), rtol=1e-9)
-    lay = B.layout_graph(as_gpu_graph(g), B.SimilarityParams(k=1),
-                         B.OptimizerParams(seed=6, iters=20))
-    assert np.isfinite(lay.positions).all()
-    assert np.abs(lay.positions[deg == 0]).max() < 1.0    # isolated nodes stay put
-
-
 def test_sgather_attraction_is_unbiased(golden):
     """update="sgather": the sampled attraction (S partners ~ W_a., weight wsum/S)
     averages to the full CSR gather of K7 (attraction only, M = 0)."""
