@@ -32,6 +32,9 @@ CONFIGS = {
                  np_sample=None),
     "mesh_small": dict(k=2, perplexity=50.0, iters=800, max_levels=4, init="normal",
                        z_pairs=None, np_sample=None),
+    # BASELINE C4 itself: 120^3 mesh, 1.73 M nodes (the bench workload)
+    "mesh": dict(k=2, perplexity=50.0, iters=800, max_levels=4, init="normal",
+                 z_pairs=None, np_sample=None),
 }
 
 
@@ -42,6 +45,8 @@ def graph_for(name):
         g = synthetic.grid(100, 100, device="host")
     elif name in ("rgg", "rgg1"):
         g = synthetic.rgg(200_000, seed=0, device="host")
+    elif name == "mesh":
+        g = synthetic.mesh3d(120, device="host")
     else:
         g = synthetic.mesh3d(40, device="host")
     return O.Graph(g.indptr, g.indices), B.Graph(g.indptr, g.indices)
