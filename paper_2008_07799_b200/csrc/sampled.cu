@@ -467,8 +467,30 @@ __device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t s
 
 template <bool AGG>
 __global__ void __launch_bounds__(256, 4) apply_kernel(PArgs A, float2 *y) {
+    // launched with programmatic stream serialization: the previous epoch's grid
+    // must be complete (and its y updates visible) before this one reads y
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     apply_epoch<AGG>(A, y, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
                      (int64_t)gridDim.x * blockDim.x);
+}
+
+// Consecutive epochs on one stream as programmatic dependent launches: the next
+// grid is set up while the previous drains (its griddepcontrol.wait holds the
+// steps back), so small levels do not pay the full launch gap per epoch.
+int launch_apply(const PArgs &P, float2 *y, unsigned grid, bool agg, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (agg) DRG_CUDA(cudaLaunchKernelEx(&cfg, apply_kernel<true>, P, y));
+    else DRG_CUDA(cudaLaunchKernelEx(&cfg, apply_kernel<false>, P, y));
+    DRG_LAUNCHED("apply_kernel");
+    return DRG_OK;
 }
 
 // Per-row alias tables (build_alias_table, optimizer.py:111-139, applied to every
@@ -937,9 +959,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
             const int t = t0 + c * K + e;
             P.lr = lr_at(t);
             P.draws = chunk_buf(c) + (size_t)e * (rec_bytes / 4);
-            if (agg) apply_kernel<true><<<grid, 256, 0, ss.hi>>>(P, reinterpret_cast<float2 *>(y));
-            else apply_kernel<false><<<grid, 256, 0, ss.hi>>>(P, reinterpret_cast<float2 *>(y));
-            DRG_LAUNCHED("apply_kernel");
+            DRG_TRY(launch_apply(P, reinterpret_cast<float2 *>(y), grid, agg, ss.hi));
         }
         DRG_CUDA(cudaEventRecord(ev.e[3 + (c & 1)], ss.hi));
     }
