@@ -477,10 +477,10 @@ __global__ void __launch_bounds__(256, 4) apply_kernel(PArgs A, float2 *y) {
 // Consecutive epochs on one stream as programmatic dependent launches: the next
 // grid is set up while the previous drains (its griddepcontrol.wait holds the
 // steps back), so small levels do not pay the full launch gap per epoch.
-int launch_apply(const PArgs &P, float2 *y, unsigned grid, bool agg, cudaStream_t st) {
+int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3((unsigned)block);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -866,8 +866,10 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     const bool agg = flags & DRG_SAMPLED_AGGREGATE;
     const char *probe_env = getenv("DRG_SAMPLED_PROBE");
     const int probe = probe_env ? atoi(probe_env) : 0;
-    const int64_t threads = std::max<int64_t>(256, std::min<int64_t>(n_steps, max_threads));
-    const unsigned grid = (unsigned)ceil_div(threads, 256);
+    // exactly min(n_steps, max_threads) steps in flight (1: the sequential kernel)
+    const int64_t threads = std::max<int64_t>(1, std::min<int64_t>(n_steps, max_threads));
+    const int block = (int)std::min<int64_t>(256, threads);
+    const unsigned grid = (unsigned)(threads / block);
     auto lr_at = [&](int t) { return (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0); };
     if ((flags & DRG_SAMPLED_FUSED) && map)
         return fail(DRG_ERR_UNSUPPORTED, "the fused form draws from level tables (map == NULL)");
@@ -894,8 +896,8 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
         for (int j = 0; j < n_iter; ++j) {
             A.t = t0 + j;
             A.lr = lr_at(A.t);
-            if (agg) sampled_kernel<true><<<grid, 256, 0, st>>>(A, reinterpret_cast<float2 *>(y));
-            else sampled_kernel<false><<<grid, 256, 0, st>>>(A, reinterpret_cast<float2 *>(y));
+            if (agg) sampled_kernel<true><<<grid, block, 0, st>>>(A, reinterpret_cast<float2 *>(y));
+            else sampled_kernel<false><<<grid, block, 0, st>>>(A, reinterpret_cast<float2 *>(y));
             DRG_LAUNCHED("sampled_kernel");
         }
         return DRG_OK;
@@ -959,7 +961,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
             const int t = t0 + c * K + e;
             P.lr = lr_at(t);
             P.draws = chunk_buf(c) + (size_t)e * (rec_bytes / 4);
-            DRG_TRY(launch_apply(P, reinterpret_cast<float2 *>(y), grid, agg, ss.hi));
+            DRG_TRY(launch_apply(P, reinterpret_cast<float2 *>(y), grid, block, agg, ss.hi));
         }
         DRG_CUDA(cudaEventRecord(ev.e[3 + (c & 1)], ss.hi));
     }

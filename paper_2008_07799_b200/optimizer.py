@@ -515,8 +515,9 @@ class LayoutPlan:
         return out
 
     def sampled_steps(self, level: int, y: torch.Tensor, step_lo: int, n_steps: int, t0: int,
-                      n_iter: int = 1) -> None:
-        """drg_layout_sampled: steps [step_lo, step_lo + n_steps) of epochs t0.. in place."""
+                      n_iter: int = 1, max_threads: int | None = None) -> None:
+        """drg_layout_sampled: steps [step_lo, step_lo + n_steps) of epochs t0.. in place,
+        n_l / sampled_concurrency(_coarse) steps in flight (or ``max_threads``)."""
         L, gamma, seed = self._level_args(level)
         S = L.sampled
         if S is None:
@@ -529,7 +530,8 @@ class LayoutPlan:
                   _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(y), step_lo, n_steps, t0, n_iter,
                   o.iters,
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
-                  o.neg_samples, seed, level, max(256, L.n // max(1, div)),
+                  o.neg_samples, seed, level,
+                  max_threads if max_threads is not None else max(32, L.n // max(1, div)),
                   int(S.hubs) | (2 if o.sampled_fused else 0), _lib.stream_ptr())
 
     def _collapse(self, level: int):

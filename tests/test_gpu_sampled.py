@@ -160,3 +160,21 @@ def test_split_and_fused_run_the_same_steps(golden):
     plan.sampled_steps(0, a, 0, L.n, 5, 1)
     assert torch.isfinite(a).all() and not torch.equal(a, y)
 
+
+
+def test_fused_and_split_epochs_agree_sequentially(golden):
+    """With one step in flight the fused kernel and the split draw/apply passes run
+    the same epochs at the finest level: equal positions after two whole epochs."""
+    plan, _, _ = _setup(golden)
+    n = plan.levels[0].n
+    rng = np.random.default_rng(12)
+    y0 = torch.from_numpy(rng.normal(0, 1.0, size=(n, 2)).astype(np.float32)).cuda()
+    outs = []
+    for fused in (False, True):
+        plan.opt.sampled_fused = fused
+        y = y0.clone()
+        plan.sampled_steps(0, y, 0, n, 2, 2, max_threads=1)
+        outs.append(y)
+    plan.opt.sampled_fused = False
+    assert not torch.equal(outs[0], y0)
+    torch.testing.assert_close(outs[0], outs[1], rtol=0, atol=1e-5)
