@@ -208,10 +208,9 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * is joined back into `stream`.  Both forms draw identical steps. */
 #define DRG_SAMPLED_AGGREGATE 1
 #define DRG_SAMPLED_FUSED 2
-/* Levels of n_y <= 28672 nodes run the update pass shared-memory-resident (positions
- * as 32-bit fixed point in one CTA's shared memory, native integer atomics, a chunk
- * of epochs per launch, <= 1024 steps in flight); DRG_SAMPLED_GLOBAL keeps the
- * global-memory pass. */
+/* Levels of n_y <= 262144 nodes run the update pass cluster-resident (positions as
+ * 32-bit fixed point in one thread-block cluster's distributed shared memory, a
+ * chunk of epochs per launch); DRG_SAMPLED_GLOBAL keeps the global-memory pass. */
 #define DRG_SAMPLED_GLOBAL 4
 
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,

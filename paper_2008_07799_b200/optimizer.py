@@ -92,8 +92,8 @@ class OptimizerParams:
     hub_levels: str = "jacobi"     # update="sampled": hub-heavy levels run this update
     sampled_fused: bool = False    # update="sampled": draw inline (one kernel per epoch)
                                    # instead of the split draw pass + update pass
-    sampled_cluster: bool = True   # update="sampled": levels <= 28672 nodes keep Y in one
-                                   # CTA's shared memory (fixed point, native atomics)
+    sampled_cluster: bool = True   # update="sampled": levels <= 262144 nodes keep Y in one
+                                   # thread-block cluster's shared memory (fixed point)
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
