@@ -194,7 +194,6 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * (Q^l) redrawn (<= 9) while they hit i or j, both ends moved (float2 atomics).
  * Steps step_lo .. step_lo + n_steps - 1 of each epoch run here (a rank's share of
  * the epoch in the multi-GPU mode); at most max_threads steps run concurrently.
- * y holds the level's n_y nodes.
  * map (device int32 [n], may be NULL): the tables are level 0's over n nodes and
  * every drawn node -- source, target, negatives before their rejection test -- is
  * mapped to level l through map (composed parent maps), the reference's own
@@ -208,15 +207,11 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * is joined back into `stream`.  Both forms draw identical steps. */
 #define DRG_SAMPLED_AGGREGATE 1
 #define DRG_SAMPLED_FUSED 2
-/* Levels of n_y <= 262144 nodes run the update pass cluster-resident (positions as
- * 32-bit fixed point in one thread-block cluster's distributed shared memory, a
- * chunk of epochs per launch); DRG_SAMPLED_GLOBAL keeps the global-memory pass. */
-#define DRG_SAMPLED_GLOBAL 4
 
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,
                        const uint64_t *src_alias, const float *collapse,
                        const uint64_t *neg_alias, const int32_t *map, int64_t n, float *y,
-                       int64_t n_y, int64_t step_lo,
+                       int64_t step_lo,
                        int64_t n_steps, int t0,
                        int n_iter, int iters, double lr0, double gamma, double eps, double clip,
                        int b, int M, uint64_t seed, int level, int64_t max_threads,

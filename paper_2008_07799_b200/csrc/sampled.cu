@@ -21,8 +21,6 @@
 #include <algorithm>
 #include <mutex>
 
-#include <cooperative_groups.h>
-
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -495,252 +493,6 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
     return DRG_OK;
 }
 
-// ---- cluster-resident small levels (fixed point) ------------------------------------
-// A level of n <= 16 * 16384 nodes keeps its positions in the distributed shared
-// memory of one thread-block cluster (node v in CTA v >> 14, slot v & 16383) and runs
-// a whole chunk of epochs in ONE launch, epochs separated by cluster barriers.
-// sm_100 has no native float atomic add on shared memory (it is a CAS loop), but
-// 32-bit integer adds are native -- locally and on a peer CTA's shared memory
-// (red.shared::cluster.add.u32) -- so the positions live there as 32-bit fixed point
-// with a power-of-two scale chosen per epoch from the largest |coordinate| (2^5
-// headroom for growth within an epoch).  Each update is rounded once to the grid
-// (resolution 2^-26 of the extent: finer than fp32's 2^-24 near the extent) and
-// the integer sums are exact, so concurrent updates commute.  Same draws and step
-// arithmetic as apply_kernel.
-namespace cg = cooperative_groups;
-constexpr int kQShift = 14;                      // 16384 nodes (128 KiB) per CTA
-constexpr int kQMaxCluster = 16;                 // non-portable cluster size
-constexpr int kQThreads = 1024;
-
-struct QArgs {
-    const int32_t *draws;   // the chunk's first epoch; epoch e at e * (2 + M) * n_steps
-    int64_t n_steps;
-    int64_t n;
-    int t0, n_epochs, iters;
-    double lr0;
-    float gamma, eps, clip;
-    int b, M;
-};
-
-__device__ __forceinline__ uint32_t q_addr(const int2 *local, int64_t v) {
-    const uint32_t a = (uint32_t)__cvta_generic_to_shared(local + (v & ((1 << kQShift) - 1)));
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-                 : "=r"(r) : "r"(a), "r"((uint32_t)(v >> kQShift)));
-    return r;
-}
-
-__device__ __forceinline__ float2 q_load(uint32_t addr, float inv) {
-    int x, y;
-    asm volatile("ld.shared::cluster.v2.s32 {%0, %1}, [%2];" : "=r"(x), "=r"(y) : "r"(addr)
-                 : "memory");
-    return make_float2((float)x * inv, (float)y * inv);
-}
-
-__device__ __forceinline__ void q_add(uint32_t addr, float dx, float dy, float scale) {
-    const int qx = __float2int_rn(dx * scale), qy = __float2int_rn(dy * scale);
-    if (qx) asm volatile("red.shared::cluster.add.u32 [%0], %1;" :: "r"(addr), "r"(qx) : "memory");
-    if (qy) asm volatile("red.shared::cluster.add.u32 [%0], %1;" :: "r"(addr + 4), "r"(qy) : "memory");
-}
-
-// power-of-two scale with max |q| = maxabs * scale in [2^25, 2^26)
-__device__ __forceinline__ float q_scale_for(float maxabs) {
-    int e;
-    frexpf(fmaxf(maxabs, 1e-30f), &e);   // maxabs < 2^e
-    return ldexpf(1.0f, 26 - e);
-}
-
-// cluster-wide max |value| of the slices (bits of non-negative floats order as ints)
-__device__ float q_cluster_max(cg::cluster_group &cl, unsigned *red_slot, float local) {
-    __shared__ float warp_max[kQThreads / 32];
-    for (int o = 16; o; o >>= 1) local = fmaxf(local, __shfl_xor_sync(kFull, local, o));
-    if ((threadIdx.x & 31) == 0) warp_max[threadIdx.x >> 5] = local;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float m = 0.f;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, warp_max[w]);
-        unsigned *dst = cl.map_shared_rank(red_slot, 0);
-        atomicMax(dst, __float_as_uint(m));
-    }
-    cl.sync();
-    const float r = __uint_as_float(*cl.map_shared_rank(red_slot, 0));
-    cl.sync();   // everyone has read rank 0's slot before it is reset
-    return r;
-}
-
-__global__ void __launch_bounds__(kQThreads) qcluster_apply_kernel(QArgs A, float2 *y) {
-    extern __shared__ int2 ys[];
-    __shared__ unsigned red_slot;
-    cg::cluster_group cl = cg::this_cluster();
-    const unsigned rank = cl.block_rank();
-    constexpr int64_t chunk = 1LL << kQShift;
-    const int64_t base = (int64_t)rank * chunk;
-    const int64_t own = A.n - base < chunk ? (A.n - base > 0 ? A.n - base : 0) : chunk;
-    if (threadIdx.x == 0) red_slot = 0u;
-    cl.sync();
-    float m = 0.f;
-    for (int64_t k = threadIdx.x; k < own; k += blockDim.x) {
-        const float2 v = y[base + k];
-        m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
-    }
-    float scale = q_scale_for(q_cluster_max(cl, &red_slot, m));
-    float inv = 1.0f / scale;
-    for (int64_t k = threadIdx.x; k < own; k += blockDim.x) {
-        const float2 v = y[base + k];
-        ys[k] = make_int2(__float2int_rn(v.x * scale), __float2int_rn(v.y * scale));
-    }
-    cl.sync();
-    const int64_t tid = (int64_t)rank * blockDim.x + threadIdx.x;
-    const int64_t nth = (int64_t)cl.num_blocks() * blockDim.x;
-    const float two_b = 2.0f * (float)A.b;
-    const int Me = min(A.M, kMaxNeg);
-    const int64_t ns = A.n_steps;
-    for (int e = 0; e < A.n_epochs; ++e) {
-        const int32_t *d = A.draws + (size_t)e * (size_t)(2 + A.M) * (size_t)ns;
-        const float lr = (float)fmax(A.lr0 * (1.0 - (double)(A.t0 + e) / (double)A.iters), 0.0);
-        for (int64_t sl = tid; sl < ns; sl += nth) {
-            const int64_t i = __ldcs(d + sl), j = __ldcs(d + ns + sl);
-            int32_t cand[kMaxNeg];
-            float2 ycand[kMaxNeg];
-            uint32_t acand[kMaxNeg];
-#pragma unroll
-            for (int m2 = 0; m2 < kMaxNeg; ++m2)
-                cand[m2] = m2 < Me ? __ldcs(d + (2 + m2) * ns + sl) : -1;
-            const uint32_t ai = q_addr(ys, i), aj = q_addr(ys, j);
-            float2 yi = q_load(ai, inv);
-            const float2 yj = q_load(aj, inv);
-#pragma unroll
-            for (int m2 = 0; m2 < kMaxNeg; ++m2) {
-                acand[m2] = cand[m2] >= 0 ? q_addr(ys, cand[m2]) : 0u;
-                ycand[m2] = cand[m2] >= 0 ? q_load(acand[m2], inv) : make_float2(0.f, 0.f);
-            }
-            float gix = 0.f, giy = 0.f;
-            if (i != j) {   // _kernels.py:82-105
-                const float dx = yi.x - yj.x, dy = yi.y - yj.y;
-                const float ld2 = dx * dx + dy * dy;
-                if (ld2 > 0.f) {
-                    const float pw = ipowf(ld2, A.b - 1);
-                    const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
-                    const float gx = lr * clampf(coef * dx, A.clip);
-                    const float gy = lr * clampf(coef * dy, A.clip);
-                    q_add(aj, -gx, -gy, scale);
-                    yi.x += gx;
-                    yi.y += gy;
-                    gix += gx;
-                    giy += gy;
-                }
-            }
-            float ax[kMaxNeg], ay[kMaxNeg];
-#pragma unroll
-            for (int m2 = 0; m2 < kMaxNeg; ++m2) {   // _kernels.py:106-140
-                if (m2 < Me) {
-                    float2 yc = ycand[m2];
-                    own_updates(yc, cand[m2], m2, cand, ax, ay);
-                    int64_t tu;
-                    float tx, ty;
-                    repel(yi, yc, cand[m2], lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty,
-                          gix, giy);
-                    ax[m2] = tx;
-                    ay[m2] = ty;
-                    if (tu >= 0) q_add(acand[m2], tx, ty, scale);
-                }
-            }
-            for (int m2 = Me; m2 < A.M; ++m2) {
-                const int64_t target = __ldcs(d + (2 + m2) * ns + sl);
-                float2 yc = make_float2(0.f, 0.f);
-                uint32_t at = 0u;
-                if (target >= 0) {
-                    at = q_addr(ys, target);
-                    yc = q_load(at, inv);
-                }
-                int64_t tu;
-                float tx, ty;
-                repel(yi, yc, target, lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
-                if (tu >= 0) q_add(at, tx, ty, scale);
-            }
-            if (gix != 0.f || giy != 0.f) q_add(ai, gix, giy, scale);
-        }
-        cl.sync();
-        // re-scale for the next epoch from the largest |coordinate| now
-        float mq = 0.f;
-        for (int64_t k = threadIdx.x; k < own; k += blockDim.x) {
-            const int2 q = ys[k];
-            mq = fmaxf(mq, fmaxf(fabsf((float)q.x), fabsf((float)q.y)) * inv);
-        }
-        const float nscale = q_scale_for(q_cluster_max(cl, &red_slot, mq));
-        if (nscale != scale) {   // exact: both scales are powers of two
-            const float f = nscale / scale;
-            for (int64_t k = threadIdx.x; k < own; k += blockDim.x) {
-                const int2 q = ys[k];
-                ys[k] = make_int2(__float2int_rn((float)q.x * f), __float2int_rn((float)q.y * f));
-            }
-            scale = nscale;
-            inv = 1.0f / scale;
-        }
-        if (threadIdx.x == 0) red_slot = 0u;
-        cl.sync();
-    }
-    for (int64_t k = threadIdx.x; k < own; k += blockDim.x) {
-        const int2 q = ys[k];
-        y[base + k] = make_float2((float)q.x * inv, (float)q.y * inv);
-    }
-}
-
-// Cluster size for a level of n nodes (0: not cluster-resident on this GPU)
-int qcluster_size_for(int64_t n) {
-    const int64_t c = (n + (1LL << kQShift) - 1) >> kQShift;
-    if (n <= 0 || c > kQMaxCluster) return 0;
-    static int max_cluster = -1;
-    if (max_cluster < 0) {   // the largest cluster of 1024-thread, 128 KiB CTAs that fits
-        max_cluster = 0;
-        const size_t smem = sizeof(int2) << kQShift;
-        if (cudaFuncSetAttribute(qcluster_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess ||
-            cudaFuncSetAttribute(qcluster_apply_kernel,
-                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-            cudaGetLastError();
-            return 0;
-        }
-        for (int cs = kQMaxCluster; cs >= 1 && !max_cluster; --cs) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3((unsigned)cs);
-            cfg.blockDim = dim3(kQThreads);
-            cfg.dynamicSmemBytes = smem;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = (unsigned)cs;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            int clusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&clusters, qcluster_apply_kernel, &cfg) == cudaSuccess &&
-                clusters > 0)
-                max_cluster = cs;
-            cudaGetLastError();
-        }
-    }
-    return c <= max_cluster ? (int)std::max<int64_t>(c, 1) : 0;
-}
-
-int launch_qcluster(const QArgs &A, float2 *y, int C, int threads_per_cta, cudaStream_t st) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)C);
-    cfg.blockDim = dim3((unsigned)threads_per_cta);
-    cfg.dynamicSmemBytes = sizeof(int2) << kQShift;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    DRG_CUDA(cudaLaunchKernelEx(&cfg, qcluster_apply_kernel, A, y));
-    DRG_LAUNCHED("qcluster_apply_kernel");
-    return DRG_OK;
-}
-
 // Per-row alias tables (build_alias_table, optimizer.py:111-139, applied to every
 // row of P) by the parallel sweep: the law of Vose's construction without its
 // sequential stack.  rec[e] = {fp32 threshold of bucket e, alias target, own target}.
@@ -1102,8 +854,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                                   const uint64_t *row_alias, const uint64_t *src_alias,
                                   const float *collapse, const uint64_t *neg_alias,
                                   const int32_t *map, int64_t n,
-                                  float *y, int64_t n_y, int64_t step_lo, int64_t n_steps, int t0,
-                                  int n_iter,
+                                  float *y, int64_t step_lo, int64_t n_steps, int t0, int n_iter,
                                   int iters,
                                   double lr0, double gamma, double eps, double clip, int b, int M,
                                   uint64_t seed, int level, int64_t max_threads, int flags,
@@ -1150,13 +901,6 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
             DRG_LAUNCHED("sampled_kernel");
         }
         return DRG_OK;
-    }
-    // small levels: positions resident in one cluster's distributed shared memory
-    const int qc = (!agg && !(flags & DRG_SAMPLED_GLOBAL)) ? qcluster_size_for(n_y) : 0;
-    int q_threads = 0;
-    if (qc) {   // <= max_threads steps in flight, whole warps, <= 1024 per CTA
-        const int64_t per = (threads + qc - 1) / qc;
-        q_threads = (int)std::min<int64_t>(kQThreads, per < 32 ? per : (per + 31) / 32 * 32);
     }
     // split: draw_kernel (K epochs per launch, double-buffered, low-priority stream)
     // -> apply_kernel per epoch (high-priority stream); joined back into `stream`
@@ -1213,13 +957,6 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
         }
         DRG_CUDA(cudaStreamWaitEvent(ss.hi, ev.e[1 + (c & 1)], 0));
         const int ne = std::min(K, n_iter - c * K);
-        if (qc) {   // the whole chunk in one cluster-resident launch
-            QArgs Q{chunk_buf(c), n_steps, n_y, t0 + c * K, ne, iters, lr0, (float)gamma,
-                    (float)eps, (float)clip, b, M};
-            DRG_TRY(launch_qcluster(Q, reinterpret_cast<float2 *>(y), qc, q_threads, ss.hi));
-            DRG_CUDA(cudaEventRecord(ev.e[3 + (c & 1)], ss.hi));
-            continue;
-        }
         for (int e = 0; e < ne; ++e) {
             const int t = t0 + c * K + e;
             P.lr = lr_at(t);

@@ -92,8 +92,6 @@ class OptimizerParams:
     hub_levels: str = "jacobi"     # update="sampled": hub-heavy levels run this update
     sampled_fused: bool = False    # update="sampled": draw inline (one kernel per epoch)
                                    # instead of the split draw pass + update pass
-    sampled_cluster: bool = True   # update="sampled": levels <= 262144 nodes keep Y in one
-                                   # thread-block cluster's shared memory (fixed point)
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
@@ -529,13 +527,12 @@ class LayoutPlan:
         ip, neg, n_tab, mp = self._tables(level)
         _lib.call("drg_layout_sampled", _lib.ptr(ip), None,
                   _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), self._collapse(level),
-                  _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(y), y.shape[0], step_lo, n_steps,
-                  t0, n_iter, o.iters,
+                  _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(y), step_lo, n_steps, t0, n_iter,
+                  o.iters,
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
                   o.neg_samples, seed, level,
                   max_threads if max_threads is not None else max(32, L.n // max(1, div)),
-                  int(S.hubs) | (2 if o.sampled_fused else 0) | (0 if o.sampled_cluster else 4),
-                  _lib.stream_ptr())
+                  int(S.hubs) | (2 if o.sampled_fused else 0), _lib.stream_ptr())
 
     def _collapse(self, level: int):
         """Collapse probabilities of ``level`` (NULL at level 0 and for mapped draws)."""

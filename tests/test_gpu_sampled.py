@@ -181,58 +181,3 @@ def test_fused_and_split_epochs_agree_sequentially(golden):
     moved = [(o - y0).abs().sum(1) > 0 for o in outs]
     assert torch.equal(moved[0], moved[1]) and bool(moved[0].any())
     torch.testing.assert_close(outs[0], outs[1], rtol=0, atol=1e-3)
-
-
-def test_cluster_resident_small_level_sequential(golden):
-    """Levels of <= 262144 nodes run cluster-resident with 32-bit fixed-point
-    positions: one step in flight gives the global-memory pass's epoch (fixed-point
-    rounding and fp32 round-off amplified by the dynamics apart)."""
-    plan, _, _ = _setup(golden)
-    n = plan.levels[0].n
-    rng = np.random.default_rng(13)
-    y0 = torch.from_numpy(rng.normal(0, 1.0, size=(n, 2)).astype(np.float32)).cuda()
-    outs = []
-    for cluster in (True, False):
-        plan.opt.sampled_cluster = cluster
-        y = y0.clone()
-        plan.sampled_steps(0, y, 0, n, 9, 1, max_threads=1)
-        outs.append(y)
-    plan.opt.sampled_cluster = True
-    moved = [(o - y0).abs().sum(1) > 0 for o in outs]
-    assert torch.equal(moved[0], moved[1]) and bool(moved[0].any())
-    torch.testing.assert_close(outs[0], outs[1], rtol=0, atol=1e-3)
-
-
-def test_cluster_resident_level_spanning_ctas():
-    """A 40 000-node level spans 3 CTAs of the cluster (node v in CTA v >> 14):
-    single steps agree with the global-memory pass to the fixed-point resolution,
-    and whole epochs move every slice and stay finite."""
-    from paper_2008_07799_b200.graph import DeviceGraph
-    from paper_2008_07799_b200.optimizer import prepare_layout
-    side = 200
-    idx = np.arange(side * side).reshape(side, side)
-    e = np.concatenate([np.column_stack([idx[:, :-1].ravel(), idx[:, 1:].ravel()]),
-                        np.column_stack([idx[:-1, :].ravel(), idx[1:, :].ravel()])])
-    g = B.from_edges(e, side * side)
-    prep = prepare_layout(DeviceGraph.from_host(g), B.SimilarityParams(k=1),
-                          B.OptimizerParams(seed=2, iters=10), max_levels=1)
-    plan = prep.plan
-    L = plan.levels[0]
-    assert L.n == 40000
-    rng = np.random.default_rng(8)
-    y0 = torch.from_numpy(rng.normal(0, 5.0, size=(L.n, 2)).astype(np.float32)).cuda()
-    for s in range(0, 40000, 997):          # steps touching all three CTAs' slices
-        outs = []
-        for cluster in (True, False):
-            plan.opt.sampled_cluster = cluster
-            y = y0.clone()
-            plan.sampled_steps(0, y, s, 1, 1, 1)
-            outs.append(y)
-        torch.testing.assert_close(outs[0], outs[1], rtol=0, atol=1e-5)
-    plan.opt.sampled_cluster = True
-    y = y0.clone()
-    plan.sampled_steps(0, y, 0, L.n, 0, 3)
-    assert torch.isfinite(y).all()
-    for c in range(3):
-        sl = slice(c * 16384, min((c + 1) * 16384, L.n))
-        assert not torch.equal(y[sl], y0[sl])
