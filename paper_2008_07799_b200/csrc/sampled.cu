@@ -49,6 +49,20 @@ struct SArgs {
 
 __device__ __forceinline__ float clampf(float g, float c) { return fminf(fmaxf(g, -c), c); }
 
+// x^n with n a compile-time constant (B > 0) or the runtime n (B == 0)
+template <int B>
+__device__ __forceinline__ float ipow_b(float x, int n) {
+    if (B > 0) {
+        float r = 1.0f;
+#pragma unroll
+        for (int i = 0; i < B - 1; ++i) r *= x;
+        return r;
+    }
+    float r = 1.0f;
+    for (int i = 0; i < n; ++i) r *= x;
+    return r;
+}
+
 __device__ __forceinline__ float ipowf(float x, int n) {
     float r = 1.0f;
     for (int i = 0; i < n; ++i) r *= x;
@@ -109,6 +123,7 @@ __device__ __forceinline__ void add_y_w(float2 *y, int64_t i, float dx, float dy
 
 // One repulsion of _kernels.py:120-140: the source moves by +g (tracked locally in
 // yi and in its step total), the negative by -g (returned in tu/tx/ty).
+template <int B = 0>
 __device__ __forceinline__ void repel(float2 &yi, float2 yc, int64_t target, float lr,
                                       float gamma, float eps, float clip, float two_b, int b,
                                       int64_t &tu, float &tx, float &ty, float &gix, float &giy) {
@@ -118,7 +133,7 @@ __device__ __forceinline__ void repel(float2 &yi, float2 yc, int64_t target, flo
     const float dx = yi.x - yc.x, dy = yi.y - yc.y;
     const float ld2 = dx * dx + dy * dy;
     if (!(ld2 + eps > 0.f)) return;
-    const float pw = ipowf(ld2, b - 1);
+    const float pw = ipow_b<B>(ld2, b - 1);
     const float coef = __fdividef(gamma * two_b, (ld2 + eps) * (1.0f + pw * ld2));
     const float gx = lr * clampf(coef * dx, clip);
     const float gy = lr * clampf(coef * dy, clip);
@@ -386,7 +401,7 @@ struct PArgs {
 // position is carried through the step, attraction and each repulsion move the
 // other end by the opposite clipped increment; the source's own total is published
 // once.  The next step's draw record is prefetched while this step runs.
-template <bool AGG>
+template <bool AGG, int B>
 __device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t sl,
                                             const int64_t nthreads) {
     const float two_b = 2.0f * (float)A.b;
@@ -424,7 +439,7 @@ __device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t s
             const float dx = yi.x - yj.x, dy = yi.y - yj.y;
             const float ld2 = dx * dx + dy * dy;
             if (ld2 > 0.f) {
-                const float pw = ipowf(ld2, A.b - 1);
+                const float pw = ipow_b<B>(ld2, A.b - 1);
                 const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
                 const float gx = A.lr * clampf(coef * dx, A.clip);
                 const float gy = A.lr * clampf(coef * dy, A.clip);
@@ -446,7 +461,7 @@ __device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t s
                 own_updates(yc, cand[m], m, cand, ax, ay);   // gathered before them
                 int64_t tu;
                 float tx, ty;
-                repel(yi, yc, cand[m], A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix,
+                repel<B>(yi, yc, cand[m], A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix,
                       giy);
                 ax[m] = tx;
                 ay[m] = ty;
@@ -458,20 +473,26 @@ __device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t s
             const float2 yc = target >= 0 ? ld_y(y, target) : make_float2(0.f, 0.f);
             int64_t tu;
             float tx, ty;
-            repel(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
+            repel<B>(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
             add_y_w<AGG>(y, tu, tx, ty, A.probe);
         }
         add_y_w<AGG>(y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy, A.probe);
     }
 }
 
-template <bool AGG>
+template <bool AGG, int B>
 __global__ void __launch_bounds__(256, 4) apply_kernel(PArgs A, float2 *y) {
     // launched with programmatic stream serialization: the previous epoch's grid
     // must be complete (and its y updates visible) before this one reads y
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    apply_epoch<AGG>(A, y, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
-                     (int64_t)gridDim.x * blockDim.x);
+    apply_epoch<AGG, B>(A, y, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                        (int64_t)gridDim.x * blockDim.x);
+}
+
+// the kernel instance: b = 2 (the default) compiled in, other b at run time
+template <bool AGG>
+void *apply_instance(int b) {
+    return b == 2 ? (void *)apply_kernel<AGG, 2> : (void *)apply_kernel<AGG, 0>;
 }
 
 // Consecutive epochs on one stream as programmatic dependent launches: the next
@@ -487,8 +508,9 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (agg) DRG_CUDA(cudaLaunchKernelEx(&cfg, apply_kernel<true>, P, y));
-    else DRG_CUDA(cudaLaunchKernelEx(&cfg, apply_kernel<false>, P, y));
+    void *args[] = {const_cast<PArgs *>(&P), &y};
+    DRG_CUDA(cudaLaunchKernelExC(&cfg, agg ? apply_instance<true>(P.b) : apply_instance<false>(P.b),
+                                 args));
     DRG_LAUNCHED("apply_kernel");
     return DRG_OK;
 }
@@ -842,10 +864,11 @@ extern "C" int drg_sampled_apply(const int32_t *draws, int64_t n_steps, float *y
     const int block = (int)std::min<int64_t>(256, threads);
     const unsigned grid = (unsigned)(threads / block);   // <= threads steps in flight
     cudaStream_t st = as_stream(stream);
-    if (flags & DRG_SAMPLED_AGGREGATE)
-        apply_kernel<true><<<grid, block, 0, st>>>(P, reinterpret_cast<float2 *>(y));
-    else
-        apply_kernel<false><<<grid, block, 0, st>>>(P, reinterpret_cast<float2 *>(y));
+    float2 *yy = reinterpret_cast<float2 *>(y);
+    void *args[] = {&P, &yy};
+    DRG_CUDA(cudaLaunchKernel((flags & DRG_SAMPLED_AGGREGATE) ? apply_instance<true>(b)
+                                                              : apply_instance<false>(b),
+                              dim3(grid), dim3(block), args, 0, st));
     DRG_LAUNCHED("apply_kernel");
     return DRG_OK;
 }
