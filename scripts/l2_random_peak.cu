@@ -41,7 +41,42 @@ __global__ void __launch_bounds__(256) probe(float2 *y, uint32_t n, int per_thre
     if (acc == 123.456f) *sink = acc;
 }
 
-int main() {
+// Size sweep (argv[1] == "sweep"): random 8-byte gathers over arrays from 13.8 MB to
+// 512 MB at 2048 threads/SM -- where the rate falls off shows the L2 capacity that
+// uniformly shared random data really gets (both dies' SMs read every line).
+int sweep() {
+    const uint32_t sizes[] = {1728000, 4000000, 6000000, 8000000, 10000000, 12500000,
+                              16777216, 67108864};
+    float2 *y;
+    float *sink;
+    cudaMalloc(&y, sizeof(float2) * 67108864u);
+    cudaMalloc(&sink, 4);
+    cudaMemset(y, 0, sizeof(float2) * 67108864u);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int grid = sms * 8, per_thread = 256;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (uint32_t n : sizes) {
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaEventRecord(a);
+            probe<0><<<grid, 256>>>(y, n, per_thread, sink);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, a, b);
+            if (rep == 2)
+                printf("{\"mode\": \"gather 8B\", \"array_MB\": %.1f, \"ms\": %.3f, "
+                       "\"G_accesses_per_s\": %.1f}\n",
+                       n * 8.0 / 1e6, ms, (double)grid * 256 * per_thread / (ms * 1e-3) / 1e9);
+        }
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int main(int argc, char **argv) {
+    if (argc > 1 && argv[1][0] == 's') return sweep();
     const uint32_t n = 1728000;
     float2 *y;
     float *sink;
