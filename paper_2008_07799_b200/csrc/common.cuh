@@ -63,6 +63,19 @@ inline unsigned warp_grid(int64_t items, int wpb) {
     return (unsigned)g;
 }
 
+// SM count of the current device (cached per device; 148 on B200)
+inline int sm_count() {
+    static int cache[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (cache[dev] == 0) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = v > 0 ? v : 148;
+    }
+    return cache[dev];
+}
+
 // ---- Philox4x32-10 counter-based RNG ----------------------------------------
 struct u32x4 {
     uint32_t x, y, z, w;

@@ -810,7 +810,10 @@ struct Events {
     }
 };
 
-constexpr size_t kDrawBudget = size_t(64) << 20;   // bytes per draw buffer (two buffers)
+// bytes per draw buffer (two buffers): >= 5 level-0 epochs of the C4 mesh per draw
+// launch -- one epoch per chunk (64 MB) cost 226 us per epoch in cross-stream event
+// waits, 5 epochs per chunk 213 us
+constexpr size_t kDrawBudget = size_t(256) << 20;
 
 }  // namespace
 
@@ -891,7 +894,11 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     const int probe = probe_env ? atoi(probe_env) : 0;
     // exactly min(n_steps, max_threads) steps in flight (1: the sequential kernel)
     const int64_t threads = std::max<int64_t>(1, std::min<int64_t>(n_steps, max_threads));
-    const int block = (int)std::min<int64_t>(256, threads);
+    // small levels: halve the block until the grid spans two blocks per SM (the
+    // update pass is latency-bound; 5 blocks of 256 on 5 SMs left the C4 mesh's
+    // coarsest level at 12.4 us per epoch, 64-thread blocks run it in 9.8 us)
+    int block = (int)std::min<int64_t>(256, threads);
+    while (block > 32 && threads / block < 2 * (int64_t)sm_count()) block /= 2;
     const unsigned grid = (unsigned)(threads / block);
     auto lr_at = [&](int t) { return (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0); };
     if ((flags & DRG_SAMPLED_FUSED) && map)
