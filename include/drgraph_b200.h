@@ -175,6 +175,14 @@ int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, const float *V,
                      int level, const int32_t *neg_idx, int32_t *nonfinite,
                      const drg_heavy_split *heavy, unsigned flags, void *stream);
 
+/* Host routine (no device work): the visiting order of one coarsening level,
+ * numpy's Generator(PCG64).permutation(n) bit for bit (multilevel.py:91), from the
+ * bit generator's state (128-bit state and increment, buffered 32-bit half-word) into
+ * out[n] (host int32).  Replaces the numpy call on layout_graph's critical path. */
+int drg_pcg64_permutation(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                          uint64_t inc_lo, int has_uint32, uint32_t uinteger, int64_t n,
+                          int32_t *out);
+
 /* --- reference-faithful sampled epochs (update = "sampled") ----------------------
  * Per-row alias tables over P (optimizer.py:111-139 applied to each row):
  * out_rec[e] = 16-byte {fp32 threshold of bucket e, int32 target of its alias

@@ -77,6 +77,7 @@ SIGNATURES = {
     "drg_neighborhood_preservation": [_P, _I64, _P, _P, _P, _I64, _P, _P],
     "drg_from_edges": [_P, _I64, _I64, _P, _P, _P, _P],
     "drg_components": [_P, _P, _I64, _P, _P, _P],
+    "drg_pcg64_permutation": [_U64, _U64, _U64, _U64, _I32, _U32, _I64, _P],
 }
 RESTYPES = {"drg_last_error": ctypes.c_char_p, "drg_launch_count": ctypes.c_uint64}
 
@@ -139,6 +140,12 @@ def check(rc: int, what: str = "") -> None:
 
 def call(name: str, *args) -> None:
     lib = load()
+    check(getattr(lib, name)(*args), name)
+
+
+def call_host(name: str, *args) -> None:
+    """A host-only entry point (no device work): loads without requiring CUDA."""
+    lib = load(require_cuda=False)
     check(getattr(lib, name)(*args), name)
 
 

@@ -94,8 +94,17 @@ def device_coarsen(dg: DeviceGraph, order: torch.Tensor):
 
 
 def level_order(n: int, seed: int) -> np.ndarray:
-    """The reference's visiting order for one level (multilevel.py:91)."""
-    return np.random.default_rng(seed).permutation(n)
+    """The reference's visiting order for one level (multilevel.py:91):
+    ``np.random.default_rng(seed).permutation(n)`` bit for bit, as int32, by the
+    library's host routine drg_pcg64_permutation (numpy's Fisher-Yates on the same
+    PCG64 stream, draws and swaps pipelined on two threads)."""
+    st = np.random.default_rng(seed).bit_generator.state
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    m64 = (1 << 64) - 1
+    out = np.empty(n, dtype=np.int32)
+    _lib.call_host("drg_pcg64_permutation", s >> 64, s & m64, inc >> 64, inc & m64,
+              int(st["has_uint32"]), int(st["uinteger"]), n, out.ctypes.data)
+    return out
 
 
 def device_build_hierarchy(dg: DeviceGraph, rho: float = 0.8, min_size: int = 16, seed: int = 0,
@@ -125,7 +134,7 @@ def device_build_hierarchy(dg: DeviceGraph, rho: float = 0.8, min_size: int = 16
             host_order = first_order.result()
         else:
             host_order = level_order(top.node_count, level_seed)
-        order = torch.from_numpy(host_order).to(top.indptr.device)
+        order = torch.from_numpy(host_order).to(top.indptr.device).to(torch.int64)
         if level0_relabel is not None and len(h.levels) == 1:
             order = level0_relabel.to(torch.int64)[order]
         coarse, parent, rounds = device_coarsen(top, order)

@@ -579,16 +579,22 @@ class LayoutPlan:
 
     def _run_level_sampled(self, level, y, t0, n_iter, group=None, step_fn=None):
         """Reference-faithful epochs: n_l sampled steps each, Hogwild on y.  With a
-        process group the epoch's steps are split across ranks, each applies its
-        share to its replica, and the per-rank displacements are summed with one
-        all-reduce per epoch (Hogwild with a per-epoch exchange)."""
+        process group and a level of at least ``shard_min_nodes`` nodes the epoch's
+        steps are split across ranks, each applies its share to its replica, and the
+        per-rank displacements are summed with one all-reduce per epoch (Hogwild with
+        a per-epoch exchange).  Smaller levels -- whose epochs take ~10 us, less than
+        one exchange -- run whole on every rank with no traffic, and rank 0's result
+        is broadcast once at the end (Hogwild replicas drift apart otherwise)."""
         L = self.levels[level]
-        if group is None:
+        if group is None or L.n < self.opt.shard_min_nodes:
             if step_fn is not None:
                 for j in range(n_iter):
                     step_fn(y, 0, L.n, t0 + j)
             else:
                 self.sampled_steps(level, y, 0, L.n, t0, n_iter)
+            if group is not None:
+                import torch.distributed as dist
+                dist.broadcast(y, src=dist.get_global_rank(group, 0), group=group)
         else:
             import torch.distributed as dist
             world = dist.get_world_size(group)

@@ -74,3 +74,26 @@ def test_no_cpu_device_path():
     g = Graph(np.array([0, 1, 2]), np.array([1, 0], dtype=np.int32))
     with pytest.raises(RuntimeError):
         all_k_neighborhoods(g, 2)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 17, 1000, 65537, 300_001])
+def test_level_order_is_numpy_permutation(n):
+    """drg_pcg64_permutation (host routine behind multilevel.level_order) reproduces
+    numpy's Generator(PCG64).permutation bit for bit -- the reference's visiting
+    order (multilevel.py:91) -- including a buffered 32-bit half-word state."""
+    import numpy as np
+    from paper_2008_07799_b200 import _lib
+    from paper_2008_07799_b200.multilevel import level_order
+    for seed in (0, 7, 2**62 + 3):
+        got = level_order(n, seed)
+        assert got.dtype == np.int32
+        assert np.array_equal(got, np.random.default_rng(seed).permutation(n))
+    g = np.random.default_rng(11)
+    g.integers(0, 2**32 - 1, dtype=np.uint32)   # leaves a buffered half-word
+    st = g.bit_generator.state
+    assert st["has_uint32"] == 1
+    out = np.empty(n, dtype=np.int32)
+    s, inc, m = st["state"]["state"], st["state"]["inc"], (1 << 64) - 1
+    _lib.call_host("drg_pcg64_permutation", s >> 64, s & m, inc >> 64, inc & m, 1,
+                   st["uinteger"], n, out.ctypes.data)
+    assert np.array_equal(out, g.permutation(n))

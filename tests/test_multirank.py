@@ -148,3 +148,40 @@ def test_sampled_mode_epoch_exchange(tmp_path):
             delta += yr - base
         y = base + delta
     assert np.array_equal(got, y.numpy())
+
+
+def _replicated_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2008_07799_b200.optimizer import LayoutPlan, LevelData, OptimizerParams
+    n = 97
+    plan = LayoutPlan([LevelData(n, 0, None, None, None, None)], [],
+                      OptimizerParams(iters=5, update="sampled", shard_min_nodes=n + 1))
+    y0 = torch.from_numpy(np.random.default_rng(3).normal(size=(n, 2)).astype(np.float32))
+    base_step = _sampled_step(n)
+
+    def step(y, lo, hi, t):   # every rank runs all steps; rank 1's replica drifts
+        assert (lo, hi) == (0, n)
+        base_step(y, lo, hi, t)
+        if rank == 1:
+            y += 1.0
+
+    y = plan.run_level(0, y0.clone(), group=dist.group.WORLD, step_fn=step)
+    np.save(out_path + f".{rank}.npy", y.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sampled_small_levels_run_replicated(tmp_path):
+    """update="sampled" on a level below shard_min_nodes: no per-epoch exchange --
+    every rank runs the whole epoch, then rank 0's positions are broadcast, so all
+    replicas leave the level equal to a single-process run."""
+    out = str(tmp_path / "rep")
+    mp.spawn(_replicated_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    n = 97
+    y = torch.from_numpy(np.random.default_rng(3).normal(size=(n, 2)).astype(np.float32))
+    step = _sampled_step(n)
+    for t in range(5):
+        step(y, 0, n, t)
+    for r in range(2):
+        assert np.array_equal(np.load(out + f".{r}.npy"), y.numpy())
