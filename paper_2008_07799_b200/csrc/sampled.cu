@@ -527,7 +527,8 @@ constexpr int kRowWarps = 4;
 // resolves its items by binary search.
 __global__ void __launch_bounds__(kRowWarps * 32)
     row_alias_warp_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ targets,
-                          const double *__restrict__ P, int64_t n, uint4 *rec, double *rowsum) {
+                          const double *__restrict__ P, int64_t n, uint4 *rec, double *rowsum,
+                          int64_t *long_rows, int *n_long) {
     __shared__ double s_w[kRowWarps][kRowWarpMax];
     __shared__ double s_ds[kRowWarps][kRowWarpMax];   // delta (lights) | sigma (heavies)
     __shared__ int16_t s_idx[kRowWarps][kRowWarpMax]; // lights from the front, heavies after
@@ -537,7 +538,10 @@ __global__ void __launch_bounds__(kRowWarps * 32)
     for (int64_t i = (int64_t)blockIdx.x * kRowWarps + wp; i < n; i += (int64_t)gridDim.x * kRowWarps) {
         const int64_t lo = indptr[i], hi = indptr[i + 1];
         const int len = (int)(hi - lo);
-        if (len > kRowWarpMax) continue;   // the thread tier takes it
+        if (len > kRowWarpMax) {   // the block tier takes it: queue the row
+            if (lane == 0) long_rows[atomicAdd(n_long, 1)] = i;
+            continue;
+        }
         if (len == 0) {
             if (lane == 0 && rowsum) rowsum[i] = 0.0;
             continue;
@@ -633,7 +637,8 @@ constexpr int kRowBlock = 512;
 __global__ void __launch_bounds__(kRowBlock)
     row_alias_block_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ targets,
                            const double *__restrict__ P, int64_t n, double *w, double *ds,
-                           int32_t *idx, uint4 *rec, double *rowsum) {
+                           int32_t *idx, uint4 *rec, double *rowsum,
+                           const int64_t *__restrict__ long_rows, const int *__restrict__ n_long) {
     using BR = cub::BlockReduce<double, kRowBlock>;
     using BSI = cub::BlockScan<int, kRowBlock>;
     using BSD = cub::BlockScan<double, kRowBlock>;
@@ -644,10 +649,11 @@ __global__ void __launch_bounds__(kRowBlock)
     } tmp;
     __shared__ double s_bcast;
     const int tid = threadIdx.x;
-    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int nl = *n_long;   // rows the warp tier queued (any order: rows are independent)
+    for (int r = blockIdx.x; r < nl; r += gridDim.x) {
+        const int64_t i = long_rows[r];
         const int64_t lo = indptr[i], hi = indptr[i + 1];
         const int64_t len = hi - lo;
-        if (len <= kRowWarpMax) continue;   // the warp tier takes it
         double part = 0.0;
         for (int64_t e = tid; e < len; e += kRowBlock) part += P[lo + e];
         const double tot_r = BR(tmp.r).Sum(part);
@@ -746,21 +752,33 @@ extern "C" int drg_row_alias(const int64_t *indptr, const int32_t *targets, cons
                              void *stream) {
     if (n <= 0) return DRG_OK;
     cudaStream_t st = as_stream(stream);
-    Scratch idx(st), w(st), ds(st);
-    DRG_CUDA(idx.alloc(sizeof(int32_t) * (size_t)std::max<int64_t>(nnz, 1)));
-    DRG_CUDA(w.alloc(sizeof(double) * (size_t)std::max<int64_t>(nnz, 1)));
-    DRG_CUDA(ds.alloc(sizeof(double) * (size_t)std::max<int64_t>(nnz, 1)));
+    // rows longer than kRowWarpMax (at most nnz / (kRowWarpMax + 1) of them) are queued
+    // by the warp tier; the block tier walks only that list (a grid-stride pass over
+    // all n rows cost 2.7 ms on the C4 mesh, which has none)
+    const int64_t max_long = nnz / (kRowWarpMax + 1) + 1;
+    Scratch lst(st), cnt(st);
+    DRG_CUDA(lst.alloc(sizeof(int64_t) * (size_t)max_long));
+    DRG_CUDA(cnt.alloc(sizeof(int)));
+    DRG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st));
     const unsigned gw = (unsigned)std::min<int64_t>(ceil_div(n, kRowWarps), kSMs * 64);
     row_alias_warp_kernel<<<gw, kRowWarps * 32, 0, st>>>(indptr, targets, P, n,
                                                          reinterpret_cast<uint4 *>(out_rec),
-                                                         out_rowsum);
+                                                         out_rowsum, lst.as<int64_t>(),
+                                                         cnt.as<int>());
     DRG_LAUNCHED("row_alias_warp_kernel");
-    const unsigned g = (unsigned)std::min<int64_t>(n, kSMs * 4);
-    row_alias_block_kernel<<<g, kRowBlock, 0, st>>>(indptr, targets, P, n, w.as<double>(),
-                                                    ds.as<double>(), idx.as<int32_t>(),
-                                                    reinterpret_cast<uint4 *>(out_rec),
-                                                    out_rowsum);
-    DRG_LAUNCHED("row_alias_block_kernel");
+    if (nnz > kRowWarpMax) {
+        Scratch idx(st), w(st), ds(st);
+        DRG_CUDA(idx.alloc(sizeof(int32_t) * (size_t)nnz));
+        DRG_CUDA(w.alloc(sizeof(double) * (size_t)nnz));
+        DRG_CUDA(ds.alloc(sizeof(double) * (size_t)nnz));
+        const unsigned g = (unsigned)std::min<int64_t>(max_long, kSMs * 4);
+        row_alias_block_kernel<<<g, kRowBlock, 0, st>>>(indptr, targets, P, n, w.as<double>(),
+                                                        ds.as<double>(), idx.as<int32_t>(),
+                                                        reinterpret_cast<uint4 *>(out_rec),
+                                                        out_rowsum, lst.as<int64_t>(),
+                                                        cnt.as<int>());
+        DRG_LAUNCHED("row_alias_block_kernel");
+    }
     return DRG_OK;
 }
 

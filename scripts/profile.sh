@@ -15,9 +15,11 @@ $CMD > $OUT/plain_${W}_${U}.log 2>&1 && \
 echo "launch list rc=$?"
 # 2) full capture of the dominant kernel (first level-0 launch of the timed step)
 K=layout_iter; S=60; C=1
-# sampled (split form): one draw_kernel + one apply_kernel of level 0 in the timed
-# step (104 matching launches per 20-iteration run of the 4 mesh levels)
-[ "$U" = "sampled" ] && K="draw_kernel|apply_kernel" && S=170 && C=2
+# sampled (split form), 20 iterations per level: coarse levels 1 draw + 20 applies
+# each, level 0 (256 MB draw chunks = 5 epochs) 4 draws + 20 applies -> 87 matching
+# launches per step; the timed step's level 0 starts at launch 87 + 63 = 150 with
+# draw(chunk 0), draw(chunk 1), apply(epoch 0)
+[ "$U" = "sampled" ] && K="draw_kernel|apply_kernel" && S=150 && C=3
 $CMD > $OUT/plain2_${W}_${U}.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k "regex:$K" -s $S -c $C -f \
       -o $OUT/full_${W}_${U} $CMD > $OUT/ncu_full_${W}_${U}.log 2>&1
