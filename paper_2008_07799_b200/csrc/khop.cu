@@ -13,6 +13,8 @@
 // count pass and a fill pass (two-phase ABI).
 #include <cub/cub.cuh>
 
+#include <climits>
+
 #include "common.cuh"
 
 namespace drg {
@@ -56,14 +58,14 @@ __device__ __forceinline__ void expand_chunk(const int64_t *__restrict__ indptr,
                                              const int32_t *__restrict__ indices,
                                              const uint32_t *list, int fb, int fe,
                                              uint32_t *table, int log2cap, int lane,
-                                             Emit &&emit) {
+                                             int64_t lim, Emit &&emit) {
     const int f = fb + lane;
     int64_t start = 0;
     int deg = 0;
     if (f < fe) {
         const uint32_t u = list[f] & kIdMask;
         start = indptr[u];
-        deg = (int)(indptr[u + 1] - start);
+        deg = (int)min(indptr[u + 1] - start, lim);
     }
     int incl = deg;
 #pragma unroll
@@ -128,10 +130,33 @@ __device__ __forceinline__ void bitonic_sort_block(uint32_t *a, int P) {
         }
 }
 
+// Neighbour cap (BASELINE C3): a capped row is the first `cap` entries of the full
+// (dist, id)-sorted row.  The last hop (d == k-1) only starts when <= cap nodes
+// (source included) are known, so at most r = cap + 1 - cnt entries come from it,
+// the smallest ids not yet seen; each frontier node's row is sorted by id and fewer
+// than cnt of its entries are already seen, so its first r + cnt = cap + 1 entries
+// hold every candidate -- reading only those leaves the capped row unchanged (a
+// Barabasi-Albert leaf next to a 5000-degree hub reads 257 entries, not 5000).
+// `trunc` says the CSR rows are sorted (checked once on the device).
+__device__ __forceinline__ int64_t last_hop_limit(int64_t cap, int d, int k, int trunc) {
+    return (trunc && cap > 0 && d == k - 1) ? cap + 1 : INT64_MAX;
+}
+
+__global__ void rows_unsorted_kernel(const int64_t *__restrict__ indptr,
+                                     const int32_t *__restrict__ indices, int64_t n, int *bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t e = indptr[i] + 1; e < indptr[i + 1]; ++e)
+            if (indices[e - 1] >= indices[e]) {
+                *bad = 1;
+                break;
+            }
+}
+
 // counts != nullptr: count pass.  Otherwise fill pass into out_ids/out_dists.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     khop_warp_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
-                     int64_t n, int k, int64_t cap, int64_t *counts,
+                     int64_t n, int k, int64_t cap, int trunc, int64_t *counts,
                      const int64_t *__restrict__ out_indptr, int32_t *out_ids,
                      int32_t *out_dists, int32_t *ovf_list, unsigned long long *ovf_count) {
     __shared__ uint32_t s_table[kWarpsPerBlock][kWarpHash];
@@ -153,8 +178,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         int lb = 0, le = 1;
         for (int d = 0; d < k && !overflow; ++d) {
             const uint32_t tag = (uint32_t)(d + 1) << kIdBits;
+            const int64_t lim = last_hop_limit(cap, d, k, trunc);
             for (int fb = lb; fb < le && !overflow; fb += 32) {
-                expand_chunk(indptr, indices, list, fb, le, table, kWarpLog2Hash, lane,
+                expand_chunk(indptr, indices, list, fb, le, table, kWarpLog2Hash, lane, lim,
                              [&](bool ins, uint32_t w) {
                                  unsigned bal = __ballot_sync(kFull, ins);
                                  int pos = cnt + __popc(bal & ((1u << lane) - 1u));
@@ -204,7 +230,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 // Tier 2: one 1024-thread block per overflowed source.
 __global__ void __launch_bounds__(kBlockThreads)
     khop_block_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
-                      int k, int64_t cap, const int32_t *__restrict__ sources,
+                      int k, int64_t cap, int trunc, const int32_t *__restrict__ sources,
                       int64_t n_sources, int64_t *counts, const int64_t *__restrict__ out_indptr,
                       int32_t *out_ids, int32_t *out_dists, int32_t *fail_source) {
     extern __shared__ uint32_t smem[];
@@ -228,9 +254,10 @@ __global__ void __launch_bounds__(kBlockThreads)
         int lb = 0, le = 1;
         for (int d = 0; d < k; ++d) {
             const uint32_t tag = (uint32_t)(d + 1) << kIdBits;
+            const int64_t lim = last_hop_limit(cap, d, k, trunc);
             for (int fb = lb + warp * 32; fb < le; fb += nwarps * 32) {
                 int fe = min(fb + 32, le);
-                expand_chunk(indptr, indices, list, fb, fe, table, kBlockLog2Hash, lane,
+                expand_chunk(indptr, indices, list, fb, fe, table, kBlockLog2Hash, lane, lim,
                              [&](bool ins, uint32_t w) {
                                  unsigned bal = __ballot_sync(kFull, ins);
                                  int base = 0;
@@ -302,10 +329,23 @@ int run_khop(const int64_t *indptr, const int32_t *indices, int64_t n, int k, in
     DRG_CUDA(failbuf.alloc(sizeof(int32_t)));
     DRG_CUDA(cudaMemsetAsync(ovf_cnt.p, 0, sizeof(unsigned long long), st));
     DRG_CUDA(cudaMemsetAsync(failbuf.p, 0xff, sizeof(int32_t), st));
+    int trunc = 0;
+    if (cap > 0) {   // the last-hop truncation needs id-sorted rows
+        Scratch bad(st);
+        DRG_CUDA(bad.alloc(sizeof(int)));
+        DRG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+        rows_unsorted_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), kSMs * 16), 256, 0,
+                               st>>>(indptr, indices, n, bad.as<int>());
+        DRG_LAUNCHED("rows_unsorted_kernel");
+        int h_bad = 1;
+        DRG_CUDA(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        DRG_CUDA(cudaStreamSynchronize(st));
+        trunc = h_bad == 0;
+    }
     unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, kWarpsPerBlock), kSMs * 32);
     khop_warp_kernel<<<blocks, kWarpsPerBlock * 32, 0, st>>>(
-        indptr, indices, n, k, cap, counts, out_indptr, out_ids, out_dists, ovf.as<int32_t>(),
-        ovf_cnt.as<unsigned long long>());
+        indptr, indices, n, k, cap, trunc, counts, out_indptr, out_ids, out_dists,
+        ovf.as<int32_t>(), ovf_cnt.as<unsigned long long>());
     DRG_LAUNCHED("khop_warp_kernel");
     unsigned long long h_ovf = 0;
     DRG_CUDA(cudaMemcpyAsync(&h_ovf, ovf_cnt.p, sizeof(h_ovf), cudaMemcpyDeviceToHost, st));
@@ -316,7 +356,7 @@ int run_khop(const int64_t *indptr, const int32_t *indices, int64_t n, int k, in
                                       (int)kBlockSmem));
         unsigned b2 = (unsigned)std::min<unsigned long long>(h_ovf, kSMs);
         khop_block_kernel<<<b2, kBlockThreads, kBlockSmem, st>>>(
-            indptr, indices, k, cap, ovf.as<int32_t>(), (int64_t)h_ovf, counts, out_indptr,
+            indptr, indices, k, cap, trunc, ovf.as<int32_t>(), (int64_t)h_ovf, counts, out_indptr,
             out_ids, out_dists, failbuf.as<int32_t>());
         DRG_LAUNCHED("khop_block_kernel");
         int32_t h_fail = -1;

@@ -707,3 +707,24 @@ def test_sampled_mode_hub_aggregation():
         lay = B.layout_graph(as_gpu_graph(g), B.SimilarityParams(k=1),
                              B.OptimizerParams(seed=1, iters=20, hub_levels=hub_levels))
         assert np.isfinite(lay.positions).all()
+
+
+@pytest.mark.parametrize("k", [2, 3])
+@pytest.mark.parametrize("cap", [1, 5, 16, 256])
+def test_khop_cap_last_hop_truncation_on_hubs(k, cap):
+    """Capped k-hop rows read only the first cap + 1 entries of each last-hop row
+    (id-sorted CSR): still bit-exact against the oracle's full BFS on a heavy-tailed
+    graph, and on the same graph with rows shuffled (the truncation is then off)."""
+    from paper_2008_07799_b200 import synthetic
+    g = synthetic.barabasi_albert(5_000, 3, seed=2, device="host")
+    og = O.Graph(g.indptr, g.indices)
+    want = O.all_k_neighborhoods(og, k, cap=cap)
+    got = B.all_k_neighborhoods(g, k, cap=cap)
+    assert np.array_equal(got.indptr, want.indptr)
+    assert np.array_equal(got.ids, want.ids) and np.array_equal(got.dists, want.dists)
+    rng = np.random.default_rng(cap)
+    shuffled = g.indices.copy()
+    for i in range(g.node_count):
+        rng.shuffle(shuffled[g.indptr[i]:g.indptr[i + 1]])
+    got2 = B.all_k_neighborhoods(B.Graph(g.indptr, shuffled), k, cap=cap)
+    assert np.array_equal(got2.ids, want.ids) and np.array_equal(got2.dists, want.dists)
