@@ -76,6 +76,8 @@ def parse():
     ap.add_argument("--update", default="sampled",
                     choices=["jacobi", "inplace", "sampled", "sgather"])
     ap.add_argument("--sampled-concurrency", type=int, default=16)
+    ap.add_argument("--hub-levels", choices=["jacobi", "sampled"], default="jacobi",
+                    help="update the hub-heavy levels of update=sampled run")
     return ap.parse_args()
 
 
@@ -155,12 +157,14 @@ def build_workload(name):
     return getattr(synthetic, fn)(*args)
 
 
-def params_for(name, iters_override=None, update="sampled", concurrency=16):
+def params_for(name, iters_override=None, update="sampled", concurrency=16,
+               hub_levels="jacobi"):
     import paper_2008_07799_b200 as B
     w = WORKLOADS[name]
     sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"], neighbor_cap=w.get("cap"))
     opt = B.OptimizerParams(neg_samples=w["M"], iters=iters_override or w["iters"], seed=0,
-                            init=w["init"], update=update, sampled_concurrency=concurrency)
+                            init=w["init"], update=update, sampled_concurrency=concurrency,
+                            hub_levels=hub_levels)
     return sim, opt, dict(w["hier"])
 
 
@@ -275,7 +279,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
     name = args.workload
-    sim, opt, hier = params_for(name, args.iters, args.update, args.sampled_concurrency)
+    sim, opt, hier = params_for(name, args.iters, args.update, args.sampled_concurrency,
+                                args.hub_levels)
 
     dg = build_workload(name)
     torch.cuda.synchronize()
@@ -468,7 +473,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": name, "desc": WORKLOADS[name]["desc"], "levels": sizes,
                        "nnz_per_level": nnzs,
-                       "iters_per_level": T, "update": opt.update,
+                       "iters_per_level": T, "update": opt.update, "hub_levels": opt.hub_levels,
                        "l2": "256 MiB flush between steps; level-0 stream "
                              f"{alg_bytes / 1e9:.2f} GB/iteration > 126 MB L2",
                        "parallelism": f"node-range x{world}" if world > 1 else "single GPU"},

@@ -61,7 +61,9 @@ class OptimizerParams:
       Hogwild-style on the GPU -- KL/NP parity with the reference, fastest on one
       GPU; run-to-run nondeterministic like the reference's threads > 1 mode.
       Levels whose busiest node is the source of > HUB_STEPS steps per epoch
-      (R-MAT hubs) run the "jacobi" gather instead (``hub_levels``).
+      use warp-aggregated atomics; above GATHER_STEPS (R-MAT coarse levels, where
+      same-address atomics serialise) they run the "jacobi" gather instead
+      (``hub_levels``).
     * "jacobi": the node-parallel expected-gradient iteration (SURVEY §8(a) A12,
       CSR gather + M negatives per node) -- bitwise deterministic and node-range
       shardable across GPUs; matches KL, lower NP on multilevel RGG.
@@ -277,6 +279,7 @@ class SampledTables:
     collapse: torch.Tensor | None   # fp32 [n]   c_a (None: no collapsed pairs)
     wsum: torch.Tensor | None       # fp32 [n]   sum_b W_ab = 2 n_l sum_b P^l_ab (sgather)
     hubs: bool = False        # some node takes part in > HUB_STEPS steps per epoch
+    gather: bool = False      # ... in > GATHER_STEPS: the level runs hub_levels' update
     # draw-then-map form (coarse levels of a "sampled" plan): the tables above are
     # level 0's, ``map`` (int32 [n_0]) the composed parent map to this level
     map: torch.Tensor | None = None
@@ -285,6 +288,12 @@ class SampledTables:
 
 
 HUB_STEPS = 512   # warp-aggregate the sampled updates above this per-node rate
+# Above this per-node rate the sampled epoch serialises on the hub's atomics even
+# warp-aggregated, and the gather (K7 + heavy-row split) is faster: R-MAT's coarse
+# levels (busiest node 2.4e5 - 4.8e6 steps per epoch) -- while R-MAT's level 0
+# (1.4e4: sampled 3.8 ms per epoch vs gather 5.2 ms) and the C3 BA levels (<= 6e3)
+# stay sampled.
+GATHER_STEPS = 32768
 
 
 def build_sampled_tables(ip, tg, P, R) -> SampledTables:
@@ -337,10 +346,18 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
     return out
 
 
-def _is_hub_level(R: torch.Tensor) -> bool:
-    """Expected steps per epoch in which the busiest node is the source > HUB_STEPS."""
+def _busiest_steps(R: torch.Tensor) -> float:
+    """Expected steps per epoch in which the busiest node is the source."""
     n = R.numel()
-    return n > 0 and float(R.max()) / max(float(R.sum()), 1e-300) * n > HUB_STEPS
+    return float(R.max()) / max(float(R.sum()), 1e-300) * n if n > 0 else 0.0
+
+
+def _is_hub_level(R: torch.Tensor) -> bool:
+    return _busiest_steps(R) > HUB_STEPS
+
+
+def _is_gather_level(R: torch.Tensor) -> bool:
+    return _busiest_steps(R) > GATHER_STEPS
 
 
 def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float = 0.75,
@@ -369,8 +386,8 @@ def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float
         rec, V = pack_level(ip, tg, P, R, Wn, 1.0 / total, n_l, sort_rows=False)
         L = LevelData(n_l, tg.numel(), ip, rec, V, alias, heavy_split(ip))
         if sampled and R.numel() > 0 and float(R.sum()) > 0:
-            if skip_hub_tables and _is_hub_level(R):
-                L.sampled = SampledTables(None, None, None, None, hubs=True)
+            if skip_hub_tables and _is_gather_level(R):
+                L.sampled = SampledTables(None, None, None, None, hubs=True, gather=True)
             else:
                 L.sampled = build_sampled_tables(ip, tg, P, R)
         out.append(L)
@@ -406,7 +423,7 @@ class LayoutPlan:
         L = self.levels[level]
         M = self.opt.neg_samples
         u = self.opt.update
-        if u == "sampled" and L.sampled is not None and L.sampled.hubs and \
+        if u == "sampled" and L.sampled is not None and L.sampled.gather and \
                 self.opt.hub_levels == "jacobi":
             u = "jacobi"
         if u == "sampled":
@@ -490,7 +507,7 @@ class LayoutPlan:
             import torch.distributed as dist
             world = dist.get_world_size(group)
         if self.opt.update == "sampled":
-            hub = L.sampled is not None and L.sampled.hubs and self.opt.hub_levels == "jacobi"
+            hub = L.sampled is not None and L.sampled.gather and self.opt.hub_levels == "jacobi"
             if not hub:
                 return self._run_level_sampled(level, y, t0, n_iter,
                                                group if world > 1 else None, step_fn)
@@ -675,12 +692,12 @@ def build_plan(ds: DeviceSimilarity, dh: DeviceHierarchy, opt: OptimizerParams) 
     if opt.update == "sampled" and not opt.sampled_fused:
         # hub-heavy levels (decided on R^l alone) need the gather's level data
         R = ds.row_mass
-        hub = _is_hub_level(R)
+        hub = _is_gather_level(R)
         for level in range(1, dh.depth + 1):
             if hub:
                 break
             R = _aggregate_nodes(R, dh.maps[level - 1], dh.levels[level].node_count)
-            hub = _is_hub_level(R)
+            hub = _is_gather_level(R)
         if not (gather_hubs and hub):
             return LayoutPlan(build_mapped_level_data(ds, dh, opt.neg_power), list(dh.maps), opt)
     return LayoutPlan(build_level_data(ds, dh, opt.neg_power,
