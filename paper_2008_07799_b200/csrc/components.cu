@@ -27,25 +27,52 @@ __global__ void cc_init_kernel(int32_t *parent, int64_t n) {
         parent[i] = (int32_t)i;
 }
 
+__device__ __forceinline__ void hook(int32_t *parent, int32_t a, int32_t b) {
+    while (true) {
+        a = find_root(parent, a);
+        b = find_root(parent, b);
+        if (a == b) return;
+        if (a < b) {
+            int32_t t = a;
+            a = b;
+            b = t;
+        }
+        if (atomicCAS(parent + a, a, b) == a) return;
+    }
+}
+
+constexpr int64_t kLongRow = 1024;   // rows above this go to the block-per-row pass
+
+// Thread per node for rows up to kLongRow entries; longer rows (R-MAT hubs: a
+// thread looping over a 10^5-entry row held the whole pass for 0.4 s) are queued.
 __global__ void cc_hook_kernel(const int64_t *__restrict__ indptr,
-                               const int32_t *__restrict__ indices, int64_t n, int32_t *parent) {
+                               const int32_t *__restrict__ indices, int64_t n, int32_t *parent,
+                               int32_t *long_rows, int *n_long) {
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
          v += (int64_t)gridDim.x * blockDim.x) {
-        for (int64_t e = indptr[v]; e < indptr[v + 1]; ++e) {
-            int32_t u = __ldg(indices + e);
-            if (u <= v) continue;
-            int32_t a = (int32_t)v, b = u;
-            while (true) {
-                a = find_root(parent, a);
-                b = find_root(parent, b);
-                if (a == b) break;
-                if (a < b) {
-                    int32_t t = a;
-                    a = b;
-                    b = t;
-                }
-                if (atomicCAS(parent + a, a, b) == a) break;
-            }
+        const int64_t lo = indptr[v], hi = indptr[v + 1];
+        if (hi - lo > kLongRow) {
+            long_rows[atomicAdd(n_long, 1)] = (int32_t)v;
+            continue;
+        }
+        for (int64_t e = lo; e < hi; ++e) {
+            const int32_t u = __ldg(indices + e);
+            if (u > v) hook(parent, (int32_t)v, u);
+        }
+    }
+}
+
+// Block per queued long row, threads striding over its entries.
+__global__ void cc_hook_long_kernel(const int64_t *__restrict__ indptr,
+                                    const int32_t *__restrict__ indices,
+                                    const int32_t *__restrict__ long_rows,
+                                    const int *__restrict__ n_long, int32_t *parent) {
+    const int nl = *n_long;
+    for (int r = blockIdx.x; r < nl; r += gridDim.x) {
+        const int32_t v = long_rows[r];
+        for (int64_t e = indptr[v] + threadIdx.x; e < indptr[v + 1]; e += blockDim.x) {
+            const int32_t u = __ldg(indices + e);
+            if (u > v) hook(parent, v, u);
         }
     }
 }
@@ -96,8 +123,16 @@ extern "C" int drg_components(const int64_t *indptr, const int32_t *indices, int
     const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 256), kSMs * 32);
     cc_init_kernel<<<g, 256, 0, st>>>(parent.as<int32_t>(), n);
     DRG_LAUNCHED("cc_init_kernel");
-    cc_hook_kernel<<<g, 256, 0, st>>>(indptr, indices, n, parent.as<int32_t>());
+    Scratch lst(st), nl(st);
+    DRG_CUDA(lst.alloc(sizeof(int32_t) * (size_t)n));
+    DRG_CUDA(nl.alloc(sizeof(int)));
+    DRG_CUDA(cudaMemsetAsync(nl.p, 0, sizeof(int), st));
+    cc_hook_kernel<<<g, 256, 0, st>>>(indptr, indices, n, parent.as<int32_t>(),
+                                      lst.as<int32_t>(), nl.as<int>());
     DRG_LAUNCHED("cc_hook_kernel");
+    cc_hook_long_kernel<<<kSMs * 4, 256, 0, st>>>(indptr, indices, lst.as<int32_t>(),
+                                                  nl.as<int>(), parent.as<int32_t>());
+    DRG_LAUNCHED("cc_hook_long_kernel");
     cc_count_kernel<<<g, 256, 0, st>>>(parent.as<int32_t>(), n, cnt.as<unsigned long long>());
     DRG_LAUNCHED("cc_count_kernel");
     unsigned long long h = 0;

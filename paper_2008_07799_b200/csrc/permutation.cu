@@ -141,7 +141,11 @@ extern "C" int drg_pcg64_permutation(uint64_t state_hi, uint64_t state_lo, uint6
     for (int64_t b = 0; b < nblocks; ++b) {
         while (ready.load(std::memory_order_acquire) <= b) std::this_thread::yield();
         const int64_t end = std::min(total, (b + 1) * kBlock);
+        // j is uniform on [0, i]: on large levels every swap misses the caches, so the
+        // swap kPrefetch steps ahead is prefetched (its j is already drawn)
+        constexpr int64_t kPrefetch = 64;
         for (int64_t k = b * kBlock; k < end; ++k) {
+            if (k + kPrefetch < end) __builtin_prefetch(out + js[k + kPrefetch], 1);
             const int64_t i = n - 1 - k, j = js[k];
             const int32_t t = out[i];
             out[i] = out[j];
