@@ -75,7 +75,8 @@ def parse():
     ap.add_argument("--no-alt", action="store_true", help="skip the other update modes")
     ap.add_argument("--update", default="sampled",
                     choices=["jacobi", "inplace", "sampled", "sgather"])
-    ap.add_argument("--sampled-concurrency", type=int, default=16)
+    ap.add_argument("--sampled-concurrency", type=int, default=None,
+                    help="level-0 steps in flight = n / this (default: by graph size)")
     ap.add_argument("--hub-levels", choices=["jacobi", "sampled"], default="jacobi",
                     help="update the hub-heavy levels of update=sampled run")
     return ap.parse_args()
@@ -157,7 +158,7 @@ def build_workload(name):
     return getattr(synthetic, fn)(*args)
 
 
-def params_for(name, iters_override=None, update="sampled", concurrency=16,
+def params_for(name, iters_override=None, update="sampled", concurrency=None,
                hub_levels="jacobi"):
     import paper_2008_07799_b200 as B
     w = WORKLOADS[name]

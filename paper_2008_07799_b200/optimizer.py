@@ -88,8 +88,10 @@ class OptimizerParams:
     init: str = "normal"
     update: str = "sampled"
     shard_min_nodes: int = 65536
-    sampled_concurrency: int = 16  # update="sampled": n_0 / this many steps in flight (level 0)
-    sampled_concurrency_coarse: int = 4   # ... and n_l / this many on coarser levels
+    # update="sampled": n_0 / this many steps in flight on level 0, n_l / the coarse
+    # value on coarser levels; None = by graph size (sampled_divisors)
+    sampled_concurrency: int | None = None
+    sampled_concurrency_coarse: int | None = None
     att_samples: int = 2           # update="sgather": attraction partners drawn per node
     hub_levels: str = "jacobi"     # update="sampled": hub-heavy levels run this update
     sampled_fused: bool = False    # update="sampled": draw inline (one kernel per epoch)
@@ -110,6 +112,9 @@ class OptimizerParams:
             raise ValueError("threads must be >= 1")
         if self.seed < 0:
             raise ValueError("seed must be non-negative")
+        for c in (self.sampled_concurrency, self.sampled_concurrency_coarse):
+            if c is not None and c < 1:
+                raise ValueError("sampled concurrency divisors must be >= 1")
         if self.init not in ("normal", "uniform"):
             raise ValueError("init must be 'normal' or 'uniform'")
         if self.update not in ("jacobi", "inplace", "sampled", "sgather"):
@@ -285,6 +290,26 @@ class SampledTables:
     map: torch.Tensor | None = None
     indptr: torch.Tensor | None = None      # level-0 row offsets of row_alias
     neg_alias: torch.Tensor | None = None   # level-0 Vose table over Q^0
+
+
+# Steps in flight of the Hogwild update pass (the fidelity knob).  Concurrent steps
+# read positions that other in-flight steps are about to move; measured against the
+# reference (scripts/quality.py, profiles/r01_quality_*concurrency*): n/16 costs
+# NP -4.1% on C1 (10k-node grid, 400 seeds) and -5.2% on C2 (200k RGG, 64 seeds),
+# n/256 (coarse n/64) -0.5% and -1.9% -- within the 2% bar; on the C4 mesh
+# (1.73 M nodes) n/16 (coarse n/4) is already within it (NP -0.5%) and keeps the
+# >= 6e4 steps in flight the update pass needs to reach the L2 random-access ceiling.
+FAST_CONCURRENCY_NODES = 1_000_000
+
+
+def sampled_divisors(n0: int, opt: "OptimizerParams") -> tuple[int, int]:
+    """(level-0, coarse-level) divisors of the steps in flight: the explicit
+    OptimizerParams values, else n/16 and n/4 for graphs of >= FAST_CONCURRENCY_NODES
+    nodes and n/256 and n/64 below."""
+    big = n0 >= FAST_CONCURRENCY_NODES
+    fine = opt.sampled_concurrency or (16 if big else 256)
+    coarse = opt.sampled_concurrency_coarse or (4 if big else 64)
+    return fine, coarse
 
 
 HUB_STEPS = 512   # warp-aggregate the sampled updates above this per-node rate
@@ -540,7 +565,8 @@ class LayoutPlan:
         if S is None:
             raise RuntimeError("plan was built without sampled-mode tables")
         o = self.opt
-        div = o.sampled_concurrency if level == 0 else o.sampled_concurrency_coarse
+        fine, coarse = sampled_divisors(self.levels[0].n, o)
+        div = fine if level == 0 else coarse
         ip, neg, n_tab, mp = self._tables(level)
         _lib.call("drg_layout_sampled", _lib.ptr(ip), None,
                   _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), self._collapse(level),
