@@ -162,7 +162,9 @@ typedef struct drg_heavy_split {
  *   y_a += lr_t * ( sum_b W_ab clip(g_att(y_a, y_b)) + V_a sum_m clip(g_rep(y_a, y_cm)) )
  * lr_t = lr0 * max(1 - t/iters, 0); negatives c_m ~ alias table, Philox keyed by
  * (seed, level, t, node, m, attempt), redrawn up to 9 times if c_m == a.
- * Only rows [row_lo, row_hi) are updated (node-range sharding).  Jacobi: reads
+ * Only rows [row_lo, row_hi) are updated (node-range sharding; with n_iter > 1 the
+ * range must be a prefix [0, row_hi) and rows past it, never written, must agree in
+ * both buffers -- the frozen isolated tail).  Jacobi: reads
  * y_in, writes y_out (ping-pong; the result is in y_out).  With
  * DRG_FLAG_INPLACE, y_in must equal y_out.  neg_idx (optional, n*M int32, -1 =
  * skip) replaces the sampled negatives (parity mode, n_iter must be 1).

@@ -769,8 +769,11 @@ extern "C" int drg_layout_iters(const int64_t *indptr, const uint64_t *rec, cons
     const unsigned grid = (unsigned)ceil_div(ceil_div(rows, npw), kWpb);
     const bool clamp = attractive_clip_active(b, clip);
     const bool partner = n <= kPartnerMaxNodes;
-    if (n_iter > 1 && (row_lo != 0 || row_hi != n))
-        return fail(DRG_ERR_INVALID, "n_iter > 1 needs the full row range");
+    // several iterations ping-pong the two buffers: only a prefix [0, row_hi) may be
+    // updated (rows past it -- a frozen isolated tail -- are never written, so the
+    // caller keeps them equal in both buffers)
+    if (n_iter > 1 && row_lo != 0)
+        return fail(DRG_ERR_INVALID, "n_iter > 1 needs a prefix row range [0, row_hi)");
     float2 *src = reinterpret_cast<float2 *>(y_in);
     float2 *dst = reinterpret_cast<float2 *>(y_out);
     if (!inplace && n_iter > 1 && n_iter % 2 == 0) {

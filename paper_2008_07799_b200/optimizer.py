@@ -202,15 +202,30 @@ class LevelData:
     alias: torch.Tensor    # int64 [n]    (fp32 prob | int32 alias << 32)
     heavy: dict | None = None   # heavy-row split tensors (rows > HEAVY_ROW entries)
     sampled: "SampledTables | None" = None   # update="sampled" tables of this level
+    # rows [n_active, n) have no P entries (the isolated nodes isolated_last puts
+    # last): the gather leaves them frozen, as the reference effectively does -- they
+    # are never sources and are drawn as negatives with ~1e-8 of the mass
+    # (optimizer.py:256-258).  None = all rows active.
+    n_active: int | None = None
+
+    @property
+    def active(self) -> int:
+        return self.n if self.n_active is None else self.n_active
 
     def algorithmic_bytes(self, M: int) -> int:
-        """16 B per P entry + (24 + 16 M) B per node (level 0) --
-        col 4 + W 4 + y_j 8 per entry; rowptr 4 + y_a 8 + y_a' 8 + V 4 and per
+        """16 B per P entry + (24 + 16 M) B per updated node (level 0)
+        -- col 4 + W 4 + y_j 8 per entry; rowptr 4 + y_a 8 + y_a' 8 + V 4 and per
         negative an 8 B alias record + 8 B y_c per node."""
-        return 16 * self.nnz + (24 + 16 * M) * self.n
+        return 16 * self.nnz + (24 + 16 * M) * self.active
 
 
 HEAVY_ROW = 4 * _lib.DRG_HEAVY_CHUNK   # rows longer than this are split across warps
+
+
+def active_rows(indptr: torch.Tensor) -> int:
+    """1 + the last row with P entries (the rows after it form the frozen tail)."""
+    nz = torch.nonzero(indptr[1:] > indptr[:-1])
+    return int(nz[-1]) + 1 if nz.numel() else 0
 
 
 def heavy_split(indptr: torch.Tensor, threshold: int = HEAVY_ROW) -> dict | None:
@@ -410,6 +425,7 @@ def build_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy, neg_power: float
         # kernel time (profiles/README.md), so it is off
         rec, V = pack_level(ip, tg, P, R, Wn, 1.0 / total, n_l, sort_rows=False)
         L = LevelData(n_l, tg.numel(), ip, rec, V, alias, heavy_split(ip))
+        L.n_active = active_rows(ip)
         if sampled and R.numel() > 0 and float(R.sum()) > 0:
             if skip_hub_tables and _is_gather_level(R):
                 L.sampled = SampledTables(None, None, None, None, hubs=True, gather=True)
@@ -466,7 +482,7 @@ class LayoutPlan:
         M = self.opt.neg_samples
         if self.opt.update == "sampled":
             return self.opt.iters * sum((1 + M) * L.n for L in self.levels)
-        return self.opt.iters * sum(L.nnz + M * L.n for L in self.levels)
+        return self.opt.iters * sum(L.nnz + M * L.active for L in self.levels)
 
     def init_positions(self) -> torch.Tensor:
         """Coarsest-level start (optimizer.py:393-395): the reference's numpy draw
@@ -549,11 +565,18 @@ class LayoutPlan:
                 if not inplace:
                     a, b = b, a
             return a
+        na = L.active   # rows past it stay frozen (LevelData.n_active)
         if inplace:
-            self.kernel_step(level, y, y, 0, L.n, t0, n_iter)
+            if na > 0:
+                self.kernel_step(level, y, y, 0, na, t0, n_iter)
             return y
         out = torch.empty_like(y)
-        self.kernel_step(level, y, out, 0, L.n, t0, n_iter)
+        if na < L.n:
+            out[na:] = y[na:]
+        if na > 0:
+            self.kernel_step(level, y, out, 0, na, t0, n_iter)
+        else:
+            out.copy_(y)
         return out
 
     def sampled_steps(self, level: int, y: torch.Tensor, step_lo: int, n_steps: int, t0: int,
@@ -889,7 +912,12 @@ def layout_graph(g: Graph, sim_params: SimilarityParams | None = None,
     dg = DeviceGraph.from_host(g)
     y, stats, _ = layout_device(dg, sim_params, opt_params, rho, min_size, max_levels,
                                 force_levels, init_positions, group, first_order=order)
-    return Layout(positions=y.cpu().numpy().astype(np.float64), stats=stats)
+    # float64 on the device, one DMA into pinned host memory (torch's caching host
+    # allocator reuses it across calls): 0.6 ms for the mesh instead of 4-12 ms for a
+    # pageable copy + host astype
+    out = torch.empty(tuple(y.shape), dtype=torch.float64, pin_memory=True)
+    out.copy_(y.to(torch.float64))
+    return Layout(positions=out.numpy(), stats=stats)
 
 
 # ---------------------------------------------------------------------------

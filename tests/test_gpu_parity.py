@@ -737,3 +737,26 @@ def test_khop_cap_last_hop_truncation_on_hubs(k, cap):
         rng.shuffle(shuffled[g.indptr[i]:g.indptr[i + 1]])
     got2 = B.all_k_neighborhoods(B.Graph(g.indptr, shuffled), k, cap=cap)
     assert np.array_equal(got2.ids, want.ids) and np.array_equal(got2.dists, want.dists)
+
+
+def test_gather_freezes_the_isolated_tail():
+    """update="jacobi" on a graph with isolated nodes (placed last): the gather
+    updates rows [0, n_active) only -- the isolated tail keeps its positions, as in
+    the reference (never a source, ~1e-8 of the negative mass) -- and the active
+    rows equal a full-range iteration bit for bit."""
+    from paper_2008_07799_b200 import synthetic
+    g = synthetic.rmat(15, 4, seed=5, device="host")
+    prep = _prepared(as_gpu_graph(g), k=1, M=5, levels=2)
+    plan = prep.plan
+    L = plan.levels[0]
+    assert 0 < L.active < L.n
+    deg = np.diff(L.indptr.cpu().numpy())
+    assert (deg[L.active:] == 0).all() and deg[L.active - 1] > 0
+    y = torch.randn(L.n, 2, device="cuda")
+    got = plan.run_level(0, y.clone(), t0=2, n_iter=1)
+    full = torch.empty_like(y)
+    plan.kernel_step(0, y, full, 0, L.n, 2, 1)
+    assert torch.equal(got[L.active:], y[L.active:])
+    assert torch.equal(got[:L.active], full[:L.active])
+    many = plan.run_level(0, y.clone(), t0=0, n_iter=4)   # ping-pong keeps the tail
+    assert torch.equal(many[L.active:], y[L.active:]) and torch.isfinite(many).all()
