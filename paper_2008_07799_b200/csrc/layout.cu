@@ -161,35 +161,45 @@ __global__ void __launch_bounds__(kWpb * 32, 5)
         const uint2 *row = A.rec + lo;
         const float2 ya = load_y<INPLACE>(y_in, a);
         float ax = 0.f, ay = 0.f, wsum = 0.f;
-        for (int base = 0; base < cnt; base += 32 * kDepth) {
-            uint2 r[kDepth];
-#pragma unroll
-            for (int j = 0; j < kDepth; ++j) {
-                const int e = base + j * 32 + lane;
-                r[j] = e < cnt ? __ldcs(row + e) : make_uint2((uint32_t)a, 0u);
+        // one entry's attraction; padding slots (w = 0, y_b = y_a: ld2 == 0) add an
+        // exact zero for every b >= 1
+        auto add_entry = [&](uint2 r, float2 yb) {
+            const float dx = ya.x - yb.x, dy = ya.y - yb.y;
+            const float ld2 = fmaf(dx, dx, dy * dy);
+            const float pw = powbm1<B>(ld2, b);
+            const float w = __uint_as_float(r.y);
+            const float inv = rcp_approx(fmaf(pw, ld2, 1.0f));
+            if (CLAMP_ATT) {
+                const float coef = -two_b * pw * inv;
+                ax = fmaf(w, clampf(coef * dx, A.clip), ax);
+                ay = fmaf(w, clampf(coef * dy, A.clip), ay);
+            } else {
+                // the constant -2b is applied once per node below
+                const float wc = (B == 1 ? w : w * pw) * inv;
+                ax = fmaf(wc, dx, ax);
+                ay = fmaf(wc, dy, ay);
             }
-            float2 yb[kDepth];
+            if (PARTNER) wsum += w;
+        };
+        if (cnt <= 32) {
+            // short row (power-law levels: most rows): one slot per lane instead of a
+            // kDepth-deep pass -- the same sums, the deep pass's extra slots being
+            // exact zeros
+            const uint2 r = lane < cnt ? __ldcs(row + lane) : make_uint2((uint32_t)a, 0u);
+            add_entry(r, load_y<INPLACE>(y_in, r.x));
+        } else {
+            for (int base = 0; base < cnt; base += 32 * kDepth) {
+                uint2 r[kDepth];
 #pragma unroll
-            for (int j = 0; j < kDepth; ++j) yb[j] = load_y<INPLACE>(y_in, r[j].x);
-#pragma unroll
-            for (int j = 0; j < kDepth; ++j) {
-                // ld2 == 0 gives an exactly zero contribution for every b >= 1
-                const float dx = ya.x - yb[j].x, dy = ya.y - yb[j].y;
-                const float ld2 = fmaf(dx, dx, dy * dy);
-                const float pw = powbm1<B>(ld2, b);
-                const float w = __uint_as_float(r[j].y);
-                const float inv = rcp_approx(fmaf(pw, ld2, 1.0f));
-                if (CLAMP_ATT) {
-                    const float coef = -two_b * pw * inv;
-                    ax = fmaf(w, clampf(coef * dx, A.clip), ax);
-                    ay = fmaf(w, clampf(coef * dy, A.clip), ay);
-                } else {
-                    // the constant -2b is applied once per node below
-                    const float wc = (B == 1 ? w : w * pw) * inv;
-                    ax = fmaf(wc, dx, ax);
-                    ay = fmaf(wc, dy, ay);
+                for (int j = 0; j < kDepth; ++j) {
+                    const int e = base + j * 32 + lane;
+                    r[j] = e < cnt ? __ldcs(row + e) : make_uint2((uint32_t)a, 0u);
                 }
-                if (PARTNER) wsum += w;
+                float2 yb[kDepth];
+#pragma unroll
+                for (int j = 0; j < kDepth; ++j) yb[j] = load_y<INPLACE>(y_in, r[j].x);
+#pragma unroll
+                for (int j = 0; j < kDepth; ++j) add_entry(r[j], yb[j]);
             }
         }
         if (!CLAMP_ATT) {
