@@ -10,6 +10,7 @@ is the deduplicated image of the fine edges (drg_coarse_graph).
 
 from __future__ import annotations
 
+import concurrent.futures
 import ctypes
 from dataclasses import dataclass, field
 
@@ -71,26 +72,37 @@ class DeviceHierarchy:
                          self.rho, self.min_size, self.levels, self.maps)
 
 
-def device_coarsen(dg: DeviceGraph, order: torch.Tensor):
-    """K4 with an explicit visiting order (device int64).  Returns
-    (coarse DeviceGraph, parent int32, MIS rounds)."""
+def device_parents(dg: DeviceGraph, order: torch.Tensor):
+    """K4's greedy pass with an explicit visiting order (device int64): (parent
+    int32, coarse node count, MIS rounds)."""
     n = dg.node_count
     if n < 1:
         raise ValueError("cannot coarsen an empty graph")
-    dev = dg.indptr.device
-    parent = torch.empty(n, dtype=torch.int32, device=dev)
+    parent = torch.empty(n, dtype=torch.int32, device=dg.indptr.device)
     nc = _lib.out_i64()
     rounds = ctypes.c_int32(0)
-    st = _lib.stream_ptr()
     _lib.call("drg_coarsen", _lib.ptr(dg.indptr), _lib.ptr(dg.indices), n, _lib.ptr(order),
-              _lib.ptr(parent), _lib.byref(nc), _lib.byref(rounds), st)
-    n_c = nc.value
+              _lib.ptr(parent), _lib.byref(nc), _lib.byref(rounds), _lib.stream_ptr())
+    return parent, nc.value, rounds.value
+
+
+def device_coarse_graph(dg: DeviceGraph, parent: torch.Tensor, n_c: int) -> DeviceGraph:
+    """The coarse CSR: the deduplicated image of the fine edges under ``parent``."""
+    dev = dg.indptr.device
     indptr = torch.empty(n_c + 1, dtype=torch.int64, device=dev)
     cols = torch.empty(max(dg.nnz, 1), dtype=torch.int32, device=dev)
     nnz = _lib.out_i64()
-    _lib.call("drg_coarse_graph", _lib.ptr(dg.indptr), _lib.ptr(dg.indices), n, _lib.ptr(parent),
-              n_c, _lib.ptr(indptr), _lib.ptr(cols), _lib.byref(nnz), st)
-    return DeviceGraph(indptr, cols[:nnz.value].clone()), parent, rounds.value
+    _lib.call("drg_coarse_graph", _lib.ptr(dg.indptr), _lib.ptr(dg.indices), dg.node_count,
+              _lib.ptr(parent), n_c, _lib.ptr(indptr), _lib.ptr(cols), _lib.byref(nnz),
+              _lib.stream_ptr())
+    return DeviceGraph(indptr, cols[:nnz.value].clone())
+
+
+def device_coarsen(dg: DeviceGraph, order: torch.Tensor):
+    """K4 with an explicit visiting order (device int64).  Returns
+    (coarse DeviceGraph, parent int32, MIS rounds)."""
+    parent, n_c, rounds = device_parents(dg, order)
+    return device_coarse_graph(dg, parent, n_c), parent, rounds
 
 
 def level_order(n: int, seed: int) -> np.ndarray:
@@ -125,25 +137,36 @@ def device_build_hierarchy(dg: DeviceGraph, rho: float = 0.8, min_size: int = 16
         raise ValueError("min_size must be >= 1")
     rng = np.random.default_rng(seed)
     h = DeviceHierarchy([dg], [], rho, min_size)
+    ahead = None   # (seed, future) of the next level's visiting order, drawn early
     while h.levels[-1].node_count > min_size:
         if max_levels is not None and len(h.levels) >= max_levels:
             break
-        level_seed = int(rng.integers(0, 2**63 - 1))
         top = h.levels[-1]
-        if first_order is not None and len(h.levels) == 1:
-            host_order = first_order.result()
+        if ahead is not None:
+            level_seed, fut = ahead
+            host_order = fut.result()
+            ahead = None
         else:
-            host_order = level_order(top.node_count, level_seed)
+            level_seed = int(rng.integers(0, 2**63 - 1))
+            if first_order is not None and len(h.levels) == 1:
+                host_order = first_order.result()
+            else:
+                host_order = level_order(top.node_count, level_seed)
         order = torch.from_numpy(host_order).to(top.indptr.device).to(torch.int64)
         if level0_relabel is not None and len(h.levels) == 1:
             order = level0_relabel.to(torch.int64)[order]
-        coarse, parent, rounds = device_coarsen(top, order)
+        parent, n_c, rounds = device_parents(top, order)
         forced = force_levels is not None and len(h.levels) < force_levels
-        if not forced and coarse.node_count > rho * top.node_count:
+        if not forced and n_c > rho * top.node_count:
             break
-        if coarse.node_count == top.node_count:
+        if n_c == top.node_count:
             break
-        h.levels.append(coarse)
+        # the next level's host permutation (its size is n_c, its seed the next draw of
+        # the same stream) runs on a host thread while the device builds this coarse CSR
+        if n_c > min_size and (max_levels is None or len(h.levels) + 1 < max_levels):
+            nxt = int(rng.integers(0, 2**63 - 1))
+            ahead = (nxt, _AHEAD_POOL.submit(level_order, n_c, nxt))
+        h.levels.append(device_coarse_graph(top, parent, n_c))
         h.maps.append(parent)
         h.rounds.append(rounds)
     return h
@@ -259,6 +282,9 @@ def relabel_coarse_levels(dh: DeviceHierarchy) -> list:
             m[rel.to(torch.int64)] = dh.maps[l]
             dh.maps[l] = m
     return rels
+
+
+_AHEAD_POOL = concurrent.futures.ThreadPoolExecutor(1)
 
 
 def first_level_order(n: int, seed: int, executor):
