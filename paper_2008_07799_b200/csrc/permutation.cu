@@ -126,7 +126,25 @@ extern "C" int drg_pcg64_permutation(uint64_t state_hi, uint64_t state_lo, uint6
         int64_t p = 0;
         for (int64_t b = 0; b < nblocks; ++b) {
             const int64_t end = std::min(total, (b + 1) * kBlock);
-            while (k < end && p < H) take(hw[p++]);
+            while (k < end && p < H) {
+                // within a power-of-two band of the bound m = n-1-k the mask is fixed,
+                // so the loop-carried chain is just compare + decrement (~1 ns per
+                // half-word instead of re-deriving the mask from k every time)
+                const uint32_t mx0 = (uint32_t)(n - 1 - k);
+                const uint32_t lowb = 1u << (31 - __builtin_clz(mx0));
+                const uint32_t mask = (uint32_t)(2ull * lowb - 1);
+                const int64_t kend = std::min<int64_t>(end, (int64_t)n - lowb);   // m >= lowb
+                uint32_t m = mx0;
+                int64_t kk = k;
+                while (kk < kend && p < H) {
+                    const uint32_t v = hw[p++] & mask;
+                    jo[kk] = (int32_t)v;
+                    const uint32_t d = v <= m;
+                    kk += d;
+                    m -= d;
+                }
+                k = kk;
+            }
             if (k < end) {   // past the generated words (not reached in practice)
                 Pcg64 tail{lcg_advance(st0, inc, (uint64_t)R), inc, false, 0};
                 while (k < total) {
