@@ -681,29 +681,58 @@ class LayoutPlan:
                                      f"at level {level}")
         return y
 
+    def shard_bounds(self, level: int, world: int) -> list[int]:
+        """Row ranges of the node-range shards: rows [0, n_active) cut
+        where the prefix sum of the gather's per-row bytes, 16 deg + 104, crosses
+        multiples of total / world -- heavy-tailed rows (R-MAT hubs) balance by
+        bytes, not by node count.  Equal node ranges without row offsets."""
+        L = self.levels[level]
+        na = L.active
+        if L.indptr is None or na == 0:
+            c = -(-na // world)
+            return [min(r * c, na) for r in range(world + 1)]
+        ip = L.indptr[:na + 1]
+        cost = (16 * (ip[1:] - ip[:-1]) + 104).to(torch.float64)
+        cum = torch.cumsum(cost, 0)
+        marks = cum[-1] * torch.arange(1, world, dtype=torch.float64, device=cum.device) / world
+        cuts = torch.searchsorted(cum, marks).tolist()
+        return [0] + [min(int(c), na) for c in cuts] + [na]
+
     def _run_level_sharded(self, level, y, t0, n_iter, group, step_fn):
+        """Node-range shards + one all-gather per iteration: rank r updates rows
+        shard_bounds[r:r+2] of the replicated Y; the slices (padded to the longest)
+        are all-gathered and scattered back into place.  Rows past n_active (the
+        frozen isolated tail) are never exchanged."""
         import torch.distributed as dist
         L = self.levels[level]
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
-        chunk = -(-L.n // world)
-        lo, hi = rank * chunk, min(rank * chunk + chunk, L.n)
+        bounds = self.shard_bounds(level, world)
+        lo, hi = bounds[rank], bounds[rank + 1]
+        lens = [bounds[r + 1] - bounds[r] for r in range(world)]
+        width = max(1, max(lens))
         inplace = self.opt.update == "inplace"
-        a = torch.zeros((world * chunk, 2), dtype=torch.float32, device=y.device)
-        a[:L.n] = y
-        b = a if inplace else torch.zeros_like(a)
-        nccl = dist.get_backend(group) == "nccl"
+        a = y.contiguous()
+        b = a if inplace else a.clone()
+        send = torch.zeros((width, 2), dtype=torch.float32, device=y.device)
+        recv = torch.empty((world * width, 2), dtype=torch.float32, device=y.device)
+        # recv row of every global row [0, n_active): rank r's rows start at r * width
+        src = torch.cat([torch.arange(r * width, r * width + lens[r], device=y.device)
+                         for r in range(world)])
+        na = bounds[-1]
         for j in range(n_iter):
             t = t0 + j
-            if step_fn is not None:
-                step_fn(a, b, lo, hi, t)
-            else:
-                self.kernel_step(level, a, b, lo, hi, t, 1)
-            mine = b[rank * chunk:(rank + 1) * chunk]
-            dist.all_gather_into_tensor(b, mine if nccl else mine.clone(), group=group)
+            if hi > lo:
+                if step_fn is not None:
+                    step_fn(a, b, lo, hi, t)
+                else:
+                    self.kernel_step(level, a, b, lo, hi, t, 1)
+            send[:hi - lo] = b[lo:hi]
+            dist.all_gather_into_tensor(recv, send, group=group)
+            b[:na] = recv[src]
             if not inplace:
                 a, b = b, a
-        return a[:L.n].contiguous()
+        return a
 
     def run(self, y0: torch.Tensor | None = None, group=None, step_fn: StepFn | None = None,
             on_level: Callable | None = None) -> torch.Tensor:

@@ -54,18 +54,19 @@ def _make_step(ip, tg, W, V, M=5, iters=10):
     return step
 
 
-def _plan(n, iters, update="jacobi"):
+def _plan(n, iters, update="jacobi", indptr=None):
     from paper_2008_07799_b200.optimizer import LayoutPlan, LevelData, OptimizerParams
     opt = OptimizerParams(iters=iters, update=update, shard_min_nodes=1)
-    return LayoutPlan([LevelData(n, 0, None, None, None, None)], [], opt)
+    ipt = None if indptr is None else torch.from_numpy(np.asarray(indptr, dtype=np.int64))
+    return LayoutPlan([LevelData(n, 0, ipt, None, None, None)], [], opt)
 
 
-def _worker(rank, world, port, out_path, update):
+def _worker(rank, world, port, out_path, update, by_bytes=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     ip, tg, W, V, y0 = _problem()
     iters = 6
-    plan = _plan(len(V), iters, update)
+    plan = _plan(len(V), iters, update, ip if by_bytes else None)
     y = plan.run_level(0, torch.from_numpy(y0.copy()), group=dist.group.WORLD,
                        step_fn=_make_step(ip, tg, W, V, iters=iters))
     if rank == 0:
@@ -74,10 +75,13 @@ def _worker(rank, world, port, out_path, update):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sharded_jacobi_equals_single_rank(tmp_path, world):
+@pytest.mark.parametrize("world,by_bytes", [(2, False), (2, True), (3, True)])
+def test_sharded_jacobi_equals_single_rank(tmp_path, world, by_bytes):
+    """Node-range shards (equal node ranges, or cut by the gather's bytes per row)
+    + one all-gather per iteration == the single-process Jacobi run, bit for bit."""
     out = str(tmp_path / "y.npy")
-    mp.spawn(_worker, args=(world, _free_port(), out, "jacobi"), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, "jacobi", by_bytes), nprocs=world,
+             join=True)
     sharded = np.load(out)
     ip, tg, W, V, y0 = _problem()
     plan = _plan(len(V), 6)
@@ -95,16 +99,23 @@ def test_sharded_inplace_runs(tmp_path):
 
 
 def test_partition_covers_rows():
-    """Node-range partition: equal chunks, padded all-gather buffer, every row
-    owned by exactly one rank."""
+    """shard_bounds: contiguous ranges covering every row once -- equal node ranges
+    without row offsets, else cut by the gather's bytes per row (16 deg + 104), each
+    rank within one row of the ideal share on a heavy-tailed row-length profile."""
     for n in (1, 7, 64, 1000, 65537):
         for world in (1, 2, 3, 4, 8):
-            chunk = -(-n // world)
-            owned = np.zeros(n, dtype=int)
-            for r in range(world):
-                lo, hi = r * chunk, min(r * chunk + chunk, n)
-                owned[lo:hi] += 1
-            assert (owned == 1).all()
+            b = _plan(n, 1).shard_bounds(0, world)
+            assert b[0] == 0 and b[-1] == n and all(x <= y for x, y in zip(b, b[1:]))
+    rng = np.random.default_rng(4)
+    deg = np.minimum(rng.pareto(1.2, size=20_000).astype(np.int64) * 3, 50_000)
+    ip = np.concatenate([[0], np.cumsum(deg)])
+    cost = 16 * deg + 104
+    for world in (2, 3, 8):
+        b = _plan(len(deg), 1, indptr=ip).shard_bounds(0, world)
+        assert b[0] == 0 and b[-1] == len(deg) and all(x <= y for x, y in zip(b, b[1:]))
+        share = cost.sum() / world
+        for r in range(world):
+            assert abs(cost[b[r]:b[r + 1]].sum() - share) <= cost.max() + 1
 
 
 def _sampled_step(n):
