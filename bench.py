@@ -436,7 +436,7 @@ def run_ours(args):
         ix = torch.from_numpy(gh.indices).pin_memory()
         g_pinned = B.Graph(ip.numpy(), ix.numpy())
         h2d = ip.numel() * 8 + ix.numel() * 4
-        d2h = sizes[0] * 2 * 4
+        d2h = sizes[0] * 2 * 8   # float64 positions (layout_graph converts on the device)
         del prep, plan
         torch.cuda.empty_cache()
         kw = dict(max_levels=hier.get("max_levels"), force_levels=hier.get("force_levels"))

@@ -1038,8 +1038,8 @@ extern "C" int drg_layout_sgather(const int64_t *indptr, const uint64_t *rec,
     if (neg_idx && n_iter != 1) return fail(DRG_ERR_INVALID, "neg_idx needs n_iter == 1");
     const bool inplace = (flags & DRG_FLAG_INPLACE) != 0;
     if (inplace != (y_in == y_out)) return fail(DRG_ERR_INVALID, "buffer / flag mismatch");
-    if (n_iter > 1 && (row_lo != 0 || row_hi != n))
-        return fail(DRG_ERR_INVALID, "n_iter > 1 needs the full row range");
+    if (n_iter > 1 && row_lo != 0)   // as drg_layout_iters: a prefix, the tail frozen
+        return fail(DRG_ERR_INVALID, "n_iter > 1 needs a prefix row range [0, row_hi)");
     cudaStream_t st = as_stream(stream);
     IterArgs A = {};
     A.indptr = indptr;
