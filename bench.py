@@ -77,6 +77,8 @@ def parse():
                     choices=["jacobi", "inplace", "sampled", "sgather"])
     ap.add_argument("--sampled-concurrency", type=int, default=None,
                     help="level-0 steps in flight = n / this (default: by graph size)")
+    ap.add_argument("--sampled-concurrency-coarse", type=int, default=None,
+                    help="coarse-level steps in flight = n_l / this (default: by graph size)")
     ap.add_argument("--hub-levels", choices=["jacobi", "sampled"], default="jacobi",
                     help="update the hub-heavy levels of update=sampled run")
     return ap.parse_args()
@@ -159,13 +161,13 @@ def build_workload(name):
 
 
 def params_for(name, iters_override=None, update="sampled", concurrency=None,
-               hub_levels="jacobi"):
+               hub_levels="jacobi", concurrency_coarse=None):
     import paper_2008_07799_b200 as B
     w = WORKLOADS[name]
     sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"], neighbor_cap=w.get("cap"))
     opt = B.OptimizerParams(neg_samples=w["M"], iters=iters_override or w["iters"], seed=0,
                             init=w["init"], update=update, sampled_concurrency=concurrency,
-                            hub_levels=hub_levels)
+                            sampled_concurrency_coarse=concurrency_coarse, hub_levels=hub_levels)
     return sim, opt, dict(w["hier"])
 
 
@@ -281,7 +283,7 @@ def run_ours(args):
         group = dist.group.WORLD
     name = args.workload
     sim, opt, hier = params_for(name, args.iters, args.update, args.sampled_concurrency,
-                                args.hub_levels)
+                                args.hub_levels, args.sampled_concurrency_coarse)
 
     dg = build_workload(name)
     torch.cuda.synchronize()

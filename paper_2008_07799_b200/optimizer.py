@@ -60,7 +60,8 @@ class OptimizerParams:
     * "sampled" (default): the reference's own step (_kernels.py:65-140) run
       Hogwild-style on the GPU -- KL/NP parity with the reference, fastest on one
       GPU; run-to-run nondeterministic like the reference's threads > 1 mode.
-      Levels whose busiest node is the source of > HUB_STEPS steps per epoch
+      Steps in flight (``sampled_concurrency[_coarse]``, default by graph size,
+      ``sampled_divisors``) trade speed for fidelity.  Levels whose busiest node is the source of > HUB_STEPS steps per epoch
       use warp-aggregated atomics; above GATHER_STEPS (R-MAT coarse levels, where
       same-address atomics serialise) they run the "jacobi" gather instead
       (``hub_levels``).
