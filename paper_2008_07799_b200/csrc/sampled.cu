@@ -19,6 +19,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <climits>
 #include <mutex>
 
 #include <cub/cub.cuh>
@@ -489,9 +490,23 @@ __global__ void __launch_bounds__(256, 4) apply_kernel(PArgs A, float2 *y) {
                         (int64_t)gridDim.x * blockDim.x);
 }
 
+// Few steps in flight (small or fidelity-capped levels): the step is a dependent
+// chain issued by one or two warps per SM, so this instance drops the 4-blocks-per-SM
+// register cap (no parameter reloads / rematerialisation in the chain).
+template <bool AGG, int B>
+__global__ void __launch_bounds__(256, 1) apply_kernel_lc(PArgs A, float2 *y) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    apply_epoch<AGG, B>(A, y, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                        (int64_t)gridDim.x * blockDim.x);
+}
+
+constexpr int64_t kLowConcurrency = 16384;   // steps in flight below which _lc runs
+
 // the kernel instance: b = 2 (the default) compiled in, other b at run time
 template <bool AGG>
-void *apply_instance(int b) {
+void *apply_instance(int b, int64_t threads = INT64_MAX) {
+    if (threads < kLowConcurrency)
+        return b == 2 ? (void *)apply_kernel_lc<AGG, 2> : (void *)apply_kernel_lc<AGG, 0>;
     return b == 2 ? (void *)apply_kernel<AGG, 2> : (void *)apply_kernel<AGG, 0>;
 }
 
@@ -509,7 +524,9 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     void *args[] = {const_cast<PArgs *>(&P), &y};
-    DRG_CUDA(cudaLaunchKernelExC(&cfg, agg ? apply_instance<true>(P.b) : apply_instance<false>(P.b),
+    const int64_t threads = (int64_t)grid * block;
+    DRG_CUDA(cudaLaunchKernelExC(&cfg, agg ? apply_instance<true>(P.b, threads)
+                                           : apply_instance<false>(P.b, threads),
                                  args));
     DRG_LAUNCHED("apply_kernel");
     return DRG_OK;
