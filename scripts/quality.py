@@ -32,6 +32,9 @@ CONFIGS = {
                  np_sample=None),
     "mesh_small": dict(k=2, perplexity=50.0, iters=800, max_levels=4, init="normal",
                        z_pairs=None, np_sample=None),
+    # BASELINE C3: Barabasi-Albert 1M, k=2 with the neighbour cap 256 (union P)
+    "ba": dict(k=2, perplexity=50.0, iters=500, max_levels=None, init="normal", z_pairs=None,
+               np_sample=None, cap=256),
     # BASELINE C4 itself: 120^3 mesh, 1.73 M nodes (the bench workload)
     "mesh": dict(k=2, perplexity=50.0, iters=800, max_levels=4, init="normal",
                  z_pairs=None, np_sample=None),
@@ -47,6 +50,8 @@ def graph_for(name):
         g = synthetic.rgg(200_000, seed=0, device="host")
     elif name == "mesh":
         g = synthetic.mesh3d(120, device="host")
+    elif name == "ba":
+        g = synthetic.barabasi_albert(1_000_000, 4, seed=0, device="host")
     else:
         g = synthetic.mesh3d(40, device="host")
     return O.Graph(g.indptr, g.indices), B.Graph(g.indptr, g.indices)
@@ -106,8 +111,10 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
     from paper_2008_07799_b200 import quality as Q
     cfg = CONFIGS[name]
     og, bg = graph_for(name)
-    nd = O.all_k_neighborhoods(og, cfg["k"])
-    ns = O.build_sparse_similarity(nd, cfg["perplexity"])
+    cap = cfg.get("cap", 0)
+    nd = O.all_k_neighborhoods(og, cfg["k"], cap=cap)
+    ns = (O.build_capped_similarity(nd, cfg["perplexity"]) if cap
+          else O.build_sparse_similarity(nd, cfg["perplexity"]))
     bns = B.SparseSimilarity(ns.indptr, ns.targets, ns.weights, ns.total_mass, ns.sigma, ns.k)
     del nd
     sample = None
@@ -122,7 +129,7 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
         t0 = time.perf_counter()
         opt = O.OptimizerParams(iters=cfg["iters"], seed=seed, threads=threads)
         pos, _, _, _ = O.layout_graph(og, k=cfg["k"], perplexity=cfg["perplexity"], params=opt,
-                                      max_levels=cfg["max_levels"], init=y0)
+                                      max_levels=cfg["max_levels"], init=y0, neighbor_cap=cap)
         t_ref = time.perf_counter() - t0
         runs = {"reference": (pos, t_ref)}
         for m in modes:
@@ -142,7 +149,8 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
                 pos_x = emulated_exchange(bg, cfg, seed, y0, int(div))
                 runs[m] = (pos_x, time.perf_counter() - t0)
                 continue
-            lay = B.layout_graph(bg, B.SimilarityParams(k=cfg["k"], perplexity=cfg["perplexity"]),
+            lay = B.layout_graph(bg, B.SimilarityParams(k=cfg["k"], perplexity=cfg["perplexity"],
+                                                        neighbor_cap=cap or None),
                                  B.OptimizerParams(iters=cfg["iters"], seed=seed, update=upd,
                                                    init=cfg["init"], **extra),
                                  max_levels=cfg["max_levels"], init_positions=y0)
