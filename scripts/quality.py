@@ -37,6 +37,10 @@ CONFIGS = {
                np_sample=20_000, np_max_degree=2048, cap=256, np_k=1),
     # (NP over 20k sampled nodes of degree <= 2048: a hub's hop set exceeds the device
     # k-NN instrument, and a hub's 2-hop ball is most of the graph)
+    # BASELINE C5 at a reduced scale (R-MAT scale 18, 262k nodes): level 0 sampled,
+    # the hub-heavy coarse levels gathered -- the mixed plan C5 runs
+    "rmat18": dict(k=1, perplexity="auto", iters=500, max_levels=5, force_levels=5,
+                   init="normal", z_pairs=None, np_sample=20_000, np_max_degree=2048, np_k=1),
     # BASELINE C4 itself: 120^3 mesh, 1.73 M nodes (the bench workload)
     "mesh": dict(k=2, perplexity=50.0, iters=800, max_levels=4, init="normal",
                  z_pairs=None, np_sample=None),
@@ -52,6 +56,8 @@ def graph_for(name):
         g = synthetic.rgg(200_000, seed=0, device="host")
     elif name == "mesh":
         g = synthetic.mesh3d(120, device="host")
+    elif name == "rmat18":
+        g = synthetic.rmat(18, 16, seed=0, device="host")
     elif name == "ba":
         g = synthetic.barabasi_albert(1_000_000, 4, seed=0, device="host")
     else:
@@ -128,12 +134,13 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
     threads = os.cpu_count() if og.node_count > 50_000 else 1
     for seed in range(seed0, seed0 + n_seeds):
         h = O.build_hierarchy(og, 0.8, 16, O.derive_seed(seed, O.HIERARCHY_TAG),
-                              max_levels=cfg["max_levels"])
+                              max_levels=cfg["max_levels"], force_levels=cfg.get("force_levels"))
         y0 = init_for(cfg, h.levels[-1].node_count, seed)
         t0 = time.perf_counter()
         opt = O.OptimizerParams(iters=cfg["iters"], seed=seed, threads=threads)
         pos, _, _, _ = O.layout_graph(og, k=cfg["k"], perplexity=cfg["perplexity"], params=opt,
-                                      max_levels=cfg["max_levels"], init=y0, neighbor_cap=cap)
+                                      max_levels=cfg["max_levels"], init=y0, neighbor_cap=cap,
+                                      force_levels=cfg.get("force_levels"))
         t_ref = time.perf_counter() - t0
         runs = {"reference": (pos, t_ref)}
         for m in modes:
@@ -157,7 +164,8 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
                                                         neighbor_cap=cap or None),
                                  B.OptimizerParams(iters=cfg["iters"], seed=seed, update=upd,
                                                    init=cfg["init"], **extra),
-                                 max_levels=cfg["max_levels"], init_positions=y0)
+                                 max_levels=cfg["max_levels"], init_positions=y0,
+                                 force_levels=cfg.get("force_levels"))
             runs[m] = (lay.positions, time.perf_counter() - t0)
         for key, (y, t) in runs.items():
             if evaluator == "gpu":   # device instruments (exact Z, exact-mode k-NN)
