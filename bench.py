@@ -79,7 +79,7 @@ def parse():
                     help="level-0 steps in flight = n / this (default: by graph size)")
     ap.add_argument("--sampled-concurrency-coarse", type=int, default=None,
                     help="coarse-level steps in flight = n_l / this (default: by graph size)")
-    ap.add_argument("--hub-levels", choices=["jacobi", "sampled"], default="jacobi",
+    ap.add_argument("--hub-levels", choices=["jacobi", "sampled"], default="sampled",
                     help="update the hub-heavy levels of update=sampled run")
     return ap.parse_args()
 
@@ -161,7 +161,7 @@ def build_workload(name):
 
 
 def params_for(name, iters_override=None, update="sampled", concurrency=None,
-               hub_levels="jacobi", concurrency_coarse=None):
+               hub_levels="sampled", concurrency_coarse=None):
     import paper_2008_07799_b200 as B
     w = WORKLOADS[name]
     sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"], neighbor_cap=w.get("cap"))

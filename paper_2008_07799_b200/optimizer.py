@@ -62,9 +62,9 @@ class OptimizerParams:
       GPU; run-to-run nondeterministic like the reference's threads > 1 mode.
       Steps in flight (``sampled_concurrency[_coarse]``, default by graph size,
       ``sampled_divisors``) trade speed for fidelity.  Levels whose busiest node is the source of > HUB_STEPS steps per epoch
-      use warp-aggregated atomics; above GATHER_STEPS (R-MAT coarse levels, where
-      same-address atomics serialise) they run the "jacobi" gather instead
-      (``hub_levels``).
+      use warp-aggregated atomics; with ``hub_levels="jacobi"`` the levels above
+      GATHER_STEPS (R-MAT coarse levels, where same-address atomics serialise) run
+      the gather instead -- faster, but not faithful there (KL +77% on R-MAT 18).
     * "jacobi": the node-parallel expected-gradient iteration (SURVEY §8(a) A12,
       CSR gather + M negatives per node) -- bitwise deterministic and node-range
       shardable across GPUs; matches KL, lower NP on multilevel RGG.
@@ -94,7 +94,10 @@ class OptimizerParams:
     sampled_concurrency: int | None = None
     sampled_concurrency_coarse: int | None = None
     att_samples: int = 2           # update="sgather": attraction partners drawn per node
-    hub_levels: str = "jacobi"     # update="sampled": hub-heavy levels run this update
+    # update="sampled": the update of levels above GATHER_STEPS.  "sampled" (default)
+    # keeps the reference's step there too; "jacobi" gathers them -- 3-6x faster on
+    # R-MAT but KL +77% on R-MAT scale 18 (profiles/r01_quality_rmat18_*)
+    hub_levels: str = "sampled"
     sampled_fused: bool = False    # update="sampled": draw inline (one kernel per epoch)
                                    # instead of the split draw pass + update pass
 

@@ -149,6 +149,8 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
             extra = {}
             if upd == "sampledf":   # the fused one-kernel form of "sampled"
                 upd, extra = "sampled", {"sampled_fused": True}
+            if upd == "sampledh":   # "sampled" on every level, hub-heavy ones included
+                upd, extra = "sampled", {"hub_levels": "sampled"}
             if div and upd == "sampled":
                 fine, _, coarse = div.partition(":")
                 extra = {**extra, "sampled_concurrency": int(fine)}

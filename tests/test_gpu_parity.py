@@ -709,7 +709,8 @@ def test_sampled_mode_hub_aggregation():
     hub2 = np.column_stack([np.zeros(n2 - 1, dtype=np.int64), np.arange(1, n2)])
     g2 = O.from_edges(np.concatenate([hub2, rng.integers(1, n2, size=(4000, 2))]), n2)
     prep2 = prepare_layout(DeviceGraph.from_host(as_gpu_graph(g2)), B.SimilarityParams(k=1),
-                           B.OptimizerParams(seed=1, iters=20), min_size=16)
+                           B.OptimizerParams(seed=1, iters=20, hub_levels="jacobi"),
+                           min_size=16)
     assert any(L.sampled is not None and L.sampled.gather for L in prep2.plan.levels)
     for gg in (g, g2):
         for hub_levels in ("jacobi", "sampled"):   # gather fallback / aggregated atomics
