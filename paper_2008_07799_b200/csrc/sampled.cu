@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(256, 1) apply_kernel_lc(PArgs A, float2 *y) {
                         (int64_t)gridDim.x * blockDim.x);
 }
 
-constexpr int64_t kLowConcurrency = 16384;   // steps in flight below which _lc runs
+constexpr int64_t kLowConcurrency = 65536;   // steps in flight below which _lc runs
 
 // the kernel instance: b = 2 (the default) compiled in, other b at run time
 template <bool AGG>
