@@ -528,8 +528,27 @@ def cpu_baseline_from_gpu(dg, sim, opt, sizes, hier):
             "setup_s": setup}
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this command under
+    torch.distributed.run with N ranks on this node (one process per GPU, NCCL over
+    NVLink, rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+           "--nproc-per-node", str(n), "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        sys.exit(spawn_ranks(args.gpus))
+    if world and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference_arm(args)
         return

@@ -60,6 +60,12 @@ int drg_khop_count(const int64_t *indptr, const int32_t *indices, int64_t n, int
 int drg_khop_fill(const int64_t *indptr, const int32_t *indices, int64_t n, int k,
                   int64_t cap, const int64_t *out_indptr, int32_t *out_ids,
                   int32_t *out_dists, void *stream);
+/* bfs_k_neighborhood (graph.py:280-305): one source's row, (dist, id)-sorted, by the
+ * global-memory tier (any ball size, any k >= 1).  out_ids == NULL: *out_count (host)
+ * only; else out_ids/out_dists (device, capacity entries) receive the row. */
+int drg_khop_source(const int64_t *indptr, const int32_t *indices, int64_t n, int k,
+                    int64_t source, int32_t *out_ids, int32_t *out_dists, int64_t capacity,
+                    int64_t *out_count, void *stream);
 
 /* --- K2 + K3: Gaussian similarity --------------------------------------------
  * Replaces build_sparse_similarity (similarity.py:216-278) with search_sigma
@@ -214,9 +220,17 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * draw of whole epochs resolved first by a full-occupancy pass on an internal
  * low-priority stream, the updates then replaying them on a high-priority stream,
  * double-buffered so the next epochs' draws overlap the current updates; the work
- * is joined back into `stream`.  Both forms draw identical steps. */
+ * is joined back into `stream`.  Both forms draw identical steps.
+ * DRG_SAMPLED_DETERMINISTIC (the reference's threads = 1 contract): each
+ * epoch runs as sub-batches of max_threads consecutive steps that read the positions
+ * frozen at the sub-batch start and sum their increments in 64-bit fixed point
+ * (integer atomics), folded into y after the sub-batch -- bitwise reproducible.
+ * n_y: nodes of y (<= 0: n).  evals (device uint64, may be NULL) accumulates the
+ * distance evaluations of the reference's counter (_kernels.py:86, 122): steps with
+ * i != j plus negatives that found a target. */
 #define DRG_SAMPLED_AGGREGATE 1
 #define DRG_SAMPLED_FUSED 2
+#define DRG_SAMPLED_DETERMINISTIC 4
 
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,
                        const uint64_t *src_alias, const float *collapse,
@@ -225,7 +239,7 @@ int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_
                        int64_t n_steps, int t0,
                        int n_iter, int iters, double lr0, double gamma, double eps, double clip,
                        int b, int M, uint64_t seed, int level, int64_t max_threads,
-                       int flags, void *stream);
+                       int flags, int64_t n_y, uint64_t *evals, void *stream);
 
 /* The two halves of the split form, exposed for callers that keep the draws (and
  * for the parity tests).  drg_sampled_draws: out[(e * (2 + M) + f) * n_steps + s]
@@ -264,6 +278,58 @@ int drg_layout_radius(const float *y, int64_t n, double *out_radius, void *strea
  * (Philox Box-Muller keyed by (seed, i); jitter <= 0 copies). */
 int drg_prolong(const float *y_coarse, const int32_t *parent, int64_t n_fine, double jitter,
                 uint64_t seed, float *y_fine, void *stream);
+
+/* --- multi-GPU sampled epochs ----------------------------
+ * One process per GPU; the level's positions partitioned by node range, rank r's
+ * rows [bounds[r], bounds[r+1]) in a part buffer every peer maps through CUDA IPC
+ * (NVLink / NVSwitch).  Hogwild on that one distributed array, as the reference's
+ * workers share one pos (optimizer.py:325-345): a rank runs the steps whose source
+ * it owns; source and attraction partner are read and updated in place through
+ * the peer table; negatives are read from a replicated snapshot of the epoch-start
+ * positions and their reactions summed into a delta array, folded in at the epoch
+ * end by a reduce-scatter + all-gather (NCCL, loaded at run time).  rank = -1: one
+ * process emulates all `world` parts locally (every rank's steps in one launch).
+ * Snapshot / delta layout: node v of part r at r * pad + v - bounds[r]. */
+int drg_shard_create(int world, int rank, int64_t capacity, void **out_ctx);
+int drg_shard_destroy(void *ctx);
+int drg_shard_ipc_handle(void *ctx, uint8_t *out_handle64);
+int drg_shard_open_peer(void *ctx, int peer, const uint8_t *handle64);
+int drg_nccl_unique_id(uint8_t *out128);
+int drg_shard_nccl_init(void *ctx, const uint8_t *uid128);
+int drg_shard_level(void *ctx, int64_t n, const int64_t *bounds, float *snap, float *delta,
+                    int64_t *out_pad);
+int drg_shard_load(void *ctx, const float *y, void *stream);
+/* drg_allgather_Y of the survey: every part gathered into y (device [n][2]). */
+int drg_shard_store(void *ctx, float *y, void *stream);
+int drg_shard_exchange(void *ctx, void *stream);
+int drg_shard_fold(void *ctx, float *recv, void *stream);
+int drg_shard_read_part(void *ctx, float *out, void *stream);
+int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
+                    const float *collapse, const uint64_t *neg_alias, const int32_t *map,
+                    int64_t n_tab, const int32_t *perm, int nseg,
+                    const uint64_t *const *seg_alias, const int64_t *seg_n, const int64_t *seg_lo,
+                    const int64_t *step_lo, const int64_t *n_steps, int t, int iters, double lr0,
+                    double gamma, double eps, double clip, int b, int M, uint64_t seed, int level,
+                    int64_t max_threads, uint64_t *evals, int32_t *out_draws, void *stream);
+
+/* --- single-row / single-interaction drop-ins -----------------------------------
+ * precompute_gaussian_table (similarity.py:110-119): out[d-1] = exp(-d^2 / (2 sigma^2)),
+ * d = 1..k (device fp64; exp evaluated in double-double and rounded once). */
+int drg_gaussian_table(int k, double sigma, double *out, void *stream);
+/* search_sigma (similarity.py:167-199) for every row of a (row offsets, hop distances)
+ * CSR (device): out_sigma[r] (rows of one entry: 1.0; empty rows untouched). */
+int drg_rows_sigma(const int64_t *indptr, const int32_t *dists, int64_t nrows, double perplexity,
+                   double tol, int max_iter, double sigma_min, double sigma_max,
+                   double *out_sigma, void *stream);
+/* conditional_similarity_row (similarity.py:122-145) for every row at bandwidth
+ * sigma[r]: out_p[e] = table[d_e] / fsum(row) (math.fsum's correctly rounded sum),
+ * uniform over the minimum-distance entries when every value underflows. */
+int drg_rows_conditional(const int64_t *indptr, const int32_t *dists, int64_t nrows,
+                         const double *sigma, double *out_p, void *stream);
+/* attractive_gradient (kind 0, optimizer.py:174-186) / repulsive_gradient (kind 1,
+ * 189-203) of n interactions y_i[q] -> y_j[q] (device fp64 [n][2]) into out. */
+int drg_gradients(const double *yi, const double *yj, int64_t n, int b, double gamma, double eps,
+                  double clip, int kind, double *out, void *stream);
 
 /* --- parity instruments -----------------------------
  * KL(P || Q) terms of a layout y (device fp32 [n][2]) with the unnormalised

@@ -854,6 +854,53 @@ def drawn_steps(pos, draws, lr, gamma, eps, clip, b):
     return pos
 
 
+def deferred_drawn_epoch(pos, draws, lr, gamma, eps, clip, b):
+    """The multi-GPU epoch of paper_2008_07799_b200/shard.py on given draws, as a
+    sequential fp64 restatement: the reference step (_kernels.py:82-140) with the
+    source and the attraction partner read and moved in place, each negative read
+    from the epoch-start snapshot (plus this step's own earlier reactions on it) and
+    its reaction deferred into a delta added at the epoch end."""
+    snap = pos.copy()
+    delta = np.zeros_like(pos)
+    bf = float(b)
+    M = draws.shape[0] - 2
+    for s in range(draws.shape[1]):
+        i, j = int(draws[0, s]), int(draws[1, s])
+        yi = pos[i].copy()
+        gi = np.zeros(2)
+        if i != j:
+            dx, dy = yi[0] - pos[j, 0], yi[1] - pos[j, 1]
+            ld2 = dx * dx + dy * dy
+            if ld2 > 0.0:
+                pw = ld2 ** (b - 1)
+                coef = -2.0 * bf * pw / (1.0 + pw * ld2)
+                g = np.array([min(max(coef * dx, -clip), clip),
+                              min(max(coef * dy, -clip), clip)]) * lr
+                pos[j] -= g
+                yi += g
+                gi += g
+        own = {}
+        for m in range(M):
+            t = int(draws[2 + m, s])
+            if t < 0:
+                continue
+            yc = snap[t] + own.get(t, 0.0)
+            dx, dy = yi[0] - yc[0], yi[1] - yc[1]
+            ld2 = dx * dx + dy * dy
+            if ld2 + eps > 0.0:
+                pw = ld2 ** (b - 1)
+                coef = gamma * 2.0 * bf / ((ld2 + eps) * (1.0 + pw * ld2))
+                g = np.array([min(max(coef * dx, -clip), clip),
+                              min(max(coef * dy, -clip), clip)]) * lr
+                delta[t] -= g
+                own[t] = own.get(t, 0.0) - g
+                yi += g
+                gi += g
+        pos[i] += gi
+    pos += delta
+    return pos
+
+
 def node_parallel_iteration(indptr, targets, W, V, y, neg_idx, lr, gamma, eps, clip, b):
     """One Jacobi iteration of K7 in fp64:
     y_a' = y_a + lr * (sum_b W_ab clip(g_att(y_a, y_b)) + V_a sum_m clip(g_rep(y_a, y_cm)))

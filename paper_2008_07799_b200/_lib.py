@@ -25,6 +25,9 @@ DRG_ERR_NONFINITE = -3
 DRG_ERR_UNSUPPORTED = -4
 DRG_ERR_NOMEM = -5
 DRG_FLAG_INPLACE = 1
+DRG_SAMPLED_AGGREGATE = 1
+DRG_SAMPLED_FUSED = 2
+DRG_SAMPLED_DETERMINISTIC = 4
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -40,6 +43,25 @@ SIGNATURES = {
     "drg_launch_count": [],
     "drg_khop_count": [_P, _P, _I64, _I32, _I64, _P, _P, _P],
     "drg_khop_fill": [_P, _P, _I64, _I32, _I64, _P, _P, _P, _P],
+    "drg_gaussian_table": [_I32, _F64, _P, _P],
+    "drg_rows_sigma": [_P, _P, _I64, _F64, _F64, _I32, _F64, _F64, _P, _P],
+    "drg_rows_conditional": [_P, _P, _I64, _P, _P, _P],
+    "drg_gradients": [_P, _P, _I64, _I32, _F64, _F64, _F64, _I32, _P, _P],
+    "drg_shard_create": [_I32, _I32, _I64, _P],
+    "drg_shard_destroy": [_P],
+    "drg_shard_ipc_handle": [_P, _P],
+    "drg_shard_open_peer": [_P, _I32, _P],
+    "drg_nccl_unique_id": [_P],
+    "drg_shard_nccl_init": [_P, _P],
+    "drg_shard_level": [_P, _I64, _P, _P, _P, _P],
+    "drg_shard_load": [_P, _P, _P],
+    "drg_shard_store": [_P, _P, _P],
+    "drg_shard_exchange": [_P, _P],
+    "drg_shard_fold": [_P, _P, _P],
+    "drg_shard_read_part": [_P, _P, _P],
+    "drg_shard_epoch": [_P, _P, _P, _P, _P, _P, _I64, _P, _I32, _P, _P, _P, _P, _P, _I32, _I32,
+                        _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _P, _P, _P],
+    "drg_khop_source": [_P, _P, _I64, _I32, _I64, _P, _P, _I64, _P, _P],
     "drg_similarity": [_P, _P, _P, _I64, _I64, _I32, _F64, _F64, _I32, _F64, _F64, _P, _P, _P,
                        _P, _P, _P],
     "drg_similarity_union": [_P, _P, _P, _I64, _I64, _I32, _F64, _F64, _I32, _F64, _F64, _P, _P,
@@ -56,7 +78,8 @@ SIGNATURES = {
                          _F64, _F64, _I32, _I32, _U64, _I32, _P, _P, _P, _U32, _P],
     "drg_row_alias": [_P, _P, _P, _I64, _I64, _P, _P, _P],
     "drg_layout_sampled": [_P, _P, _P, _P, _P, _P, _P, _I64, _P, _I64, _I64, _I32, _I32, _I32,
-                           _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _I32, _P],
+                           _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _I32, _I64, _P,
+                           _P],
     "drg_sampled_draws": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _U64, _I32,
                           _P, _P],
     "drg_sampled_apply": [_P, _I64, _P, _F64, _F64, _F64, _F64, _I32, _I32, _I64, _I32, _P],

@@ -167,7 +167,7 @@ __global__ void iota_kernel(int32_t *out, int64_t n) {
 }
 
 inline unsigned flat_grid(int64_t n, int threads = 256) {
-    return (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n, threads), 1), kSMs * 32);
+    return (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n, threads), 1), sm_count() * 32);
 }
 
 inline int bits_for(uint64_t v) {
@@ -262,7 +262,7 @@ extern "C" int drg_coarsen(const int64_t *indptr, const int32_t *indices, int64_
     unsigned long long *d_und = ctr.as<unsigned long long>();
     rank_kernel<<<flat_grid(n), 256, 0, st>>>(order, n, rank.as<int32_t>(), d_bad);
     DRG_LAUNCHED("rank_kernel");
-    const unsigned wg = (unsigned)std::min<int64_t>(ceil_div(n, kWpb), kSMs * 64);
+    const unsigned wg = (unsigned)std::min<int64_t>(ceil_div(n, kWpb), sm_count() * 64);
     int rounds = 0;
     for (;;) {
         DRG_CUDA(cudaMemsetAsync(d_und, 0, sizeof(unsigned long long), st));
@@ -318,7 +318,7 @@ extern "C" int drg_coarse_graph(const int64_t *indptr, const int32_t *indices, i
     }
     Scratch keys(st);
     DRG_CUDA(keys.alloc(sizeof(uint64_t) * (size_t)nnz));
-    const unsigned wg = (unsigned)std::min<int64_t>(ceil_div(n, kWpb), kSMs * 64);
+    const unsigned wg = (unsigned)std::min<int64_t>(ceil_div(n, kWpb), sm_count() * 64);
     pair_keys_kernel<double><<<wg, kWpb * 32, 0, st>>>(indptr, indices, nullptr, n, parent,
                                                        n_coarse, keys.as<uint64_t>(), nullptr);
     DRG_LAUNCHED("pair_keys_kernel");
@@ -355,7 +355,7 @@ extern "C" int drg_aggregate_pairs(const int64_t *indptr, const int32_t *targets
     Scratch keys(st), vals(st);
     DRG_CUDA(keys.alloc(sizeof(uint64_t) * (size_t)nnz));
     DRG_CUDA(vals.alloc(sizeof(double) * (size_t)nnz));
-    const unsigned wg = (unsigned)std::min<int64_t>(ceil_div(n, kWpb), kSMs * 64);
+    const unsigned wg = (unsigned)std::min<int64_t>(ceil_div(n, kWpb), sm_count() * 64);
     pair_keys_kernel<double><<<wg, kWpb * 32, 0, st>>>(indptr, targets, weights, n, parent,
                                                        n_coarse, keys.as<uint64_t>(),
                                                        vals.as<double>());

@@ -17,7 +17,6 @@ int cuda_fail(cudaError_t e, const char *what);
 
 constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 

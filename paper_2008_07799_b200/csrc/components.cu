@@ -120,7 +120,7 @@ extern "C" int drg_components(const int64_t *indptr, const int32_t *indices, int
     DRG_CUDA(parent.alloc(sizeof(int32_t) * (size_t)n));
     DRG_CUDA(cnt.alloc(sizeof(unsigned long long)));
     DRG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), st));
-    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 256), kSMs * 32);
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 256), sm_count() * 32);
     cc_init_kernel<<<g, 256, 0, st>>>(parent.as<int32_t>(), n);
     DRG_LAUNCHED("cc_init_kernel");
     Scratch lst(st), nl(st);
@@ -130,7 +130,7 @@ extern "C" int drg_components(const int64_t *indptr, const int32_t *indices, int
     cc_hook_kernel<<<g, 256, 0, st>>>(indptr, indices, n, parent.as<int32_t>(),
                                       lst.as<int32_t>(), nl.as<int>());
     DRG_LAUNCHED("cc_hook_kernel");
-    cc_hook_long_kernel<<<kSMs * 4, 256, 0, st>>>(indptr, indices, lst.as<int32_t>(),
+    cc_hook_long_kernel<<<sm_count() * 4, 256, 0, st>>>(indptr, indices, lst.as<int32_t>(),
                                                   nl.as<int>(), parent.as<int32_t>());
     DRG_LAUNCHED("cc_hook_long_kernel");
     cc_count_kernel<<<g, 256, 0, st>>>(parent.as<int32_t>(), n, cnt.as<unsigned long long>());

@@ -316,7 +316,7 @@ __global__ void lower_bound_kernel(int64_t *ids, int64_t m, const int64_t *sorte
 }
 
 unsigned grid_for(int64_t items, int block = 256) {
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, block), kSMs * 32));
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, block), sm_count() * 32));
 }
 
 }  // namespace

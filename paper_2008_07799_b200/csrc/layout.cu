@@ -662,7 +662,7 @@ __global__ void prolong_kernel(const float2 *__restrict__ yc, const int32_t *__r
 }
 
 inline unsigned flat_grid(int64_t n, int threads = 256) {
-    return (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n, threads), 1), kSMs * 32);
+    return (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n, threads), 1), sm_count() * 32);
 }
 
 }  // namespace
@@ -989,7 +989,7 @@ extern "C" int drg_alias_build(const double *weights, int64_t n, uint64_t *out_t
     DRG_CUDA(cudaStreamSynchronize(st));
     if (!(total > 0.0)) return fail(DRG_ERR_INVALID, "all weights are zero");
     if (out_total) *out_total = total;
-    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 256), kSMs * 16);
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n, 256), sm_count() * 16);
     alias_norm_kernel<<<g, 256, 0, st>>>(weights, n, tot.as<double>(), wn.as<double>(),
                                          lf.as<uint8_t>(), hf.as<uint8_t>(), bad.as<int>());
     DRG_LAUNCHED("alias_norm_kernel");

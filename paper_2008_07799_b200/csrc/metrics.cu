@@ -129,14 +129,14 @@ extern "C" int drg_kl_terms(const int64_t *indptr, const int32_t *targets, const
     DRG_CUDA(cudaMemsetAsync(acc.p, 0, 4 * sizeof(double), st));
     double *d = acc.as<double>();
     const float2 *yy = reinterpret_cast<const float2 *>(y);
-    p_terms_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n * 32, kThreads), kSMs * 16), kThreads,
+    p_terms_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n * 32, kThreads), sm_count() * 16), kThreads,
                      0, st>>>(indptr, targets, P, yy, n, b, d);
     DRG_LAUNCHED("p_terms_kernel");
     if (z_pairs <= 0) {
         z_exact_kernel<<<(unsigned)ceil_div(n, kThreads), kThreads, 0, st>>>(yy, n, b, d + 3);
         DRG_LAUNCHED("z_exact_kernel");
     } else {
-        z_mc_kernel<<<(unsigned)std::min<int64_t>(ceil_div(z_pairs, kThreads), kSMs * 32), kThreads,
+        z_mc_kernel<<<(unsigned)std::min<int64_t>(ceil_div(z_pairs, kThreads), sm_count() * 32), kThreads,
                       0, st>>>(yy, n, b, z_pairs, (uint32_t)seed, (uint32_t)(seed >> 32), d + 3);
         DRG_LAUNCHED("z_mc_kernel");
     }
@@ -484,7 +484,7 @@ extern "C" int drg_neighborhood_preservation(const float *y, int64_t n,
     DRG_CUDA(bb.alloc(16));
     const unsigned init[4] = {0xffffffffu, 0xffffffffu, 0u, 0u};
     DRG_CUDA(cudaMemcpyAsync(bb.p, init, 16, cudaMemcpyHostToDevice, st));
-    bbox_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), kSMs * 8), 256, 0, st>>>(
+    bbox_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), sm_count() * 8), 256, 0, st>>>(
         yy, n, bb.as<float>());
     DRG_LAUNCHED("bbox_kernel");
     unsigned hb[4];
@@ -503,7 +503,7 @@ extern "C" int drg_neighborhood_preservation(const float *y, int64_t n,
     DRG_CUDA(counts.alloc(sizeof(int32_t) * (size_t)(ncell + 1)));
     DRG_CUDA(start.alloc(sizeof(int32_t) * (size_t)(ncell + 1)));
     DRG_CUDA(cudaMemsetAsync(counts.p, 0, sizeof(int32_t) * (size_t)(ncell + 1), st));
-    const unsigned fg = (unsigned)std::min<int64_t>(ceil_div(n, 256), kSMs * 16);
+    const unsigned fg = (unsigned)std::min<int64_t>(ceil_div(n, 256), sm_count() * 16);
     cell_kernel<<<fg, 256, 0, st>>>(yy, n, x0, y0, cs, gx, gy, cell_of.as<int32_t>(),
                                     counts.as<int32_t>());
     DRG_LAUNCHED("cell_kernel");
@@ -528,7 +528,7 @@ extern "C" int drg_neighborhood_preservation(const float *y, int64_t n,
     DRG_CUDA(big.alloc(sizeof(int32_t) * (size_t)std::max<int64_t>(nq, 1)));
     DRG_CUDA(bigc.alloc(sizeof(unsigned long long)));
     DRG_CUDA(cudaMemsetAsync(bigc.p, 0, sizeof(unsigned long long), st));
-    np_warp_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nq, kNpWarps), kSMs * 64),
+    np_warp_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nq, kNpWarps), sm_count() * 64),
                      kNpWarps * 32, 0, st>>>(G, yy, n, hop_indptr, hop_ids, queries, nq,
                                              out_score, big.as<int32_t>(),
                                              bigc.as<unsigned long long>());
@@ -540,7 +540,7 @@ extern "C" int drg_neighborhood_preservation(const float *y, int64_t n,
         const size_t smem = (size_t)kNpBlockCap * (8 + 4);
         DRG_CUDA(cudaFuncSetAttribute(np_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-        np_block_kernel<<<(unsigned)std::min<unsigned long long>(h_big, kSMs * 2), 256, smem, st>>>(
+        np_block_kernel<<<(unsigned)std::min<unsigned long long>(h_big, sm_count() * 2), 256, smem, st>>>(
             G, yy, n, hop_indptr, hop_ids, queries, big.as<int32_t>(), (int64_t)h_big, out_score);
         DRG_LAUNCHED("np_block_kernel");
     }

@@ -282,7 +282,7 @@ __global__ void minmax2_kernel(const double *pos, int64_t n, double *out) {
 }
 
 unsigned grid_for(int64_t items) {
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), kSMs * 32));
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), sm_count() * 32));
 }
 
 // pass 1 -> scan -> pass 2; *out_len = total bytes; out == NULL: size only

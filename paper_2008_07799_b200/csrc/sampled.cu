@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <climits>
 #include <mutex>
+#include <string.h>
+#include <dlfcn.h>
 
 #include <cub/cub.cuh>
 
@@ -46,6 +48,7 @@ struct SArgs {
     uint32_t key0, key1, level;
     int t;
     int probe;   // latency probe (DRG_SAMPLED_PROBE, tests only): 1 = no atomics, 2 = no row draw
+    unsigned long long *evals;   // optional: distance evaluations (_kernels.py:86, 122)
 };
 
 __device__ __forceinline__ float clampf(float g, float c) { return fminf(fmaxf(g, -c), c); }
@@ -167,6 +170,7 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
     const float two_b = 2.0f * (float)A.b;
     const int Me = min(A.M, kMaxNeg);
+    unsigned nev = 0;
     for (int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; sl < A.n_steps;
          sl += nthreads) {
         const int64_t s = A.step_lo + sl;
@@ -209,6 +213,7 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
         float gix = 0.f, giy = 0.f;   // the source's own increments of this step
         int64_t upd = -1;
         float ux = 0.f, uy = 0.f;
+        nev += i != j;
         if (i != j) {  // _kernels.py:82-105
             const float2 yj = ld_y(y, j);
             const float dx = yi.x - yj.x, dy = yi.y - yj.y;
@@ -251,6 +256,7 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
                 }
                 int64_t tu;
                 float tx, ty;
+                nev += target >= 0;
                 repel(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix,
                       giy);
                 at[m] = (int32_t)tu;
@@ -273,12 +279,18 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
             }
             int64_t tu;
             float tx, ty;
+            nev += target >= 0;
             repel(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
             add_y_w<AGG>(y, tu, tx, ty, A.probe);
         }
         // the source's own increments of the step, published once (the step sees
         // them locally in sequence, as the reference kernel does)
         add_y_w<AGG>(y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy, A.probe);
+    }
+    if (A.evals) {
+        const unsigned act = __activemask();
+        nev = __reduce_add_sync(act, nev);
+        if ((threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(A.evals, (unsigned long long)nev);
     }
 }
 
@@ -309,6 +321,12 @@ struct DArgs {
     int t_first;
     int probe;
     int32_t *out;
+    unsigned long long *evals;   // optional: distance evaluations (_kernels.py:86, 122)
+    // source segment (multi-GPU: the sources a rank owns): the source alias table is
+    // over n_src items; item q is node src_perm[src_lo + q] (src_perm NULL: src_lo + q)
+    int64_t n_src, src_lo;
+    const int32_t *src_perm;
+    int64_t out_stride;   // field stride of out (>= n_steps; ranks' slices of one buffer)
 };
 
 // small blocks: they fit beside the update pass's resident blocks
@@ -328,7 +346,7 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
                                   A.key0, A.key1);
     const u32x4 r2 = philox4x32<7>(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xfe00u, 0x3c6ef372u},
                                    A.key0, A.key1);
-    const int64_t sb = bucket(A.n, r.x, r.y);
+    const int64_t sb = bucket(A.n_src, r.x, r.y);
     const uint2 srec = __ldg(A.src_alias + sb);
     const int Me = min(A.M, kMaxNeg);
     int32_t cand[kMaxNeg];
@@ -341,6 +359,7 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
         }
     }
     int64_t i = accept(srec, sb, r.z);
+    i = A.src_perm ? (int64_t)__ldg(A.src_perm + A.src_lo + i) : A.src_lo + i;
     const int64_t lo = __ldg(A.indptr + i), hi = __ldg(A.indptr + i + 1);
     const float cprob = A.collapse ? __ldg(A.collapse + i) : 0.0f;   // NULL: none
     int64_t j = i;
@@ -359,9 +378,10 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
         for (int m = 0; m < kMaxNeg; ++m)
             if (m < Me) cand[m] = __ldg(A.map + cand[m]);
     }
-    int32_t *o = A.out + ep * (int64_t)(2 + A.M) * A.n_steps + sl;
+    int32_t *o = A.out + ep * (int64_t)(2 + A.M) * A.out_stride + sl;
     __stcs(o, (int32_t)i);   // read once by the update pass: streaming stores
-    __stcs(o + A.n_steps, (int32_t)j);
+    __stcs(o + A.out_stride, (int32_t)j);
+    unsigned nev = i != j;
     for (int m = 0; m < A.M; ++m) {
         int64_t target = -1;
         int first = 0;
@@ -380,7 +400,13 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
             if (A.map) c0 = __ldg(A.map + c0);
             if (c0 != i && c0 != j) target = c0;
         }
-        __stcs(o + (int64_t)(2 + m) * A.n_steps, (int32_t)target);
+        __stcs(o + (int64_t)(2 + m) * A.out_stride, (int32_t)target);
+        nev += target >= 0;
+    }
+    if (A.evals) {   // one atomic per warp
+        const unsigned act = __activemask();
+        nev = __reduce_add_sync(act, nev);
+        if ((threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(A.evals, (unsigned long long)nev);
     }
 }
 
@@ -391,8 +417,10 @@ int launch_draws(const DArgs &D, cudaStream_t st) {
 }
 
 struct PArgs {
-    const int32_t *draws;   // one epoch of draw records
-    int64_t n_steps;
+    const int32_t *draws;   // one epoch of draw records (or a sub-batch's first step)
+    int64_t n_steps;        // steps this launch applies
+    int64_t stride;         // field stride of the draw records (the epoch's step count)
+    unsigned long long *delta;   // deterministic mode: fixed-point increments [n][2]
     float lr, gamma, eps, clip;
     int b, M;
     int probe;
@@ -402,17 +430,52 @@ struct PArgs {
 // position is carried through the step, attraction and each repulsion move the
 // other end by the opposite clipped increment; the source's own total is published
 // once.  The next step's draw record is prefetched while this step runs.
-template <bool AGG, int B>
+// Deterministic mode (threads = 1): the epoch runs as sub-batches of steps that all
+// read the positions frozen at the sub-batch start and add their increments to a
+// 64-bit fixed-point buffer (integer atomics: the sum is independent of the order),
+// which flush_kernel folds into y -- bitwise reproducible, with the same staleness
+// law as Hogwild at that many steps in flight.
+constexpr double kFixScale = 1099511627776.0;   // 2^40: |increment sum| < 2^23 per sub-batch
+
+__device__ __forceinline__ void add_fixed(unsigned long long *d, int64_t i, float dx, float dy) {
+    if (i < 0) return;
+    atomicAdd(d + 2 * i, (unsigned long long)__double2ll_rn((double)dx * kFixScale));
+    atomicAdd(d + 2 * i + 1, (unsigned long long)__double2ll_rn((double)dy * kFixScale));
+}
+
+template <bool AGG, bool DET>
+__device__ __forceinline__ void add_step(const PArgs &A, float2 *y, int64_t i, float dx,
+                                         float dy) {
+    if (DET) add_fixed(A.delta, i, dx, dy);
+    else add_y_w<AGG>(y, i, dx, dy, A.probe);
+}
+
+__global__ void flush_kernel(float2 *y, unsigned long long *d, int64_t n) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const ulonglong2 q = reinterpret_cast<ulonglong2 *>(d)[v];
+        if (q.x | q.y) {
+            float2 p = y[v];
+            p.x = (float)((double)p.x + (double)(long long)q.x * (1.0 / kFixScale));
+            p.y = (float)((double)p.y + (double)(long long)q.y * (1.0 / kFixScale));
+            y[v] = p;
+            reinterpret_cast<ulonglong2 *>(d)[v] = make_ulonglong2(0ull, 0ull);
+        }
+    }
+}
+
+template <bool AGG, int B, bool DET = false>
 __device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t sl,
                                             const int64_t nthreads) {
     const float two_b = 2.0f * (float)A.b;
     const int Me = min(A.M, kMaxNeg);
-    const int64_t ns = A.n_steps;
+    const int64_t ns = A.n_steps, sd = A.stride;
     if (sl >= ns) return;
-    int32_t ci = __ldcs(A.draws + sl), cj = __ldcs(A.draws + ns + sl);
+    int32_t ci = __ldcs(A.draws + sl), cj = __ldcs(A.draws + sd + sl);
     int32_t cc[kMaxNeg];
 #pragma unroll
-    for (int m = 0; m < kMaxNeg; ++m) cc[m] = m < Me ? __ldcs(A.draws + (2 + m) * ns + sl) : -1;
+    for (int m = 0; m < kMaxNeg; ++m) cc[m] = m < Me ? __ldcs(A.draws + (2 + m) * sd + sl) : -1;
     for (; sl < ns; sl += nthreads) {
         const int64_t i = ci, j = cj;
         int32_t cand[kMaxNeg];
@@ -422,10 +485,10 @@ __device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t s
         const int64_t nx = sl + nthreads;
         if (nx < ns) {
             ci = __ldcs(A.draws + nx);
-            cj = __ldcs(A.draws + ns + nx);
+            cj = __ldcs(A.draws + sd + nx);
 #pragma unroll
             for (int m = 0; m < kMaxNeg; ++m)
-                if (m < Me) cc[m] = __ldcs(A.draws + (2 + m) * ns + nx);
+                if (m < Me) cc[m] = __ldcs(A.draws + (2 + m) * sd + nx);
         }
         float2 yi = ld_y(y, i);
         const float2 yj = ld_y(y, j);
@@ -453,7 +516,7 @@ __device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t s
                 giy += gy;
             }
         }
-        add_y_w<AGG>(y, upd, ux, uy, A.probe);
+        add_step<AGG, DET>(A, y, upd, ux, uy);
         float ax[kMaxNeg], ay[kMaxNeg];   // this step's updates of its first negatives
 #pragma unroll
         for (int m = 0; m < kMaxNeg; ++m) {  // _kernels.py:106-140
@@ -466,18 +529,18 @@ __device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t s
                       giy);
                 ax[m] = tx;
                 ay[m] = ty;
-                add_y_w<AGG>(y, tu, tx, ty, A.probe);
+                add_step<AGG, DET>(A, y, tu, tx, ty);
             }
         }
         for (int m = Me; m < A.M; ++m) {   // negatives past kMaxNeg: gathered after the atomics
-            const int64_t target = __ldcs(A.draws + (2 + m) * ns + sl);
+            const int64_t target = __ldcs(A.draws + (2 + m) * sd + sl);
             const float2 yc = target >= 0 ? ld_y(y, target) : make_float2(0.f, 0.f);
             int64_t tu;
             float tx, ty;
             repel<B>(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
-            add_y_w<AGG>(y, tu, tx, ty, A.probe);
+            add_step<AGG, DET>(A, y, tu, tx, ty);
         }
-        add_y_w<AGG>(y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy, A.probe);
+        add_step<AGG, DET>(A, y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy);
     }
 }
 
@@ -498,6 +561,14 @@ __global__ void __launch_bounds__(256, 1) apply_kernel_lc(PArgs A, float2 *y) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     apply_epoch<AGG, B>(A, y, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
                         (int64_t)gridDim.x * blockDim.x);
+}
+
+// deterministic sub-batch: one step per thread, positions frozen for the launch
+template <int B>
+__global__ void __launch_bounds__(256) apply_det_kernel(PArgs A, float2 *y) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    apply_epoch<false, B, true>(A, y, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                                (int64_t)gridDim.x * blockDim.x);
 }
 
 constexpr int64_t kLowConcurrency = 65536;   // steps in flight below which _lc runs
@@ -529,6 +600,37 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
                                            : apply_instance<false>(P.b, threads),
                                  args));
     DRG_LAUNCHED("apply_kernel");
+    return DRG_OK;
+}
+
+// One epoch in the deterministic mode: sub-batches of `batch` consecutive steps,
+// each an apply_det_kernel (positions frozen, fixed-point increments) and a
+// flush_kernel, as programmatic dependent launches on one stream.
+int launch_det_epoch(PArgs P, float2 *y, int64_t batch, int64_t n_y, cudaStream_t st) {
+    const int64_t total = P.n_steps;
+    const int32_t *base = P.draws;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    for (int64_t lo = 0; lo < total; lo += batch) {
+        P.draws = base + lo;
+        P.n_steps = std::min(batch, total - lo);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)ceil_div(P.n_steps, 256));
+        cfg.blockDim = dim3(256);
+        cfg.stream = st;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        void *args[] = {&P, &y};
+        DRG_CUDA(cudaLaunchKernelExC(&cfg, P.b == 2 ? (void *)apply_det_kernel<2>
+                                                    : (void *)apply_det_kernel<0>, args));
+        DRG_LAUNCHED("apply_det_kernel");
+        cfg.gridDim = dim3((unsigned)std::min<int64_t>(ceil_div(n_y, 256), sm_count() * 8));
+        unsigned long long *d = P.delta;
+        void *fargs[] = {&y, &d, &n_y};
+        DRG_CUDA(cudaLaunchKernelExC(&cfg, (void *)flush_kernel, fargs));
+        DRG_LAUNCHED("flush_kernel");
+    }
     return DRG_OK;
 }
 
@@ -777,7 +879,7 @@ extern "C" int drg_row_alias(const int64_t *indptr, const int32_t *targets, cons
     DRG_CUDA(lst.alloc(sizeof(int64_t) * (size_t)max_long));
     DRG_CUDA(cnt.alloc(sizeof(int)));
     DRG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st));
-    const unsigned gw = (unsigned)std::min<int64_t>(ceil_div(n, kRowWarps), kSMs * 64);
+    const unsigned gw = (unsigned)std::min<int64_t>(ceil_div(n, kRowWarps), sm_count() * 64);
     row_alias_warp_kernel<<<gw, kRowWarps * 32, 0, st>>>(indptr, targets, P, n,
                                                          reinterpret_cast<uint4 *>(out_rec),
                                                          out_rowsum, lst.as<int64_t>(),
@@ -788,7 +890,7 @@ extern "C" int drg_row_alias(const int64_t *indptr, const int32_t *targets, cons
         DRG_CUDA(idx.alloc(sizeof(int32_t) * (size_t)nnz));
         DRG_CUDA(w.alloc(sizeof(double) * (size_t)nnz));
         DRG_CUDA(ds.alloc(sizeof(double) * (size_t)nnz));
-        const unsigned g = (unsigned)std::min<int64_t>(max_long, kSMs * 4);
+        const unsigned g = (unsigned)std::min<int64_t>(max_long, sm_count() * 4);
         row_alias_block_kernel<<<g, kRowBlock, 0, st>>>(indptr, targets, P, n, w.as<double>(),
                                                         ds.as<double>(), idx.as<int32_t>(),
                                                         reinterpret_cast<uint4 *>(out_rec),
@@ -879,6 +981,11 @@ extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alia
     D.t_first = t0;
     D.probe = 0;
     D.out = out;
+    D.evals = nullptr;
+    D.n_src = n;
+    D.src_lo = 0;
+    D.src_perm = nullptr;
+    D.out_stride = n_steps;
     DRG_TRY(launch_draws(D, as_stream(stream)));
     return DRG_OK;
 }
@@ -891,6 +998,8 @@ extern "C" int drg_sampled_apply(const int32_t *draws, int64_t n_steps, float *y
     PArgs P;
     P.draws = draws;
     P.n_steps = n_steps;
+    P.stride = n_steps;
+    P.delta = nullptr;
     P.lr = (float)lr;
     P.gamma = (float)gamma;
     P.eps = (float)eps;
@@ -919,8 +1028,13 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                                   int iters,
                                   double lr0, double gamma, double eps, double clip, int b, int M,
                                   uint64_t seed, int level, int64_t max_threads, int flags,
-                                  void *stream) {
+                                  int64_t n_y, uint64_t *evals, void *stream) {
     if (n <= 0 || n_steps <= 0 || n_iter <= 0) return DRG_OK;
+    if (n_y <= 0) n_y = n;
+    unsigned long long *ev_ctr = reinterpret_cast<unsigned long long *>(evals);
+    const bool det = flags & DRG_SAMPLED_DETERMINISTIC;
+    if (det && (flags & DRG_SAMPLED_FUSED))
+        return fail(DRG_ERR_INVALID, "the deterministic mode runs the split form");
     if (n >= 0x7fffffffLL) return fail(DRG_ERR_INVALID, "level exceeds 2^31 - 1 nodes");
     if (b < 1 || M < 0 || iters < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
     cudaStream_t st = as_stream(stream);
@@ -958,6 +1072,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
         A.key1 = (uint32_t)(seed >> 32);
         A.level = (uint32_t)level;
         A.probe = probe;
+        A.evals = ev_ctr;
         for (int j = 0; j < n_iter; ++j) {
             A.t = t0 + j;
             A.lr = lr_at(A.t);
@@ -996,6 +1111,11 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     D.key1 = (uint32_t)(seed >> 32);
     D.level = (uint32_t)level;
     D.probe = probe;
+    D.evals = ev_ctr;
+    D.n_src = n;
+    D.src_lo = 0;
+    D.src_perm = nullptr;
+    D.out_stride = n_steps;
     auto chunk_buf = [&](int c) { return buf.as<int32_t>() + (size_t)(c & 1) * K * (rec_bytes / 4); };
     auto draw = [&](int c) -> int {
         D.t_first = t0 + c * K;
@@ -1009,12 +1129,20 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     if (rc) return rc;
     PArgs P;
     P.n_steps = n_steps;
+    P.stride = n_steps;
+    P.delta = nullptr;
     P.gamma = (float)gamma;
     P.eps = (float)eps;
     P.clip = (float)clip;
     P.b = b;
     P.M = M;
     P.probe = probe;
+    Scratch delta(st);
+    if (det) {   // fixed-point increments of a sub-batch, zero between sub-batches
+        DRG_CUDA(delta.alloc(sizeof(unsigned long long) * 2 * (size_t)n_y));
+        DRG_CUDA(cudaMemsetAsync(delta.p, 0, sizeof(unsigned long long) * 2 * (size_t)n_y, st));
+        P.delta = delta.as<unsigned long long>();
+    }
     for (int c = 0; c < nchunks; ++c) {
         if (c + 1 < nchunks) {
             if (c >= 1) DRG_CUDA(cudaStreamWaitEvent(ss.lo, ev.e[3 + ((c + 1) & 1)], 0));
@@ -1026,6 +1154,10 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
             const int t = t0 + c * K + e;
             P.lr = lr_at(t);
             P.draws = chunk_buf(c) + (size_t)e * (rec_bytes / 4);
+            if (det) {
+                DRG_TRY(launch_det_epoch(P, reinterpret_cast<float2 *>(y), threads, n_y, ss.hi));
+                continue;
+            }
             DRG_TRY(launch_apply(P, reinterpret_cast<float2 *>(y), grid, block, agg, ss.hi));
         }
         DRG_CUDA(cudaEventRecord(ev.e[3 + (c & 1)], ss.hi));
@@ -1034,5 +1166,518 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     DRG_CUDA(cudaStreamWaitEvent(st, ev.e[5], 0));
     DRG_CUDA(cudaEventRecord(ev.e[0], ss.hi));
     DRG_CUDA(cudaStreamWaitEvent(st, ev.e[0], 0));
+    return DRG_OK;
+}
+
+// =============================================================================
+// Multi-GPU sampled epochs: one process per GPU, the level's
+// positions partitioned by node range -- rank r owns rows [lo_r, hi_r) in a buffer
+// every peer maps (CUDA IPC over NVLink / NVSwitch) -- and Hogwild on that ONE
+// distributed array, as the reference's worker threads share one pos
+// (optimizer.py:325-345):
+//   * a rank runs the steps whose source it owns (sources drawn from its segment
+//     of the level-0 nodes; n_l R(segment) / R steps per epoch);
+//   * the source and the attraction partner are read and updated in place through
+//     the peer table (a cut edge's partner is a remote load / remote atomics);
+//   * a negative is read from the rank's replicated snapshot of the epoch-start
+//     positions and its reaction summed into a delta array; at the epoch end one
+//     reduce-scatter of the deltas and one all-gather of the parts (NCCL over
+//     NVLink) fold the reactions in and refresh every snapshot.
+// Only the negatives (weak, long-range repulsion) see epoch-start positions; the
+// law of a step is otherwise the reference's.  One GPU emulates W ranks with all
+// W parts local and every rank's steps in ONE apply launch (no rank ever waits on
+// another), which is also the fidelity emulation of any W.
+// Snapshot and delta use a padded layout: node v of part r at r * pad + v - lo_r.
+// =============================================================================
+namespace drg {
+namespace {
+
+constexpr int kMaxParts = 8;
+
+struct ShardView {
+    float2 *part[kMaxParts];
+    int64_t lo[kMaxParts + 1];
+    int64_t pad;
+    int nparts;
+    int self;               // the caller's part; -1: every part is local (emulation)
+    const float2 *snap;     // [nparts * pad]
+    float2 *delta;          // [nparts * pad]
+};
+
+__device__ __forceinline__ int owner_of(const ShardView &V, int64_t v) {
+    int r = 0;
+#pragma unroll
+    for (int q = 1; q < kMaxParts; ++q) r += (q < V.nparts && v >= V.lo[q]);
+    return r;
+}
+
+__device__ __forceinline__ int64_t padded(const ShardView &V, int64_t v) {
+    const int r = owner_of(V, v);
+    return r * V.pad + (v - V.lo[r]);
+}
+
+__device__ __forceinline__ float2 *addr_of(const ShardView &V, int64_t v, bool &remote) {
+    const int r = owner_of(V, v);
+    remote = V.self >= 0 && r != V.self;
+    return V.part[r] + (v - V.lo[r]);
+}
+
+// remote: two scalar float reductions (always supported on peer memory over
+// NVLink); local: one float2 reduction
+__device__ __forceinline__ void add_at(float2 *p, bool remote, float dx, float dy) {
+    if (remote) {
+        atomicAdd(&p->x, dx);
+        atomicAdd(&p->y, dy);
+    } else {
+        atomicAdd(p, make_float2(dx, dy));
+    }
+}
+
+template <int B>
+__device__ __forceinline__ void apply_shard_epoch(const PArgs &A, const ShardView &V, int64_t sl,
+                                                  const int64_t nthreads) {
+    const float two_b = 2.0f * (float)A.b;
+    const int Me = min(A.M, kMaxNeg);
+    const int64_t ns = A.n_steps, sd = A.stride;
+    for (; sl < ns; sl += nthreads) {
+        const int64_t i = __ldcs(A.draws + sl), j = __ldcs(A.draws + sd + sl);
+        int32_t cand[kMaxNeg];
+#pragma unroll
+        for (int m = 0; m < kMaxNeg; ++m) cand[m] = m < Me ? __ldcs(A.draws + (2 + m) * sd + sl) : -1;
+        bool ri, rj;
+        float2 *pi = addr_of(V, i, ri);
+        float2 *pj = addr_of(V, j, rj);
+        float2 yi = __ldcg(pi);
+        const float2 yj = __ldcg(pj);
+        float2 ycand[kMaxNeg];
+#pragma unroll
+        for (int m = 0; m < kMaxNeg; ++m)
+            ycand[m] = (m < Me && cand[m] >= 0) ? __ldcg(V.snap + padded(V, cand[m]))
+                                                : make_float2(0.f, 0.f);
+        float gix = 0.f, giy = 0.f;
+        if (i != j) {  // _kernels.py:82-105
+            const float dx = yi.x - yj.x, dy = yi.y - yj.y;
+            const float ld2 = dx * dx + dy * dy;
+            if (ld2 > 0.f) {
+                const float pw = ipow_b<B>(ld2, A.b - 1);
+                const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
+                const float gx = A.lr * clampf(coef * dx, A.clip);
+                const float gy = A.lr * clampf(coef * dy, A.clip);
+                add_at(pj, rj, -gx, -gy);
+                yi.x += gx;
+                yi.y += gy;
+                gix += gx;
+                giy += gy;
+            }
+        }
+        float ax[kMaxNeg], ay[kMaxNeg];
+#pragma unroll
+        for (int m = 0; m < kMaxNeg; ++m) {  // _kernels.py:106-140, reactions deferred
+            if (m < Me) {
+                float2 yc = ycand[m];
+                own_updates(yc, cand[m], m, cand, ax, ay);
+                int64_t tu;
+                float tx, ty;
+                repel<B>(yi, yc, cand[m], A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix,
+                         giy);
+                ax[m] = tx;
+                ay[m] = ty;
+                if (tu >= 0) atomicAdd(V.delta + padded(V, tu), make_float2(tx, ty));
+            }
+        }
+        for (int m = Me; m < A.M; ++m) {
+            const int64_t target = __ldcs(A.draws + (2 + m) * sd + sl);
+            const float2 yc = target >= 0 ? __ldcg(V.snap + padded(V, target)) : make_float2(0.f, 0.f);
+            int64_t tu;
+            float tx, ty;
+            repel<B>(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
+            if (tu >= 0) atomicAdd(V.delta + padded(V, tu), make_float2(tx, ty));
+        }
+        if (gix != 0.f || giy != 0.f) add_at(pi, ri, gix, giy);
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(256) apply_shard_kernel(PArgs A, ShardView V) {
+    apply_shard_epoch<B>(A, V, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                         (int64_t)gridDim.x * blockDim.x);
+}
+
+// part[r][q] += src[r * pad + q] for q < cnt_r (atomics: peers may be updating the
+// part at the same time); src zeroed when `clear`
+__global__ void fold_kernel(ShardView V, int r0, int r1, float2 *src, int64_t src_base, int clear) {
+    for (int r = r0; r < r1; ++r) {
+        const int64_t cnt = V.lo[r + 1] - V.lo[r];
+        for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt;
+             q += (int64_t)gridDim.x * blockDim.x) {
+            float2 *s = src + (r - src_base) * V.pad + q;
+            const float2 d = *s;
+            if (d.x != 0.f || d.y != 0.f) {
+                atomicAdd(V.part[r] + q, d);
+                if (clear) *s = make_float2(0.f, 0.f);
+            }
+        }
+    }
+}
+
+// padded snapshot of the local parts (emulation) / of a full array
+__global__ void snap_parts_kernel(ShardView V, float2 *snap) {
+    for (int r = 0; r < V.nparts; ++r) {
+        const int64_t cnt = V.lo[r + 1] - V.lo[r];
+        for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < cnt;
+             q += (int64_t)gridDim.x * blockDim.x)
+            snap[r * V.pad + q] = __ldcg(V.part[r] + q);
+    }
+}
+
+// full y -> local parts (r0..r1) and the padded snapshot; or padded -> full y
+__global__ void load_parts_kernel(ShardView V, int r0, int r1, const float2 *y, float2 *snap) {
+    const int64_t n = V.lo[V.nparts];
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int r = owner_of(V, v);
+        const float2 p = y[v];
+        snap[r * V.pad + v - V.lo[r]] = p;
+        if (r >= r0 && r < r1) V.part[r][v - V.lo[r]] = p;
+    }
+}
+
+__global__ void unpad_kernel(ShardView V, const float2 *padded_y, float2 *y) {
+    const int64_t n = V.lo[V.nparts];
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        y[v] = padded_y[padded(V, v)];
+}
+
+// ---- NCCL, loaded at run time (torch's libnccl.so.2; no link-time dependency) --
+typedef int nccl_result_t;
+typedef void *nccl_comm_t;
+struct NcclUid {
+    char internal[128];
+};
+struct Nccl {
+    nccl_result_t (*get_unique_id)(NcclUid *) = nullptr;
+    nccl_result_t (*comm_init_rank)(nccl_comm_t *, int, NcclUid, int) = nullptr;
+    nccl_result_t (*comm_destroy)(nccl_comm_t) = nullptr;
+    nccl_result_t (*all_gather)(const void *, void *, size_t, int, nccl_comm_t, cudaStream_t) = nullptr;
+    nccl_result_t (*reduce_scatter)(const void *, void *, size_t, int, int, nccl_comm_t,
+                                    cudaStream_t) = nullptr;
+    const char *(*error_string)(nccl_result_t) = nullptr;
+    bool ok = false;
+};
+constexpr int kNcclFloat32 = 7, kNcclSum = 0;
+
+const Nccl &nccl() {
+    static Nccl N;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        N.get_unique_id = (decltype(N.get_unique_id))dlsym(h, "ncclGetUniqueId");
+        N.comm_init_rank = (decltype(N.comm_init_rank))dlsym(h, "ncclCommInitRank");
+        N.comm_destroy = (decltype(N.comm_destroy))dlsym(h, "ncclCommDestroy");
+        N.all_gather = (decltype(N.all_gather))dlsym(h, "ncclAllGather");
+        N.reduce_scatter = (decltype(N.reduce_scatter))dlsym(h, "ncclReduceScatter");
+        N.error_string = (decltype(N.error_string))dlsym(h, "ncclGetErrorString");
+        N.ok = N.get_unique_id && N.comm_init_rank && N.comm_destroy && N.all_gather &&
+               N.reduce_scatter && N.error_string;
+    });
+    return N;
+}
+
+#define DRG_NCCL(call)                                                                  \
+    do {                                                                                \
+        nccl_result_t _r = (call);                                                      \
+        if (_r != 0) return fail(DRG_ERR_CUDA, "%s: %s", #call, nccl().error_string(_r)); \
+    } while (0)
+
+}  // namespace
+
+// The communication context behind drg_shard_* (SURVEY §8(b) item 7).
+struct ShardCtx {
+    int world = 1, rank = 0;       // rank -1: one process emulates all `world` parts
+    int64_t capacity = 0;          // nodes per part buffer
+    float2 *own[kMaxParts] = {};   // cudaMalloc'd part buffers of this process
+    float2 *peer[kMaxParts] = {};  // opened IPC mappings of the peers' buffers
+    ShardView view = {};
+    nccl_comm_t comm = nullptr;
+    float2 *recv = nullptr;        // reduce-scatter landing buffer [pad]
+    int64_t recv_cap = 0;
+};
+
+}  // namespace drg
+
+extern "C" int drg_shard_create(int world, int rank, int64_t capacity, void **out_ctx) {
+    if (world < 1 || world > kMaxParts) return fail(DRG_ERR_INVALID, "world must be in [1, %d]", kMaxParts);
+    if (rank < -1 || rank >= world) return fail(DRG_ERR_INVALID, "bad rank %d", rank);
+    if (capacity < 1) return fail(DRG_ERR_INVALID, "capacity must be >= 1");
+    ShardCtx *c = new ShardCtx();
+    c->world = world;
+    c->rank = rank;
+    c->capacity = capacity;
+    const int nlocal = rank < 0 ? world : 1;
+    for (int q = 0; q < nlocal; ++q) {
+        cudaError_t e = cudaMalloc(&c->own[q], sizeof(float2) * (size_t)capacity);
+        if (e != cudaSuccess) {
+            for (int z = 0; z < q; ++z) cudaFree(c->own[z]);
+            delete c;
+            return cuda_fail(e, "cudaMalloc(part)");
+        }
+        c->view.part[rank < 0 ? q : rank] = c->own[q];
+    }
+    c->view.nparts = world;
+    c->view.self = rank;
+    *out_ctx = c;
+    return DRG_OK;
+}
+
+extern "C" int drg_shard_destroy(void *ctx) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    if (!c) return DRG_OK;
+    if (c->comm) nccl().comm_destroy(c->comm);
+    for (float2 *p : c->peer)
+        if (p) cudaIpcCloseMemHandle(p);
+    for (float2 *p : c->own)
+        if (p) cudaFree(p);
+    if (c->recv) cudaFree(c->recv);
+    delete c;
+    return DRG_OK;
+}
+
+extern "C" int drg_shard_ipc_handle(void *ctx, uint8_t *out_handle64) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    if (c->rank < 0) return fail(DRG_ERR_INVALID, "an emulated context has no peers");
+    cudaIpcMemHandle_t h;
+    DRG_CUDA(cudaIpcGetMemHandle(&h, c->own[0]));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    memcpy(out_handle64, &h, 64);
+    return DRG_OK;
+}
+
+extern "C" int drg_shard_open_peer(void *ctx, int r, const uint8_t *handle64) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    if (c->rank < 0 || r < 0 || r >= c->world || r == c->rank)
+        return fail(DRG_ERR_INVALID, "bad peer %d", r);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    void *p = nullptr;
+    DRG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->peer[r] = static_cast<float2 *>(p);
+    c->view.part[r] = c->peer[r];
+    return DRG_OK;
+}
+
+extern "C" int drg_nccl_unique_id(uint8_t *out128) {
+    if (!nccl().ok) return fail(DRG_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
+    NcclUid u;
+    DRG_NCCL(nccl().get_unique_id(&u));
+    memcpy(out128, &u, 128);
+    return DRG_OK;
+}
+
+extern "C" int drg_shard_nccl_init(void *ctx, const uint8_t *uid128) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    if (c->rank < 0) return fail(DRG_ERR_INVALID, "an emulated context has no communicator");
+    if (!nccl().ok) return fail(DRG_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
+    NcclUid u;
+    memcpy(&u, uid128, 128);
+    DRG_NCCL(nccl().comm_init_rank(&c->comm, c->world, u, c->rank));
+    return DRG_OK;
+}
+
+// Level layout: bounds[0..world] (host) partition [0, n); snap / delta are caller
+// device buffers of world * pad float2 (pad = the longest part), delta zeroed.
+extern "C" int drg_shard_level(void *ctx, int64_t n, const int64_t *bounds, float *snap,
+                               float *delta, int64_t *out_pad) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    if (bounds[0] != 0 || bounds[c->world] != n) return fail(DRG_ERR_INVALID, "bounds must span [0, n)");
+    int64_t pad = 1;
+    for (int r = 0; r < c->world; ++r) {
+        if (bounds[r + 1] < bounds[r]) return fail(DRG_ERR_INVALID, "bounds must be sorted");
+        pad = std::max<int64_t>(pad, bounds[r + 1] - bounds[r]);
+    }
+    if (pad > c->capacity) return fail(DRG_ERR_INVALID, "part of %lld nodes > capacity %lld",
+                                       (long long)pad, (long long)c->capacity);
+    for (int r = 0; r < c->world; ++r)
+        if (!c->view.part[r]) return fail(DRG_ERR_INVALID, "peer %d not opened", r);
+    for (int r = 0; r <= c->world; ++r) c->view.lo[r] = bounds[r];
+    for (int r = c->world + 1; r <= kMaxParts; ++r) c->view.lo[r] = n;
+    c->view.pad = pad;
+    c->view.snap = reinterpret_cast<const float2 *>(snap);
+    c->view.delta = reinterpret_cast<float2 *>(delta);
+    *out_pad = pad;
+    return DRG_OK;
+}
+
+namespace {
+std::pair<int, int> local_parts(const ShardCtx *c) {
+    return c->rank < 0 ? std::make_pair(0, c->world) : std::make_pair(c->rank, c->rank + 1);
+}
+unsigned shard_grid(int64_t n) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), sm_count() * 8));
+}
+}  // namespace
+
+// y (device [n][2], full level) -> this process's parts + the snapshot
+extern "C" int drg_shard_load(void *ctx, const float *y, void *stream) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    const auto lp = local_parts(c);
+    const int64_t n = c->view.lo[c->world];
+    load_parts_kernel<<<shard_grid(n), 256, 0, as_stream(stream)>>>(
+        c->view, lp.first, lp.second, reinterpret_cast<const float2 *>(y),
+        const_cast<float2 *>(c->view.snap));
+    DRG_LAUNCHED("load_parts_kernel");
+    return DRG_OK;
+}
+
+// the level's positions gathered from every part into y (device [n][2]): the
+// all-gather of the parts into the snapshot (NCCL or local), then unpadded
+extern "C" int drg_shard_store(void *ctx, float *y, void *stream) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    cudaStream_t st = as_stream(stream);
+    float2 *snap = const_cast<float2 *>(c->view.snap);
+    if (c->rank < 0 || c->world == 1) {
+        snap_parts_kernel<<<shard_grid(c->view.pad), 256, 0, st>>>(c->view, snap);
+        DRG_LAUNCHED("snap_parts_kernel");
+    } else if (c->comm) {
+        DRG_NCCL(nccl().all_gather(c->own[0], snap, (size_t)c->view.pad * 2, kNcclFloat32, c->comm, st));
+    } else {
+        return fail(DRG_ERR_INVALID, "multi-process context without a communicator: the caller "
+                                     "gathers the parts");
+    }
+    unpad_kernel<<<shard_grid(c->view.lo[c->world]), 256, 0, st>>>(c->view, snap,
+                                                                    reinterpret_cast<float2 *>(y));
+    DRG_LAUNCHED("unpad_kernel");
+    return DRG_OK;
+}
+
+// The epoch-end exchange: deltas reduced onto their owners and folded in, the
+// parts gathered into every snapshot.  Emulation: local kernels.  Multi-process
+// without a communicator: not available (the caller exchanges with
+// drg_shard_fold / drg_shard_read_part).
+extern "C" int drg_shard_exchange(void *ctx, void *stream) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    cudaStream_t st = as_stream(stream);
+    float2 *snap = const_cast<float2 *>(c->view.snap);
+    if (c->rank < 0 || c->world == 1) {
+        const auto lp = local_parts(c);
+        fold_kernel<<<shard_grid(c->view.pad), 256, 0, st>>>(c->view, lp.first, lp.second,
+                                                             c->view.delta, 0, 1);
+        DRG_LAUNCHED("fold_kernel");
+        snap_parts_kernel<<<shard_grid(c->view.pad), 256, 0, st>>>(c->view, snap);
+        DRG_LAUNCHED("snap_parts_kernel");
+        return DRG_OK;
+    }
+    if (!c->comm) return fail(DRG_ERR_INVALID, "no communicator");
+    if (c->recv_cap < c->view.pad) {
+        if (c->recv) cudaFree(c->recv);
+        c->recv = nullptr;
+        DRG_CUDA(cudaMalloc(&c->recv, sizeof(float2) * (size_t)c->view.pad));
+        c->recv_cap = c->view.pad;
+    }
+    const size_t cnt = (size_t)c->view.pad * 2;
+    DRG_NCCL(nccl().reduce_scatter(c->view.delta, c->recv, cnt, kNcclFloat32, kNcclSum, c->comm, st));
+    fold_kernel<<<shard_grid(c->view.pad), 256, 0, st>>>(c->view, c->rank, c->rank + 1, c->recv,
+                                                         c->rank, 0);
+    DRG_LAUNCHED("fold_kernel");
+    DRG_CUDA(cudaMemsetAsync(c->view.delta, 0, sizeof(float2) * (size_t)c->view.pad * c->world, st));
+    DRG_NCCL(nccl().all_gather(c->own[0], snap, cnt, kNcclFloat32, c->comm, st));
+    return DRG_OK;
+}
+
+// host-collective path (tests over gloo): fold a reduced delta slice [pad] into the
+// own part; copy the own part [pad] out
+extern "C" int drg_shard_fold(void *ctx, float *recv, void *stream) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    if (c->rank < 0) return fail(DRG_ERR_INVALID, "emulated context");
+    fold_kernel<<<shard_grid(c->view.pad), 256, 0, as_stream(stream)>>>(
+        c->view, c->rank, c->rank + 1, reinterpret_cast<float2 *>(recv), c->rank, 0);
+    DRG_LAUNCHED("fold_kernel");
+    return DRG_OK;
+}
+
+extern "C" int drg_shard_read_part(void *ctx, float *out, void *stream) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    if (c->rank < 0) return fail(DRG_ERR_INVALID, "emulated context");
+    DRG_CUDA(cudaMemcpyAsync(out, c->own[0], sizeof(float2) * (size_t)c->view.pad,
+                             cudaMemcpyDeviceToDevice, as_stream(stream)));
+    return DRG_OK;
+}
+
+// One sampled epoch t of a sharded level for the sources this process owns:
+// per segment s (one per local part) the draws of steps [step_lo[s], +n_steps[s])
+// from the segment's source table (seg_alias[s] over seg_n[s] items, node
+// perm[seg_lo[s] + q] or seg_lo[s] + q), all segments' steps then applied by one
+// launch with <= max_threads steps in flight.  No exchange (drg_shard_exchange).
+// out_draws (optional, device int32 [2 + M][total]) receives the draw records.
+extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
+                               const float *collapse, const uint64_t *neg_alias,
+                               const int32_t *map, int64_t n_tab, const int32_t *perm,
+                               int nseg, const uint64_t *const *seg_alias, const int64_t *seg_n,
+                               const int64_t *seg_lo, const int64_t *step_lo,
+                               const int64_t *n_steps, int t, int iters, double lr0,
+                               double gamma, double eps, double clip, int b, int M, uint64_t seed,
+                               int level, int64_t max_threads, uint64_t *evals,
+                               int32_t *out_draws, void *stream) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    cudaStream_t st = as_stream(stream);
+    if (M < 0 || b < 1 || iters < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
+    if (nseg < 1 || nseg > kMaxParts) return fail(DRG_ERR_INVALID, "bad segment count");
+    int64_t total = 0;
+    for (int s = 0; s < nseg; ++s) total += n_steps[s];
+    if (total == 0) return DRG_OK;
+    Scratch buf(st);
+    DRG_CUDA(buf.alloc(sizeof(int32_t) * (size_t)(2 + M) * (size_t)total));
+    DArgs D;
+    D.indptr = indptr;
+    D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
+    D.collapse = collapse;
+    D.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+    D.map = map;
+    D.n = n_tab;
+    D.n_epochs = 1;
+    D.M = M;
+    D.key0 = (uint32_t)seed;
+    D.key1 = (uint32_t)(seed >> 32);
+    D.level = (uint32_t)level;
+    D.t_first = t;
+    D.probe = 0;
+    D.evals = reinterpret_cast<unsigned long long *>(evals);
+    D.src_perm = perm;
+    D.out_stride = total;
+    int64_t off = 0;
+    for (int s = 0; s < nseg; ++s) {
+        if (n_steps[s] == 0) continue;
+        D.src_alias = reinterpret_cast<const uint2 *>(seg_alias[s]);
+        D.n_src = seg_n[s];
+        D.src_lo = seg_lo[s];
+        D.step_lo = step_lo[s];
+        D.n_steps = n_steps[s];
+        D.out = buf.as<int32_t>() + off;
+        DRG_TRY(launch_draws(D, st));
+        off += n_steps[s];
+    }
+    if (out_draws)   // the epoch's draw records, [2 + M][total] (tests)
+        DRG_CUDA(cudaMemcpyAsync(out_draws, buf.p, sizeof(int32_t) * (size_t)(2 + M) * total,
+                                 cudaMemcpyDeviceToDevice, st));
+    PArgs P;
+    P.draws = buf.as<int32_t>();
+    P.n_steps = total;
+    P.stride = total;
+    P.delta = nullptr;
+    P.lr = (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0);
+    P.gamma = (float)gamma;
+    P.eps = (float)eps;
+    P.clip = (float)clip;
+    P.b = b;
+    P.M = M;
+    P.probe = 0;
+    const int64_t threads = std::max<int64_t>(1, std::min<int64_t>(total, max_threads));
+    int block = (int)std::min<int64_t>(256, threads);
+    while (block > 32 && threads / block < 2 * (int64_t)sm_count()) block /= 2;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, threads / block);
+    if (b == 2) apply_shard_kernel<2><<<grid, block, 0, st>>>(P, c->view);
+    else apply_shard_kernel<0><<<grid, block, 0, st>>>(P, c->view);
+    DRG_LAUNCHED("apply_shard_kernel");
     return DRG_OK;
 }

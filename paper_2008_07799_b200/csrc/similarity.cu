@@ -266,7 +266,7 @@ extern "C" int drg_similarity_union(const int64_t *nd_indptr, const int32_t *nd_
     DRG_CUDA(cudaMemsetAsync(flags.p, 0, 16, st));
     int *d_maxd = flags.as<int>();
     unsigned long long *d_ne = reinterpret_cast<unsigned long long *>(flags.as<char>() + 8);
-    const unsigned wg = (unsigned)std::min<int64_t>(ceil_div(n, kWpb), kSMs * 64);
+    const unsigned wg = (unsigned)std::min<int64_t>(ceil_div(n, kWpb), sm_count() * 64);
     hist_kernel<<<wg, kWpb * 32, 0, st>>>(nd_indptr, nd_dists, n, k, hist.as<int32_t>(), d_maxd,
                                           d_ne);
     DRG_LAUNCHED("hist_kernel");
@@ -277,7 +277,7 @@ extern "C" int drg_similarity_union(const int64_t *nd_indptr, const int32_t *nd_
     memcpy(&n_ne, &h_flags[2], sizeof(n_ne));
     if (out_n_nonisolated) *out_n_nonisolated = (int64_t)n_ne;
     const int uniform = (k == 1 || h_flags[0] <= 1) ? 1 : 0;
-    sigma_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 128), kSMs * 64), 128, 0, st>>>(
+    sigma_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 128), sm_count() * 64), 128, 0, st>>>(
         hist.as<int32_t>(), n, k, uniform, perplexity, tol, max_iter, sigma_min, sigma_max,
         out_sigma, pcond.as<double>());
     DRG_LAUNCHED("sigma_kernel");
@@ -287,7 +287,7 @@ extern "C" int drg_similarity_union(const int64_t *nd_indptr, const int32_t *nd_
         return DRG_OK;
     }
     DRG_CUDA(lastkey.alloc(sizeof(uint32_t) * (size_t)n));
-    lastkey_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), kSMs * 32), 256, 0, st>>>(
+    lastkey_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), sm_count() * 32), 256, 0, st>>>(
         nd_indptr, nd_ids, nd_dists, n, lastkey.as<uint32_t>());
     DRG_LAUNCHED("lastkey_kernel");
     DRG_CUDA(keys.alloc(sizeof(uint64_t) * (size_t)(2 * nnz)));
@@ -337,7 +337,7 @@ extern "C" int drg_similarity(const int64_t *nd_indptr, const int32_t *nd_ids,
     DRG_CUDA(cudaMemsetAsync(flags.p, 0, 16, st));
     int *d_maxd = flags.as<int>();
     unsigned long long *d_ne = reinterpret_cast<unsigned long long *>(flags.as<char>() + 8);
-    const unsigned wg = (unsigned)std::min<int64_t>(ceil_div(n, kWpb), kSMs * 64);
+    const unsigned wg = (unsigned)std::min<int64_t>(ceil_div(n, kWpb), sm_count() * 64);
     hist_kernel<<<wg, kWpb * 32, 0, st>>>(nd_indptr, nd_dists, n, k, hist.as<int32_t>(), d_maxd,
                                           d_ne);
     DRG_LAUNCHED("hist_kernel");
@@ -349,7 +349,7 @@ extern "C" int drg_similarity(const int64_t *nd_indptr, const int32_t *nd_ids,
     memcpy(&n_ne, &h_flags[2], sizeof(n_ne));
     if (out_n_nonisolated) *out_n_nonisolated = (int64_t)n_ne;
     const int uniform = (k == 1 || maxd <= 1) ? 1 : 0;  // similarity.py:236-237
-    sigma_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 128), kSMs * 64), 128, 0, st>>>(
+    sigma_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 128), sm_count() * 64), 128, 0, st>>>(
         hist.as<int32_t>(), n, k, uniform, perplexity, tol, max_iter, sigma_min, sigma_max,
         out_sigma, pcond.as<double>());
     DRG_LAUNCHED("sigma_kernel");

@@ -438,6 +438,36 @@ def all_k_neighborhoods(g: Graph, k: int, with_stats: bool = False,
     return (nd, len(nd.ids)) if with_stats else nd
 
 
+def device_k_neighborhood(dg: DeviceGraph, source: int, k: int
+                          ) -> tuple[torch.Tensor, torch.Tensor]:
+    """One source's (ids, dists) row, (dist, id)-sorted: drg_khop_source (K1's
+    global-memory tier on one source)."""
+    n = dg.node_count
+    cnt = _lib.out_i64()
+    st = _lib.stream_ptr()
+    _lib.call("drg_khop_source", _lib.ptr(dg.indptr), _lib.ptr(dg.indices), n, k, int(source),
+              None, None, 0, _lib.byref(cnt), st)
+    m = cnt.value
+    ids = torch.empty(max(m, 1), dtype=torch.int32, device=dg.indptr.device)
+    dists = torch.empty(max(m, 1), dtype=torch.int32, device=dg.indptr.device)
+    if m:
+        _lib.call("drg_khop_source", _lib.ptr(dg.indptr), _lib.ptr(dg.indices), n, k, int(source),
+                  _lib.ptr(ids), _lib.ptr(dists), m, _lib.byref(cnt), st)
+    return ids[:m], dists[:m]
+
+
+def bfs_k_neighborhood(g: Graph, source: int, k: int) -> list[tuple[int, int]]:
+    """All nodes within k hops of ``source`` with their exact hop distance, sorted by
+    (distance, id), the source excluded (graph.py:280-305), on the device."""
+    if not 0 <= source < g.node_count:
+        raise ValueError(f"source {source} out of range for {g.node_count} nodes")
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    _lib.load()
+    ids, dists = device_k_neighborhood(DeviceGraph.from_host(g), source, k)
+    return [(int(i), int(d)) for i, d in zip(ids.cpu().tolist(), dists.cpu().tolist())]
+
+
 def device_components(dg: DeviceGraph, labels: bool = False):
     n = dg.node_count
     out = torch.empty(max(n, 1), dtype=torch.int32, device=dg.indptr.device) if labels else None

@@ -22,7 +22,9 @@ smaller levels run replicated (identical on every rank, no traffic).
 from __future__ import annotations
 
 import concurrent.futures
+import ctypes
 import logging
+import math
 from dataclasses import dataclass, field
 from typing import Callable
 
@@ -71,7 +73,12 @@ class OptimizerParams:
     * "inplace": the gather with in-place (Hogwild) updates.
     * "sgather": the gather with S sampled attraction partners (fast, lower NP).
 
-    ``threads`` is accepted and ignored (the GPU replaces the Hogwild threads)."""
+    ``threads`` keeps the reference's contract (optimizer.py:325-345):
+    threads = 1 (the default) is bitwise deterministic for a fixed seed -- the
+    sampled epochs run as sub-batches of concurrent steps over positions frozen at
+    the sub-batch start with fixed-point (order-independent) increments
+    (DRG_SAMPLED_DETERMINISTIC); threads > 1 runs them Hogwild, like the reference's
+    worker threads: faster, run-to-run nondeterministic."""
 
     neg_samples: int = 5
     gamma: float = 0.1
@@ -100,6 +107,10 @@ class OptimizerParams:
     hub_levels: str = "sampled"
     sampled_fused: bool = False    # update="sampled": draw inline (one kernel per epoch)
                                    # instead of the split draw pass + update pass
+    # update="sampled": run levels of >= shard_min_nodes nodes as this many ranks
+    # emulated on one GPU (the multi-GPU path of shard.py, all parts local) -- the
+    # fidelity emulation of a multi-GPU run; 0 = off
+    virtual_ranks: int = 0
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
@@ -119,6 +130,8 @@ class OptimizerParams:
         for c in (self.sampled_concurrency, self.sampled_concurrency_coarse):
             if c is not None and c < 1:
                 raise ValueError("sampled concurrency divisors must be >= 1")
+        if not 0 <= self.virtual_ranks <= 8:
+            raise ValueError("virtual_ranks must be in [0, 8]")
         if self.init not in ("normal", "uniform"):
             raise ValueError("init must be 'normal' or 'uniform'")
         if self.update not in ("jacobi", "inplace", "sampled", "sgather"):
@@ -147,6 +160,43 @@ class AliasTable:
     def __len__(self) -> int:
         return len(self.prob)
 
+    # host-side draws from a built table, with the caller's numpy generator (the
+    # reference's own sampling helpers, optimizer.py:96-108)
+    def sample(self, rng: np.random.Generator) -> int:
+        u = rng.random(2)
+        idx = min(int(u[0] * len(self.prob)), len(self.prob) - 1)
+        return idx if u[1] < self.prob[idx] else int(self.alias[idx])
+
+    def sample_many(self, rng: np.random.Generator, size: int) -> np.ndarray:
+        idx = np.minimum((rng.random(size) * len(self.prob)).astype(np.int64),
+                         len(self.prob) - 1)
+        coin = rng.random(size)
+        out = idx.copy()
+        take = coin >= self.prob[idx]
+        out[take] = self.alias[idx[take]]
+        return out
+
+
+@dataclass(frozen=True)
+class PositiveSampler:
+    """Alias table over the canonical pairs (i < j) of P plus a direction coin
+    (optimizer.py:206-229): (i, j) lands with probability P_ij / total."""
+
+    table: AliasTable
+    lo: np.ndarray  # int32
+    hi: np.ndarray  # int32
+
+    def sample(self, rng: np.random.Generator) -> tuple[int, int]:
+        e = self.table.sample(rng)
+        if rng.random() < 0.5:
+            return int(self.lo[e]), int(self.hi[e])
+        return int(self.hi[e]), int(self.lo[e])
+
+    def sample_many(self, rng: np.random.Generator, size: int):
+        e = self.table.sample_many(rng, size)
+        flip = rng.random(size) >= 0.5
+        return (np.where(flip, self.hi[e], self.lo[e]), np.where(flip, self.lo[e], self.hi[e]))
+
 
 def _alias_device(w: torch.Tensor) -> tuple[torch.Tensor, float]:
     n = w.numel()
@@ -168,6 +218,10 @@ def build_alias_table(weights) -> AliasTable:
     w = np.asarray(weights, dtype=np.float64)
     if len(w) == 0:
         raise ValueError("cannot build an alias table over zero items")
+    if w.min() < 0:
+        raise ValueError("negative weight")
+    if not float(w.sum()) > 0:
+        raise ValueError("all weights are zero")
     _lib.load()
     table, total = _alias_device(torch.from_numpy(np.ascontiguousarray(w)).cuda())
     return _unpack_alias(table, total)
@@ -179,6 +233,69 @@ def device_negative_weights(row_mass: torch.Tensor, power: float) -> torch.Tenso
     _lib.call("drg_negative_weights", _lib.ptr(row_mass), row_mass.numel(), float(power),
               _lib.ptr(w), _lib.stream_ptr())
     return w
+
+
+def build_positive_sampler(ns: SparseSimilarity) -> PositiveSampler:
+    """O(1) sampler of directed pairs proportional to their similarity
+    (optimizer.py:232-240): the device Vose table over the canonical pairs."""
+    if ns.entry_count == 0 or float(ns.weights.sum()) <= 0.0:
+        raise ValueError("similarity carries no mass; nothing to sample")
+    src = ns.sources()
+    canonical = src < ns.targets
+    return PositiveSampler(build_alias_table(ns.weights[canonical]),
+                           src[canonical].astype(np.int32),
+                           ns.targets[canonical].astype(np.int32))
+
+
+def _gradients(y_i, y_j, b: int, gamma: float, eps: float, clip: float, kind: int) -> np.ndarray:
+    _lib.load()
+    a = torch.tensor([[float(y_i[0]), float(y_i[1])]], dtype=torch.float64, device="cuda")
+    c = torch.tensor([[float(y_j[0]), float(y_j[1])]], dtype=torch.float64, device="cuda")
+    out = torch.empty((1, 2), dtype=torch.float64, device="cuda")
+    _lib.call("drg_gradients", _lib.ptr(a), _lib.ptr(c), 1, int(b), float(gamma), float(eps),
+              float(clip), kind, _lib.ptr(out), _lib.stream_ptr())
+    return out.cpu().numpy()[0]
+
+
+def attractive_gradient(y_i, y_j, b: int) -> np.ndarray:
+    """Gradient of log(1 / (1 + d^(2b))) w.r.t. y_i (optimizer.py:174-186; zero at
+    coincident positions, not clipped), by drg_gradients -- the device function the
+    layout kernels inline."""
+    return _gradients(y_i, y_j, b, 0.0, 0.0, math.inf, 0)
+
+
+def repulsive_gradient(y_i, y_jm, b: int, gamma: float, eps: float,
+                       clip: float = math.inf) -> np.ndarray:
+    """Gradient of gamma log(1 - 1/(1 + d^(2b))) w.r.t. y_i with the eps floor, each
+    component clamped to +-clip (optimizer.py:189-203), by drg_gradients."""
+    return _gradients(y_i, y_jm, b, gamma, eps, clip, 1)
+
+
+def lp_kernel(ld: float, b: int) -> float:
+    """Unnormalised layout-proximity kernel 1 / (1 + ld^(2b)) (optimizer.py:150-152)."""
+    x = ld * ld
+    r = 1.0
+    for _ in range(b):
+        r *= x
+    return 1.0 / (1.0 + r)
+
+
+@dataclass(frozen=True)
+class GradientSample:
+    """One sampled interaction, for tracing (optimizer.py:155-171)."""
+
+    i: int
+    j: int
+    ld: float
+    lp_kernel: float
+    kind: str
+
+    @classmethod
+    def from_positions(cls, i: int, j: int, y_i, y_j, b: int, kind: str) -> "GradientSample":
+        dx = float(y_i[0]) - float(y_j[0])
+        dy = float(y_i[1]) - float(y_j[1])
+        ld = math.sqrt(dx * dx + dy * dy)
+        return cls(i=i, j=j, ld=ld, lp_kernel=lp_kernel(ld, b), kind=kind)
 
 
 def build_negative_sampler(ns: SparseSimilarity, power: float = 0.75) -> AliasTable:
@@ -309,6 +426,7 @@ class SampledTables:
     map: torch.Tensor | None = None
     indptr: torch.Tensor | None = None      # level-0 row offsets of row_alias
     neg_alias: torch.Tensor | None = None   # level-0 Vose table over Q^0
+    mass: torch.Tensor | None = None        # R^l (fp64 [n_l]): partitions for multi-GPU
 
 
 # Steps in flight of the Hogwild update pass (the fidelity knob).  Concurrent steps
@@ -353,7 +471,7 @@ def build_sampled_tables(ip, tg, P, R) -> SampledTables:
                         torch.zeros_like(R)).clamp_(0.0, 1.0).to(torch.float32)
         wsum = (2.0 * n * rowsum[:n]).to(torch.float32)
         hubs = _is_hub_level(R)
-    return SampledTables(src, rows[:nnz], c, wsum, hubs)
+    return SampledTables(src, rows[:nnz], c, wsum, hubs, mass=R)
 
 
 def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
@@ -385,7 +503,7 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
         R = _aggregate_nodes(R, parent, n_l)
         hubs = _is_hub_level(R)
         S = SampledTables(S0.src_alias, S0.row_alias, None, None, hubs, map=flat, indptr=ip,
-                          neg_alias=alias0)
+                          neg_alias=alias0, mass=R)
         out.append(LevelData(n_l, 0, None, None, None, None, None, S))
     return out
 
@@ -450,6 +568,14 @@ class LayoutPlan:
     maps: list
     opt: OptimizerParams
     nonfinite: torch.Tensor = None
+    # old -> new ids of the coarsest level (isolated_last), applied to the default Y0
+    coarsest_relabel: torch.Tensor | None = None
+    evals: torch.Tensor = None   # device counter of distance evaluations (sampled)
+    _shard_cache: dict = field(default_factory=dict)   # multi-GPU layouts / contexts
+
+    def distance_evals(self) -> int:
+        """Distance evaluations so far (the reference's counter, _kernels.py:86, 122)."""
+        return 0 if self.evals is None else int(self.evals.item())
 
     @property
     def depth(self) -> int:
@@ -479,6 +605,16 @@ class LayoutPlan:
             return "sgather_kernel", L.n * (32 + 24 * S + 16 * M)
         return "layout_iter_kernel", L.algorithmic_bytes(M)
 
+    def total_distance_evals(self) -> int:
+        """The reference's distance-evaluation count of the run (_kernels.py:86, 122):
+        counted on the device by the sampled epochs (attractions with i != j plus
+        negatives that found a target); a gather iteration evaluates every P entry
+        and M negatives per active node."""
+        if self.opt.update == "sampled":
+            return self.distance_evals()
+        M = self.opt.neg_samples
+        return self.opt.iters * sum(L.nnz + M * L.active for L in self.levels)
+
     def interactions(self) -> int:
         """Interactions applied over the whole layout stage: per gather iteration every
         P entry + M negatives per node; per sampled epoch n_l steps of one pair + M
@@ -497,7 +633,13 @@ class LayoutPlan:
             y = rng.uniform(-self.opt.init_scale, self.opt.init_scale, size=(n, 2))
         else:
             y = rng.normal(0.0, self.opt.init_scale, size=(n, 2))
-        return torch.from_numpy(y.astype(np.float32)).cuda()
+        y = torch.from_numpy(y.astype(np.float32)).cuda()
+        rel = self.coarsest_relabel
+        if rel is not None:   # the draw is in reference id order
+            out = torch.empty_like(y)
+            out[rel.to(torch.int64)] = y
+            y = out
+        return y
 
     def _level_args(self, level: int):
         L = self.levels[level]
@@ -584,7 +726,7 @@ class LayoutPlan:
         return out
 
     def sampled_steps(self, level: int, y: torch.Tensor, step_lo: int, n_steps: int, t0: int,
-                      n_iter: int = 1, max_threads: int | None = None) -> None:
+                      n_iter: int = 1, max_threads: int | None = None, count: bool = True) -> None:
         """drg_layout_sampled: steps [step_lo, step_lo + n_steps) of epochs t0.. in place,
         n_l / sampled_concurrency(_coarse) steps in flight (or ``max_threads``)."""
         L, gamma, seed = self._level_args(level)
@@ -595,6 +737,12 @@ class LayoutPlan:
         fine, coarse = sampled_divisors(self.levels[0].n, o)
         div = fine if level == 0 else coarse
         ip, neg, n_tab, mp = self._tables(level)
+        det = o.threads == 1 and not o.sampled_fused
+        flags = (int(S.hubs) * _lib.DRG_SAMPLED_AGGREGATE
+                 | (_lib.DRG_SAMPLED_FUSED if o.sampled_fused else 0)
+                 | (_lib.DRG_SAMPLED_DETERMINISTIC if det else 0))
+        if self.evals is None:
+            self.evals = torch.zeros(1, dtype=torch.int64, device=y.device)
         _lib.call("drg_layout_sampled", _lib.ptr(ip), None,
                   _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), self._collapse(level),
                   _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(y), step_lo, n_steps, t0, n_iter,
@@ -602,7 +750,7 @@ class LayoutPlan:
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
                   o.neg_samples, seed, level,
                   max_threads if max_threads is not None else max(32, L.n // max(1, div)),
-                  int(S.hubs) | (2 if o.sampled_fused else 0), _lib.stream_ptr())
+                  flags, L.n, _lib.ptr(self.evals) if count else None, _lib.stream_ptr())
 
     def _collapse(self, level: int):
         """Collapse probabilities of ``level`` (NULL at level 0 and for mapped draws)."""
@@ -648,42 +796,118 @@ class LayoutPlan:
                   max_threads, 0, _lib.stream_ptr())
 
     def _run_level_sampled(self, level, y, t0, n_iter, group=None, step_fn=None):
-        """Reference-faithful epochs: n_l sampled steps each, Hogwild on y.  With a
-        process group and a level of at least ``shard_min_nodes`` nodes the epoch's
-        steps are split across ranks, each applies its share to its replica, and the
-        per-rank displacements are summed with one all-reduce per epoch (Hogwild with
-        a per-epoch exchange).  Smaller levels -- whose epochs take ~10 us, less than
-        one exchange -- run whole on every rank with no traffic, and rank 0's result
-        is broadcast once at the end (Hogwild replicas drift apart otherwise)."""
+        """Reference-faithful epochs: n_l sampled steps each, Hogwild on y.  Levels of
+        at least ``shard_min_nodes`` nodes run on every rank of a process group as one
+        distributed array (shard.py; or on ``virtual_ranks`` ranks emulated on this
+        GPU).  Smaller levels -- whose epochs take ~10 us, less than one exchange --
+        run whole on every rank with no traffic, and rank 0's result is broadcast once
+        at the end (Hogwild replicas drift apart otherwise)."""
         L = self.levels[level]
-        if group is None or L.n < self.opt.shard_min_nodes:
+        world = 1
+        if group is not None:
+            import torch.distributed as dist
+            world = dist.get_world_size(group)
+        big = L.n >= self.opt.shard_min_nodes and step_fn is None
+        if big and world > 1:
+            y = self._run_level_shard(level, y, t0, n_iter, group, world)
+        elif big and self.opt.virtual_ranks > 1 and group is None:
+            y = self._run_level_shard(level, y, t0, n_iter, None, self.opt.virtual_ranks)
+        else:
             if step_fn is not None:
                 for j in range(n_iter):
                     step_fn(y, 0, L.n, t0 + j)
-            else:
-                self.sampled_steps(level, y, 0, L.n, t0, n_iter)
-            if group is not None:
+            else:   # replicated: rank 0 alone counts the level's evaluations
+                import torch.distributed as dist
+                count = group is None or world == 1 or dist.get_rank(group) == 0
+                self.sampled_steps(level, y, 0, L.n, t0, n_iter, count=count)
+            if group is not None and world > 1:
                 import torch.distributed as dist
                 dist.broadcast(y, src=dist.get_global_rank(group, 0), group=group)
-        else:
-            import torch.distributed as dist
-            world = dist.get_world_size(group)
-            rank = dist.get_rank(group)
-            chunk = -(-L.n // world)
-            lo, hi = min(rank * chunk, L.n), min(rank * chunk + chunk, L.n)
-            for j in range(n_iter):
-                base = y.clone()
-                if step_fn is not None:
-                    step_fn(y, lo, hi, t0 + j)
-                elif hi > lo:
-                    self.sampled_steps(level, y, lo, hi - lo, t0 + j, 1)
-                y.sub_(base)
-                dist.all_reduce(y, op=dist.ReduceOp.SUM, group=group)
-                y.add_(base)
         if not bool(torch.isfinite(y).all()):
             raise FloatingPointError(f"non-finite coordinate in epochs {t0}..{t0 + n_iter - 1} "
                                      f"at level {level}")
         return y
+
+    def shard_layouts(self, world: int) -> dict:
+        """shard.shard_layout of every level the multi-GPU path shards."""
+        from .shard import shard_layout
+        key = ("layouts", world)
+        if key not in self._shard_cache:
+            out = {}
+            for level, L in enumerate(self.levels):
+                S = L.sampled
+                if L.n < self.opt.shard_min_nodes or S is None or S.mass is None:
+                    continue
+                if S.map is None:
+                    out[level] = shard_layout(S.mass, world)
+                else:
+                    out[level] = shard_layout(S.mass, world, self.levels[0].sampled.mass, S.map)
+            self._shard_cache[key] = out
+        return self._shard_cache[key]
+
+    def _shard_context(self, group, world: int):
+        from .shard import ShardContext
+        key = ("ctx", world, id(group))
+        if key not in self._shard_cache:
+            cap = max([lay.pad for lay in self.shard_layouts(world).values()] + [1])
+            self._shard_cache[key] = ShardContext(world, cap, group)
+        return self._shard_cache[key]
+
+    def _run_level_shard(self, level, y, t0, n_iter, group, world):
+        """One level on W ranks as one distributed Y (shard.py, drg_shard_*)."""
+        lay = self.shard_layouts(world)[level]
+        ctx = self._shard_context(group, world)
+        ctx.level(lay, y.device)
+        ctx.load(y)
+        for j in range(n_iter):
+            self.shard_epoch(level, world, ctx, t0 + j)
+            ctx.exchange()
+        return ctx.store(y)
+
+    def shard_epoch(self, level: int, world: int, ctx, t: int, max_threads: int | None = None,
+                    out_draws: torch.Tensor | None = None) -> int:
+        """drg_shard_epoch: the draws and updates of epoch t for the sources the
+        context's process owns (all ranks when emulating); no exchange.  Returns the
+        number of steps run.  Concurrency: the level's n_l / divisor steps in flight
+        in total, split over the ranks by their share of the epoch."""
+        L, gamma, seed = self._level_args(level)
+        S = L.sampled
+        o = self.opt
+        lay = self.shard_layouts(world)[level]
+        own = list(range(world)) if ctx.rank < 0 else [ctx.rank]
+        segs, tabs = [], []
+        for r in own:
+            key = ("seg", world, level, r)
+            if key not in self._shard_cache:
+                a, m = lay.seg_lo[r], lay.seg_n[r]
+                base = S.mass if S.map is None else self.levels[0].sampled.mass
+                w = base[a:a + m] if lay.perm is None else base[lay.perm[a:a + m].to(torch.int64)]
+                self._shard_cache[key] = (_alias_device(w.contiguous())[0]
+                                          if m > 0 and float(w.sum()) > 0 else None)
+            if self._shard_cache[key] is not None and lay.n_steps[r] > 0:
+                segs.append(r)
+                tabs.append(self._shard_cache[key])
+        if not segs:
+            return 0
+        if self.evals is None:
+            self.evals = torch.zeros(1, dtype=torch.int64, device=tabs[0].device)
+        k = len(segs)
+        arr = lambda v: (ctypes.c_int64 * k)(*v)   # noqa: E731
+        if max_threads is None:
+            fine, coarse = sampled_divisors(self.levels[0].n, o)
+            div = fine if level == 0 else coarse
+            share = sum(lay.n_steps[r] for r in segs) / max(1, L.n)
+            max_threads = max(32, int(L.n // max(1, div) * share))
+        ip, neg, n_tab, mp = self._tables(level)
+        _lib.call("drg_shard_epoch", ctx.ctx, _lib.ptr(ip), _lib.ptr(S.row_alias),
+                  self._collapse(level), _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(lay.perm),
+                  k, (ctypes.c_void_p * k)(*[tb.data_ptr() for tb in tabs]),
+                  arr([lay.seg_n[r] for r in segs]), arr([lay.seg_lo[r] for r in segs]),
+                  arr([lay.step_lo[r] for r in segs]), arr([lay.n_steps[r] for r in segs]),
+                  t, o.iters, float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
+                  o.neg_samples, seed, level, int(max_threads), _lib.ptr(self.evals),
+                  _lib.ptr(out_draws), _lib.stream_ptr())
+        return sum(lay.n_steps[r] for r in segs)
 
     def shard_bounds(self, level: int, world: int) -> list[int]:
         """Row ranges of the node-range shards: rows [0, n_active) cut
@@ -884,6 +1108,7 @@ def prepare_layout(dg: DeviceGraph, sim: SimilarityParams, opt: OptimizerParams,
     plan = None
     if ds.entry_count > 0:
         plan = build_plan(ds, dh, opt)
+        plan.coarsest_relabel = relabel[-1]
         stamp("level_data")
     if ev is not None:
         torch.cuda.synchronize()
@@ -914,17 +1139,18 @@ def layout_device(dg: DeviceGraph, sim: SimilarityParams | None = None,
         # through the maps without jitter (optimizer.py:397-402)
         stats["skipped_optimization"] = True
         n_top = dh.levels[-1].node_count
-        tmp = LayoutPlan([LevelData(n_top, 0, None, None, None, None)], [], opt)
+        tmp = LayoutPlan([LevelData(n_top, 0, None, None, None, None)], [], opt,
+                         coarsest_relabel=prep.relabel[-1] if prep.relabel else None)
         y = tmp.init_positions() if y0 is None else y0
         for level in range(dh.depth, 0, -1):
             y = device_prolong(y, dh.maps[level - 1], 0.0, 0)
         return prep.to_original(y), stats, prep
     y = prep.to_original(prep.plan.run(y0, group=group))
-    M = opt.neg_samples
+    if group is not None and prep.plan.evals is not None:   # every rank's share
+        import torch.distributed as dist
+        dist.all_reduce(prep.plan.evals, group=group)
     stats["gradient_steps"] = opt.iters * sum(dh.sizes)
-    # reference-equivalent interaction count: each iteration stands for n_l steps of
-    # (1 + M) interactions (an upper bound, like the reference's counter)
-    stats["distance_evals"] = opt.iters * (1 + M) * sum(dh.sizes)
+    stats["distance_evals"] = prep.plan.total_distance_evals()
     stats["interactions"] = prep.plan.interactions()
     return y, stats, prep
 
@@ -1014,17 +1240,24 @@ def sgd_epoch(positions: np.ndarray, h: Hierarchy, samplers: Samplers,
     level = _infer_level(h, n)
     plan = samplers.plan_for(h, params)
     y = torch.from_numpy(np.ascontiguousarray(positions, dtype=np.float32)).cuda()
+    before = plan.distance_evals()
     y = plan.run_level(level, y, t0=t, n_iter=1)
     plan.check_finite(level)
     positions[:] = y.cpu().numpy()
     if stats is not None:
         stats["gradient_steps"] = stats.get("gradient_steps", 0) + n
-        stats["distance_evals"] = stats.get("distance_evals", 0) + n * (1 + params.neg_samples)
+        if params.update == "sampled":
+            ev = plan.distance_evals() - before
+        else:
+            L = plan.levels[level]
+            ev = L.nnz + params.neg_samples * L.active
+        stats["distance_evals"] = stats.get("distance_evals", 0) + ev
     return positions
 
 
 
 __all__ = ["OptimizerParams", "Layout", "AliasTable", "build_alias_table",
-           "build_negative_sampler", "build_samplers", "Samplers", "sgd_epoch", "layout_graph",
+           "build_negative_sampler", "build_positive_sampler", "PositiveSampler",
+           "attractive_gradient", "repulsive_gradient", "lp_kernel", "GradientSample", "build_samplers", "Samplers", "sgd_epoch", "layout_graph",
            "layout_device", "prepare_layout", "LayoutPlan", "LevelData", "build_level_data",
            "device_radius"]

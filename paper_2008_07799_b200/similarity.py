@@ -173,3 +173,62 @@ def build_sparse_similarity(nd: NeighborDistances,
     ds = device_similarity(dnd, params)
     return ds.to_host()
 
+
+# ---------------------------------------------------------------------------
+# single-row helpers of the reference API, on the device (rowops.cu)
+# ---------------------------------------------------------------------------
+
+def _row_tensors(row) -> tuple[torch.Tensor, torch.Tensor]:
+    d = np.fromiter((int(dd) for _, dd in row), dtype=np.int32, count=len(row))
+    indptr = torch.tensor([0, len(d)], dtype=torch.int64, device="cuda")
+    return indptr, torch.from_numpy(d).cuda()
+
+
+def precompute_gaussian_table(k: int, sigma: float) -> np.ndarray:
+    """Gaussian kernel values exp(-d^2 / (2 sigma^2)) for the hop distances 1..k
+    (similarity.py:110-119), by drg_gaussian_table."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    _lib.load()
+    out = torch.empty(k, dtype=torch.float64, device="cuda")
+    _lib.call("drg_gaussian_table", int(k), float(sigma), _lib.ptr(out), _lib.stream_ptr())
+    return out.cpu().numpy()
+
+
+def conditional_similarity_row(row, sigma: float) -> list[tuple[int, float]]:
+    """Gaussian conditional probabilities of one node's (neighbour id, hop distance)
+    pairs (similarity.py:122-145): p = table[d] / fsum(row); [] for an empty row;
+    uniform over the nearest entries if every kernel value underflows
+    (drg_rows_conditional)."""
+    row = list(row)
+    if not row:
+        return []
+    if sigma <= 0:
+        raise ValueError("sigma must be positive")
+    _lib.load()
+    indptr, dists = _row_tensors(row)
+    sig = torch.tensor([float(sigma)], dtype=torch.float64, device="cuda")
+    p = torch.empty(len(row), dtype=torch.float64, device="cuda")
+    _lib.call("drg_rows_conditional", _lib.ptr(indptr), _lib.ptr(dists), 1, _lib.ptr(sig),
+              _lib.ptr(p), _lib.stream_ptr())
+    return [(int(j), float(v)) for (j, _), v in zip(row, p.cpu().tolist())]
+
+
+def search_sigma(row, perplexity: float, tol: float = 1e-5, max_iter: int = 64,
+                 sigma_min: float = 1e-5, sigma_max: float = 1e5) -> float:
+    """Geometric bisection for the bandwidth whose row perplexity matches the target
+    clamped to [1, len(row)] (similarity.py:167-199), by drg_rows_sigma -- the same
+    device routine build_sparse_similarity's rows use."""
+    row = list(row)
+    if not row:
+        raise ValueError("cannot search sigma for an empty row")
+    if len(row) == 1:
+        return 1.0
+    _lib.load()
+    indptr, dists = _row_tensors(row)
+    out = torch.ones(1, dtype=torch.float64, device="cuda")
+    _lib.call("drg_rows_sigma", _lib.ptr(indptr), _lib.ptr(dists), 1, float(perplexity),
+              float(tol), int(max_iter), float(sigma_min), float(sigma_max), _lib.ptr(out),
+              _lib.stream_ptr())
+    return float(out.item())
+

@@ -72,47 +72,6 @@ def init_for(cfg, n, seed):
     return rng.normal(0.0, 1e-4, size=(n, 2)).astype(np.float32).astype(np.float64)
 
 
-def emulated_exchange(bg, cfg, seed, y0, world):
-    """update="sampled" as W ranks run it (optimizer.LayoutPlan._run_level_sampled with
-    a process group): on levels of >= shard_min_nodes nodes each epoch's steps are
-    split into W rank ranges, each applied to its own copy of the epoch-start Y, and
-    the displacements summed (the all-reduce); smaller levels run whole on every rank.
-    The ranks run one after another on one device: a fidelity emulation, not a
-    timing."""
-    import torch
-    import paper_2008_07799_b200 as B
-    from paper_2008_07799_b200.graph import DeviceGraph
-    from paper_2008_07799_b200.optimizer import (_JITTER_TAG, _derive_seed, device_prolong,
-                                                 device_radius, prepare_layout)
-    opt = B.OptimizerParams(iters=cfg["iters"], seed=seed, update="sampled", init=cfg["init"])
-    prep = prepare_layout(DeviceGraph.from_host(bg), B.SimilarityParams(k=cfg["k"],
-                          perplexity=cfg["perplexity"]), opt, max_levels=cfg["max_levels"])
-    plan = prep.plan
-    y = prep.from_original_coarsest(torch.as_tensor(np.asarray(y0, dtype=np.float32)).cuda())
-    for level in range(plan.depth, -1, -1):
-        L = plan.levels[level]
-        if world > 1 and L.n >= opt.shard_min_nodes:
-            chunk = -(-L.n // world)
-            for t in range(opt.iters):
-                base = y.clone()
-                delta = torch.zeros_like(y)
-                for r in range(world):
-                    lo, hi = min(r * chunk, L.n), min(r * chunk + chunk, L.n)
-                    yr = base.clone()
-                    if hi > lo:
-                        plan.sampled_steps(level, yr, lo, hi - lo, t, 1)
-                    delta += yr - base
-                y = base + delta
-        else:
-            y = plan.run_level(level, y)
-        if level > 0:
-            radius = device_radius(y)
-            jitter = opt.jitter_rel * radius if radius > 0 else opt.init_scale
-            y = device_prolong(y, plan.maps[level - 1], jitter,
-                               _derive_seed(opt.seed, _JITTER_TAG, level))
-    return prep.to_original(y).cpu().numpy().astype(np.float64)
-
-
 def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evaluator="gpu",
          seed0=0):
     import paper_2008_07799_b200 as B
@@ -158,10 +117,12 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
                     extra["sampled_concurrency_coarse"] = int(coarse)
             elif div and upd == "sgather":
                 extra = {"att_samples": int(div)}
-            if upd == "sampledx":   # W-rank per-epoch exchange, emulated on one device
-                pos_x = emulated_exchange(bg, cfg, seed, y0, int(div))
-                runs[m] = (pos_x, time.perf_counter() - t0)
-                continue
+            if upd == "sampledv":   # the multi-GPU path on W ranks emulated on this GPU
+                upd, extra = "sampled", {"virtual_ranks": int(div), "threads": 16}
+            elif upd == "sampledd":   # threads = 1: the deterministic sub-batch form
+                upd, extra = "sampled", {"threads": 1}
+            elif upd == "sampled":
+                extra = {**extra, "threads": 16}
             lay = B.layout_graph(bg, B.SimilarityParams(k=cfg["k"], perplexity=cfg["perplexity"],
                                                         neighbor_cap=cap or None),
                                  B.OptimizerParams(iters=cfg["iters"], seed=seed, update=upd,
@@ -189,6 +150,13 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
                 "seconds_median": statistics.median(r["s"] for r in rs)}
         if key != "reference":
             ref = results["reference"]
+            # paired per-seed differences (same graph, P, hierarchy and Y0 per seed):
+            # mean relative gap and its standard error
+            for q in ("kl", "np"):
+                d = [a[q] / b[q] - 1 for a, b in zip(rs, ref) if b[q] != 0]
+                if len(d) > 1:
+                    line[f"{q}_paired_rel_mean"] = statistics.fmean(d)
+                    line[f"{q}_paired_rel_sem"] = statistics.stdev(d) / len(d) ** 0.5
             line["kl_rel_vs_ref"] = line["kl_median"] / statistics.median(r["kl"] for r in ref) - 1
             line["np_rel_vs_ref"] = line["np_median"] / statistics.median(r["np"] for r in ref) - 1
             line["kl_mean_rel_vs_ref"] = line["kl_mean"] / statistics.fmean(r["kl"] for r in ref) - 1

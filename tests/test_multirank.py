@@ -127,38 +127,52 @@ def _sampled_step(n):
     return step
 
 
-def _sampled_worker(rank, world, port, out_path):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    n = 97
-    plan = _plan(n, 5, "sampled")
-    y0 = torch.from_numpy(np.random.default_rng(3).normal(size=(n, 2)).astype(np.float32))
-    y = plan.run_level(0, y0.clone(), group=dist.group.WORLD, step_fn=_sampled_step(n))
-    if rank == 0:
-        np.save(out_path, y.numpy())
-    dist.barrier()
-    dist.destroy_process_group()
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_shard_layout_level0(world):
+    """shard.shard_layout at level 0: contiguous parts covering every node once; each
+    rank's sources are its own range; the epoch's n steps split by R mass (rounded on
+    the cumulative sum: they add up to n); parts balanced on mass + node count."""
+    from paper_2008_07799_b200.shard import shard_layout
+    rng = np.random.default_rng(world)
+    n = 5000
+    mass = torch.from_numpy(rng.pareto(1.5, n) * (rng.random(n) > 0.3))   # 30% isolated
+    lay = shard_layout(mass, world)
+    b = lay.bounds
+    assert b[0] == 0 and b[-1] == n and all(x <= y for x, y in zip(b, b[1:]))
+    assert lay.seg_lo == b[:-1] and lay.seg_n == [y - x for x, y in zip(b, b[1:])]
+    assert sum(lay.n_steps) == n
+    assert lay.step_lo == list(np.concatenate([[0], np.cumsum(lay.n_steps)[:-1]]))
+    tot = float(mass.sum())
+    for r in range(world):
+        m = float(mass[b[r]:b[r + 1]].sum())
+        assert abs(lay.seg_mass[r] - m) <= 1e-9 * tot
+        assert abs(lay.n_steps[r] - n * m / tot) <= 1.0
+    cost = mass.numpy() / tot + 1.0 / n
+    for r in range(world):
+        assert abs(cost[b[r]:b[r + 1]].sum() - cost.sum() / world) <= cost.max() + 1e-9
+    assert lay.pad == max(y - x for x, y in zip(b, b[1:]))
 
 
-def test_sampled_mode_epoch_exchange(tmp_path):
-    """update="sampled" on 2 ranks: each rank runs its share of the epoch's steps on
-    its replica; displacements are summed by one all-reduce per epoch."""
-    out = str(tmp_path / "ys.npy")
-    mp.spawn(_sampled_worker, args=(2, _free_port(), out), nprocs=2, join=True)
-    got = np.load(out)
-    n, world = 97, 2
-    step = _sampled_step(n)
-    y = torch.from_numpy(np.random.default_rng(3).normal(size=(n, 2)).astype(np.float32))
-    chunk = -(-n // world)
-    for t in range(5):
-        base = y.clone()
-        delta = torch.zeros_like(y)
-        for r in range(world):
-            yr = base.clone()
-            step(yr, r * chunk, min(n, r * chunk + chunk), t)
-            delta += yr - base
-        y = base + delta
-    assert np.array_equal(got, y.numpy())
+@pytest.mark.parametrize("world", [2, 5])
+def test_shard_layout_coarse_level_segments(world):
+    """A coarse level (draw-then-map): rank r's source segment is exactly the set of
+    level-0 nodes whose level-l image it owns, and its steps follow their R mass."""
+    from paper_2008_07799_b200.shard import shard_layout
+    rng = np.random.default_rng(7)
+    n0, nl = 4000, 700
+    mp = torch.from_numpy(rng.integers(0, nl, n0).astype(np.int32))
+    m0 = torch.from_numpy(rng.random(n0))
+    ml = torch.zeros(nl, dtype=torch.float64).index_add_(0, mp.to(torch.int64), m0)
+    lay = shard_layout(ml, world, m0, mp)
+    assert sum(lay.n_steps) == nl
+    perm = lay.perm.to(torch.int64)
+    assert sorted(perm.tolist()) == list(range(n0))
+    for r in range(world):
+        seg = perm[lay.seg_lo[r]:lay.seg_lo[r] + lay.seg_n[r]]
+        want = torch.nonzero((mp >= lay.bounds[r]) & (mp < lay.bounds[r + 1])).flatten()
+        assert sorted(seg.tolist()) == want.tolist()
+        share = float(m0[seg].sum()) / float(m0.sum())
+        assert abs(lay.n_steps[r] - nl * share) <= 1.0
 
 
 def _replicated_worker(rank, world, port, out_path):
