@@ -165,9 +165,13 @@ def params_for(name, iters_override=None, update="sampled", concurrency=None,
     import paper_2008_07799_b200 as B
     w = WORKLOADS[name]
     sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"], neighbor_cap=w.get("cap"))
+    # threads = the host's cores, as the reference arm's Hogwild workers: the
+    # sampled epochs run Hogwild (threads = 1 would select the deterministic form,
+    # timed separately under other_update_modes)
     opt = B.OptimizerParams(neg_samples=w["M"], iters=iters_override or w["iters"], seed=0,
                             init=w["init"], update=update, sampled_concurrency=concurrency,
-                            sampled_concurrency_coarse=concurrency_coarse, hub_levels=hub_levels)
+                            sampled_concurrency_coarse=concurrency_coarse, hub_levels=hub_levels,
+                            threads=max(2, os.cpu_count() or 2))
     return sim, opt, dict(w["hier"])
 
 
@@ -356,9 +360,12 @@ def run_ours(args):
         from paper_2008_07799_b200.optimizer import build_plan
         variants = {"jacobi": {}, "inplace": {}, "sampled": {"sampled_fused": False},
                     "sampled_fused": {"update": "sampled", "sampled_fused": True},
+                    "sampled_deterministic": {"update": "sampled", "threads": 1},
                     "sgather": {}}
         for label, extra in variants.items():
             kw2 = {"update": label, **extra}
+            if label == "sampled":
+                kw2["threads"] = opt.threads
             if all(getattr(opt, k) == v for k, v in kw2.items()):
                 continue
             o2 = B.OptimizerParams(**{**opt.__dict__, **kw2})
@@ -520,8 +527,12 @@ def cpu_baseline_from_gpu(dg, sim, opt, sizes, hier):
     samplers, h = cpu_reference_setup(ns, maps, sizes, opt.neg_power)
     setup = time.perf_counter() - t0
     dt = cpu_reference_step(samplers, h, opt, threads)
+    dt1 = cpu_reference_step(samplers, h, opt, 1)
     L = len(sizes)
     return {"value": L / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "one_thread": {"value": L / dt1, "unit": UNIT, "cores": 1,
+                           "sample": f"1 epoch at each of {L} levels on one host thread "
+                                     f"(the reference's default threads = 1)"},
             "sample": f"1 epoch at each of {L} levels, Hogwild over {threads} threads "
                       f"(oracle C port of _kernels.sgd_steps, same P and hierarchy)",
             "interactions_per_s": sum(n * (1 + opt.neg_samples) for n in sizes) / dt,

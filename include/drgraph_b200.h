@@ -227,7 +227,11 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * (integer atomics), folded into y after the sub-batch -- bitwise reproducible.
  * n_y: nodes of y (<= 0: n).  evals (device uint64, may be NULL) accumulates the
  * distance evaluations of the reference's counter (_kernels.py:86, 122): steps with
- * i != j plus negatives that found a target. */
+ * i != j plus negatives that found a target.  hot (device int32 [n_hot], may be
+ * NULL): hub levels -- up to 32 nodes whose positions each block stages in shared
+ * memory (read from there, increments summed there and added to y once per block
+ * per round of steps) instead of serialising every step's reduction on their L2
+ * lines. */
 #define DRG_SAMPLED_AGGREGATE 1
 #define DRG_SAMPLED_FUSED 2
 #define DRG_SAMPLED_DETERMINISTIC 4
@@ -239,7 +243,8 @@ int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_
                        int64_t n_steps, int t0,
                        int n_iter, int iters, double lr0, double gamma, double eps, double clip,
                        int b, int M, uint64_t seed, int level, int64_t max_threads,
-                       int flags, int64_t n_y, uint64_t *evals, void *stream);
+                       int flags, int64_t n_y, uint64_t *evals, const int32_t *hot,
+                       int n_hot, void *stream);
 
 /* The two halves of the split form, exposed for callers that keep the draws (and
  * for the parity tests).  drg_sampled_draws: out[(e * (2 + M) + f) * n_steps + s]

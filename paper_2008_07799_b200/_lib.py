@@ -79,7 +79,7 @@ SIGNATURES = {
     "drg_row_alias": [_P, _P, _P, _I64, _I64, _P, _P, _P],
     "drg_layout_sampled": [_P, _P, _P, _P, _P, _P, _P, _I64, _P, _I64, _I64, _I32, _I32, _I32,
                            _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _I32, _I64, _P,
-                           _P],
+                           _P, _I32, _P],
     "drg_sampled_draws": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _I32, _U64, _I32,
                           _P, _P],
     "drg_sampled_apply": [_P, _I64, _P, _F64, _F64, _F64, _F64, _I32, _I32, _I64, _I32, _P],

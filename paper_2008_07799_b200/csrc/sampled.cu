@@ -421,6 +421,7 @@ struct PArgs {
     int64_t n_steps;        // steps this launch applies
     int64_t stride;         // field stride of the draw records (the epoch's step count)
     unsigned long long *delta;   // deterministic mode: fixed-point increments [n][2]
+    uint64_t spread;        // != 0: step sl runs column (sl * spread) % n_steps (see below)
     float lr, gamma, eps, clip;
     int b, M;
     int probe;
@@ -443,12 +444,32 @@ __device__ __forceinline__ void add_fixed(unsigned long long *d, int64_t i, floa
     atomicAdd(d + 2 * i + 1, (unsigned long long)__double2ll_rn((double)dy * kFixScale));
 }
 
-template <bool AGG, bool DET>
-__device__ __forceinline__ void add_step(const PArgs &A, float2 *y, int64_t i, float dx,
-                                         float dy) {
-    if (DET) add_fixed(A.delta, i, dx, dy);
-    else add_y_w<AGG>(y, i, dx, dy, A.probe);
-}
+// ---- position stores: where a step reads and moves the nodes it touches -------
+// (one step body, step_body below, serves every mode)
+template <bool AGG>
+struct GlobalStore {   // Hogwild on y: float2 reductions (warp-aggregated on hub levels)
+    float2 *y;
+    int probe;
+    __device__ __forceinline__ float2 load(int64_t v) const { return ld_y(y, v); }
+    __device__ __forceinline__ float2 load_neg(int64_t v) const { return ld_y(y, v); }
+    __device__ __forceinline__ void add(int64_t v, float dx, float dy) const {
+        add_y_w<AGG>(y, v, dx, dy, probe);
+    }
+    __device__ __forceinline__ void add_neg(int64_t v, float dx, float dy) const { add(v, dx, dy); }
+};
+
+struct FixedStore {    // deterministic sub-batch: y frozen, fixed-point increments
+    const float2 *y;
+    unsigned long long *delta;
+    __device__ __forceinline__ float2 load(int64_t v) const { return __ldcg(y + v); }
+    __device__ __forceinline__ float2 load_neg(int64_t v) const { return __ldcg(y + v); }
+    __device__ __forceinline__ void add(int64_t v, float dx, float dy) const {
+        add_fixed(delta, v, dx, dy);
+    }
+    __device__ __forceinline__ void add_neg(int64_t v, float dx, float dy) const {
+        add_fixed(delta, v, dx, dy);
+    }
+};
 
 __global__ void flush_kernel(float2 *y, unsigned long long *d, int64_t n) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -465,82 +486,217 @@ __global__ void flush_kernel(float2 *y, unsigned long long *d, int64_t n) {
     }
 }
 
-template <bool AGG, int B, bool DET = false>
-__device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t sl,
-                                            const int64_t nthreads) {
+// One reference step (_kernels.py:82-140) on drawn (i, j, negatives) through a store.
+// Negatives past kMaxNeg are read from the draw records at column sl.
+template <int B, class St>
+__device__ __forceinline__ void step_body(const PArgs &A, const St &st, int64_t i, int64_t j,
+                                          const int32_t *cand, int64_t sl) {
     const float two_b = 2.0f * (float)A.b;
+    const int Me = min(A.M, kMaxNeg);
+    float2 yi = st.load(i);
+    const float2 yj = st.load(j);
+    float2 ycand[kMaxNeg];
+#pragma unroll
+    for (int m = 0; m < kMaxNeg; ++m)
+        ycand[m] = (m < Me && cand[m] >= 0) ? st.load_neg(cand[m]) : make_float2(0.f, 0.f);
+    float gix = 0.f, giy = 0.f;
+    int64_t upd = -1;
+    float ux = 0.f, uy = 0.f;
+    if (i != j) {  // _kernels.py:82-105
+        const float dx = yi.x - yj.x, dy = yi.y - yj.y;
+        const float ld2 = dx * dx + dy * dy;
+        if (ld2 > 0.f) {
+            const float pw = ipow_b<B>(ld2, A.b - 1);
+            const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
+            const float gx = A.lr * clampf(coef * dx, A.clip);
+            const float gy = A.lr * clampf(coef * dy, A.clip);
+            upd = j;
+            ux = -gx;
+            uy = -gy;
+            yi.x += gx;
+            yi.y += gy;
+            gix += gx;
+            giy += gy;
+        }
+    }
+    st.add(upd, ux, uy);
+    float ax[kMaxNeg], ay[kMaxNeg];   // this step's updates of its first negatives
+#pragma unroll
+    for (int m = 0; m < kMaxNeg; ++m) {  // _kernels.py:106-140
+        if (m < Me) {
+            float2 yc = ycand[m];
+            own_updates(yc, cand[m], m, cand, ax, ay);   // gathered before them
+            int64_t tu;
+            float tx, ty;
+            repel<B>(yi, yc, cand[m], A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix,
+                     giy);
+            ax[m] = tx;
+            ay[m] = ty;
+            st.add_neg(tu, tx, ty);
+        }
+    }
+    for (int m = Me; m < A.M; ++m) {   // negatives past kMaxNeg: gathered after the atomics
+        const int64_t target = __ldcs(A.draws + (2 + m) * A.stride + sl);
+        const float2 yc = target >= 0 ? st.load_neg(target) : make_float2(0.f, 0.f);
+        int64_t tu;
+        float tx, ty;
+        repel<B>(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
+        st.add_neg(tu, tx, ty);
+    }
+    st.add((gix != 0.f || giy != 0.f) ? i : -1, gix, giy);
+}
+
+// grid-stride over the launch's steps; the next step's record is prefetched while
+// this step runs
+// The columns of several ranks' draws (emulated multi-GPU: rank after rank in one
+// buffer) are visited in a spread order so the steps in flight at any time are
+// drawn from every rank, as on W GPUs, not from one rank's part at a time.
+__device__ __forceinline__ int64_t column(const PArgs &A, int64_t sl) {
+    return A.spread ? (int64_t)(((uint64_t)sl * A.spread) % (uint64_t)A.n_steps) : sl;
+}
+
+template <int B, class St>
+__device__ __forceinline__ void apply_steps(const PArgs &A, const St &st, int64_t sl,
+                                            const int64_t nthreads) {
     const int Me = min(A.M, kMaxNeg);
     const int64_t ns = A.n_steps, sd = A.stride;
     if (sl >= ns) return;
-    int32_t ci = __ldcs(A.draws + sl), cj = __ldcs(A.draws + sd + sl);
+    int64_t col = column(A, sl);
+    int32_t ci = __ldcs(A.draws + col), cj = __ldcs(A.draws + sd + col);
     int32_t cc[kMaxNeg];
 #pragma unroll
-    for (int m = 0; m < kMaxNeg; ++m) cc[m] = m < Me ? __ldcs(A.draws + (2 + m) * sd + sl) : -1;
+    for (int m = 0; m < kMaxNeg; ++m) cc[m] = m < Me ? __ldcs(A.draws + (2 + m) * sd + col) : -1;
     for (; sl < ns; sl += nthreads) {
-        const int64_t i = ci, j = cj;
+        const int64_t i = ci, j = cj, cur = col;
         int32_t cand[kMaxNeg];
 #pragma unroll
         for (int m = 0; m < kMaxNeg; ++m) cand[m] = cc[m];
-        // prefetch the next step's record
         const int64_t nx = sl + nthreads;
         if (nx < ns) {
-            ci = __ldcs(A.draws + nx);
-            cj = __ldcs(A.draws + sd + nx);
+            col = column(A, nx);
+            ci = __ldcs(A.draws + col);
+            cj = __ldcs(A.draws + sd + col);
 #pragma unroll
             for (int m = 0; m < kMaxNeg; ++m)
-                if (m < Me) cc[m] = __ldcs(A.draws + (2 + m) * sd + nx);
+                if (m < Me) cc[m] = __ldcs(A.draws + (2 + m) * sd + col);
         }
-        float2 yi = ld_y(y, i);
-        const float2 yj = ld_y(y, j);
-        float2 ycand[kMaxNeg];
-#pragma unroll
-        for (int m = 0; m < kMaxNeg; ++m)
-            ycand[m] = (m < Me && cand[m] >= 0) ? ld_y(y, cand[m]) : make_float2(0.f, 0.f);
-        float gix = 0.f, giy = 0.f;
-        int64_t upd = -1;
-        float ux = 0.f, uy = 0.f;
-        if (i != j) {  // _kernels.py:82-105
-            const float dx = yi.x - yj.x, dy = yi.y - yj.y;
-            const float ld2 = dx * dx + dy * dy;
-            if (ld2 > 0.f) {
-                const float pw = ipow_b<B>(ld2, A.b - 1);
-                const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
-                const float gx = A.lr * clampf(coef * dx, A.clip);
-                const float gy = A.lr * clampf(coef * dy, A.clip);
-                upd = j;
-                ux = -gx;
-                uy = -gy;
-                yi.x += gx;
-                yi.y += gy;
-                gix += gx;
-                giy += gy;
+        step_body<B>(A, st, i, j, cand, cur);
+    }
+}
+
+template <bool AGG, int B, bool DET = false>
+__device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t sl,
+                                            const int64_t nthreads) {
+    if (DET) apply_steps<B>(A, FixedStore{y, A.delta}, sl, nthreads);
+    else apply_steps<B>(A, GlobalStore<AGG>{y, A.probe}, sl, nthreads);
+}
+
+// ---- hub levels: the hottest nodes staged per block ------------------------------
+// On hub-heavy levels (R-MAT's coarse levels: one node is the source of a third of
+// an epoch's steps) every step reads and moves the same few nodes, and their
+// float2 reductions serialise on one L2 line each.  Here each block stages the K
+// hottest nodes: their positions are read from shared memory (refreshed from y
+// after every round of steps) and their increments summed in shared memory
+// (warp-aggregated), then added to y with one reduction per node per block and
+// round.  A hub thus moves between rounds, where the plain form moves it as its
+// reductions land; within a round the steps in flight see the same hub position in
+// both forms.  Rounds are block-uniform (one step per thread per round).
+constexpr int kHot = 32;
+constexpr int kHotSlots = 128;
+
+template <bool AGG>
+struct HotStore {
+    float2 *y;
+    int probe;
+    const int *key;            // shared open-addressing table: node id -> slot
+    const unsigned char *slot;
+    const float2 *pos;         // shared: staged positions
+    float *accx, *accy;        // shared: this round's increments
+    __device__ __forceinline__ int find(int64_t v) const {
+        if (v < 0) return -1;
+        uint32_t h = ((uint32_t)v * 2654435761u) >> (32 - 7);
+        for (int p = 0; p < kHotSlots; ++p) {
+            const int k = key[h];
+            if (k == (int)v) return slot[h];
+            if (k < 0) return -1;
+            h = (h + 1) & (kHotSlots - 1);
+        }
+        return -1;
+    }
+    __device__ __forceinline__ float2 load(int64_t v) const {
+        const int q = find(v);
+        return q >= 0 ? pos[q] : ld_y(y, v);
+    }
+    __device__ __forceinline__ float2 load_neg(int64_t v) const { return load(v); }
+    __device__ __forceinline__ void add(int64_t v, float dx, float dy) const {
+        const int q = find(v);
+        if (q < 0) {
+            add_y_w<AGG>(y, v, dx, dy, probe);
+            return;
+        }
+        // lanes staging the same node combine first; one shared update per node
+        const unsigned act = __activemask();
+        const unsigned peers = __match_any_sync(act, q);
+        const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+        for (unsigned rest = peers & ~(1u << leader); rest; rest &= rest - 1) {
+            const int src = __ffs(rest) - 1;
+            const float tx = __shfl_sync(peers, dx, src);
+            const float ty = __shfl_sync(peers, dy, src);
+            if (lane == leader) {
+                dx += tx;
+                dy += ty;
             }
         }
-        add_step<AGG, DET>(A, y, upd, ux, uy);
-        float ax[kMaxNeg], ay[kMaxNeg];   // this step's updates of its first negatives
+        if (lane == leader) {
+            atomicAdd(accx + q, dx);
+            atomicAdd(accy + q, dy);
+        }
+    }
+    __device__ __forceinline__ void add_neg(int64_t v, float dx, float dy) const { add(v, dx, dy); }
+};
+
+template <bool AGG, int B>
+__global__ void __launch_bounds__(256, 4)
+    apply_hot_kernel(PArgs A, float2 *y, const int32_t *__restrict__ hot, int n_hot) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ int s_key[kHotSlots];
+    __shared__ unsigned char s_slot[kHotSlots];
+    __shared__ float2 s_pos[kHot];
+    __shared__ float s_accx[kHot], s_accy[kHot];
+    const int tid = threadIdx.x;
+    const int K = min(n_hot, kHot);
+    for (int q = tid; q < kHotSlots; q += blockDim.x) s_key[q] = -1;
+    __syncthreads();
+    if (tid < K) {
+        const int v = hot[tid];
+        uint32_t h = ((uint32_t)v * 2654435761u) >> (32 - 7);
+        while (atomicCAS(&s_key[h], -1, v) != -1) h = (h + 1) & (kHotSlots - 1);
+        s_slot[h] = (unsigned char)tid;
+        s_pos[tid] = ld_y(y, v);
+        s_accx[tid] = s_accy[tid] = 0.f;
+    }
+    __syncthreads();
+    const HotStore<AGG> st{y, A.probe, s_key, s_slot, s_pos, s_accx, s_accy};
+    const int Me = min(A.M, kMaxNeg);
+    const int64_t ns = A.n_steps, sd = A.stride;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ns; base += nthreads) {
+        const int64_t sl = base + tid;
+        if (sl < ns) {
+            int32_t cand[kMaxNeg];
 #pragma unroll
-        for (int m = 0; m < kMaxNeg; ++m) {  // _kernels.py:106-140
-            if (m < Me) {
-                float2 yc = ycand[m];
-                own_updates(yc, cand[m], m, cand, ax, ay);   // gathered before them
-                int64_t tu;
-                float tx, ty;
-                repel<B>(yi, yc, cand[m], A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix,
-                      giy);
-                ax[m] = tx;
-                ay[m] = ty;
-                add_step<AGG, DET>(A, y, tu, tx, ty);
-            }
+            for (int m = 0; m < kMaxNeg; ++m) cand[m] = m < Me ? __ldcs(A.draws + (2 + m) * sd + sl) : -1;
+            step_body<B>(A, st, __ldcs(A.draws + sl), __ldcs(A.draws + sd + sl), cand, sl);
         }
-        for (int m = Me; m < A.M; ++m) {   // negatives past kMaxNeg: gathered after the atomics
-            const int64_t target = __ldcs(A.draws + (2 + m) * sd + sl);
-            const float2 yc = target >= 0 ? ld_y(y, target) : make_float2(0.f, 0.f);
-            int64_t tu;
-            float tx, ty;
-            repel<B>(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
-            add_step<AGG, DET>(A, y, tu, tx, ty);
+        __syncthreads();
+        if (tid < K) {   // publish the round's increments, refresh the staged position
+            const int v = hot[tid];
+            const float dx = s_accx[tid], dy = s_accy[tid];
+            if (dx != 0.f || dy != 0.f) add_y(y, v, dx, dy);
+            s_accx[tid] = s_accy[tid] = 0.f;
+            s_pos[tid] = ld_y(y, v);
         }
-        add_step<AGG, DET>(A, y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy);
+        __syncthreads();
     }
 }
 
@@ -584,7 +740,8 @@ void *apply_instance(int b, int64_t threads = INT64_MAX) {
 // Consecutive epochs on one stream as programmatic dependent launches: the next
 // grid is set up while the previous drains (its griddepcontrol.wait holds the
 // steps back), so small levels do not pay the full launch gap per epoch.
-int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, cudaStream_t st) {
+int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, cudaStream_t st,
+                 const int32_t *hot = nullptr, int n_hot = 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3((unsigned)block);
@@ -594,11 +751,15 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    void *args[] = {const_cast<PArgs *>(&P), &y};
+    void *args[] = {const_cast<PArgs *>(&P), &y, &hot, &n_hot};
     const int64_t threads = (int64_t)grid * block;
-    DRG_CUDA(cudaLaunchKernelExC(&cfg, agg ? apply_instance<true>(P.b, threads)
-                                           : apply_instance<false>(P.b, threads),
-                                 args));
+    void *fn;
+    if (hot && n_hot > 0)   // hub level: the hottest nodes staged per block
+        fn = agg ? (P.b == 2 ? (void *)apply_hot_kernel<true, 2> : (void *)apply_hot_kernel<true, 0>)
+                 : (P.b == 2 ? (void *)apply_hot_kernel<false, 2> : (void *)apply_hot_kernel<false, 0>);
+    else
+        fn = agg ? apply_instance<true>(P.b, threads) : apply_instance<false>(P.b, threads);
+    DRG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
     DRG_LAUNCHED("apply_kernel");
     return DRG_OK;
 }
@@ -1000,6 +1161,7 @@ extern "C" int drg_sampled_apply(const int32_t *draws, int64_t n_steps, float *y
     P.n_steps = n_steps;
     P.stride = n_steps;
     P.delta = nullptr;
+    P.spread = 0;
     P.lr = (float)lr;
     P.gamma = (float)gamma;
     P.eps = (float)eps;
@@ -1028,7 +1190,8 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                                   int iters,
                                   double lr0, double gamma, double eps, double clip, int b, int M,
                                   uint64_t seed, int level, int64_t max_threads, int flags,
-                                  int64_t n_y, uint64_t *evals, void *stream) {
+                                  int64_t n_y, uint64_t *evals, const int32_t *hot, int n_hot,
+                                  void *stream) {
     if (n <= 0 || n_steps <= 0 || n_iter <= 0) return DRG_OK;
     if (n_y <= 0) n_y = n;
     unsigned long long *ev_ctr = reinterpret_cast<unsigned long long *>(evals);
@@ -1131,6 +1294,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     P.n_steps = n_steps;
     P.stride = n_steps;
     P.delta = nullptr;
+    P.spread = 0;
     P.gamma = (float)gamma;
     P.eps = (float)eps;
     P.clip = (float)clip;
@@ -1158,7 +1322,8 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                 DRG_TRY(launch_det_epoch(P, reinterpret_cast<float2 *>(y), threads, n_y, ss.hi));
                 continue;
             }
-            DRG_TRY(launch_apply(P, reinterpret_cast<float2 *>(y), grid, block, agg, ss.hi));
+            DRG_TRY(launch_apply(P, reinterpret_cast<float2 *>(y), grid, block, agg, ss.hi, hot,
+                                 n_hot));
         }
         DRG_CUDA(cudaEventRecord(ev.e[3 + (c & 1)], ss.hi));
     }
@@ -1233,75 +1398,34 @@ __device__ __forceinline__ void add_at(float2 *p, bool remote, float dx, float d
     }
 }
 
-template <int B>
-__device__ __forceinline__ void apply_shard_epoch(const PArgs &A, const ShardView &V, int64_t sl,
-                                                  const int64_t nthreads) {
-    const float two_b = 2.0f * (float)A.b;
-    const int Me = min(A.M, kMaxNeg);
-    const int64_t ns = A.n_steps, sd = A.stride;
-    for (; sl < ns; sl += nthreads) {
-        const int64_t i = __ldcs(A.draws + sl), j = __ldcs(A.draws + sd + sl);
-        int32_t cand[kMaxNeg];
-#pragma unroll
-        for (int m = 0; m < kMaxNeg; ++m) cand[m] = m < Me ? __ldcs(A.draws + (2 + m) * sd + sl) : -1;
-        bool ri, rj;
-        float2 *pi = addr_of(V, i, ri);
-        float2 *pj = addr_of(V, j, rj);
-        float2 yi = __ldcg(pi);
-        const float2 yj = __ldcg(pj);
-        float2 ycand[kMaxNeg];
-#pragma unroll
-        for (int m = 0; m < kMaxNeg; ++m)
-            ycand[m] = (m < Me && cand[m] >= 0) ? __ldcg(V.snap + padded(V, cand[m]))
-                                                : make_float2(0.f, 0.f);
-        float gix = 0.f, giy = 0.f;
-        if (i != j) {  // _kernels.py:82-105
-            const float dx = yi.x - yj.x, dy = yi.y - yj.y;
-            const float ld2 = dx * dx + dy * dy;
-            if (ld2 > 0.f) {
-                const float pw = ipow_b<B>(ld2, A.b - 1);
-                const float coef = __fdividef(-two_b * pw, 1.0f + pw * ld2);
-                const float gx = A.lr * clampf(coef * dx, A.clip);
-                const float gy = A.lr * clampf(coef * dy, A.clip);
-                add_at(pj, rj, -gx, -gy);
-                yi.x += gx;
-                yi.y += gy;
-                gix += gx;
-                giy += gy;
-            }
-        }
-        float ax[kMaxNeg], ay[kMaxNeg];
-#pragma unroll
-        for (int m = 0; m < kMaxNeg; ++m) {  // _kernels.py:106-140, reactions deferred
-            if (m < Me) {
-                float2 yc = ycand[m];
-                own_updates(yc, cand[m], m, cand, ax, ay);
-                int64_t tu;
-                float tx, ty;
-                repel<B>(yi, yc, cand[m], A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix,
-                         giy);
-                ax[m] = tx;
-                ay[m] = ty;
-                if (tu >= 0) atomicAdd(V.delta + padded(V, tu), make_float2(tx, ty));
-            }
-        }
-        for (int m = Me; m < A.M; ++m) {
-            const int64_t target = __ldcs(A.draws + (2 + m) * sd + sl);
-            const float2 yc = target >= 0 ? __ldcg(V.snap + padded(V, target)) : make_float2(0.f, 0.f);
-            int64_t tu;
-            float tx, ty;
-            repel<B>(yi, yc, target, A.lr, A.gamma, A.eps, A.clip, two_b, A.b, tu, tx, ty, gix, giy);
-            if (tu >= 0) atomicAdd(V.delta + padded(V, tu), make_float2(tx, ty));
-        }
-        if (gix != 0.f || giy != 0.f) add_at(pi, ri, gix, giy);
+// the multi-GPU store: source and partner through the peer table, negatives from
+// the snapshot with their reactions deferred into the delta array
+struct ShardStore {
+    ShardView V;
+    __device__ __forceinline__ float2 load(int64_t v) const {
+        bool remote;
+        return __ldcg(addr_of(V, v, remote));
     }
-}
+    __device__ __forceinline__ float2 load_neg(int64_t v) const {
+        return __ldcg(V.snap + padded(V, v));
+    }
+    __device__ __forceinline__ void add(int64_t v, float dx, float dy) const {
+        if (v < 0) return;
+        bool remote;
+        float2 *p = addr_of(V, v, remote);
+        add_at(p, remote, dx, dy);
+    }
+    __device__ __forceinline__ void add_neg(int64_t v, float dx, float dy) const {
+        if (v >= 0) atomicAdd(V.delta + padded(V, v), make_float2(dx, dy));
+    }
+};
 
 template <int B>
 __global__ void __launch_bounds__(256) apply_shard_kernel(PArgs A, ShardView V) {
-    apply_shard_epoch<B>(A, V, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
-                         (int64_t)gridDim.x * blockDim.x);
+    apply_steps<B>(A, ShardStore{V}, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                   (int64_t)gridDim.x * blockDim.x);
 }
+
 
 // part[r][q] += src[r * pad + q] for q < cnt_r (atomics: peers may be updating the
 // part at the same time); src zeroed when `clear`
@@ -1665,6 +1789,9 @@ extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t 
     P.n_steps = total;
     P.stride = total;
     P.delta = nullptr;
+    // several local segments (emulation): a prime stride > total visits the columns
+    // in a spread order (a bijection of [0, total))
+    P.spread = (nseg > 1 && max_threads > 1) ? 4294967291ull : 0;
     P.lr = (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0);
     P.gamma = (float)gamma;
     P.eps = (float)eps;

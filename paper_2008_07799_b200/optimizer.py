@@ -25,6 +25,7 @@ import concurrent.futures
 import ctypes
 import logging
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Callable
 
@@ -427,6 +428,7 @@ class SampledTables:
     indptr: torch.Tensor | None = None      # level-0 row offsets of row_alias
     neg_alias: torch.Tensor | None = None   # level-0 Vose table over Q^0
     mass: torch.Tensor | None = None        # R^l (fp64 [n_l]): partitions for multi-GPU
+    hot: torch.Tensor | None = None         # int32: hub level's hottest nodes (staged per block)
 
 
 # Steps in flight of the Hogwild update pass (the fidelity knob).  Concurrent steps
@@ -450,6 +452,11 @@ def sampled_divisors(n0: int, opt: "OptimizerParams") -> tuple[int, int]:
 
 
 HUB_STEPS = 512   # warp-aggregate the sampled updates above this per-node rate
+# Above this per-node rate each block stages the level's HOT_NODES busiest nodes in
+# shared memory (apply_hot_kernel): R-MAT's coarse levels, where one node is the
+# source of up to a third of an epoch's steps, and the C3 BA coarsest level.
+HOT_STEPS = int(os.environ.get("DRG_HOT_STEPS", 4096))   # (env: experiments)
+HOT_NODES = 32
 # Above this per-node rate the sampled epoch serialises on the hub's atomics even
 # warp-aggregated, and the gather (K7 + heavy-row split) is faster: R-MAT's coarse
 # levels (busiest node 2.4e5 - 4.8e6 steps per epoch) -- while R-MAT's level 0
@@ -471,7 +478,7 @@ def build_sampled_tables(ip, tg, P, R) -> SampledTables:
                         torch.zeros_like(R)).clamp_(0.0, 1.0).to(torch.float32)
         wsum = (2.0 * n * rowsum[:n]).to(torch.float32)
         hubs = _is_hub_level(R)
-    return SampledTables(src, rows[:nnz], c, wsum, hubs, mass=R)
+    return SampledTables(src, rows[:nnz], c, wsum, hubs, mass=R, hot=_hot_nodes(R))
 
 
 def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
@@ -503,7 +510,7 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
         R = _aggregate_nodes(R, parent, n_l)
         hubs = _is_hub_level(R)
         S = SampledTables(S0.src_alias, S0.row_alias, None, None, hubs, map=flat, indptr=ip,
-                          neg_alias=alias0, mass=R)
+                          neg_alias=alias0, mass=R, hot=_hot_nodes(R))
         out.append(LevelData(n_l, 0, None, None, None, None, None, S))
     return out
 
@@ -516,6 +523,15 @@ def _busiest_steps(R: torch.Tensor) -> float:
 
 def _is_hub_level(R: torch.Tensor) -> bool:
     return _busiest_steps(R) > HUB_STEPS
+
+
+def _hot_nodes(R: torch.Tensor) -> torch.Tensor | None:
+    """The HOT_NODES nodes of largest R on a level whose busiest node is the source
+    of more than HOT_STEPS steps per epoch (None elsewhere)."""
+    if R.numel() == 0 or _busiest_steps(R) <= HOT_STEPS:
+        return None
+    k = min(HOT_NODES, R.numel())
+    return torch.topk(R, k).indices.to(torch.int32).contiguous()
 
 
 def _is_gather_level(R: torch.Tensor) -> bool:
@@ -750,7 +766,9 @@ class LayoutPlan:
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
                   o.neg_samples, seed, level,
                   max_threads if max_threads is not None else max(32, L.n // max(1, div)),
-                  flags, L.n, _lib.ptr(self.evals) if count else None, _lib.stream_ptr())
+                  flags, L.n, _lib.ptr(self.evals) if count else None,
+                  _lib.ptr(S.hot) if (S.hot is not None and not det) else None,
+                  0 if S.hot is None else S.hot.numel(), _lib.stream_ptr())
 
     def _collapse(self, level: int):
         """Collapse probabilities of ``level`` (NULL at level 0 and for mapped draws)."""
@@ -846,12 +864,9 @@ class LayoutPlan:
         return self._shard_cache[key]
 
     def _shard_context(self, group, world: int):
-        from .shard import ShardContext
-        key = ("ctx", world, id(group))
-        if key not in self._shard_cache:
-            cap = max([lay.pad for lay in self.shard_layouts(world).values()] + [1])
-            self._shard_cache[key] = ShardContext(world, cap, group)
-        return self._shard_cache[key]
+        from .shard import context_for
+        cap = max([lay.pad for lay in self.shard_layouts(world).values()] + [1])
+        return context_for(world, cap, group)
 
     def _run_level_shard(self, level, y, t0, n_iter, group, world):
         """One level on W ranks as one distributed Y (shard.py, drg_shard_*)."""

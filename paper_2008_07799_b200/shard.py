@@ -212,3 +212,21 @@ class ShardContext:
         parts = [torch.empty((self.pad, 2), dtype=torch.float32) for _ in range(self.world)]
         dist.all_gather(parts, part.cpu(), group=self.group)
         self.snap.copy_(torch.cat(parts).to(self.snap.device))
+
+
+_CONTEXTS: dict = {}
+
+
+def context_for(world: int, capacity: int, group=None) -> ShardContext:
+    """A ShardContext for (world, group) with at least ``capacity`` nodes per part,
+    kept across layouts (IPC mappings and the NCCL communicator are set up once).
+    Every rank asks with the same capacity (the layouts are deterministic), so a
+    re-creation is collective."""
+    key = (world, None if group is None else id(group))
+    c = _CONTEXTS.get(key)
+    if c is None or c.capacity < capacity:
+        if c is not None:
+            c.close()
+        c = ShardContext(world, capacity, group)
+        _CONTEXTS[key] = c
+    return c

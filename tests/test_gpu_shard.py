@@ -66,10 +66,11 @@ def test_emulated_epoch_matches_sequential_restatement(world):
         lr = o.lr0 * (1 - t / o.iters)
         want = O.deferred_drawn_epoch(y0.cpu().numpy().astype(np.float64), d, lr, gamma,
                                       o.eps, o.grad_clip, o.b)
-        # fp32 against fp64 over ~n chained steps: 99% of coordinates within 1e-5,
-        # all within 1e-3 (a few chains amplify the rounding)
+        # fp32 against fp64 over ~n chained steps at lr ~ 1: the median coordinate
+        # within 1e-6, 99% within 1e-4, all within 1e-3 (chains amplify rounding)
         err = np.abs(got - want) / np.maximum(1.0, np.abs(want))
-        assert np.quantile(err, 0.99) <= 1e-5 and err.max() <= 1e-3, float(err.max())
+        assert np.median(err) <= 1e-6 and np.quantile(err, 0.99) <= 1e-4 and err.max() <= 1e-3, \
+            float(err.max())
 
 
 def test_rank_draws_union_is_independent_of_the_process_layout():
