@@ -194,6 +194,14 @@ static double row_perplexity(const int64_t *counts, const double *dvals, int nb,
     return pow(2.0, h);
 }
 
+/* math.fsum over an array (the total_mass of similarity.py:272, long P arrays). */
+double orc_fsum(const double *x, int64_t n) {
+    double partials[128];
+    int np_ = 0;
+    for (int64_t i = 0; i < n; ++i) fsum_add(partials, &np_, x[i]);
+    return fsum_result(partials, np_);
+}
+
 double orc_search_sigma(const int64_t *counts, const double *dvals, int nb, int64_t n_row,
                         double target_in, double tol, int max_iter, double smin, double smax) {
     if (n_row == 1) return 1.0;                                   /* similarity.py:179-180 */

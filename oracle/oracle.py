@@ -58,6 +58,8 @@ def lib():
         L.orc_sigma_rows.argtypes = [P, i64, i32, f64, f64, i32, f64, f64, P, P, i32]
         L.orc_search_sigma.argtypes = [P, P, i32, i64, f64, f64, i32, f64, f64]
         L.orc_search_sigma.restype = f64
+        L.orc_fsum.argtypes = [P, i64]
+        L.orc_fsum.restype = f64
         L.orc_coarsen_with_order.argtypes = [P, P, i64, P, P]
         L.orc_coarsen_with_order.restype = i64
         L.orc_build_alias.argtypes = [P, i64, f64, P, P]
@@ -481,7 +483,7 @@ def build_sparse_similarity(nd: NeighborDistances, perplexity="auto", tol=1e-5,
         cond = pcond[src, d]
         mirror = pcond[nd.ids.astype(np.int64), d]   # p_{i|j}: same hop distance
         weights = (cond + mirror) / (2.0 * n_ne)
-    total = float(math.fsum(weights.tolist()))
+    total = fsum(weights)
     return SparseSimilarity(nd.indptr.copy(), nd.ids.copy(), weights, total, sigma, nd.k)
 
 
@@ -511,19 +513,26 @@ def build_capped_similarity(nd_capped: NeighborDistances, perplexity="auto", tol
     dst = nd_capped.ids.astype(np.int64)
     keys = np.concatenate([src * n + dst, dst * n + src])
     vals = np.concatenate([cond, cond])
-    order = np.argsort(keys, kind="stable")
+    # one or two contributions per key: their sum does not depend on their order
+    # (IEEE addition commutes), so any sort will do
+    order = np.argsort(keys)
     keys = keys[order]
     vals = vals[order]
-    uniq, start = np.unique(keys, return_index=True)
-    # exactly one or two contributions per key; sum in a fixed order
+    start = np.flatnonzero(np.concatenate([[True], keys[1:] != keys[:-1]]))
+    uniq = keys[start]
     w = np.add.reduceat(vals, start) / (2.0 * n_ne)
     rows = uniq // n
     tgt = (uniq % n).astype(np.int32)
     indptr = np.zeros(n + 1, dtype=np.int64)
-    np.add.at(indptr, rows + 1, 1)
-    np.cumsum(indptr, out=indptr)
-    total = float(math.fsum(w.tolist()))
+    indptr[1:] = np.cumsum(np.bincount(rows, minlength=n))
+    total = fsum(w)
     return SparseSimilarity(indptr, tgt, w, total, sigma, nd_capped.k)
+
+
+def fsum(x) -> float:
+    """math.fsum of a float64 array (C restatement of CPython's algorithm)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    return float(lib().orc_fsum(_p(x), len(x)))
 
 
 # --------------------------------------------------------------------------
@@ -854,13 +863,15 @@ def drawn_steps(pos, draws, lr, gamma, eps, clip, b):
     return pos
 
 
-def deferred_drawn_epoch(pos, draws, lr, gamma, eps, clip, b):
+def deferred_drawn_epoch(pos, draws, lr, gamma, eps, clip, b, snap=None, fold=True):
     """The multi-GPU epoch of paper_2008_07799_b200/shard.py on given draws, as a
     sequential fp64 restatement: the reference step (_kernels.py:82-140) with the
     source and the attraction partner read and moved in place, each negative read
     from the epoch-start snapshot (plus this step's own earlier reactions on it) and
-    its reaction deferred into a delta added at the epoch end."""
-    snap = pos.copy()
+    its reaction deferred into a delta added at the epoch end.  ``snap``: an older
+    snapshot to read the negatives from; ``fold=False`` returns (pos, delta)
+    without adding the delta."""
+    snap = pos.copy() if snap is None else snap
     delta = np.zeros_like(pos)
     bf = float(b)
     M = draws.shape[0] - 2
@@ -897,7 +908,27 @@ def deferred_drawn_epoch(pos, draws, lr, gamma, eps, clip, b):
                 yi += g
                 gi += g
         pos[i] += gi
+    if not fold:
+        return pos, delta
     pos += delta
+    return pos
+
+
+def lagged_drawn_epochs(pos, draws_per_epoch, lrs, gamma, eps, clip, b):
+    """drg_shard_run with DRG_SHARD_LAGGED as its emulation runs it (the worst case of
+    the overlapped exchange): epoch j reads the negatives from the snapshot taken at
+    the end of epoch j - 2 and its reactions are folded in after epoch j + 1."""
+    pos = np.array(pos, dtype=np.float64)
+    snaps = [pos.copy(), pos.copy()]
+    deltas = [np.zeros_like(pos), np.zeros_like(pos)]
+    n = len(draws_per_epoch)
+    for j in range(n):
+        pos, deltas[j & 1] = deferred_drawn_epoch(pos, draws_per_epoch[j], lrs[j], gamma, eps,
+                                                  clip, b, snap=snaps[j & 1], fold=False)
+        pos += deltas[(j + 1) & 1]
+        deltas[(j + 1) & 1] = np.zeros_like(pos)
+        snaps[j & 1] = pos.copy()
+    pos += deltas[(n - 1) & 1]
     return pos
 
 

@@ -28,6 +28,7 @@ DRG_FLAG_INPLACE = 1
 DRG_SAMPLED_AGGREGATE = 1
 DRG_SAMPLED_FUSED = 2
 DRG_SAMPLED_DETERMINISTIC = 4
+DRG_SHARD_LAGGED = 1
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -61,6 +62,8 @@ SIGNATURES = {
     "drg_shard_read_part": [_P, _P, _P],
     "drg_shard_epoch": [_P, _P, _P, _P, _P, _P, _I64, _P, _I32, _P, _P, _P, _P, _P, _I32, _I32,
                         _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _P, _P, _P],
+    "drg_shard_run": [_P, _P, _P, _P, _P, _P, _I64, _P, _I32, _P, _P, _P, _P, _P, _I32, _I32,
+                      _I32, _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _I32, _P, _P],
     "drg_khop_source": [_P, _P, _I64, _I32, _I64, _P, _P, _I64, _P, _P],
     "drg_similarity": [_P, _P, _P, _I64, _I64, _I32, _F64, _F64, _I32, _F64, _F64, _P, _P, _P,
                        _P, _P, _P],

@@ -33,6 +33,27 @@ namespace {
 
 constexpr int kMaxNeg = 6;  // negatives whose first draw is issued early
 
+// Distance-evaluation counts (_kernels.py:86, 122).  One counter would take one
+// same-address atomic per warp -- ~3e5 per 5-epoch draw launch on the mesh,
+// serialised in one L2 slice -- so warps add into kEvalSlots counters 128 B apart
+// (EvalSlots below), summed into the caller's counter once per call.
+constexpr int kEvalSlots = 64, kEvalStride = 16;
+
+__device__ __forceinline__ void count_evals(unsigned long long *slots, unsigned nev) {
+    if (!slots) return;
+    const unsigned act = __activemask();
+    nev = __reduce_add_sync(act, nev);
+    if ((threadIdx.x & 31) == __ffs(act) - 1 && nev)
+        atomicAdd(slots + (blockIdx.x % kEvalSlots) * kEvalStride, (unsigned long long)nev);
+}
+
+__global__ void evals_finish_kernel(unsigned long long *slots, unsigned long long *evals) {
+    unsigned long long v = 0;
+    for (int q = threadIdx.x; q < kEvalSlots; q += 32) v += slots[q * kEvalStride];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if (threadIdx.x == 0) *evals += v;
+}
+
 struct SArgs {
     const int64_t *indptr;
     const uint2 *rec;        // level CSR records {target, W}
@@ -287,11 +308,7 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
         // them locally in sequence, as the reference kernel does)
         add_y_w<AGG>(y, (gix != 0.f || giy != 0.f) ? i : -1, gix, giy, A.probe);
     }
-    if (A.evals) {
-        const unsigned act = __activemask();
-        nev = __reduce_add_sync(act, nev);
-        if ((threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(A.evals, (unsigned long long)nev);
-    }
+    count_evals(A.evals, nev);
 }
 
 // ---- split formulation: draws, then updates -----------------------------------
@@ -403,11 +420,7 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
         __stcs(o + (int64_t)(2 + m) * A.out_stride, (int32_t)target);
         nev += target >= 0;
     }
-    if (A.evals) {   // one atomic per warp
-        const unsigned act = __activemask();
-        nev = __reduce_add_sync(act, nev);
-        if ((threadIdx.x & 31) == __ffs(act) - 1) atomicAdd(A.evals, (unsigned long long)nev);
-    }
+    count_evals(A.evals, nev);
 }
 
 int launch_draws(const DArgs &D, cudaStream_t st) {
@@ -551,17 +564,19 @@ __device__ __forceinline__ void step_body(const PArgs &A, const St &st, int64_t 
 // The columns of several ranks' draws (emulated multi-GPU: rank after rank in one
 // buffer) are visited in a spread order so the steps in flight at any time are
 // drawn from every rank, as on W GPUs, not from one rank's part at a time.
+// (SPREAD: a compile-time switch, the 64-bit modulo stays out of the 1-GPU kernels)
+template <bool SPREAD>
 __device__ __forceinline__ int64_t column(const PArgs &A, int64_t sl) {
-    return A.spread ? (int64_t)(((uint64_t)sl * A.spread) % (uint64_t)A.n_steps) : sl;
+    return SPREAD ? (int64_t)(((uint64_t)sl * A.spread) % (uint64_t)A.n_steps) : sl;
 }
 
-template <int B, class St>
+template <int B, class St, bool SPREAD = false>
 __device__ __forceinline__ void apply_steps(const PArgs &A, const St &st, int64_t sl,
                                             const int64_t nthreads) {
     const int Me = min(A.M, kMaxNeg);
     const int64_t ns = A.n_steps, sd = A.stride;
     if (sl >= ns) return;
-    int64_t col = column(A, sl);
+    int64_t col = column<SPREAD>(A, sl);
     int32_t ci = __ldcs(A.draws + col), cj = __ldcs(A.draws + sd + col);
     int32_t cc[kMaxNeg];
 #pragma unroll
@@ -573,7 +588,7 @@ __device__ __forceinline__ void apply_steps(const PArgs &A, const St &st, int64_
         for (int m = 0; m < kMaxNeg; ++m) cand[m] = cc[m];
         const int64_t nx = sl + nthreads;
         if (nx < ns) {
-            col = column(A, nx);
+            col = column<SPREAD>(A, nx);
             ci = __ldcs(A.draws + col);
             cj = __ldcs(A.draws + sd + col);
 #pragma unroll
@@ -1022,6 +1037,28 @@ __global__ void __launch_bounds__(kRowBlock)
     }
 }
 
+// the per-call slot array behind count_evals (no slots when the caller counts nothing)
+struct EvalSlots {
+    Scratch buf;
+    unsigned long long *target = nullptr;
+    explicit EvalSlots(cudaStream_t st) : buf(st) {}
+    int init(unsigned long long *evals, cudaStream_t st) {
+        target = evals;
+        if (!evals) return DRG_OK;
+        const size_t bytes = sizeof(unsigned long long) * kEvalSlots * kEvalStride;
+        DRG_CUDA(buf.alloc(bytes));
+        DRG_CUDA(cudaMemsetAsync(buf.p, 0, bytes, st));
+        return DRG_OK;
+    }
+    unsigned long long *slots() const { return target ? buf.as<unsigned long long>() : nullptr; }
+    int finish(cudaStream_t st) {
+        if (!target) return DRG_OK;
+        evals_finish_kernel<<<1, 32, 0, st>>>(slots(), target);
+        DRG_LAUNCHED("evals_finish_kernel");
+        return DRG_OK;
+    }
+};
+
 }  // namespace
 }  // namespace drg
 
@@ -1194,13 +1231,15 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                                   void *stream) {
     if (n <= 0 || n_steps <= 0 || n_iter <= 0) return DRG_OK;
     if (n_y <= 0) n_y = n;
-    unsigned long long *ev_ctr = reinterpret_cast<unsigned long long *>(evals);
     const bool det = flags & DRG_SAMPLED_DETERMINISTIC;
     if (det && (flags & DRG_SAMPLED_FUSED))
         return fail(DRG_ERR_INVALID, "the deterministic mode runs the split form");
     if (n >= 0x7fffffffLL) return fail(DRG_ERR_INVALID, "level exceeds 2^31 - 1 nodes");
     if (b < 1 || M < 0 || iters < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
     cudaStream_t st = as_stream(stream);
+    EvalSlots evs(st);
+    DRG_TRY(evs.init(reinterpret_cast<unsigned long long *>(evals), st));
+    unsigned long long *ev_ctr = evs.slots();
     const bool agg = flags & DRG_SAMPLED_AGGREGATE;
     const char *probe_env = getenv("DRG_SAMPLED_PROBE");
     const int probe = probe_env ? atoi(probe_env) : 0;
@@ -1243,7 +1282,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
             else sampled_kernel<false><<<grid, block, 0, st>>>(A, reinterpret_cast<float2 *>(y));
             DRG_LAUNCHED("sampled_kernel");
         }
-        return DRG_OK;
+        return evs.finish(st);
     }
     // split: draw_kernel (K epochs per launch, double-buffered, low-priority stream)
     // -> apply_kernel per epoch (high-priority stream); joined back into `stream`
@@ -1331,7 +1370,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     DRG_CUDA(cudaStreamWaitEvent(st, ev.e[5], 0));
     DRG_CUDA(cudaEventRecord(ev.e[0], ss.hi));
     DRG_CUDA(cudaStreamWaitEvent(st, ev.e[0], 0));
-    return DRG_OK;
+    return evs.finish(st);
 }
 
 // =============================================================================
@@ -1420,10 +1459,11 @@ struct ShardStore {
     }
 };
 
-template <int B>
+template <int B, bool SPREAD>
 __global__ void __launch_bounds__(256) apply_shard_kernel(PArgs A, ShardView V) {
-    apply_steps<B>(A, ShardStore{V}, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
-                   (int64_t)gridDim.x * blockDim.x);
+    apply_steps<B, ShardStore, SPREAD>(A, ShardStore{V},
+                                       (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                                       (int64_t)gridDim.x * blockDim.x);
 }
 
 
@@ -1527,6 +1567,11 @@ struct ShardCtx {
     nccl_comm_t comm = nullptr;
     float2 *recv = nullptr;        // reduce-scatter landing buffer [pad]
     int64_t recv_cap = 0;
+    // lagged exchange (drg_shard_run, DRG_SHARD_LAGGED): the second snapshot and
+    // delta buffers [world * pad] and the stream the exchange overlaps on
+    float2 *snap2 = nullptr, *delta2 = nullptr;
+    int64_t buf2_cap = 0;
+    cudaStream_t comm_stream = nullptr;
 };
 
 }  // namespace drg
@@ -1564,6 +1609,9 @@ extern "C" int drg_shard_destroy(void *ctx) {
     for (float2 *p : c->own)
         if (p) cudaFree(p);
     if (c->recv) cudaFree(c->recv);
+    if (c->snap2) cudaFree(c->snap2);
+    if (c->delta2) cudaFree(c->delta2);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     delete c;
     return DRG_OK;
 }
@@ -1679,14 +1727,14 @@ extern "C" int drg_shard_store(void *ctx, float *y, void *stream) {
 // parts gathered into every snapshot.  Emulation: local kernels.  Multi-process
 // without a communicator: not available (the caller exchanges with
 // drg_shard_fold / drg_shard_read_part).
-extern "C" int drg_shard_exchange(void *ctx, void *stream) {
-    ShardCtx *c = static_cast<ShardCtx *>(ctx);
-    cudaStream_t st = as_stream(stream);
-    float2 *snap = const_cast<float2 *>(c->view.snap);
+namespace drg {
+namespace {
+// fold `delta` (reactions) into the parts, then refresh `snap` from the parts
+int shard_exchange(ShardCtx *c, float2 *snap, float2 *delta, cudaStream_t st) {
     if (c->rank < 0 || c->world == 1) {
         const auto lp = local_parts(c);
         fold_kernel<<<shard_grid(c->view.pad), 256, 0, st>>>(c->view, lp.first, lp.second,
-                                                             c->view.delta, 0, 1);
+                                                             delta, 0, 1);
         DRG_LAUNCHED("fold_kernel");
         snap_parts_kernel<<<shard_grid(c->view.pad), 256, 0, st>>>(c->view, snap);
         DRG_LAUNCHED("snap_parts_kernel");
@@ -1700,13 +1748,23 @@ extern "C" int drg_shard_exchange(void *ctx, void *stream) {
         c->recv_cap = c->view.pad;
     }
     const size_t cnt = (size_t)c->view.pad * 2;
-    DRG_NCCL(nccl().reduce_scatter(c->view.delta, c->recv, cnt, kNcclFloat32, kNcclSum, c->comm, st));
+    DRG_NCCL(nccl().reduce_scatter(delta, c->recv, cnt, kNcclFloat32, kNcclSum, c->comm, st));
     fold_kernel<<<shard_grid(c->view.pad), 256, 0, st>>>(c->view, c->rank, c->rank + 1, c->recv,
                                                          c->rank, 0);
     DRG_LAUNCHED("fold_kernel");
-    DRG_CUDA(cudaMemsetAsync(c->view.delta, 0, sizeof(float2) * (size_t)c->view.pad * c->world, st));
+    DRG_CUDA(cudaMemsetAsync(delta, 0, sizeof(float2) * (size_t)c->view.pad * c->world, st));
     DRG_NCCL(nccl().all_gather(c->own[0], snap, cnt, kNcclFloat32, c->comm, st));
     return DRG_OK;
+}
+}  // namespace
+}  // namespace drg
+
+extern "C" int drg_shard_exchange(void *ctx, void *stream) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    cudaStream_t st = as_stream(stream);
+    float2 *snap = const_cast<float2 *>(c->view.snap);
+    if (c->rank < 0 || c->world == 1) return shard_exchange(c, snap, c->view.delta, st);
+    return shard_exchange(c, snap, c->view.delta, st);
 }
 
 // host-collective path (tests over gloo): fold a reduced delta slice [pad] into the
@@ -1734,6 +1792,100 @@ extern "C" int drg_shard_read_part(void *ctx, float *out, void *stream) {
 // perm[seg_lo[s] + q] or seg_lo[s] + q), all segments' steps then applied by one
 // launch with <= max_threads steps in flight.  No exchange (drg_shard_exchange).
 // out_draws (optional, device int32 [2 + M][total]) receives the draw records.
+namespace drg {
+namespace {
+// the draw arguments common to a sharded level's segments (drg_shard_epoch / _run)
+DArgs shard_dargs(const int64_t *indptr, const uint64_t *row_alias, const float *collapse,
+                  const uint64_t *neg_alias, const int32_t *map, int64_t n_tab,
+                  const int32_t *perm, int M, uint64_t seed, int level, int64_t total,
+                  unsigned long long *evals) {
+    DArgs D;
+    D.indptr = indptr;
+    D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
+    D.collapse = collapse;
+    D.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+    D.map = map;
+    D.n = n_tab;
+    D.n_epochs = 1;
+    D.M = M;
+    D.key0 = (uint32_t)seed;
+    D.key1 = (uint32_t)(seed >> 32);
+    D.level = (uint32_t)level;
+    D.t_first = 0;
+    D.probe = 0;
+    D.evals = evals;
+    D.src_perm = perm;
+    D.out_stride = total;
+    return D;
+}
+
+// every local segment's draws of epochs [t, t + n_epochs) into out ([epoch][2 + M][total])
+int shard_draws(DArgs D, int nseg, const uint64_t *const *seg_alias, const int64_t *seg_n,
+                const int64_t *seg_lo, const int64_t *step_lo, const int64_t *n_steps, int t,
+                int n_epochs, int32_t *out, cudaStream_t st) {
+    D.t_first = t;
+    D.n_epochs = n_epochs;
+    int64_t off = 0;
+    for (int s = 0; s < nseg; ++s) {
+        if (n_steps[s] == 0) continue;
+        D.src_alias = reinterpret_cast<const uint2 *>(seg_alias[s]);
+        D.n_src = seg_n[s];
+        D.src_lo = seg_lo[s];
+        D.step_lo = step_lo[s];
+        D.n_steps = n_steps[s];
+        D.out = out + off;
+        DRG_TRY(launch_draws(D, st));
+        off += n_steps[s];
+    }
+    return DRG_OK;
+}
+
+PArgs shard_pargs(int64_t total, int nseg, int64_t max_threads, double gamma, double eps,
+                  double clip, int b, int M) {
+    PArgs P;
+    P.n_steps = total;
+    P.stride = total;
+    P.delta = nullptr;
+    // several local segments (emulation): a prime stride > total visits the columns
+    // in a spread order (a bijection of [0, total))
+    P.spread = (nseg > 1 && max_threads > 1) ? 4294967291ull : 0;
+    P.gamma = (float)gamma;
+    P.eps = (float)eps;
+    P.clip = (float)clip;
+    P.b = b;
+    P.M = M;
+    P.probe = 0;
+    return P;
+}
+
+int launch_shard_apply(const PArgs &P, const ShardView &V, int64_t max_threads, cudaStream_t st) {
+    const int64_t threads = std::max<int64_t>(1, std::min<int64_t>(P.n_steps, max_threads));
+    int block = (int)std::min<int64_t>(256, threads);
+    while (block > 32 && threads / block < 2 * (int64_t)sm_count()) block /= 2;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, threads / block);
+    if (P.spread) {
+        if (P.b == 2) apply_shard_kernel<2, true><<<grid, block, 0, st>>>(P, V);
+        else apply_shard_kernel<0, true><<<grid, block, 0, st>>>(P, V);
+    } else {
+        if (P.b == 2) apply_shard_kernel<2, false><<<grid, block, 0, st>>>(P, V);
+        else apply_shard_kernel<0, false><<<grid, block, 0, st>>>(P, V);
+    }
+    DRG_LAUNCHED("apply_shard_kernel");
+    return DRG_OK;
+}
+
+float lr_of(double lr0, int t, int iters) {
+    return (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0);
+}
+}  // namespace
+}  // namespace drg
+
+// One sampled epoch t of a sharded level for the sources this process owns:
+// per segment s (one per local part) the draws of steps [step_lo[s], +n_steps[s])
+// from the segment's source table (seg_alias[s] over seg_n[s] items, node
+// perm[seg_lo[s] + q] or seg_lo[s] + q), all segments' steps then applied by one
+// launch with <= max_threads steps in flight.  No exchange (drg_shard_exchange).
+// out_draws (optional, device int32 [2 + M][total]) receives the draw records.
 extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
                                const float *collapse, const uint64_t *neg_alias,
                                const int32_t *map, int64_t n_tab, const int32_t *perm,
@@ -1752,59 +1904,150 @@ extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t 
     if (total == 0) return DRG_OK;
     Scratch buf(st);
     DRG_CUDA(buf.alloc(sizeof(int32_t) * (size_t)(2 + M) * (size_t)total));
-    DArgs D;
-    D.indptr = indptr;
-    D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
-    D.collapse = collapse;
-    D.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
-    D.map = map;
-    D.n = n_tab;
-    D.n_epochs = 1;
-    D.M = M;
-    D.key0 = (uint32_t)seed;
-    D.key1 = (uint32_t)(seed >> 32);
-    D.level = (uint32_t)level;
-    D.t_first = t;
-    D.probe = 0;
-    D.evals = reinterpret_cast<unsigned long long *>(evals);
-    D.src_perm = perm;
-    D.out_stride = total;
-    int64_t off = 0;
-    for (int s = 0; s < nseg; ++s) {
-        if (n_steps[s] == 0) continue;
-        D.src_alias = reinterpret_cast<const uint2 *>(seg_alias[s]);
-        D.n_src = seg_n[s];
-        D.src_lo = seg_lo[s];
-        D.step_lo = step_lo[s];
-        D.n_steps = n_steps[s];
-        D.out = buf.as<int32_t>() + off;
-        DRG_TRY(launch_draws(D, st));
-        off += n_steps[s];
-    }
+    EvalSlots evs(st);
+    DRG_TRY(evs.init(reinterpret_cast<unsigned long long *>(evals), st));
+    const DArgs D = shard_dargs(indptr, row_alias, collapse, neg_alias, map, n_tab, perm, M, seed,
+                                level, total, evs.slots());
+    DRG_TRY(shard_draws(D, nseg, seg_alias, seg_n, seg_lo, step_lo, n_steps, t, 1,
+                        buf.as<int32_t>(), st));
     if (out_draws)   // the epoch's draw records, [2 + M][total] (tests)
         DRG_CUDA(cudaMemcpyAsync(out_draws, buf.p, sizeof(int32_t) * (size_t)(2 + M) * total,
                                  cudaMemcpyDeviceToDevice, st));
-    PArgs P;
+    PArgs P = shard_pargs(total, nseg, max_threads, gamma, eps, clip, b, M);
     P.draws = buf.as<int32_t>();
-    P.n_steps = total;
-    P.stride = total;
-    P.delta = nullptr;
-    // several local segments (emulation): a prime stride > total visits the columns
-    // in a spread order (a bijection of [0, total))
-    P.spread = (nseg > 1 && max_threads > 1) ? 4294967291ull : 0;
-    P.lr = (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0);
-    P.gamma = (float)gamma;
-    P.eps = (float)eps;
-    P.clip = (float)clip;
-    P.b = b;
-    P.M = M;
-    P.probe = 0;
-    const int64_t threads = std::max<int64_t>(1, std::min<int64_t>(total, max_threads));
-    int block = (int)std::min<int64_t>(256, threads);
-    while (block > 32 && threads / block < 2 * (int64_t)sm_count()) block /= 2;
-    const unsigned grid = (unsigned)std::max<int64_t>(1, threads / block);
-    if (b == 2) apply_shard_kernel<2><<<grid, block, 0, st>>>(P, c->view);
-    else apply_shard_kernel<0><<<grid, block, 0, st>>>(P, c->view);
-    DRG_LAUNCHED("apply_shard_kernel");
-    return DRG_OK;
+    P.lr = lr_of(lr0, t, iters);
+    DRG_TRY(launch_shard_apply(P, c->view, max_threads, st));
+    return evs.finish(st);
+}
+
+// Epochs t0 .. t0 + n_iter - 1 of a sharded level, exchange included, in one call
+// (no host round trip per epoch).  Draws: K epochs per launch, double-buffered one
+// chunk ahead on the low-priority stream.  Exchange after every epoch: on the
+// caller's stream (epoch t + 1 sees every update of epoch t), or with
+// DRG_SHARD_LAGGED on the context's exchange stream, overlapped with the next epoch
+// -- two snapshot and two delta buffers, epoch t reading the snapshot of the end of
+// epoch t - 2 (at the latest) and its reactions folded in by the end of epoch t + 1.
+// The emulation (rank -1) runs the lagged form in that worst-case order, so its
+// fidelity bounds the real one.
+extern "C" int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
+                             const float *collapse, const uint64_t *neg_alias,
+                             const int32_t *map, int64_t n_tab, const int32_t *perm, int nseg,
+                             const uint64_t *const *seg_alias, const int64_t *seg_n,
+                             const int64_t *seg_lo, const int64_t *step_lo,
+                             const int64_t *n_steps, int t0, int n_iter, int iters, double lr0,
+                             double gamma, double eps, double clip, int b, int M, uint64_t seed,
+                             int level, int64_t max_threads, int flags, uint64_t *evals,
+                             void *stream) {
+    ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    cudaStream_t st = as_stream(stream);
+    if (M < 0 || b < 1 || iters < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
+    if (nseg < 1 || nseg > kMaxParts) return fail(DRG_ERR_INVALID, "bad segment count");
+    if (c->rank >= 0 && c->world > 1 && !c->comm)
+        return fail(DRG_ERR_INVALID, "multi-process context without a communicator: run the "
+                                     "epochs with drg_shard_epoch and exchange on the host");
+    if (n_iter <= 0) return DRG_OK;
+    int64_t total = 0;
+    for (int s = 0; s < nseg; ++s) total += n_steps[s];
+    const bool lagged = (flags & DRG_SHARD_LAGGED) && c->world > 1;
+    const size_t nbuf = (size_t)c->view.pad * c->world;
+    if (lagged && c->buf2_cap < (int64_t)nbuf) {
+        if (c->snap2) cudaFree(c->snap2);
+        if (c->delta2) cudaFree(c->delta2);
+        c->snap2 = c->delta2 = nullptr;
+        c->buf2_cap = 0;
+        DRG_CUDA(cudaMalloc(&c->snap2, sizeof(float2) * nbuf));
+        DRG_CUDA(cudaMalloc(&c->delta2, sizeof(float2) * nbuf));
+        c->buf2_cap = (int64_t)nbuf;
+    }
+    if (lagged && !c->comm_stream)
+        DRG_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    float2 *snap[2] = {const_cast<float2 *>(c->view.snap), c->snap2};
+    float2 *delta[2] = {c->view.delta, c->delta2};
+    if (lagged) {   // both buffers start as the epoch-start snapshot / zero
+        DRG_CUDA(cudaMemcpyAsync(snap[1], snap[0], sizeof(float2) * nbuf,
+                                 cudaMemcpyDeviceToDevice, st));
+        DRG_CUDA(cudaMemsetAsync(delta[1], 0, sizeof(float2) * nbuf, st));
+    }
+    EvalSlots evs(st);
+    DRG_TRY(evs.init(reinterpret_cast<unsigned long long *>(evals), st));
+    if (total == 0) {   // nothing drawn here; the exchanges still pair with the peers'
+        for (int j = 0; j < n_iter; ++j) DRG_TRY(shard_exchange(c, snap[0], delta[0], st));
+        return evs.finish(st);
+    }
+    const DArgs D = shard_dargs(indptr, row_alias, collapse, neg_alias, map, n_tab, perm, M, seed,
+                                level, total, evs.slots());
+    const size_t rec_bytes = (size_t)(2 + M) * sizeof(int32_t) * (size_t)total;
+    const int K = (int)std::max<int64_t>(1, std::min<int64_t>(n_iter, (int64_t)(kDrawBudget / rec_bytes)));
+    const int nchunks = (n_iter + K - 1) / K;
+    Scratch buf(st);
+    DRG_CUDA(buf.alloc(rec_bytes * (size_t)K * (nchunks > 1 ? 2 : 1)));
+    SideStreams ss;
+    DRG_CUDA(side_streams(&ss));
+    Events ev;   // 0 start, 1-2 drawn[2], 3-4 applied[2], 5 draws done
+    DRG_CUDA(ev.create());
+    Events xev;  // lagged: 0-1 exchange of an even / odd epoch done, 2-3 epoch applied
+    if (lagged) DRG_CUDA(xev.create());
+    DRG_CUDA(cudaEventRecord(ev.e[0], st));
+    DRG_CUDA(cudaStreamWaitEvent(ss.lo, ev.e[0], 0));
+    auto chunk_buf = [&](int q) { return buf.as<int32_t>() + (size_t)(q & 1) * K * (rec_bytes / 4); };
+    auto draw = [&](int q) -> int {
+        DRG_TRY(shard_draws(D, nseg, seg_alias, seg_n, seg_lo, step_lo, n_steps, t0 + q * K,
+                            std::min(K, n_iter - q * K), chunk_buf(q), ss.lo));
+        DRG_CUDA(cudaEventRecord(ev.e[1 + (q & 1)], ss.lo));
+        return DRG_OK;
+    };
+    DRG_TRY(draw(0));
+    PArgs P = shard_pargs(total, nseg, max_threads, gamma, eps, clip, b, M);
+    ShardView V = c->view;
+    cudaStream_t xs = c->rank < 0 ? st : c->comm_stream;   // emulation: worst-case order
+    if (lagged && xs != st) {
+        DRG_CUDA(cudaEventRecord(xev.e[0], st));
+        DRG_CUDA(cudaStreamWaitEvent(xs, xev.e[0], 0));
+    }
+    for (int q = 0; q < nchunks; ++q) {
+        if (q + 1 < nchunks) {
+            if (q >= 1) DRG_CUDA(cudaStreamWaitEvent(ss.lo, ev.e[3 + ((q + 1) & 1)], 0));
+            DRG_TRY(draw(q + 1));
+        }
+        DRG_CUDA(cudaStreamWaitEvent(st, ev.e[1 + (q & 1)], 0));
+        const int ne = std::min(K, n_iter - q * K);
+        for (int e = 0; e < ne; ++e) {
+            const int j = q * K + e, t = t0 + j;
+            P.lr = lr_of(lr0, t, iters);
+            P.draws = chunk_buf(q) + (size_t)e * (rec_bytes / 4);
+            if (!lagged) {
+                DRG_TRY(launch_shard_apply(P, V, max_threads, st));
+                DRG_TRY(shard_exchange(c, snap[0], delta[0], st));
+                continue;
+            }
+            // epoch j reads snap[j & 1] and writes delta[j & 1]: both last touched
+            // by the exchange of epoch j - 2
+            if (xs != st && j >= 2) DRG_CUDA(cudaStreamWaitEvent(st, xev.e[j & 1], 0));
+            V.snap = snap[j & 1];
+            V.delta = delta[j & 1];
+            DRG_TRY(launch_shard_apply(P, V, max_threads, st));
+            if (xs == st) {   // emulation, the worst case: after epoch j fold epoch
+                // j - 1's reactions (delta[(j + 1) & 1]; zero at j = 0) and snapshot
+                // for epoch j + 2
+                DRG_TRY(shard_exchange(c, snap[j & 1], delta[(j + 1) & 1], st));
+                continue;
+            }
+            DRG_CUDA(cudaEventRecord(xev.e[2 + (j & 1)], st));
+            DRG_CUDA(cudaStreamWaitEvent(xs, xev.e[2 + (j & 1)], 0));
+            DRG_TRY(shard_exchange(c, snap[j & 1], delta[j & 1], xs));
+            DRG_CUDA(cudaEventRecord(xev.e[j & 1], xs));
+        }
+        DRG_CUDA(cudaEventRecord(ev.e[3 + (q & 1)], st));
+    }
+    if (lagged) {   // the outstanding reactions: the last epoch's
+        if (xs == st) {
+            DRG_TRY(shard_exchange(c, snap[0], delta[(n_iter - 1) & 1], st));
+        } else {
+            DRG_CUDA(cudaEventRecord(xev.e[4], xs));
+            DRG_CUDA(cudaStreamWaitEvent(st, xev.e[4], 0));
+        }
+    }
+    DRG_CUDA(cudaEventRecord(ev.e[5], ss.lo));
+    DRG_CUDA(cudaStreamWaitEvent(st, ev.e[5], 0));
+    return evs.finish(st);
 }

@@ -112,6 +112,10 @@ class OptimizerParams:
     # emulated on one GPU (the multi-GPU path of shard.py, all parts local) -- the
     # fidelity emulation of a multi-GPU run; 0 = off
     virtual_ranks: int = 0
+    # multi-GPU sampled levels: overlap each epoch's exchange with the next epoch
+    # (negatives read positions up to two epochs old, reactions fold in one epoch
+    # later; DRG_SHARD_LAGGED) instead of exchanging between epochs
+    shard_lagged: bool = False
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
@@ -874,20 +878,18 @@ class LayoutPlan:
         ctx = self._shard_context(group, world)
         ctx.level(lay, y.device)
         ctx.load(y)
-        for j in range(n_iter):
-            self.shard_epoch(level, world, ctx, t0 + j)
-            ctx.exchange()
+        if ctx.rank < 0 or ctx.nccl:   # the level's epochs and exchanges in one call
+            self.shard_run(level, world, ctx, t0, n_iter)
+        else:   # host collectives (gloo): epoch by epoch
+            for j in range(n_iter):
+                self.shard_epoch(level, world, ctx, t0 + j)
+                ctx.exchange()
         return ctx.store(y)
 
-    def shard_epoch(self, level: int, world: int, ctx, t: int, max_threads: int | None = None,
-                    out_draws: torch.Tensor | None = None) -> int:
-        """drg_shard_epoch: the draws and updates of epoch t for the sources the
-        context's process owns (all ranks when emulating); no exchange.  Returns the
-        number of steps run.  Concurrency: the level's n_l / divisor steps in flight
-        in total, split over the ranks by their share of the epoch."""
-        L, gamma, seed = self._level_args(level)
+    def _shard_segments(self, level: int, world: int, ctx):
+        """(ranks, per-rank source alias tables) of the segments this process owns."""
+        L = self.levels[level]
         S = L.sampled
-        o = self.opt
         lay = self.shard_layouts(world)[level]
         own = list(range(world)) if ctx.rank < 0 else [ctx.rank]
         segs, tabs = [], []
@@ -902,6 +904,54 @@ class LayoutPlan:
             if self._shard_cache[key] is not None and lay.n_steps[r] > 0:
                 segs.append(r)
                 tabs.append(self._shard_cache[key])
+        return segs, tabs
+
+    def _shard_threads(self, level: int, lay, segs) -> int:
+        """Steps in flight for this process: the level's n_l / divisor in total, split
+        over the ranks by their share of the epoch."""
+        fine, coarse = sampled_divisors(self.levels[0].n, self.opt)
+        div = fine if level == 0 else coarse
+        n = self.levels[level].n
+        share = sum(lay.n_steps[r] for r in segs) / max(1, n)
+        return max(32, int(n // max(1, div) * share))
+
+    def shard_run(self, level: int, world: int, ctx, t0: int, n_iter: int,
+                  max_threads: int | None = None) -> None:
+        """drg_shard_run: epochs t0 .. t0 + n_iter - 1 of a sharded level, exchanges
+        included, in one library call (emulated ranks or NCCL)."""
+        L, gamma, seed = self._level_args(level)
+        S = L.sampled
+        o = self.opt
+        lay = self.shard_layouts(world)[level]
+        segs, tabs = self._shard_segments(level, world, ctx)
+        k = max(1, len(segs))
+        arr = lambda v: (ctypes.c_int64 * k)(*(v or [0]))   # noqa: E731
+        if self.evals is None:
+            self.evals = torch.zeros(1, dtype=torch.int64, device=ctx.snap.device)
+        ip, neg, n_tab, mp = self._tables(level)
+        flags = _lib.DRG_SHARD_LAGGED if o.shard_lagged else 0
+        _lib.call("drg_shard_run", ctx.ctx, _lib.ptr(ip), _lib.ptr(S.row_alias),
+                  self._collapse(level), _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(lay.perm),
+                  k, (ctypes.c_void_p * k)(*([tb.data_ptr() for tb in tabs] or [None])),
+                  arr([lay.seg_n[r] for r in segs]), arr([lay.seg_lo[r] for r in segs]),
+                  arr([lay.step_lo[r] for r in segs]), arr([lay.n_steps[r] for r in segs]),
+                  t0, n_iter, o.iters, float(o.lr0), float(gamma), float(o.eps),
+                  float(o.grad_clip), o.b, o.neg_samples, seed, level,
+                  max_threads or self._shard_threads(level, lay, segs), flags,
+                  _lib.ptr(self.evals),
+                  _lib.stream_ptr())
+
+    def shard_epoch(self, level: int, world: int, ctx, t: int, max_threads: int | None = None,
+                    out_draws: torch.Tensor | None = None) -> int:
+        """drg_shard_epoch: the draws and updates of epoch t for the sources the
+        context's process owns (all ranks when emulating); no exchange.  Returns the
+        number of steps run.  Concurrency: the level's n_l / divisor steps in flight
+        in total, split over the ranks by their share of the epoch."""
+        L, gamma, seed = self._level_args(level)
+        S = L.sampled
+        o = self.opt
+        lay = self.shard_layouts(world)[level]
+        segs, tabs = self._shard_segments(level, world, ctx)
         if not segs:
             return 0
         if self.evals is None:
@@ -909,10 +959,7 @@ class LayoutPlan:
         k = len(segs)
         arr = lambda v: (ctypes.c_int64 * k)(*v)   # noqa: E731
         if max_threads is None:
-            fine, coarse = sampled_divisors(self.levels[0].n, o)
-            div = fine if level == 0 else coarse
-            share = sum(lay.n_steps[r] for r in segs) / max(1, L.n)
-            max_threads = max(32, int(L.n // max(1, div) * share))
+            max_threads = self._shard_threads(level, lay, segs)
         ip, neg, n_tab, mp = self._tables(level)
         _lib.call("drg_shard_epoch", ctx.ctx, _lib.ptr(ip), _lib.ptr(S.row_alias),
                   self._collapse(level), _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(lay.perm),

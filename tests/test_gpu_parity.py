@@ -338,7 +338,10 @@ def test_layout_graph_deterministic_and_stats(golden):
                 "gradient_steps", "distance_evals"):
         assert key in st
     assert st["gradient_steps"] == 30 * sum(st["levels"])
-    assert st["distance_evals"] <= st["gradient_steps"] * 6
+    # the sampled steps count real evaluations (<= 1 + M per step, _kernels.py:86,
+    # 122); a gather iteration evaluates every P entry and M negatives per node
+    assert 0 < d.stats["distance_evals"] <= d.stats["gradient_steps"] * 6
+    assert st["distance_evals"] > st["gradient_steps"]
     c = B.layout_graph(g, opt_params=B.OptimizerParams(seed=6, iters=30, update="jacobi"))
     assert not np.array_equal(a.positions, c.positions)
 

@@ -73,6 +73,48 @@ def test_emulated_epoch_matches_sequential_restatement(world):
             float(err.max())
 
 
+@pytest.mark.parametrize("lagged", [False, True])
+def test_shard_run_matches_epoch_restatement(lagged):
+    """drg_shard_run (a level's epochs and exchanges in one call, emulated 3 ranks,
+    one step in flight) against the oracle's sequential restatement on the same
+    draws: exchange after every epoch, or the lagged worst case (negatives from the
+    snapshot of epoch t - 2, reactions folded one epoch late)."""
+    world, n_ep, t0 = 3, 4, 1
+    plan, _ = _plan(world=world)
+    o = plan.opt
+    o.shard_lagged = lagged
+    for level in sorted({0, plan.depth}):
+        n = plan.levels[level].n
+        ctx = plan._shard_context(None, world)
+        lay = plan.shard_layouts(world)[level]
+        draws = []
+        for j in range(n_ep):   # the draws only depend on the counters
+            ctx.level(lay, "cuda")
+            ctx.load(torch.zeros((n, 2), device="cuda"))
+            d = torch.empty((2 + o.neg_samples, n), dtype=torch.int32, device="cuda")
+            plan.shard_epoch(level, world, ctx, t0 + j, max_threads=1, out_draws=d)
+            draws.append(d.cpu().numpy())
+        y0 = torch.randn((n, 2), device="cuda",
+                         generator=torch.Generator("cuda").manual_seed(level + 7))
+        ctx.level(lay, "cuda")
+        ctx.load(y0)
+        plan.shard_run(level, world, ctx, t0, n_ep, max_threads=1)
+        got = ctx.store(torch.empty_like(y0)).cpu().numpy().astype(np.float64)
+        gamma = o.gamma_coarsest if level == plan.depth else o.gamma
+        lrs = [o.lr0 * (1 - (t0 + j) / o.iters) for j in range(n_ep)]
+        y = y0.cpu().numpy().astype(np.float64)
+        if lagged:
+            want = O.lagged_drawn_epochs(y, draws, lrs, gamma, o.eps, o.grad_clip, o.b)
+        else:
+            want = y
+            for j in range(n_ep):
+                want = O.deferred_drawn_epoch(want, draws[j], lrs[j], gamma, o.eps,
+                                              o.grad_clip, o.b)
+        err = np.abs(got - want) / np.maximum(1.0, np.abs(want))
+        assert np.median(err) <= 1e-6 and np.quantile(err, 0.99) <= 1e-4 and err.max() <= 1e-3, \
+            float(err.max())
+
+
 def test_rank_draws_union_is_independent_of_the_process_layout():
     """The draws rank r makes alone equal its slice of the emulated epoch's draws."""
     from paper_2008_07799_b200.shard import ShardContext
