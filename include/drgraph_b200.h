@@ -206,14 +206,17 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * (collapse = NULL: no collapsed pairs, as at level 0)
  * (pairs inside a coarse node, which the reference draws at level 0 and maps),
  * else b from the row's alias table (targets from rec = the level's {target, W}
- * records); clipped attraction on both ends if i != j; M negatives ~ neg_alias
- * (Q^l) redrawn (<= 9) while they hit i or j, both ends moved (float2 atomics).
+ * records); clipped attraction on both ends if i != j; M negatives ~ Q^l redrawn
+ * (<= 9) while they hit i or j, both ends moved (float2 atomics).  Q^l is the
+ * level's own table: neg_alias (Vose records) over the level's nodes [0, neg_n)
+ * and, with probability neg_tail_p, a uniform pick in [neg_n, neg_n + neg_tail_n)
+ * (isolated nodes at equal floor weight, numbered last; neg_tail_n = 0: none).
  * Steps step_lo .. step_lo + n_steps - 1 of each epoch run here (a rank's share of
  * the epoch in the multi-GPU mode); at most max_threads steps run concurrently.
- * map (device int32 [n], may be NULL): the tables are level 0's over n nodes and
- * every drawn node -- source, target, negatives before their rejection test -- is
- * mapped to level l through map (composed parent maps), the reference's own
- * draw-then-map (_kernels.py:76-81, 115); y then holds the level's nodes.
+ * n: entries of src_alias.  map (device int32, may be NULL): the pair tables are
+ * level 0's and the drawn source and target are mapped to level l through map
+ * (composed parent maps), the reference's own draw-then-map (_kernels.py:76-81);
+ * the negatives drawn from Q^l directly have the law of its draw-then-map (115).
  * flags: DRG_SAMPLED_AGGREGATE combines the updates of a warp's lanes that hit the
  * same node before the atomic (hub-heavy levels); DRG_SAMPLED_FUSED draws inline in
  * the update kernel (one launch per epoch) instead of the default split -- every
@@ -238,7 +241,8 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
 
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,
                        const uint64_t *src_alias, const float *collapse,
-                       const uint64_t *neg_alias, const int32_t *map, int64_t n, float *y,
+                       const uint64_t *neg_alias, const int32_t *map, int64_t n,
+                       int64_t neg_n, int64_t neg_tail_n, double neg_tail_p, float *y,
                        int64_t step_lo,
                        int64_t n_steps, int t0,
                        int n_iter, int iters, double lr0, double gamma, double eps, double clip,
@@ -255,7 +259,8 @@ int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_
  * flight (max_threads = 1: sequential, the reference kernel's order). */
 int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alias,
                       const uint64_t *src_alias, const float *collapse,
-                      const uint64_t *neg_alias, const int32_t *map, int64_t n, int64_t step_lo,
+                      const uint64_t *neg_alias, const int32_t *map, int64_t n,
+                      int64_t neg_n, int64_t neg_tail_n, double neg_tail_p, int64_t step_lo,
                       int64_t n_steps,
                       int t0, int n_epochs, int M, uint64_t seed, int level, int32_t *out,
                       void *stream);
@@ -311,7 +316,8 @@ int drg_shard_fold(void *ctx, float *recv, void *stream);
 int drg_shard_read_part(void *ctx, float *out, void *stream);
 int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
                     const float *collapse, const uint64_t *neg_alias, const int32_t *map,
-                    int64_t n_tab, const int32_t *perm, int nseg,
+                    int64_t n_tab, int64_t neg_n, int64_t neg_tail_n, double neg_tail_p,
+                    const int32_t *perm, int nseg,
                     const uint64_t *const *seg_alias, const int64_t *seg_n, const int64_t *seg_lo,
                     const int64_t *step_lo, const int64_t *n_steps, int t, int iters, double lr0,
                     double gamma, double eps, double clip, int b, int M, uint64_t seed, int level,
@@ -326,7 +332,8 @@ int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
 #define DRG_SHARD_LAGGED 1
 int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
                   const float *collapse, const uint64_t *neg_alias, const int32_t *map,
-                  int64_t n_tab, const int32_t *perm, int nseg, const uint64_t *const *seg_alias,
+                  int64_t n_tab, int64_t neg_n, int64_t neg_tail_n, double neg_tail_p,
+                  const int32_t *perm, int nseg, const uint64_t *const *seg_alias,
                   const int64_t *seg_n, const int64_t *seg_lo, const int64_t *step_lo,
                   const int64_t *n_steps, int t0, int n_iter, int iters, double lr0, double gamma,
                   double eps, double clip, int b, int M, uint64_t seed, int level,

@@ -776,6 +776,8 @@ def layout_graph(g: Graph, k=1, perplexity="auto", params: OptimizerParams | Non
     if init is None:
         rng = np.random.default_rng(derive_seed(opt.seed, INIT_TAG))
         positions = rng.normal(0.0, opt.init_scale, size=(h.levels[-1].node_count, 2))
+    elif callable(init):   # init(n_coarsest) -> positions
+        positions = np.array(init(h.levels[-1].node_count), dtype=np.float64)
     else:
         positions = np.array(init, dtype=np.float64)
     if ns.entry_count == 0:

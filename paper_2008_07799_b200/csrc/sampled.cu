@@ -54,13 +54,36 @@ __global__ void evals_finish_kernel(unsigned long long *slots, unsigned long lon
     if (threadIdx.x == 0) *evals += v;
 }
 
+// The level's negative table (Q^l, optimizer.py:243-259): Vose over the nodes
+// [0, n) that carry graph mass and, with probability tail_thr / 2^32, a uniform
+// pick among the tail [n, n + tail_n) -- the isolated nodes, all at the same floor
+// weight (optimizer.py:258), which isolated_last numbers last.  The law of one
+// table over every node, from a table the size of the connected part (R-MAT: 53%
+// at level 0, 40% at the coarse levels, where it stays in L2).  Drawn at the
+// level itself: a level-0 draw mapped through the parent map has the same law
+// (Q^l_a = sum of the level-0 weights in a) and costs a second random load.
+struct NegTab {
+    const uint2 *alias;
+    int64_t n, tail_n;
+    uint32_t tail_thr;
+};
+
+__device__ __forceinline__ int64_t bucket(int64_t n, uint32_t hi, uint32_t lo);
+__device__ __forceinline__ int64_t accept(const uint2 rec, int64_t idx, uint32_t coin);
+
+__device__ __forceinline__ int64_t pick_neg(const NegTab &T, const u32x4 &q) {
+    if (q.w < T.tail_thr) return T.n + bucket(T.tail_n, q.x, q.y);
+    const int64_t bk = bucket(T.n, q.x, q.y);
+    return accept(__ldg(T.alias + bk), bk, q.z);
+}
+
 struct SArgs {
     const int64_t *indptr;
     const uint2 *rec;        // level CSR records {target, W}
     const uint4 *row_alias;  // per entry {fp32 threshold, alias target, own target, 0}
     const uint2 *src_alias;  // Vose over R^l
     const float *collapse;   // probability that the drawn pair collapses into the source
-    const uint2 *neg_alias;  // Vose over Q^l
+    NegTab neg;              // Q^l
     int64_t n;
     int64_t step_lo;
     int64_t n_steps;
@@ -131,7 +154,7 @@ __device__ __forceinline__ void add_y_w(float2 *y, int64_t i, float dx, float dy
         return;
     }
     const unsigned active = __activemask();
-    const unsigned peers = __match_any_sync(active, (unsigned long long)i);
+    const unsigned peers = __match_any_sync(active, (int)i);   // ids < 2^31 (-1: none)
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(peers) - 1;
     for (unsigned rest = peers & ~(1u << leader); rest; rest &= rest - 1) {
@@ -208,9 +231,7 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
 #pragma unroll
         for (int m = 0; m < kMaxNeg; ++m) {
             if (m < Me) {
-                const u32x4 q = neg_draw(A, s, c1, m, 0);
-                const int32_t bk = (int32_t)bucket(A.n, q.x, q.y);
-                cand[m] = (int32_t)accept(__ldg(A.neg_alias + bk), bk, q.z);
+                cand[m] = (int32_t)pick_neg(A.neg, neg_draw(A, s, c1, m, 0));
             }
         }
         // speculative gathers of the candidates (redrawn below only if they hit i/j)
@@ -267,9 +288,7 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
                     own_updates(yc, target, m, at, ax, ay);   // gathered before them
                 }
                 for (int attempt = 1; target < 0 && attempt < 9; ++attempt) {
-                    const u32x4 q = neg_draw(A, s, c1, m, attempt);
-                    const int64_t bk = bucket(A.n, q.x, q.y);
-                    const int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
+                    const int64_t c0 = pick_neg(A.neg, neg_draw(A, s, c1, m, attempt));
                     if (c0 != i && c0 != j) {
                         target = c0;
                         yc = ld_y(y, c0);   // after this step's own atomics
@@ -290,9 +309,7 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
             int64_t target = -1;
             float2 yc = make_float2(0.f, 0.f);
             for (int attempt = 0; target < 0 && attempt < 9; ++attempt) {
-                const u32x4 q = neg_draw(A, s, c1, m, attempt);
-                const int64_t bk = bucket(A.n, q.x, q.y);
-                const int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
+                const int64_t c0 = pick_neg(A.neg, neg_draw(A, s, c1, m, attempt));
                 if (c0 != i && c0 != j) {
                     target = c0;
                     yc = ld_y(y, c0);
@@ -327,8 +344,8 @@ struct DArgs {
     const uint4 *row_alias;
     const uint2 *src_alias;
     const float *collapse;
-    const uint2 *neg_alias;
-    const int32_t *map;   // non-NULL: level-0 tables, drawn nodes mapped to level l
+    NegTab neg;           // Q^l of the level itself
+    const int32_t *map;   // non-NULL: level-0 pair tables, the pair mapped to level l
     int64_t n;            // nodes of the tables
     int64_t step_lo;
     int64_t n_steps;
@@ -370,9 +387,7 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
 #pragma unroll
     for (int m = 0; m < kMaxNeg; ++m) {
         if (m < Me) {
-            const u32x4 q = neg_draw(K, s, c1, m, 0);
-            const int32_t bk = (int32_t)bucket(A.n, q.x, q.y);
-            cand[m] = (int32_t)accept(__ldg(A.neg_alias + bk), bk, q.z);
+            cand[m] = (int32_t)pick_neg(A.neg, neg_draw(K, s, c1, m, 0));
         }
     }
     int64_t i = accept(srec, sb, r.z);
@@ -388,12 +403,9 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
         const uint4 rrec = __ldcs(A.row_alias + lo + bucket(hi - lo, r2.x, r2.y));
         j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)rrec.z : (int64_t)rrec.y;
     }
-    if (A.map) {   // the level-0 pair and negatives as seen at level l (_kernels.py:76-81, 115)
+    if (A.map) {   // the level-0 pair as seen at level l (_kernels.py:76-81)
         i = __ldg(A.map + i);
         j = __ldg(A.map + j);
-#pragma unroll
-        for (int m = 0; m < kMaxNeg; ++m)
-            if (m < Me) cand[m] = __ldg(A.map + cand[m]);
     }
     int32_t *o = A.out + ep * (int64_t)(2 + A.M) * A.out_stride + sl;
     __stcs(o, (int32_t)i);   // read once by the update pass: streaming stores
@@ -411,16 +423,23 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
             first = 1;
         }
         for (int attempt = first; target < 0 && attempt < 9; ++attempt) {
-            const u32x4 q = neg_draw(K, s, c1, m, attempt);
-            const int64_t bk = bucket(A.n, q.x, q.y);
-            int64_t c0 = accept(__ldg(A.neg_alias + bk), bk, q.z);
-            if (A.map) c0 = __ldg(A.map + c0);
+            const int64_t c0 = pick_neg(A.neg, neg_draw(K, s, c1, m, attempt));
             if (c0 != i && c0 != j) target = c0;
         }
         __stcs(o + (int64_t)(2 + m) * A.out_stride, (int32_t)target);
         nev += target >= 0;
     }
     count_evals(A.evals, nev);
+}
+
+NegTab make_negtab(const uint64_t *alias, int64_t n, int64_t tail_n, double tail_p) {
+    NegTab T;
+    T.alias = reinterpret_cast<const uint2 *>(alias);
+    T.n = n;
+    T.tail_n = tail_n > 0 ? tail_n : 0;
+    const double thr = std::floor(std::min(std::max(tail_p, 0.0), 1.0) * 4294967296.0 + 0.5);
+    T.tail_thr = T.tail_n > 0 ? (uint32_t)std::min(thr, 4294967295.0) : 0u;
+    return T;
 }
 
 int launch_draws(const DArgs &D, cudaStream_t st) {
@@ -436,6 +455,7 @@ struct PArgs {
     unsigned long long *delta;   // deterministic mode: fixed-point increments [n][2]
     uint64_t spread;        // != 0: step sl runs column (sl * spread) % n_steps (see below)
     float lr, gamma, eps, clip;
+    float hot_scale;        // apply_hot_kernel's fixed-point scale (set by launch_apply)
     int b, M;
     int probe;
 };
@@ -616,20 +636,32 @@ __device__ __forceinline__ void apply_epoch(const PArgs &A, float2 *y, int64_t s
 // round.  A hub thus moves between rounds, where the plain form moves it as its
 // reductions land; within a round the steps in flight see the same hub position in
 // both forms.  Rounds are block-uniform (one step per thread per round).
-constexpr int kHot = 32;
-constexpr int kHotSlots = 128;
+// Membership is a 8192-bit filter on the low id bits (one shared load rejects
+// almost every non-hot node) before an open-addressing probe; the block's
+// increments of a hot node are summed in 32-bit fixed point by native shared
+// ATOMS.ADD (shared float atomics are CAS loops on sm_100): each increment
+// v = rint(dx * scale), |v| < 2^30, split into v >> 16 and v & 0xffff summed in
+// two words (no overflow for any block size), scale = the power of two that keeps
+// the largest increment lr * clip * (1 + M) below 2^30 (PArgs::hot_scale).
+constexpr int kHot = 64;
+constexpr int kHotSlots = 256;
+constexpr int kHotFilterWords = 256;
 
 template <bool AGG>
 struct HotStore {
     float2 *y;
     int probe;
+    float scale;
+    const unsigned *filter;    // shared: bit (v & 8191) set for every hot node
     const int *key;            // shared open-addressing table: node id -> slot
     const unsigned char *slot;
     const float2 *pos;         // shared: staged positions
-    float *accx, *accy;        // shared: this round's increments
+    int *acc;                  // shared: [kHot][4] x >> 16, x & 0xffff, y >> 16, y & 0xffff
     __device__ __forceinline__ int find(int64_t v) const {
         if (v < 0) return -1;
-        uint32_t h = ((uint32_t)v * 2654435761u) >> (32 - 7);
+        const uint32_t b = (uint32_t)v & 8191u;
+        if (!((filter[b >> 5] >> (b & 31)) & 1u)) return -1;
+        uint32_t h = ((uint32_t)v * 2654435761u) >> (32 - 8);
         for (int p = 0; p < kHotSlots; ++p) {
             const int k = key[h];
             if (k == (int)v) return slot[h];
@@ -649,49 +681,47 @@ struct HotStore {
             add_y_w<AGG>(y, v, dx, dy, probe);
             return;
         }
-        // lanes staging the same node combine first; one shared update per node
-        const unsigned act = __activemask();
-        const unsigned peers = __match_any_sync(act, q);
-        const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
-        for (unsigned rest = peers & ~(1u << leader); rest; rest &= rest - 1) {
-            const int src = __ffs(rest) - 1;
-            const float tx = __shfl_sync(peers, dx, src);
-            const float ty = __shfl_sync(peers, dy, src);
-            if (lane == leader) {
-                dx += tx;
-                dy += ty;
-            }
-        }
-        if (lane == leader) {
-            atomicAdd(accx + q, dx);
-            atomicAdd(accy + q, dy);
-        }
+        const int fx = __float2int_rn(dx * scale), fy = __float2int_rn(dy * scale);
+        int *a = acc + 4 * q;
+        atomicAdd(a + 0, fx >> 16);
+        atomicAdd(a + 1, fx & 0xffff);
+        atomicAdd(a + 2, fy >> 16);
+        atomicAdd(a + 3, fy & 0xffff);
     }
     __device__ __forceinline__ void add_neg(int64_t v, float dx, float dy) const { add(v, dx, dy); }
 };
+
+__device__ __forceinline__ float hot_sum(const int *a, float inv_scale) {
+    return (float)((double)((int64_t)a[0] * 65536 + (int64_t)a[1]) * (double)inv_scale);
+}
 
 template <bool AGG, int B>
 __global__ void __launch_bounds__(256, 4)
     apply_hot_kernel(PArgs A, float2 *y, const int32_t *__restrict__ hot, int n_hot) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ unsigned s_filter[kHotFilterWords];
     __shared__ int s_key[kHotSlots];
     __shared__ unsigned char s_slot[kHotSlots];
     __shared__ float2 s_pos[kHot];
-    __shared__ float s_accx[kHot], s_accy[kHot];
+    __shared__ int s_acc[kHot * 4];
     const int tid = threadIdx.x;
     const int K = min(n_hot, kHot);
     for (int q = tid; q < kHotSlots; q += blockDim.x) s_key[q] = -1;
+    for (int q = tid; q < kHotFilterWords; q += blockDim.x) s_filter[q] = 0u;
     __syncthreads();
     if (tid < K) {
         const int v = hot[tid];
-        uint32_t h = ((uint32_t)v * 2654435761u) >> (32 - 7);
+        uint32_t h = ((uint32_t)v * 2654435761u) >> (32 - 8);
         while (atomicCAS(&s_key[h], -1, v) != -1) h = (h + 1) & (kHotSlots - 1);
         s_slot[h] = (unsigned char)tid;
+        const uint32_t b = (uint32_t)v & 8191u;
+        atomicOr(&s_filter[b >> 5], 1u << (b & 31));
         s_pos[tid] = ld_y(y, v);
-        s_accx[tid] = s_accy[tid] = 0.f;
     }
+    for (int q = tid; q < kHot * 4; q += blockDim.x) s_acc[q] = 0;
     __syncthreads();
-    const HotStore<AGG> st{y, A.probe, s_key, s_slot, s_pos, s_accx, s_accy};
+    const float inv = 1.0f / A.hot_scale;
+    const HotStore<AGG> st{y, A.probe, A.hot_scale, s_filter, s_key, s_slot, s_pos, s_acc};
     const int Me = min(A.M, kMaxNeg);
     const int64_t ns = A.n_steps, sd = A.stride;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -706,9 +736,10 @@ __global__ void __launch_bounds__(256, 4)
         __syncthreads();
         if (tid < K) {   // publish the round's increments, refresh the staged position
             const int v = hot[tid];
-            const float dx = s_accx[tid], dy = s_accy[tid];
+            int *a = s_acc + 4 * tid;
+            const float dx = hot_sum(a, inv), dy = hot_sum(a + 2, inv);
             if (dx != 0.f || dy != 0.f) add_y(y, v, dx, dy);
-            s_accx[tid] = s_accy[tid] = 0.f;
+            a[0] = a[1] = a[2] = a[3] = 0;
             s_pos[tid] = ld_y(y, v);
         }
         __syncthreads();
@@ -766,7 +797,12 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    void *args[] = {const_cast<PArgs *>(&P), &y, &hot, &n_hot};
+    PArgs Q = P;
+    {   // the largest increment one add carries: lr * clip per clipped term, 1 + M terms
+        const double big = std::max(1e-30, (double)P.lr * (double)P.clip * (1.0 + P.M));
+        Q.hot_scale = (float)std::exp2(std::min(40.0, std::floor(std::log2(1073741824.0 / big))));
+    }
+    void *args[] = {&Q, &y, &hot, &n_hot};
     const int64_t threads = (int64_t)grid * block;
     void *fn;
     if (hot && n_hot > 0)   // hub level: the hottest nodes staged per block
@@ -1155,6 +1191,7 @@ constexpr size_t kDrawBudget = size_t(256) << 20;
 extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alias,
                                  const uint64_t *src_alias, const float *collapse,
                                  const uint64_t *neg_alias, const int32_t *map, int64_t n,
+                                 int64_t neg_n, int64_t neg_tail_n, double neg_tail_p,
                                  int64_t step_lo,
                                  int64_t n_steps, int t0, int n_epochs, int M, uint64_t seed,
                                  int level, int32_t *out, void *stream) {
@@ -1166,7 +1203,7 @@ extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alia
     D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
     D.src_alias = reinterpret_cast<const uint2 *>(src_alias);
     D.collapse = collapse;
-    D.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+    D.neg = make_negtab(neg_alias, neg_n, neg_tail_n, neg_tail_p);
     D.map = map;
     D.n = n;
     D.step_lo = step_lo;
@@ -1223,6 +1260,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
                                   const uint64_t *row_alias, const uint64_t *src_alias,
                                   const float *collapse, const uint64_t *neg_alias,
                                   const int32_t *map, int64_t n,
+                                  int64_t neg_n, int64_t neg_tail_n, double neg_tail_p,
                                   float *y, int64_t step_lo, int64_t n_steps, int t0, int n_iter,
                                   int iters,
                                   double lr0, double gamma, double eps, double clip, int b, int M,
@@ -1261,7 +1299,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
         A.row_alias = reinterpret_cast<const uint4 *>(row_alias);
         A.src_alias = reinterpret_cast<const uint2 *>(src_alias);
         A.collapse = collapse;
-        A.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+        A.neg = make_negtab(neg_alias, neg_n, neg_tail_n, neg_tail_p);
         A.n = n;
         A.step_lo = step_lo;
         A.n_steps = n_steps;
@@ -1303,7 +1341,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
     D.src_alias = reinterpret_cast<const uint2 *>(src_alias);
     D.collapse = collapse;
-    D.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+    D.neg = make_negtab(neg_alias, neg_n, neg_tail_n, neg_tail_p);
     D.map = map;
     D.n = n;
     D.step_lo = step_lo;
@@ -1796,14 +1834,15 @@ namespace drg {
 namespace {
 // the draw arguments common to a sharded level's segments (drg_shard_epoch / _run)
 DArgs shard_dargs(const int64_t *indptr, const uint64_t *row_alias, const float *collapse,
-                  const uint64_t *neg_alias, const int32_t *map, int64_t n_tab,
+                  const uint64_t *neg_alias, const int32_t *map, int64_t n_tab, NegTab neg,
                   const int32_t *perm, int M, uint64_t seed, int level, int64_t total,
                   unsigned long long *evals) {
     DArgs D;
     D.indptr = indptr;
     D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
     D.collapse = collapse;
-    D.neg_alias = reinterpret_cast<const uint2 *>(neg_alias);
+    (void)neg_alias;
+    D.neg = neg;
     D.map = map;
     D.n = n_tab;
     D.n_epochs = 1;
@@ -1888,7 +1927,8 @@ float lr_of(double lr0, int t, int iters) {
 // out_draws (optional, device int32 [2 + M][total]) receives the draw records.
 extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
                                const float *collapse, const uint64_t *neg_alias,
-                               const int32_t *map, int64_t n_tab, const int32_t *perm,
+                               const int32_t *map, int64_t n_tab, int64_t neg_n,
+                               int64_t neg_tail_n, double neg_tail_p, const int32_t *perm,
                                int nseg, const uint64_t *const *seg_alias, const int64_t *seg_n,
                                const int64_t *seg_lo, const int64_t *step_lo,
                                const int64_t *n_steps, int t, int iters, double lr0,
@@ -1906,7 +1946,8 @@ extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t 
     DRG_CUDA(buf.alloc(sizeof(int32_t) * (size_t)(2 + M) * (size_t)total));
     EvalSlots evs(st);
     DRG_TRY(evs.init(reinterpret_cast<unsigned long long *>(evals), st));
-    const DArgs D = shard_dargs(indptr, row_alias, collapse, neg_alias, map, n_tab, perm, M, seed,
+    const DArgs D = shard_dargs(indptr, row_alias, collapse, neg_alias, map, n_tab,
+                                make_negtab(neg_alias, neg_n, neg_tail_n, neg_tail_p), perm, M, seed,
                                 level, total, evs.slots());
     DRG_TRY(shard_draws(D, nseg, seg_alias, seg_n, seg_lo, step_lo, n_steps, t, 1,
                         buf.as<int32_t>(), st));
@@ -1931,7 +1972,8 @@ extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t 
 // fidelity bounds the real one.
 extern "C" int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
                              const float *collapse, const uint64_t *neg_alias,
-                             const int32_t *map, int64_t n_tab, const int32_t *perm, int nseg,
+                             const int32_t *map, int64_t n_tab, int64_t neg_n,
+                             int64_t neg_tail_n, double neg_tail_p, const int32_t *perm, int nseg,
                              const uint64_t *const *seg_alias, const int64_t *seg_n,
                              const int64_t *seg_lo, const int64_t *step_lo,
                              const int64_t *n_steps, int t0, int n_iter, int iters, double lr0,
@@ -1974,7 +2016,8 @@ extern "C" int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *r
         for (int j = 0; j < n_iter; ++j) DRG_TRY(shard_exchange(c, snap[0], delta[0], st));
         return evs.finish(st);
     }
-    const DArgs D = shard_dargs(indptr, row_alias, collapse, neg_alias, map, n_tab, perm, M, seed,
+    const DArgs D = shard_dargs(indptr, row_alias, collapse, neg_alias, map, n_tab,
+                                make_negtab(neg_alias, neg_n, neg_tail_n, neg_tail_p), perm, M, seed,
                                 level, total, evs.slots());
     const size_t rec_bytes = (size_t)(2 + M) * sizeof(int32_t) * (size_t)total;
     const int K = (int)std::max<int64_t>(1, std::min<int64_t>(n_iter, (int64_t)(kDrawBudget / rec_bytes)));

@@ -430,9 +430,45 @@ class SampledTables:
     # level 0's, ``map`` (int32 [n_0]) the composed parent map to this level
     map: torch.Tensor | None = None
     indptr: torch.Tensor | None = None      # level-0 row offsets of row_alias
-    neg_alias: torch.Tensor | None = None   # level-0 Vose table over Q^0
     mass: torch.Tensor | None = None        # R^l (fp64 [n_l]): partitions for multi-GPU
     hot: torch.Tensor | None = None         # int32: hub level's hottest nodes (staged per block)
+    # the level's negative table Q^l (NegTable); None: the level's own full table
+    neg: "NegTable | None" = None
+
+
+@dataclass
+class NegTable:
+    """Q^l as drawn by the sampled kernels (drg_layout_sampled's neg_* arguments):
+    Vose over the nodes [0, n) and, with probability tail_p, a uniform pick in the
+    tail [n, n + tail_n) -- the isolated nodes, which isolated_last numbers last and
+    which all carry the same floor weight (optimizer.py:258).  Same law as one table
+    over every node, from a table the size of the connected part."""
+
+    alias: torch.Tensor
+    n: int
+    tail_n: int = 0
+    tail_p: float = 0.0
+
+
+def connected_prefix(R: torch.Tensor) -> int:
+    """1 + the last node with graph mass (R > 0): the nodes past it are isolated."""
+    nz = torch.nonzero(R > 0)
+    return int(nz[-1, 0]) + 1 if nz.numel() else 0
+
+
+def build_neg_table(Wn: torch.Tensor, R: torch.Tensor) -> NegTable:
+    """Q^l over the connected prefix + the uniform isolated tail (exact in law: the
+    tail's weights are all equal; otherwise one table over every node)."""
+    n = Wn.numel()
+    k = connected_prefix(R)
+    if 0 < k < n:
+        tail = Wn[k:]
+        if float(tail.max()) == float(tail.min()):
+            tot = float(Wn.sum())
+            alias, _ = _alias_device(Wn[:k].contiguous())
+            return NegTable(alias, k, n - k, float(tail.sum()) / tot if tot > 0 else 0.0)
+    alias, _ = _alias_device(Wn)
+    return NegTable(alias, n)
 
 
 # Steps in flight of the Hogwild update pass (the fidelity knob).  Concurrent steps
@@ -469,20 +505,25 @@ HOT_NODES = 32
 GATHER_STEPS = 32768
 
 
-def build_sampled_tables(ip, tg, P, R) -> SampledTables:
+def build_sampled_tables(ip, tg, P, R, Wn=None) -> SampledTables:
+    """Per-row Vose over P (16-byte records), Vose over R -- over the connected
+    prefix only (isolated nodes have R = 0 and are never a source) -- collapse
+    probabilities, and with ``Wn`` the negative table."""
     n = ip.numel() - 1
     nnz = tg.numel()
     rows = torch.empty((max(nnz, 1), 2), dtype=torch.int64, device=R.device)   # 16 B per entry
     rowsum = torch.empty(max(n, 1), dtype=torch.float64, device=R.device)
     _lib.call("drg_row_alias", _lib.ptr(ip), _lib.ptr(tg), _lib.ptr(P), n, nnz, _lib.ptr(rows),
               _lib.ptr(rowsum), _lib.stream_ptr())
-    src, _ = _alias_device(R)
+    k = connected_prefix(R)
+    src, _ = _alias_device(R[:max(k, 1)].contiguous())
     with torch.no_grad():
         c = torch.where(R > 0, 1.0 - rowsum[:n] / torch.clamp(R, min=1e-300),
                         torch.zeros_like(R)).clamp_(0.0, 1.0).to(torch.float32)
         wsum = (2.0 * n * rowsum[:n]).to(torch.float32)
         hubs = _is_hub_level(R)
-    return SampledTables(src, rows[:nnz], c, wsum, hubs, mass=R, hot=_hot_nodes(R))
+    return SampledTables(src, rows[:nnz], c, wsum, hubs, mass=R, hot=_hot_nodes(R),
+                         neg=None if Wn is None else build_neg_table(Wn, R))
 
 
 def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
@@ -495,11 +536,10 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
     records: the gather modes build them with build_level_data."""
     ip, tg, P, R = ds.indptr, ds.targets, ds.weights, ds.row_mass
     Wn = device_negative_weights(R, neg_power)
-    alias0, _ = _alias_device(Wn)
-    S0 = build_sampled_tables(ip, tg, P, R)
+    S0 = build_sampled_tables(ip, tg, P, R, Wn)
     S0.collapse = None   # no pair collapses at level 0
     n0 = dh.levels[0].node_count
-    out = [LevelData(n0, tg.numel(), ip, None, None, alias0, None, S0)]
+    out = [LevelData(n0, tg.numel(), ip, None, None, None, None, S0)]
     flat = None
     st = _lib.stream_ptr()
     for level in range(1, dh.depth + 1):
@@ -512,9 +552,10 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
             _lib.call("drg_compose_maps", _lib.ptr(flat), _lib.ptr(parent), n0, _lib.ptr(nxt), st)
             flat = nxt
         R = _aggregate_nodes(R, parent, n_l)
+        Wn = _aggregate_nodes(Wn, parent, n_l)   # Q^l: drawn at the level (same law)
         hubs = _is_hub_level(R)
         S = SampledTables(S0.src_alias, S0.row_alias, None, None, hubs, map=flat, indptr=ip,
-                          neg_alias=alias0, mass=R, hot=_hot_nodes(R))
+                          mass=R, hot=_hot_nodes(R), neg=build_neg_table(Wn, R))
         out.append(LevelData(n_l, 0, None, None, None, None, None, S))
     return out
 
@@ -756,7 +797,7 @@ class LayoutPlan:
         o = self.opt
         fine, coarse = sampled_divisors(self.levels[0].n, o)
         div = fine if level == 0 else coarse
-        ip, neg, n_tab, mp = self._tables(level)
+        ip, n_tab, mp, neg = self._tables(level)
         det = o.threads == 1 and not o.sampled_fused
         flags = (int(S.hubs) * _lib.DRG_SAMPLED_AGGREGATE
                  | (_lib.DRG_SAMPLED_FUSED if o.sampled_fused else 0)
@@ -765,7 +806,8 @@ class LayoutPlan:
             self.evals = torch.zeros(1, dtype=torch.int64, device=y.device)
         _lib.call("drg_layout_sampled", _lib.ptr(ip), None,
                   _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), self._collapse(level),
-                  _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(y), step_lo, n_steps, t0, n_iter,
+                  _lib.ptr(neg.alias), _lib.ptr(mp), n_tab, neg.n, neg.tail_n, float(neg.tail_p),
+                  _lib.ptr(y), step_lo, n_steps, t0, n_iter,
                   o.iters,
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
                   o.neg_samples, seed, level,
@@ -780,13 +822,15 @@ class LayoutPlan:
         return None if level == 0 or c is None else _lib.ptr(c)
 
     def _tables(self, level: int):
-        """(row offsets, negative table, table size, map) the draws of ``level`` use:
-        the level's own, or level 0's with the composed map (draw-then-map)."""
+        """(row offsets, source-table size, map, Q^l) the draws of ``level`` use: the
+        level's own pair tables, or level 0's with the composed map (draw-then-map);
+        Q^l always the level's (NegTable)."""
         L = self.levels[level]
         S = L.sampled
+        neg = S.neg if S.neg is not None else NegTable(L.alias, L.n)
         if S.map is None:
-            return L.indptr, L.alias, L.n, None
-        return S.indptr, S.neg_alias, S.map.numel(), S.map
+            return L.indptr, S.src_alias.numel(), None, neg
+        return S.indptr, S.src_alias.numel(), S.map, neg
 
     def sampled_draws(self, level: int, step_lo: int, n_steps: int, t0: int,
                       n_epochs: int = 1) -> torch.Tensor:
@@ -797,11 +841,12 @@ class LayoutPlan:
         if S is None:
             raise RuntimeError("plan was built without sampled-mode tables")
         M = self.opt.neg_samples
-        ip, neg, n_tab, mp = self._tables(level)
+        ip, n_tab, mp, neg = self._tables(level)
         out = torch.empty((n_epochs, 2 + M, n_steps), dtype=torch.int32, device=ip.device)
         _lib.call("drg_sampled_draws", _lib.ptr(ip), _lib.ptr(S.row_alias),
-                  _lib.ptr(S.src_alias), self._collapse(level), _lib.ptr(neg), _lib.ptr(mp),
-                  n_tab, step_lo, n_steps, t0, n_epochs, M, seed, level, _lib.ptr(out),
+                  _lib.ptr(S.src_alias), self._collapse(level), _lib.ptr(neg.alias),
+                  _lib.ptr(mp), n_tab, neg.n, neg.tail_n, float(neg.tail_p), step_lo, n_steps,
+                  t0, n_epochs, M, seed, level, _lib.ptr(out),
                   _lib.stream_ptr())
         return out
 
@@ -928,10 +973,11 @@ class LayoutPlan:
         arr = lambda v: (ctypes.c_int64 * k)(*(v or [0]))   # noqa: E731
         if self.evals is None:
             self.evals = torch.zeros(1, dtype=torch.int64, device=ctx.snap.device)
-        ip, neg, n_tab, mp = self._tables(level)
+        ip, n_tab, mp, neg = self._tables(level)
         flags = _lib.DRG_SHARD_LAGGED if o.shard_lagged else 0
         _lib.call("drg_shard_run", ctx.ctx, _lib.ptr(ip), _lib.ptr(S.row_alias),
-                  self._collapse(level), _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(lay.perm),
+                  self._collapse(level), _lib.ptr(neg.alias), _lib.ptr(mp), n_tab, neg.n,
+                  neg.tail_n, float(neg.tail_p), _lib.ptr(lay.perm),
                   k, (ctypes.c_void_p * k)(*([tb.data_ptr() for tb in tabs] or [None])),
                   arr([lay.seg_n[r] for r in segs]), arr([lay.seg_lo[r] for r in segs]),
                   arr([lay.step_lo[r] for r in segs]), arr([lay.n_steps[r] for r in segs]),
@@ -960,9 +1006,10 @@ class LayoutPlan:
         arr = lambda v: (ctypes.c_int64 * k)(*v)   # noqa: E731
         if max_threads is None:
             max_threads = self._shard_threads(level, lay, segs)
-        ip, neg, n_tab, mp = self._tables(level)
+        ip, n_tab, mp, neg = self._tables(level)
         _lib.call("drg_shard_epoch", ctx.ctx, _lib.ptr(ip), _lib.ptr(S.row_alias),
-                  self._collapse(level), _lib.ptr(neg), _lib.ptr(mp), n_tab, _lib.ptr(lay.perm),
+                  self._collapse(level), _lib.ptr(neg.alias), _lib.ptr(mp), n_tab, neg.n,
+                  neg.tail_n, float(neg.tail_p), _lib.ptr(lay.perm),
                   k, (ctypes.c_void_p * k)(*[tb.data_ptr() for tb in tabs]),
                   arr([lay.seg_n[r] for r in segs]), arr([lay.seg_lo[r] for r in segs]),
                   arr([lay.step_lo[r] for r in segs]), arr([lay.n_steps[r] for r in segs]),

@@ -94,25 +94,80 @@ def barabasi_albert(n: int = 1_000_000, m: int = 4, seed: int = 0, device="cuda"
     return _finish(device_from_edges(pairs, n), device)
 
 
+# R-MAT quadrant draws from a counter-based hash (splitmix64 of (seed, edge, level)):
+# the same edges from torch on the device (the bench) and from numpy on any host
+# (the CPU reference arm of the C5 parity runs, scripts/quality_c5.py)
+_SM_GAMMA = 0x9E3779B97F4A7C15
+_SM_M1 = 0xBF58476D1CE4E5B9
+_SM_M2 = 0x94D049BB133111EB
+_SEED_MIX = 0xD1B54A32D192ED03
+
+
+def _s64(c: int) -> int:   # uint64 constant as the int64 torch holds
+    return c - (1 << 64) if c >= 1 << 63 else c
+
+
+def _rmat_uniform_torch(x: torch.Tensor) -> torch.Tensor:
+    """splitmix64(x) -> float64 in [0, 1) (53 bits); int64 tensors wrap like uint64,
+    right shifts made logical by masking."""
+    def srl(z, k):
+        return (z >> k) & ((1 << (64 - k)) - 1)
+    z = x + _s64(_SM_GAMMA)
+    z = (z ^ srl(z, 30)) * _s64(_SM_M1)
+    z = (z ^ srl(z, 27)) * _s64(_SM_M2)
+    z = z ^ srl(z, 31)
+    return srl(z, 11).to(torch.float64) * (1.0 / (1 << 53))
+
+
+def _rmat_uniform_numpy(x: np.ndarray) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = x + np.uint64(_SM_GAMMA)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(_SM_M1)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(_SM_M2)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * (1.0 / (1 << 53))
+
+
+def rmat_edges(scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19, seed: int = 0,
+               lo: int = 0, hi: int | None = None, device="cuda"):
+    """Draws [lo, hi) of R-MAT(2^scale, edge_factor * 2^scale): level l of draw e takes
+    quadrant a / b / c / d from u = splitmix64(seed * K + 32 e + l) -- an int64 [m, 2]
+    torch tensor (``device``), or a numpy array for device="numpy"."""
+    m = edge_factor << scale
+    hi = m if hi is None else min(hi, m)
+    ab, abc = a + b, a + b + c
+    base = (seed * _SEED_MIX) & ((1 << 64) - 1)
+    if device == "numpy":
+        e = np.arange(lo, hi, dtype=np.uint64)
+        u = np.zeros(hi - lo, dtype=np.int64)
+        v = np.zeros(hi - lo, dtype=np.int64)
+        with np.errstate(over="ignore"):
+            key = e * np.uint64(32) + np.uint64(base)
+        for lev in range(scale):
+            with np.errstate(over="ignore"):
+                r = _rmat_uniform_numpy(key + np.uint64(lev))
+            u = (u << 1) | (r >= ab)
+            v = (v << 1) | (((r >= a) & (r < ab)) | (r >= abc))
+        return np.stack([u, v], 1)
+    e = torch.arange(lo, hi, dtype=torch.int64, device=device)
+    key = e * 32 + _s64(base)
+    u = torch.zeros(hi - lo, dtype=torch.int64, device=device)
+    v = torch.zeros(hi - lo, dtype=torch.int64, device=device)
+    for lev in range(scale):
+        r = _rmat_uniform_torch(key + lev)
+        u = (u << 1) | (r >= ab).to(torch.int64)                          # quadrants c, d
+        v = (v << 1) | (((r >= a) & (r < ab)) | (r >= abc)).to(torch.int64)  # b, d
+    return torch.stack([u, v], 1)
+
+
 def rmat(scale: int = 24, edge_factor: int = 16, a=0.57, b=0.19, c=0.19, seed: int = 0,
          device="cuda", chunk: int = 1 << 26):
-    """R-MAT with 2^scale nodes and edge_factor * 2^scale draws (no relabelling),
-    symmetrised, self-loops and duplicates removed by drg_from_edges."""
+    """R-MAT with 2^scale nodes and edge_factor * 2^scale draws (rmat_edges; no
+    relabelling), symmetrised, self-loops and duplicates removed by drg_from_edges."""
     n = 1 << scale
     m = edge_factor * n
-    g = torch.Generator(device="cuda")
-    g.manual_seed(seed)
-    parts = []
-    for lo in range(0, m, chunk):
-        cnt = min(chunk, m - lo)
-        u = torch.zeros(cnt, dtype=torch.int64, device="cuda")
-        v = torch.zeros(cnt, dtype=torch.int64, device="cuda")
-        for _ in range(scale):
-            r = torch.rand(cnt, device="cuda", generator=g)
-            bit_u = (r >= a + b).to(torch.int64)                    # quadrants c, d
-            bit_v = (((r >= a) & (r < a + b)) | (r >= a + b + c)).to(torch.int64)  # b, d
-            u = (u << 1) | bit_u
-            v = (v << 1) | bit_v
-        parts.append(torch.stack([u, v], 1))
+    parts = [rmat_edges(scale, edge_factor, a, b, c, seed, lo, lo + chunk, device="cuda")
+             for lo in range(0, m, chunk)]
     e = torch.cat(parts)
+    del parts
     return _finish(device_from_edges(e, n), device)

@@ -40,7 +40,8 @@ CONFIGS = {
     # BASELINE C5 at a reduced scale (R-MAT scale 18, 262k nodes): level 0 sampled,
     # the hub-heavy coarse levels gathered -- the mixed plan C5 runs
     "rmat18": dict(k=1, perplexity="auto", iters=500, max_levels=5, force_levels=5,
-                   init="normal", z_pairs=None, np_sample=20_000, np_max_degree=2048, np_k=1),
+                   init="normal", z_pairs=None, np_sample=20_000, np_max_degree=2048, np_k=1,
+                   np_min_degree=1),   # (isolated nodes score 1 in both arms)
     # BASELINE C4 itself: 120^3 mesh, 1.73 M nodes (the bench workload)
     "mesh": dict(k=2, perplexity=50.0, iters=800, max_levels=4, init="normal",
                  z_pairs=None, np_sample=None),
@@ -87,7 +88,8 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
     sample = None
     if cfg["np_sample"]:
         deg = np.diff(og.indptr)
-        pool = np.flatnonzero(deg <= cfg.get("np_max_degree", deg.max()))
+        pool = np.flatnonzero((deg <= cfg.get("np_max_degree", deg.max()))
+                              & (deg >= cfg.get("np_min_degree", 0)))
         sample = np.sort(np.random.default_rng(7).choice(pool, cfg["np_sample"], replace=False))
     results = {"reference": [], **{m: [] for m in modes}}
     threads = os.cpu_count() if og.node_count > 50_000 else 1
@@ -119,6 +121,9 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
                 extra = {"att_samples": int(div)}
             if upd == "sampledv":   # the multi-GPU path on W ranks emulated on this GPU
                 upd, extra = "sampled", {"virtual_ranks": int(div), "threads": 16}
+            elif upd == "sampledvl":   # ... with the lagged (overlapped) exchange
+                upd, extra = "sampled", {"virtual_ranks": int(div), "threads": 16,
+                                         "shard_lagged": True}
             elif upd == "sampledd":   # threads = 1: the deterministic sub-batch form
                 upd, extra = "sampled", {"threads": 1}
             elif upd == "sampled":

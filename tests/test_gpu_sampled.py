@@ -97,6 +97,49 @@ def test_sampled_negative_law(golden, pick):
     assert _chi2(counts, expected) > 1e-6
 
 
+def _negative_law_expected(Q, i, j, M, n):
+    """Per-step law of the negatives: Q redrawn (<= 9) while it hits i or j."""
+    q = Q[i] + np.where(j != i, Q[j], 0.0)
+    f = np.where(q < 1, (1 - q ** 9) / np.maximum(1 - q, 1e-300), 9.0)
+    exp = Q * f.sum() - np.bincount(i, weights=f * Q[i], minlength=n) \
+        - np.bincount(j, weights=np.where(j != i, f * Q[j], 0.0), minlength=n)
+    return np.concatenate([[np.sum(q ** 9)], exp]) * M
+
+
+def test_negative_table_with_isolated_tail():
+    """Q^l drawn as NegTable -- Vose over the connected prefix plus a uniform pick in
+    the isolated tail (isolated_last numbers the isolated nodes last) -- has the law
+    of one table over every node.  The reference's tail weight is a 1e-8 floor; a
+    heavy uniform tail (half the top weight) makes the split visible to chi-square."""
+    from paper_2008_07799_b200.graph import DeviceGraph
+    from paper_2008_07799_b200.optimizer import build_neg_table, prepare_layout
+    rng = np.random.default_rng(4)
+    n_conn, n_iso = 300, 200
+    g = B.from_edges(rng.integers(0, n_conn, size=(900, 2)), n_conn + n_iso)
+    prep = prepare_layout(DeviceGraph.from_host(g), B.SimilarityParams(k=1),
+                          B.OptimizerParams(seed=1, iters=5, threads=4), max_levels=1)
+    plan = prep.plan
+    S = plan.levels[0].sampled
+    R = S.mass
+    n, M = R.numel(), plan.opt.neg_samples
+    w = R.pow(0.75)
+    W = torch.where(R > 0, w, torch.full_like(w, 0.5 * float(w.max())))
+    S.neg = build_neg_table(W, R)
+    assert S.neg.tail_n == int((R == 0).sum()) >= n_iso and S.neg.tail_p > 0.1
+    assert bool((R[:S.neg.n] > 0).any()) and bool((R[S.neg.n:] == 0).all())
+    d = plan.sampled_draws(0, 0, n, 2, 4000).cpu().numpy()
+    i = d[:, 0, :].ravel().astype(np.int64)
+    j = d[:, 1, :].ravel().astype(np.int64)
+    Q = W.cpu().numpy() / float(W.sum())
+    expected = _negative_law_expected(Q, i, j, M, n)
+    negs = d[:, 2:, :].transpose(1, 0, 2).reshape(M, -1)
+    counts = np.bincount(negs.ravel().astype(np.int64) + 1, minlength=n + 1).astype(np.float64)
+    assert _chi2(counts, expected) > 1e-6
+    # the tail as a whole: its share of the first-attempt draws is tail_p
+    tail = (negs >= S.neg.n).mean()
+    assert abs(tail - S.neg.tail_p) < 5 * np.sqrt(S.neg.tail_p / negs.size) + 0.01
+
+
 @pytest.mark.parametrize("b", [1, 2, 3])
 @pytest.mark.parametrize("pick", ["finest", "coarsest"])
 def test_sampled_drawn_step_parity(golden, b, pick):

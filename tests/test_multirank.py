@@ -210,3 +210,16 @@ def test_sampled_small_levels_run_replicated(tmp_path):
         step(y, 0, n, t)
     for r in range(2):
         assert np.array_equal(np.load(out + f".{r}.npy"), y.numpy())
+
+
+def test_rmat_generator_numpy_equals_torch():
+    """synthetic.rmat_edges: the counter-based R-MAT draws are the same from numpy
+    (the CPU reference arm of scripts/quality_c5.py) and from torch (the device)."""
+    from paper_2008_07799_b200 import synthetic
+    for seed, lo, hi in ((0, 0, 40_000), (5, 123_456, 150_000)):
+        a = synthetic.rmat_edges(16, 16, seed=seed, lo=lo, hi=hi, device="numpy")
+        b = synthetic.rmat_edges(16, 16, seed=seed, lo=lo, hi=hi, device="cpu").numpy()
+        assert np.array_equal(a, b)
+    # quadrant law: the high bit of u is set with probability c + d = 0.24
+    a = synthetic.rmat_edges(12, 16, seed=1, device="numpy")
+    assert abs((a[:, 0] >= 2048).mean() - 0.24) < 0.01
