@@ -496,7 +496,7 @@ HUB_STEPS = 512   # warp-aggregate the sampled updates above this per-node rate
 # shared memory (apply_hot_kernel): R-MAT's coarse levels, where one node is the
 # source of up to a third of an epoch's steps, and the C3 BA coarsest level.
 HOT_STEPS = int(os.environ.get("DRG_HOT_STEPS", 4096))   # (env: experiments)
-HOT_NODES = 32
+HOT_NODES = 64
 # Above this per-node rate the sampled epoch serialises on the hub's atomics even
 # warp-aggregated, and the gather (K7 + heavy-row split) is faster: R-MAT's coarse
 # levels (busiest node 2.4e5 - 4.8e6 steps per epoch) -- while R-MAT's level 0
