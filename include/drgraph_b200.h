@@ -200,6 +200,9 @@ int drg_pcg64_permutation(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
  * reference's canonical-pair table plus direction coin (optimizer.py:206-240). */
 int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P, int64_t n,
                   int64_t nnz, uint64_t *out_rec, double *out_rowsum, void *stream);
+/* out_span[i] = {indptr[i], indptr[i+1] - indptr[i]} as two uint32 (requires
+ * indptr[n] < 2^32): the sampled draws' per-node row record. */
+int drg_row_spans(const int64_t *indptr, int64_t n, uint64_t *out_span, void *stream);
 /* n_iter epochs t = t0.. of n_steps steps each, every step being the reference
  * step (_kernels.py:65-140) on the level's positions y (in place, Hogwild):
  * source a ~ src_alias (R^l), collapsed pair (a, a) with probability collapse[a]
@@ -213,7 +216,9 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
  * (isolated nodes at equal floor weight, numbered last; neg_tail_n = 0: none).
  * Steps step_lo .. step_lo + n_steps - 1 of each epoch run here (a rank's share of
  * the epoch in the multi-GPU mode); at most max_threads steps run concurrently.
- * n: entries of src_alias.  map (device int32, may be NULL): the pair tables are
+ * n: entries of src_alias.  row_span (device uint64 per node, may be NULL): {row start,
+ * row length} as two uint32 (drg_row_spans; nnz < 2^32) -- one load per drawn
+ * source instead of the two row offsets.  map (device int32, may be NULL): the pair tables are
  * level 0's and the drawn source and target are mapped to level l through map
  * (composed parent maps), the reference's own draw-then-map (_kernels.py:76-81);
  * the negatives drawn from Q^l directly have the law of its draw-then-map (115).
@@ -239,7 +244,8 @@ int drg_row_alias(const int64_t *indptr, const int32_t *targets, const double *P
 #define DRG_SAMPLED_FUSED 2
 #define DRG_SAMPLED_DETERMINISTIC 4
 
-int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_t *row_alias,
+int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_span, const uint64_t *rec,
+                       const uint64_t *row_alias,
                        const uint64_t *src_alias, const float *collapse,
                        const uint64_t *neg_alias, const int32_t *map, int64_t n,
                        int64_t neg_n, int64_t neg_tail_n, double neg_tail_p, float *y,
@@ -257,7 +263,7 @@ int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec, const uint64_
  * attempts hit i or j) -- exactly the steps drg_layout_sampled runs.
  * drg_sampled_apply: one epoch of those steps on y, at most max_threads steps in
  * flight (max_threads = 1: sequential, the reference kernel's order). */
-int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alias,
+int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_span, const uint64_t *row_alias,
                       const uint64_t *src_alias, const float *collapse,
                       const uint64_t *neg_alias, const int32_t *map, int64_t n,
                       int64_t neg_n, int64_t neg_tail_n, double neg_tail_p, int64_t step_lo,
@@ -314,7 +320,8 @@ int drg_shard_store(void *ctx, float *y, void *stream);
 int drg_shard_exchange(void *ctx, void *stream);
 int drg_shard_fold(void *ctx, float *recv, void *stream);
 int drg_shard_read_part(void *ctx, float *out, void *stream);
-int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
+int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_span,
+                    const uint64_t *row_alias,
                     const float *collapse, const uint64_t *neg_alias, const int32_t *map,
                     int64_t n_tab, int64_t neg_n, int64_t neg_tail_n, double neg_tail_p,
                     const int32_t *perm, int nseg,
@@ -330,7 +337,8 @@ int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
  * emulation, rank -1, runs exactly that worst case).  Needs the NCCL communicator (or
  * rank -1). */
 #define DRG_SHARD_LAGGED 1
-int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
+int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *row_span,
+                  const uint64_t *row_alias,
                   const float *collapse, const uint64_t *neg_alias, const int32_t *map,
                   int64_t n_tab, int64_t neg_n, int64_t neg_tail_n, double neg_tail_p,
                   const int32_t *perm, int nseg, const uint64_t *const *seg_alias,

@@ -60,9 +60,9 @@ SIGNATURES = {
     "drg_shard_exchange": [_P, _P],
     "drg_shard_fold": [_P, _P, _P],
     "drg_shard_read_part": [_P, _P, _P],
-    "drg_shard_epoch": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _P, _I32, _P, _P, _P, _P, _P, _I32, _I32,
+    "drg_shard_epoch": [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _P, _I32, _P, _P, _P, _P, _P, _I32, _I32,
                         _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _P, _P, _P],
-    "drg_shard_run": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _P, _I32, _P, _P, _P, _P, _P, _I32, _I32,
+    "drg_shard_run": [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _P, _I32, _P, _P, _P, _P, _P, _I32, _I32,
                       _I32, _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _I32, _P, _P],
     "drg_khop_source": [_P, _P, _I64, _I32, _I64, _P, _P, _I64, _P, _P],
     "drg_similarity": [_P, _P, _P, _I64, _I64, _I32, _F64, _F64, _I32, _F64, _F64, _P, _P, _P,
@@ -80,11 +80,12 @@ SIGNATURES = {
     "drg_layout_iters": [_P, _P, _P, _P, _I64, _I64, _I64, _P, _P, _I32, _I32, _I32, _F64, _F64,
                          _F64, _F64, _I32, _I32, _U64, _I32, _P, _P, _P, _U32, _P],
     "drg_row_alias": [_P, _P, _P, _I64, _I64, _P, _P, _P],
-    "drg_layout_sampled": [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _P, _I64, _I64, _I32, _I32, _I32,
+    "drg_layout_sampled": [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _P, _I64, _I64, _I32, _I32, _I32,
                            _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _I32, _I64, _P,
                            _P, _I32, _P],
-    "drg_sampled_draws": [_P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _I64, _I64, _I32, _I32, _I32, _U64, _I32,
+    "drg_sampled_draws": [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _I64, _I64, _I32, _I32, _I32, _U64, _I32,
                           _P, _P],
+    "drg_row_spans": [_P, _I64, _P, _P],
     "drg_sampled_apply": [_P, _I64, _P, _F64, _F64, _F64, _F64, _I32, _I32, _I64, _I32, _P],
     "drg_text_lines": [_P, _I64, _I32, _P, _P, _P, _P],
     "drg_parse_lines": [_P, _I64, _P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P],

@@ -71,10 +71,42 @@ struct NegTab {
 __device__ __forceinline__ int64_t bucket(int64_t n, uint32_t hi, uint32_t lo);
 __device__ __forceinline__ int64_t accept(const uint2 rec, int64_t idx, uint32_t coin);
 
-__device__ __forceinline__ int64_t pick_neg(const NegTab &T, const u32x4 &q) {
+// L2 eviction-priority hints (createpolicy + ld.global.nc.L2::cache_hint): in the
+// draw pass the negative table (re-read ~5 times per step) is kept, the one-touch
+// random reads of the multi-GB / 100+ MB tables (row offsets, source table, maps)
+// are evicted first, so the level's Q^l table stays in L2 on R-MAT.
+__device__ __forceinline__ uint64_t l2_keep() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_stream() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint2 ld_hint(const uint2 *a, uint64_t pol) {
+    uint2 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                 : "=r"(r.x), "=r"(r.y) : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int64_t ld_hint(const int64_t *a, uint64_t pol) {
+    int64_t r;
+    asm volatile("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(r) : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int32_t ld_hint(const int32_t *a, uint64_t pol) {
+    int32_t r;
+    asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+    return r;
+}
+
+template <bool HINT = false>
+__device__ __forceinline__ int64_t pick_neg(const NegTab &T, const u32x4 &q, uint64_t pol = 0) {
     if (q.w < T.tail_thr) return T.n + bucket(T.tail_n, q.x, q.y);
     const int64_t bk = bucket(T.n, q.x, q.y);
-    return accept(__ldg(T.alias + bk), bk, q.z);
+    return accept(HINT ? ld_hint(T.alias + bk, pol) : __ldg(T.alias + bk), bk, q.z);
 }
 
 struct SArgs {
@@ -341,6 +373,7 @@ __global__ void __launch_bounds__(256, 3) sampled_kernel(SArgs A, float2 *y) {
 // pair, no attraction), 2 + m = negative m (-1: all 9 attempts hit i or j).
 struct DArgs {
     const int64_t *indptr;
+    const uint2 *span;    // optional {row start, row length} per node: one load, not two
     const uint4 *row_alias;
     const uint2 *src_alias;
     const float *collapse;
@@ -366,12 +399,16 @@ struct DArgs {
 // small blocks: they fit beside the update pass's resident blocks
 constexpr int kDrawBlock = 128;
 
-__global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= A.n_steps * A.n_epochs) return;
-    const int64_t ep = g / A.n_steps, sl = g - ep * A.n_steps;
-    const int64_t s = A.step_lo + sl;
-    const uint32_t c1 = (uint32_t)(s >> 32) ^ ((uint32_t)(A.t_first + (int)ep) << 1);
+// One step's draws, the reference's sequence (_kernels.py:66-119): the directed
+// pair (source ~ R, target by the row's alias table, both mapped to the level) and
+// the M negatives ~ Q^l redrawn (<= 9) while they hit i or j.  The first kMaxNeg
+// negatives land in neg[] (-1: all attempts hit i or j); later ones are written to
+// rest[m * stride] (the split form's records; NULL: M <= kMaxNeg).
+template <bool HINT>
+__device__ __forceinline__ void draw_step(const DArgs &A, int64_t s, uint32_t c1, int64_t &i_out,
+                                          int64_t &j_out, int32_t *neg, int32_t *rest,
+                                          int64_t stride, unsigned &nev) {
+    const uint64_t keep = HINT ? l2_keep() : 0, once = HINT ? l2_stream() : 0;
     SArgs K;   // the counter layout of sampled_kernel
     K.key0 = A.key0;
     K.key1 = A.key1;
@@ -381,18 +418,26 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
     const u32x4 r2 = philox4x32<7>(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xfe00u, 0x3c6ef372u},
                                    A.key0, A.key1);
     const int64_t sb = bucket(A.n_src, r.x, r.y);
-    const uint2 srec = __ldg(A.src_alias + sb);
+    const uint2 srec = HINT ? ld_hint(A.src_alias + sb, once) : __ldg(A.src_alias + sb);
     const int Me = min(A.M, kMaxNeg);
     int32_t cand[kMaxNeg];
 #pragma unroll
     for (int m = 0; m < kMaxNeg; ++m) {
         if (m < Me) {
-            cand[m] = (int32_t)pick_neg(A.neg, neg_draw(K, s, c1, m, 0));
+            cand[m] = (int32_t)pick_neg<HINT>(A.neg, neg_draw(K, s, c1, m, 0), keep);
         }
     }
     int64_t i = accept(srec, sb, r.z);
     i = A.src_perm ? (int64_t)__ldg(A.src_perm + A.src_lo + i) : A.src_lo + i;
-    const int64_t lo = __ldg(A.indptr + i), hi = __ldg(A.indptr + i + 1);
+    int64_t lo, hi;
+    if (A.span) {
+        const uint2 sp = HINT ? ld_hint(A.span + i, once) : __ldg(A.span + i);
+        lo = sp.x;
+        hi = lo + sp.y;
+    } else {
+        lo = HINT ? ld_hint(A.indptr + i, once) : __ldg(A.indptr + i);
+        hi = HINT ? ld_hint(A.indptr + i + 1, once) : __ldg(A.indptr + i + 1);
+    }
     const float cprob = A.collapse ? __ldg(A.collapse + i) : 0.0f;   // NULL: none
     int64_t j = i;
     if ((A.probe & 2) && hi > lo) {
@@ -404,13 +449,10 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
         j = (u32_to_unit(r2.z) < __uint_as_float(rrec.x)) ? (int64_t)rrec.z : (int64_t)rrec.y;
     }
     if (A.map) {   // the level-0 pair as seen at level l (_kernels.py:76-81)
-        i = __ldg(A.map + i);
-        j = __ldg(A.map + j);
+        i = HINT ? ld_hint(A.map + i, once) : __ldg(A.map + i);
+        j = HINT ? ld_hint(A.map + j, once) : __ldg(A.map + j);
     }
-    int32_t *o = A.out + ep * (int64_t)(2 + A.M) * A.out_stride + sl;
-    __stcs(o, (int32_t)i);   // read once by the update pass: streaming stores
-    __stcs(o + A.out_stride, (int32_t)j);
-    unsigned nev = i != j;
+    nev += i != j;
     for (int m = 0; m < A.M; ++m) {
         int64_t target = -1;
         int first = 0;
@@ -423,12 +465,40 @@ __global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
             first = 1;
         }
         for (int attempt = first; target < 0 && attempt < 9; ++attempt) {
-            const int64_t c0 = pick_neg(A.neg, neg_draw(K, s, c1, m, attempt));
+            const int64_t c0 = pick_neg<HINT>(A.neg, neg_draw(K, s, c1, m, attempt), keep);
             if (c0 != i && c0 != j) target = c0;
         }
-        __stcs(o + (int64_t)(2 + m) * A.out_stride, (int32_t)target);
         nev += target >= 0;
+        if (m < Me) {
+#pragma unroll
+            for (int q = 0; q < kMaxNeg; ++q)
+                if (q == m) neg[q] = (int32_t)target;
+        } else {
+            __stcs(rest + (int64_t)(m - Me) * stride, (int32_t)target);
+        }
     }
+    i_out = i;
+    j_out = j;
+}
+
+template <bool HINT>
+__global__ void __launch_bounds__(kDrawBlock) draw_kernel(DArgs A) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= A.n_steps * A.n_epochs) return;
+    const int64_t ep = g / A.n_steps, sl = g - ep * A.n_steps;
+    const int64_t s = A.step_lo + sl;
+    const uint32_t c1 = (uint32_t)(s >> 32) ^ ((uint32_t)(A.t_first + (int)ep) << 1);
+    const int Me = min(A.M, kMaxNeg);
+    int32_t *o = A.out + ep * (int64_t)(2 + A.M) * A.out_stride + sl;
+    int64_t i, j;
+    int32_t neg[kMaxNeg];
+    unsigned nev = 0;
+    draw_step<HINT>(A, s, c1, i, j, neg, o + (int64_t)(2 + Me) * A.out_stride, A.out_stride, nev);
+    __stcs(o, (int32_t)i);   // read once by the update pass: streaming stores
+    __stcs(o + A.out_stride, (int32_t)j);
+#pragma unroll
+    for (int m = 0; m < kMaxNeg; ++m)
+        if (m < Me) __stcs(o + (int64_t)(2 + m) * A.out_stride, neg[m]);
     count_evals(A.evals, nev);
 }
 
@@ -443,7 +513,15 @@ NegTab make_negtab(const uint64_t *alias, int64_t n, int64_t tail_n, double tail
 }
 
 int launch_draws(const DArgs &D, cudaStream_t st) {
-    draw_kernel<<<(unsigned)ceil_div(D.n_steps * D.n_epochs, kDrawBlock), kDrawBlock, 0, st>>>(D);
+    static const bool hints = [] {
+        // measured: R-MAT scale 24 +1%, the C4 mesh -6% (its tables fit L2 and the
+        // evict-first reads are re-read there): off unless DRG_DRAW_HINTS=1
+        const char *e = getenv("DRG_DRAW_HINTS");
+        return e && e[0] == '1';
+    }();
+    const unsigned grid = (unsigned)ceil_div(D.n_steps * D.n_epochs, kDrawBlock);
+    if (hints) draw_kernel<true><<<grid, kDrawBlock, 0, st>>>(D);
+    else draw_kernel<false><<<grid, kDrawBlock, 0, st>>>(D);
     DRG_LAUNCHED("draw_kernel");
     return DRG_OK;
 }
@@ -709,14 +787,14 @@ __global__ void __launch_bounds__(256, 4)
     for (int q = tid; q < kHotSlots; q += blockDim.x) s_key[q] = -1;
     for (int q = tid; q < kHotFilterWords; q += blockDim.x) s_filter[q] = 0u;
     __syncthreads();
-    if (tid < K) {
-        const int v = hot[tid];
+    for (int q = tid; q < K; q += blockDim.x) {   // (blocks may be smaller than K)
+        const int v = hot[q];
         uint32_t h = ((uint32_t)v * 2654435761u) >> (32 - 8);
         while (atomicCAS(&s_key[h], -1, v) != -1) h = (h + 1) & (kHotSlots - 1);
-        s_slot[h] = (unsigned char)tid;
+        s_slot[h] = (unsigned char)q;
         const uint32_t b = (uint32_t)v & 8191u;
         atomicOr(&s_filter[b >> 5], 1u << (b & 31));
-        s_pos[tid] = ld_y(y, v);
+        s_pos[q] = ld_y(y, v);
     }
     for (int q = tid; q < kHot * 4; q += blockDim.x) s_acc[q] = 0;
     __syncthreads();
@@ -734,16 +812,75 @@ __global__ void __launch_bounds__(256, 4)
             step_body<B>(A, st, __ldcs(A.draws + sl), __ldcs(A.draws + sd + sl), cand, sl);
         }
         __syncthreads();
-        if (tid < K) {   // publish the round's increments, refresh the staged position
-            const int v = hot[tid];
-            int *a = s_acc + 4 * tid;
+        for (int q = tid; q < K; q += blockDim.x) {   // publish the round's increments,
+            const int v = hot[q];                        // refresh the staged position
+            int *a = s_acc + 4 * q;
             const float dx = hot_sum(a, inv), dy = hot_sum(a + 2, inv);
             if (dx != 0.f || dy != 0.f) add_y(y, v, dx, dy);
             a[0] = a[1] = a[2] = a[3] = 0;
-            s_pos[tid] = ld_y(y, v);
+            s_pos[q] = ld_y(y, v);
         }
         __syncthreads();
     }
+}
+
+// Hub levels drawn inline: each round's steps drawn by draw_step (no draw records
+// written and re-read) and applied through the hot store.  The draws' random DRAM
+// reads then overlap other warps' updates inside one kernel, where the split form
+// runs a draw pass and an update pass that each fill the SMs.  M <= kMaxNeg.
+template <bool AGG, int B>
+__global__ void __launch_bounds__(256, 4)
+    apply_hot_fused_kernel(DArgs D, PArgs A, float2 *y, const int32_t *__restrict__ hot,
+                           int n_hot) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ unsigned s_filter[kHotFilterWords];
+    __shared__ int s_key[kHotSlots];
+    __shared__ unsigned char s_slot[kHotSlots];
+    __shared__ float2 s_pos[kHot];
+    __shared__ int s_acc[kHot * 4];
+    const int tid = threadIdx.x;
+    const int K = min(n_hot, kHot);
+    for (int q = tid; q < kHotSlots; q += blockDim.x) s_key[q] = -1;
+    for (int q = tid; q < kHotFilterWords; q += blockDim.x) s_filter[q] = 0u;
+    __syncthreads();
+    for (int q = tid; q < K; q += blockDim.x) {   // (blocks may be smaller than K)
+        const int v = hot[q];
+        uint32_t h = ((uint32_t)v * 2654435761u) >> (32 - 8);
+        while (atomicCAS(&s_key[h], -1, v) != -1) h = (h + 1) & (kHotSlots - 1);
+        s_slot[h] = (unsigned char)q;
+        const uint32_t b = (uint32_t)v & 8191u;
+        atomicOr(&s_filter[b >> 5], 1u << (b & 31));
+        s_pos[q] = ld_y(y, v);
+    }
+    for (int q = tid; q < kHot * 4; q += blockDim.x) s_acc[q] = 0;
+    __syncthreads();
+    const float inv = 1.0f / A.hot_scale;
+    const HotStore<AGG> st{y, A.probe, A.hot_scale, s_filter, s_key, s_slot, s_pos, s_acc};
+    const int64_t ns = A.n_steps;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const uint32_t tt = (uint32_t)D.t_first << 1;
+    unsigned nev = 0;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ns; base += nthreads) {
+        const int64_t sl = base + tid;
+        if (sl < ns) {
+            const int64_t s = D.step_lo + sl;
+            int64_t i, j;
+            int32_t cand[kMaxNeg];
+            draw_step<false>(D, s, (uint32_t)(s >> 32) ^ tt, i, j, cand, nullptr, 0, nev);
+            step_body<B>(A, st, i, j, cand, sl);
+        }
+        __syncthreads();
+        for (int q = tid; q < K; q += blockDim.x) {   // publish the round's increments,
+            const int v = hot[q];                        // refresh the staged position
+            int *a = s_acc + 4 * q;
+            const float dx = hot_sum(a, inv), dy = hot_sum(a + 2, inv);
+            if (dx != 0.f || dy != 0.f) add_y(y, v, dx, dy);
+            a[0] = a[1] = a[2] = a[3] = 0;
+            s_pos[q] = ld_y(y, v);
+        }
+        __syncthreads();
+    }
+    count_evals(D.evals, nev);
 }
 
 template <bool AGG, int B>
@@ -786,6 +923,38 @@ void *apply_instance(int b, int64_t threads = INT64_MAX) {
 // Consecutive epochs on one stream as programmatic dependent launches: the next
 // grid is set up while the previous drains (its griddepcontrol.wait holds the
 // steps back), so small levels do not pay the full launch gap per epoch.
+// apply_hot_kernel's fixed-point scale: the largest increment one add carries is
+// lr * clip per clipped term, 1 + M terms; kept below 2^30
+float hot_scale_for(const PArgs &P) {
+    const double big = std::max(1e-30, (double)P.lr * (double)P.clip * (1.0 + P.M));
+    return (float)std::exp2(std::min(40.0, std::floor(std::log2(1073741824.0 / big))));
+}
+
+// one epoch of a hub level with the draws inline (apply_hot_fused_kernel), PDL
+int launch_hot_fused(const DArgs &D, const PArgs &P, float2 *y, unsigned grid, int block,
+                     bool agg, const int32_t *hot, int n_hot, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PArgs Q = P;
+    Q.hot_scale = hot_scale_for(P);
+    DArgs E = D;
+    void *args[] = {&E, &Q, &y, &hot, &n_hot};
+    void *fn = agg ? (P.b == 2 ? (void *)apply_hot_fused_kernel<true, 2>
+                               : (void *)apply_hot_fused_kernel<true, 0>)
+                   : (P.b == 2 ? (void *)apply_hot_fused_kernel<false, 2>
+                               : (void *)apply_hot_fused_kernel<false, 0>);
+    DRG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+    DRG_LAUNCHED("apply_hot_fused_kernel");
+    return DRG_OK;
+}
+
 int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, cudaStream_t st,
                  const int32_t *hot = nullptr, int n_hot = 0) {
     cudaLaunchConfig_t cfg = {};
@@ -798,10 +967,7 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     PArgs Q = P;
-    {   // the largest increment one add carries: lr * clip per clipped term, 1 + M terms
-        const double big = std::max(1e-30, (double)P.lr * (double)P.clip * (1.0 + P.M));
-        Q.hot_scale = (float)std::exp2(std::min(40.0, std::floor(std::log2(1073741824.0 / big))));
-    }
+    Q.hot_scale = hot_scale_for(P);
     void *args[] = {&Q, &y, &hot, &n_hot};
     const int64_t threads = (int64_t)grid * block;
     void *fn;
@@ -1188,7 +1354,33 @@ constexpr size_t kDrawBudget = size_t(256) << 20;
 
 }  // namespace
 
-extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alias,
+namespace drg {
+namespace {
+__global__ void row_spans_kernel(const int64_t *__restrict__ indptr, int64_t n, uint2 *out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t lo = indptr[i];
+        out[i] = make_uint2((uint32_t)lo, (uint32_t)(indptr[i + 1] - lo));
+    }
+}
+}  // namespace
+}  // namespace drg
+
+extern "C" int drg_row_spans(const int64_t *indptr, int64_t n, uint64_t *out_span, void *stream) {
+    if (n <= 0) return DRG_OK;
+    int64_t last = 0;
+    DRG_CUDA(cudaMemcpyAsync(&last, indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                             as_stream(stream)));
+    DRG_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    if (last >= (int64_t)1 << 32) return fail(DRG_ERR_UNSUPPORTED, "row spans need nnz < 2^32");
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, 256), sm_count() * 16);
+    row_spans_kernel<<<grid, 256, 0, as_stream(stream)>>>(indptr, n, reinterpret_cast<uint2 *>(out_span));
+    DRG_LAUNCHED("row_spans_kernel");
+    return DRG_OK;
+}
+
+extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_span,
+                                 const uint64_t *row_alias,
                                  const uint64_t *src_alias, const float *collapse,
                                  const uint64_t *neg_alias, const int32_t *map, int64_t n,
                                  int64_t neg_n, int64_t neg_tail_n, double neg_tail_p,
@@ -1200,6 +1392,7 @@ extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_alia
     if (M < 0) return fail(DRG_ERR_INVALID, "M must be >= 0");
     DArgs D;
     D.indptr = indptr;
+    D.span = reinterpret_cast<const uint2 *>(row_span);
     D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
     D.src_alias = reinterpret_cast<const uint2 *>(src_alias);
     D.collapse = collapse;
@@ -1256,7 +1449,8 @@ extern "C" int drg_sampled_apply(const int32_t *draws, int64_t n_steps, float *y
     return DRG_OK;
 }
 
-extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
+extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_span,
+                                  const uint64_t *rec,
                                   const uint64_t *row_alias, const uint64_t *src_alias,
                                   const float *collapse, const uint64_t *neg_alias,
                                   const int32_t *map, int64_t n,
@@ -1338,6 +1532,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     DRG_CUDA(cudaStreamWaitEvent(ss.hi, ev.e[0], 0));
     DArgs D;
     D.indptr = indptr;
+    D.span = reinterpret_cast<const uint2 *>(row_span);
     D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
     D.src_alias = reinterpret_cast<const uint2 *>(src_alias);
     D.collapse = collapse;
@@ -1365,8 +1560,6 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
         DRG_CUDA(cudaEventRecord(ev.e[1 + (c & 1)], ss.lo));
         return DRG_OK;
     };
-    int rc = draw(0);
-    if (rc) return rc;
     PArgs P;
     P.n_steps = n_steps;
     P.stride = n_steps;
@@ -1378,6 +1571,25 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *rec,
     P.b = b;
     P.M = M;
     P.probe = probe;
+    // hub levels whose hottest nodes are staged: the draws inline, no draw pass
+    static const bool hot_fused = [] {   // DRG_HOT_FUSED=0: the split form there too
+        const char *e = getenv("DRG_HOT_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    if (hot && n_hot > 0 && !det && M <= kMaxNeg && hot_fused) {
+        for (int j = 0; j < n_iter; ++j) {
+            D.t_first = t0 + j;
+            D.n_epochs = 1;
+            P.lr = lr_at(t0 + j);
+            DRG_TRY(launch_hot_fused(D, P, reinterpret_cast<float2 *>(y), grid, block, agg, hot,
+                                     n_hot, ss.hi));
+        }
+        DRG_CUDA(cudaEventRecord(ev.e[0], ss.hi));
+        DRG_CUDA(cudaStreamWaitEvent(st, ev.e[0], 0));
+        return evs.finish(st);
+    }
+    int rc = draw(0);
+    if (rc) return rc;
     Scratch delta(st);
     if (det) {   // fixed-point increments of a sub-batch, zero between sub-batches
         DRG_CUDA(delta.alloc(sizeof(unsigned long long) * 2 * (size_t)n_y));
@@ -1833,12 +2045,14 @@ extern "C" int drg_shard_read_part(void *ctx, float *out, void *stream) {
 namespace drg {
 namespace {
 // the draw arguments common to a sharded level's segments (drg_shard_epoch / _run)
-DArgs shard_dargs(const int64_t *indptr, const uint64_t *row_alias, const float *collapse,
+DArgs shard_dargs(const int64_t *indptr, const uint64_t *row_span, const uint64_t *row_alias,
+                  const float *collapse,
                   const uint64_t *neg_alias, const int32_t *map, int64_t n_tab, NegTab neg,
                   const int32_t *perm, int M, uint64_t seed, int level, int64_t total,
                   unsigned long long *evals) {
     DArgs D;
     D.indptr = indptr;
+    D.span = reinterpret_cast<const uint2 *>(row_span);
     D.row_alias = reinterpret_cast<const uint4 *>(row_alias);
     D.collapse = collapse;
     (void)neg_alias;
@@ -1925,7 +2139,8 @@ float lr_of(double lr0, int t, int iters) {
 // perm[seg_lo[s] + q] or seg_lo[s] + q), all segments' steps then applied by one
 // launch with <= max_threads steps in flight.  No exchange (drg_shard_exchange).
 // out_draws (optional, device int32 [2 + M][total]) receives the draw records.
-extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
+extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_span,
+                               const uint64_t *row_alias,
                                const float *collapse, const uint64_t *neg_alias,
                                const int32_t *map, int64_t n_tab, int64_t neg_n,
                                int64_t neg_tail_n, double neg_tail_p, const int32_t *perm,
@@ -1946,7 +2161,7 @@ extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t 
     DRG_CUDA(buf.alloc(sizeof(int32_t) * (size_t)(2 + M) * (size_t)total));
     EvalSlots evs(st);
     DRG_TRY(evs.init(reinterpret_cast<unsigned long long *>(evals), st));
-    const DArgs D = shard_dargs(indptr, row_alias, collapse, neg_alias, map, n_tab,
+    const DArgs D = shard_dargs(indptr, row_span, row_alias, collapse, neg_alias, map, n_tab,
                                 make_negtab(neg_alias, neg_n, neg_tail_n, neg_tail_p), perm, M, seed,
                                 level, total, evs.slots());
     DRG_TRY(shard_draws(D, nseg, seg_alias, seg_n, seg_lo, step_lo, n_steps, t, 1,
@@ -1970,7 +2185,8 @@ extern "C" int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t 
 // epoch t - 2 (at the latest) and its reactions folded in by the end of epoch t + 1.
 // The emulation (rank -1) runs the lagged form in that worst-case order, so its
 // fidelity bounds the real one.
-extern "C" int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *row_alias,
+extern "C" int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *row_span,
+                             const uint64_t *row_alias,
                              const float *collapse, const uint64_t *neg_alias,
                              const int32_t *map, int64_t n_tab, int64_t neg_n,
                              int64_t neg_tail_n, double neg_tail_p, const int32_t *perm, int nseg,
@@ -2016,7 +2232,7 @@ extern "C" int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *r
         for (int j = 0; j < n_iter; ++j) DRG_TRY(shard_exchange(c, snap[0], delta[0], st));
         return evs.finish(st);
     }
-    const DArgs D = shard_dargs(indptr, row_alias, collapse, neg_alias, map, n_tab,
+    const DArgs D = shard_dargs(indptr, row_span, row_alias, collapse, neg_alias, map, n_tab,
                                 make_negtab(neg_alias, neg_n, neg_tail_n, neg_tail_p), perm, M, seed,
                                 level, total, evs.slots());
     const size_t rec_bytes = (size_t)(2 + M) * sizeof(int32_t) * (size_t)total;

@@ -14,9 +14,12 @@ north star); parity is single-step (tests/test_gpu_parity.py) and final-layout
 KL / neighbourhood preservation (tests/test_gpu_quality.py).
 
 Multi-GPU: with a torch.distributed process group, levels with at least
-``shard_min_nodes`` nodes are node-range sharded -- each rank updates its rows and
-an all-gather (NCCL over NVLink) refreshes the replicated Y every iteration;
-smaller levels run replicated (identical on every rank, no traffic).
+``shard_min_nodes`` nodes are partitioned by node range.  update="sampled"
+(shard.py): one distributed Y that every rank maps over NVLink, each rank running
+the steps whose source it owns, negatives' reactions folded by a reduce-scatter +
+all-gather per epoch (drg_shard_run); the gather modes: each rank updates its rows
+and an all-gather refreshes the replicated Y every iteration.  Smaller levels run
+replicated (an epoch there is shorter than one exchange).
 """
 
 from __future__ import annotations
@@ -96,7 +99,10 @@ class OptimizerParams:
     threads: int = 1
     init: str = "normal"
     update: str = "sampled"
-    shard_min_nodes: int = 65536
+    # multi-GPU: levels of at least this many nodes are partitioned over the ranks;
+    # smaller ones run replicated -- their epochs (C4 level 1: 21 us for 142 k
+    # nodes) are shorter than one NVLink exchange
+    shard_min_nodes: int = 1 << 20
     # update="sampled": n_0 / this many steps in flight on level 0, n_l / the coarse
     # value on coarser levels; None = by graph size (sampled_divisors)
     sampled_concurrency: int | None = None
@@ -434,6 +440,7 @@ class SampledTables:
     hot: torch.Tensor | None = None         # int32: hub level's hottest nodes (staged per block)
     # the level's negative table Q^l (NegTable); None: the level's own full table
     neg: "NegTable | None" = None
+    span: torch.Tensor | None = None        # int64 [n_0] {row start, length} (drg_row_spans)
 
 
 @dataclass
@@ -517,13 +524,17 @@ def build_sampled_tables(ip, tg, P, R, Wn=None) -> SampledTables:
               _lib.ptr(rowsum), _lib.stream_ptr())
     k = connected_prefix(R)
     src, _ = _alias_device(R[:max(k, 1)].contiguous())
+    span = None
+    if nnz < (1 << 32):
+        span = torch.empty(max(n, 1), dtype=torch.int64, device=R.device)
+        _lib.call("drg_row_spans", _lib.ptr(ip), n, _lib.ptr(span), _lib.stream_ptr())
     with torch.no_grad():
         c = torch.where(R > 0, 1.0 - rowsum[:n] / torch.clamp(R, min=1e-300),
                         torch.zeros_like(R)).clamp_(0.0, 1.0).to(torch.float32)
         wsum = (2.0 * n * rowsum[:n]).to(torch.float32)
         hubs = _is_hub_level(R)
     return SampledTables(src, rows[:nnz], c, wsum, hubs, mass=R, hot=_hot_nodes(R),
-                         neg=None if Wn is None else build_neg_table(Wn, R))
+                         neg=None if Wn is None else build_neg_table(Wn, R), span=span)
 
 
 def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
@@ -555,7 +566,7 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
         Wn = _aggregate_nodes(Wn, parent, n_l)   # Q^l: drawn at the level (same law)
         hubs = _is_hub_level(R)
         S = SampledTables(S0.src_alias, S0.row_alias, None, None, hubs, map=flat, indptr=ip,
-                          mass=R, hot=_hot_nodes(R), neg=build_neg_table(Wn, R))
+                          mass=R, hot=_hot_nodes(R), neg=build_neg_table(Wn, R), span=S0.span)
         out.append(LevelData(n_l, 0, None, None, None, None, None, S))
     return out
 
@@ -804,7 +815,7 @@ class LayoutPlan:
                  | (_lib.DRG_SAMPLED_DETERMINISTIC if det else 0))
         if self.evals is None:
             self.evals = torch.zeros(1, dtype=torch.int64, device=y.device)
-        _lib.call("drg_layout_sampled", _lib.ptr(ip), None,
+        _lib.call("drg_layout_sampled", _lib.ptr(ip), _lib.ptr(S.span), None,
                   _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), self._collapse(level),
                   _lib.ptr(neg.alias), _lib.ptr(mp), n_tab, neg.n, neg.tail_n, float(neg.tail_p),
                   _lib.ptr(y), step_lo, n_steps, t0, n_iter,
@@ -843,7 +854,7 @@ class LayoutPlan:
         M = self.opt.neg_samples
         ip, n_tab, mp, neg = self._tables(level)
         out = torch.empty((n_epochs, 2 + M, n_steps), dtype=torch.int32, device=ip.device)
-        _lib.call("drg_sampled_draws", _lib.ptr(ip), _lib.ptr(S.row_alias),
+        _lib.call("drg_sampled_draws", _lib.ptr(ip), _lib.ptr(S.span), _lib.ptr(S.row_alias),
                   _lib.ptr(S.src_alias), self._collapse(level), _lib.ptr(neg.alias),
                   _lib.ptr(mp), n_tab, neg.n, neg.tail_n, float(neg.tail_p), step_lo, n_steps,
                   t0, n_epochs, M, seed, level, _lib.ptr(out),
@@ -975,7 +986,7 @@ class LayoutPlan:
             self.evals = torch.zeros(1, dtype=torch.int64, device=ctx.snap.device)
         ip, n_tab, mp, neg = self._tables(level)
         flags = _lib.DRG_SHARD_LAGGED if o.shard_lagged else 0
-        _lib.call("drg_shard_run", ctx.ctx, _lib.ptr(ip), _lib.ptr(S.row_alias),
+        _lib.call("drg_shard_run", ctx.ctx, _lib.ptr(ip), _lib.ptr(S.span), _lib.ptr(S.row_alias),
                   self._collapse(level), _lib.ptr(neg.alias), _lib.ptr(mp), n_tab, neg.n,
                   neg.tail_n, float(neg.tail_p), _lib.ptr(lay.perm),
                   k, (ctypes.c_void_p * k)(*([tb.data_ptr() for tb in tabs] or [None])),
@@ -1007,7 +1018,7 @@ class LayoutPlan:
         if max_threads is None:
             max_threads = self._shard_threads(level, lay, segs)
         ip, n_tab, mp, neg = self._tables(level)
-        _lib.call("drg_shard_epoch", ctx.ctx, _lib.ptr(ip), _lib.ptr(S.row_alias),
+        _lib.call("drg_shard_epoch", ctx.ctx, _lib.ptr(ip), _lib.ptr(S.span), _lib.ptr(S.row_alias),
                   self._collapse(level), _lib.ptr(neg.alias), _lib.ptr(mp), n_tab, neg.n,
                   neg.tail_n, float(neg.tail_p), _lib.ptr(lay.perm),
                   k, (ctypes.c_void_p * k)(*[tb.data_ptr() for tb in tabs]),

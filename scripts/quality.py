@@ -120,10 +120,11 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
             elif div and upd == "sgather":
                 extra = {"att_samples": int(div)}
             if upd == "sampledv":   # the multi-GPU path on W ranks emulated on this GPU
-                upd, extra = "sampled", {"virtual_ranks": int(div), "threads": 16}
+                upd, extra = "sampled", {"virtual_ranks": int(div), "threads": 16,
+                                         "shard_min_nodes": 65536}
             elif upd == "sampledvl":   # ... with the lagged (overlapped) exchange
                 upd, extra = "sampled", {"virtual_ranks": int(div), "threads": 16,
-                                         "shard_lagged": True}
+                                         "shard_lagged": True, "shard_min_nodes": 65536}
             elif upd == "sampledd":   # threads = 1: the deterministic sub-batch form
                 upd, extra = "sampled", {"threads": 1}
             elif upd == "sampled":

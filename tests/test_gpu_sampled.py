@@ -224,3 +224,40 @@ def test_fused_and_split_epochs_agree_sequentially(golden):
     moved = [(o - y0).abs().sum(1) > 0 for o in outs]
     assert torch.equal(moved[0], moved[1]) and bool(moved[0].any())
     torch.testing.assert_close(outs[0], outs[1], rtol=0, atol=1e-3)
+
+
+@pytest.mark.parametrize("threads", [1, 256])
+def test_hub_level_inline_draws_run_the_drawn_steps(threads):
+    """Hub levels (hot nodes staged per block) draw inline (apply_hot_fused_kernel):
+    one step in flight, the epoch equals the oracle's sequential replay of exactly
+    the steps drg_sampled_draws reports; many in flight, it stays finite and moves
+    the hub."""
+    from paper_2008_07799_b200.graph import DeviceGraph
+    from paper_2008_07799_b200.optimizer import prepare_layout
+    rng = np.random.default_rng(8)
+    n = 20_001
+    hub = np.column_stack([np.zeros(n - 1, dtype=np.int64), np.arange(1, n)])
+    g = O.from_edges(np.concatenate([hub, rng.integers(1, n, size=(4000, 2))]), n)
+    gg = B.Graph(np.asarray(g.indptr, dtype=np.int64), np.asarray(g.indices, dtype=np.int32))
+    prep = prepare_layout(DeviceGraph.from_host(gg), B.SimilarityParams(k=1),
+                          B.OptimizerParams(seed=1, iters=10, threads=4), min_size=16)
+    plan = prep.plan
+    S = plan.levels[0].sampled
+    assert S.hot is not None and S.hubs
+    # every step moves the hub: at lr ~ 1 the star's sequential dynamics amplify
+    # fp32-vs-fp64 rounding chaotically; at lr0 = 0.02 they stay near-linear
+    plan.opt.lr0 = 0.02
+    t = 2
+    _, gamma, _ = plan._level_args(0)
+    d = plan.sampled_draws(0, 0, n, t)[0]
+    y = rng.normal(0, 1.0, size=(n, 2)).astype(np.float32)
+    yd = torch.from_numpy(y).cuda()
+    plan.sampled_steps(0, yd, 0, n, t, 1, max_threads=threads)
+    got = yd.cpu().numpy()
+    assert np.isfinite(got).all()
+    hub_id = int(S.hot[0])
+    assert not np.array_equal(got[hub_id], y[hub_id])
+    if threads == 1:
+        want = O.drawn_steps(y.astype(np.float64), d.cpu().numpy(), 0.02 * (1.0 - t / 10),
+                             gamma, 1e-3, 5.0, plan.opt.b)
+        np.testing.assert_allclose(got, want, rtol=0, atol=1e-4)
