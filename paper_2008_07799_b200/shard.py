@@ -25,6 +25,7 @@ The CUDA side is the drg_shard_* family of include/drgraph_b200.h.
 from __future__ import annotations
 
 import ctypes
+import logging
 from dataclasses import dataclass
 
 import numpy as np
@@ -33,6 +34,7 @@ import torch
 from . import _lib
 
 MAX_PARTS = 8
+log = logging.getLogger("drgraph")
 
 
 @dataclass
@@ -141,15 +143,25 @@ class ShardContext:
         for r, hb in enumerate(handles):
             if r != self.rank:
                 _lib.call("drg_shard_open_peer", self.ctx, r, (ctypes.c_uint8 * 64)(*hb))
-        if dist.get_backend(self.group) == "nccl":
+        self.device_collectives = dist.get_backend(self.group) == "nccl"
+        if self.device_collectives:
+            # the library's own communicator (the exchange inside drg_shard_run);
+            # should libnccl not load, torch's NCCL group does the same exchange
+            # epoch by epoch (_exchange_host with device tensors)
             uid = (ctypes.c_uint8 * 128)()
+            ok = 1
             if self.rank == 0:
-                _lib.call("drg_nccl_unique_id", uid)
-            obj = [bytes(uid)]
+                try:
+                    _lib.call("drg_nccl_unique_id", uid)
+                except (RuntimeError, NotImplementedError) as e:   # pragma: no cover
+                    ok = 0
+                    log.warning("library NCCL unavailable (%s): torch collectives", e)
+            obj = [bytes(uid), ok]
             dist.broadcast_object_list(obj, src=dist.get_global_rank(self.group, 0),
                                        group=self.group)
-            _lib.call("drg_shard_nccl_init", self.ctx, (ctypes.c_uint8 * 128)(*obj[0]))
-            self.nccl = True
+            if obj[1]:
+                _lib.call("drg_shard_nccl_init", self.ctx, (ctypes.c_uint8 * 128)(*obj[0]))
+                self.nccl = True
 
     def close(self) -> None:
         if self.ctx:
@@ -195,12 +207,17 @@ class ShardContext:
             y[a:b] = self.snap[r * self.pad:r * self.pad + b - a]
         return y
 
-    # host collectives (a process group without NCCL, e.g. gloo in tests)
+    # the exchange through torch.distributed (gloo in the CPU tests: host copies; a
+    # torch NCCL group without the library's communicator: device tensors)
     def _exchange_host(self) -> None:
         import torch.distributed as dist
-        d = self.delta.cpu()
-        dist.all_reduce(d, group=self.group)
-        own = d[self.rank * self.pad:(self.rank + 1) * self.pad].contiguous().cuda()
+        if getattr(self, "device_collectives", False):
+            own = torch.empty((self.pad, 2), dtype=torch.float32, device=self.delta.device)
+            dist.reduce_scatter_tensor(own, self.delta, group=self.group)
+        else:
+            d = self.delta.cpu()
+            dist.all_reduce(d, group=self.group)
+            own = d[self.rank * self.pad:(self.rank + 1) * self.pad].contiguous().cuda()
         _lib.call("drg_shard_fold", self.ctx, _lib.ptr(own), _lib.stream_ptr())
         self.delta.zero_()
         self._gather_host()
@@ -209,6 +226,9 @@ class ShardContext:
         import torch.distributed as dist
         part = torch.empty((self.pad, 2), dtype=torch.float32, device=self.snap.device)
         _lib.call("drg_shard_read_part", self.ctx, _lib.ptr(part), _lib.stream_ptr())
+        if getattr(self, "device_collectives", False):
+            dist.all_gather_into_tensor(self.snap, part, group=self.group)
+            return
         parts = [torch.empty((self.pad, 2), dtype=torch.float32) for _ in range(self.world)]
         dist.all_gather(parts, part.cpu(), group=self.group)
         self.snap.copy_(torch.cat(parts).to(self.snap.device))
