@@ -1315,23 +1315,34 @@ class Samplers:
     def level_map(self, h: Hierarchy, level: int) -> np.ndarray:
         return compose_maps(h, level)
 
-    def plan_for(self, h: Hierarchy, params: OptimizerParams) -> LayoutPlan:
-        key = id(h)
-        if key not in self._plans:
-            levels = h.device_levels or [DeviceGraph.from_host(g) for g in h.levels]
-            maps = h.device_maps or [torch.from_numpy(np.ascontiguousarray(m, dtype=np.int32))
-                                     .cuda() for m in h.maps]
-            dh = DeviceHierarchy(list(levels), list(maps), h.rho, h.min_size)
+    def _device_similarity(self) -> DeviceSimilarity:
+        """P on the device, uploaded once per Samplers (shared by its hierarchies)."""
+        if "ds" not in self._plans:
             ns = self.ns
-            ds = DeviceSimilarity(
+            self._plans["ds"] = DeviceSimilarity(
                 torch.from_numpy(np.ascontiguousarray(ns.indptr, dtype=np.int64)).cuda(),
                 torch.from_numpy(np.ascontiguousarray(ns.targets, dtype=np.int32)).cuda(),
                 torch.from_numpy(np.ascontiguousarray(ns.weights, dtype=np.float64)).cuda(),
                 torch.from_numpy(np.ascontiguousarray(ns.sigma)).cuda(),
                 torch.from_numpy(np.ascontiguousarray(ns.row_masses())).cuda(),
                 ns.total_mass, int((np.diff(ns.indptr) > 0).sum()), ns.k)
-            self._plans[key] = (h, LayoutPlan(build_level_data(ds, dh, self.neg_power, True),
-                                              list(dh.maps), params))
+        return self._plans["ds"]
+
+    def plan_for(self, h: Hierarchy, params: OptimizerParams) -> LayoutPlan:
+        """The device plan of hierarchy ``h`` (built once per hierarchy object and
+        update family): the sampled update needs only the level-0 tables, one map
+        and one Q^l per level (build_mapped_level_data); the gather modes P^l."""
+        sampled = params.update == "sampled"
+        key = (id(h), sampled)
+        if key not in self._plans:
+            levels = h.device_levels or [DeviceGraph.from_host(g) for g in h.levels]
+            maps = h.device_maps or [torch.from_numpy(np.ascontiguousarray(m, dtype=np.int32))
+                                     .cuda() for m in h.maps]
+            dh = DeviceHierarchy(list(levels), list(maps), h.rho, h.min_size)
+            ds = self._device_similarity()
+            data = (build_mapped_level_data(ds, dh, self.neg_power) if sampled
+                    else build_level_data(ds, dh, self.neg_power, True))
+            self._plans[key] = (h, LayoutPlan(data, list(dh.maps), params))
         plan = self._plans[key][1]
         plan.opt = params
         return plan
