@@ -243,6 +243,9 @@ int drg_row_spans(const int64_t *indptr, int64_t n, uint64_t *out_span, void *st
 #define DRG_SAMPLED_AGGREGATE 1
 #define DRG_SAMPLED_FUSED 2
 #define DRG_SAMPLED_DETERMINISTIC 4
+/* hub levels drawn inline: L2 eviction-priority hints on the draws' table reads (for
+ * tables far above L2: R-MAT scale 24 +3.5%, BA-1M -7% on its hub level) */
+#define DRG_SAMPLED_L2_HINTS 8
 
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_span, const uint64_t *rec,
                        const uint64_t *row_alias,

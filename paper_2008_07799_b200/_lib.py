@@ -29,6 +29,7 @@ DRG_SAMPLED_AGGREGATE = 1
 DRG_SAMPLED_FUSED = 2
 DRG_SAMPLED_DETERMINISTIC = 4
 DRG_SHARD_LAGGED = 1
+DRG_SAMPLED_L2_HINTS = 8
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

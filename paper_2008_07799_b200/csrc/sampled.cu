@@ -828,7 +828,7 @@ __global__ void __launch_bounds__(256, 4)
 // written and re-read) and applied through the hot store.  The draws' random DRAM
 // reads then overlap other warps' updates inside one kernel, where the split form
 // runs a draw pass and an update pass that each fill the SMs.  M <= kMaxNeg.
-template <bool AGG, int B>
+template <bool AGG, int B, bool HINT>
 __global__ void __launch_bounds__(256, 4)
     apply_hot_fused_kernel(DArgs D, PArgs A, float2 *y, const int32_t *__restrict__ hot,
                            int n_hot) {
@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(256, 4)
             const int64_t s = D.step_lo + sl;
             int64_t i, j;
             int32_t cand[kMaxNeg];
-            draw_step<false>(D, s, (uint32_t)(s >> 32) ^ tt, i, j, cand, nullptr, 0, nev);
+            draw_step<HINT>(D, s, (uint32_t)(s >> 32) ^ tt, i, j, cand, nullptr, 0, nev);
             step_body<B>(A, st, i, j, cand, sl);
         }
         __syncthreads();
@@ -932,7 +932,7 @@ float hot_scale_for(const PArgs &P) {
 
 // one epoch of a hub level with the draws inline (apply_hot_fused_kernel), PDL
 int launch_hot_fused(const DArgs &D, const PArgs &P, float2 *y, unsigned grid, int block,
-                     bool agg, const int32_t *hot, int n_hot, cudaStream_t st) {
+                     bool agg, const int32_t *hot, int n_hot, bool hints, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3((unsigned)block);
@@ -946,10 +946,17 @@ int launch_hot_fused(const DArgs &D, const PArgs &P, float2 *y, unsigned grid, i
     Q.hot_scale = hot_scale_for(P);
     DArgs E = D;
     void *args[] = {&E, &Q, &y, &hot, &n_hot};
-    void *fn = agg ? (P.b == 2 ? (void *)apply_hot_fused_kernel<true, 2>
-                               : (void *)apply_hot_fused_kernel<true, 0>)
-                   : (P.b == 2 ? (void *)apply_hot_fused_kernel<false, 2>
-                               : (void *)apply_hot_fused_kernel<false, 0>);
+    // hints: the draws' one-touch table reads L2 evict-first and the Q table
+    // evict-last (DRG_SAMPLED_L2_HINTS; R-MAT scale 24: 295.6 -> 306 iters/s; the
+    // BA-1M hub level, whose tables fit L2, 7% slower -- the caller sets it for big
+    // tables only).  Keeping the positions evict-last as well measured no gain.
+#define DRG_FUSED_FN(H)                                                                \
+    (agg ? (P.b == 2 ? (void *)apply_hot_fused_kernel<true, 2, H>                      \
+                     : (void *)apply_hot_fused_kernel<true, 0, H>)                     \
+         : (P.b == 2 ? (void *)apply_hot_fused_kernel<false, 2, H>                     \
+                     : (void *)apply_hot_fused_kernel<false, 0, H>))
+    void *fn = hints ? DRG_FUSED_FN(true) : DRG_FUSED_FN(false);
+#undef DRG_FUSED_FN
     DRG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
     DRG_LAUNCHED("apply_hot_fused_kernel");
     return DRG_OK;
@@ -1582,7 +1589,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
             D.n_epochs = 1;
             P.lr = lr_at(t0 + j);
             DRG_TRY(launch_hot_fused(D, P, reinterpret_cast<float2 *>(y), grid, block, agg, hot,
-                                     n_hot, ss.hi));
+                                     n_hot, flags & DRG_SAMPLED_L2_HINTS, ss.hi));
         }
         DRG_CUDA(cudaEventRecord(ev.e[0], ss.hi));
         DRG_CUDA(cudaStreamWaitEvent(st, ev.e[0], 0));

@@ -499,6 +499,9 @@ def sampled_divisors(n0: int, opt: "OptimizerParams") -> tuple[int, int]:
 
 
 HUB_STEPS = 512   # warp-aggregate the sampled updates above this per-node rate
+# level-0 node count from which the per-node tables (8 B per node each) are far above
+# L2 and the inline draws of hub levels take L2 eviction hints (DRG_SAMPLED_L2_HINTS)
+L2_HINT_NODES = 1 << 22
 # Above this per-node rate each block stages the level's HOT_NODES busiest nodes in
 # shared memory (apply_hot_kernel): R-MAT's coarse levels, where one node is the
 # source of up to a third of an epoch's steps, and the C3 BA coarsest level.
@@ -812,7 +815,8 @@ class LayoutPlan:
         det = o.threads == 1 and not o.sampled_fused
         flags = (int(S.hubs) * _lib.DRG_SAMPLED_AGGREGATE
                  | (_lib.DRG_SAMPLED_FUSED if o.sampled_fused else 0)
-                 | (_lib.DRG_SAMPLED_DETERMINISTIC if det else 0))
+                 | (_lib.DRG_SAMPLED_DETERMINISTIC if det else 0)
+                 | (_lib.DRG_SAMPLED_L2_HINTS if self.levels[0].n >= L2_HINT_NODES else 0))
         if self.evals is None:
             self.evals = torch.zeros(1, dtype=torch.int64, device=y.device)
         _lib.call("drg_layout_sampled", _lib.ptr(ip), _lib.ptr(S.span), None,
