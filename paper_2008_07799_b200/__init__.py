@@ -18,6 +18,7 @@ from .optimizer import (AliasTable, Layout, LayoutPlan, OptimizerParams, Positiv
                         build_negative_sampler, build_positive_sampler, build_samplers,
                         layout_device, layout_graph, prepare_layout, repulsive_gradient,
                         sgd_epoch)
+from .quality import neighborhood_preservation
 from .similarity import (DeviceSimilarity, SimilarityParams, SparseSimilarity,
                          build_sparse_similarity, conditional_similarity_row, device_similarity,
                          precompute_gaussian_table, search_sigma)
@@ -35,6 +36,8 @@ __all__ = [
     "build_negative_sampler", "build_positive_sampler", "PositiveSampler",
     "attractive_gradient", "repulsive_gradient",
     "build_samplers", "Samplers", "sgd_epoch", "layout_graph",
+    # metrics.py:114-145 (the one metric on the path: the parity instrument)
+    "neighborhood_preservation",
     # device-resident API
     "DeviceGraph", "DeviceNeighborDistances", "DeviceSimilarity", "DeviceHierarchy",
     "LayoutPlan", "device_from_edges", "device_k_neighborhoods", "device_similarity",

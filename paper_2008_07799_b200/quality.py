@@ -50,6 +50,8 @@ def neighborhood_preservation(g: Graph | DeviceGraph, positions, k_eval: int = 2
     _lib.load()
     dg = g if isinstance(g, DeviceGraph) else DeviceGraph.from_host(g)
     n = dg.node_count
+    if len(positions) != n:   # metrics.py:126-127
+        raise ValueError("layout does not cover all nodes")
     if isinstance(positions, torch.Tensor):
         y = positions.to(device="cuda", dtype=torch.float32).contiguous()
     else:

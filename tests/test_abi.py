@@ -97,3 +97,33 @@ def test_level_order_is_numpy_permutation(n):
     _lib.call_host("drg_pcg64_permutation", s >> 64, s & m, inc >> 64, inc & m, 1,
                    st["uinteger"], n, out.ctypes.data)
     assert np.array_equal(out, g.permutation(n))
+
+
+# The reference's metrics module is out of scope except the metric the
+# parity protocol uses (neighborhood_preservation, exported as the device instrument).
+OUT_OF_SCOPE = {"MetricsReport", "MetricError", "stress", "count_crossings", "crosslessness",
+                "minimum_angle", "compute_metrics"}
+
+
+def test_public_names_and_parameters_match_the_reference():
+    """Every public name of drgraph (__init__.py:57-70; tests/golden/reference_api.json,
+    written by make_api_golden.py from the reference itself) on the path is exported,
+    and every callable / parameter dataclass takes the reference's parameters, in the
+    reference's order (B200 extensions only after them, as keyword-only or defaulted)."""
+    import inspect
+    import json
+
+    import paper_2008_07799_b200 as B
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                      "reference_api.json")))
+    missing = [n for n in ref["__all__"] if n not in OUT_OF_SCOPE and n not in B.__all__]
+    assert not missing, missing
+    for name, params in ref["params"].items():
+        if name in OUT_OF_SCOPE:
+            continue
+        obj = getattr(B, name)
+        if inspect.isclass(obj):
+            ours = list(obj.__dataclass_fields__)
+        else:
+            ours = [p.name for p in inspect.signature(obj).parameters.values()]
+        assert ours[:len(params)] == params, (name, ours, params)
