@@ -42,6 +42,10 @@ CONFIGS = {
     "rmat18": dict(k=1, perplexity="auto", iters=500, max_levels=5, force_levels=5,
                    init="normal", z_pairs=None, np_sample=20_000, np_max_degree=2048, np_k=1,
                    np_min_degree=1),   # (isolated nodes score 1 in both arms)
+    # C5 at scale 20 (1 M nodes, 5 forced levels)
+    "rmat20": dict(k=1, perplexity="auto", iters=500, max_levels=5, force_levels=5,
+                   init="normal", z_pairs=None, np_sample=20_000, np_max_degree=2048, np_k=1,
+                   np_min_degree=1),
     # BASELINE C4 itself: 120^3 mesh, 1.73 M nodes (the bench workload)
     "mesh": dict(k=2, perplexity=50.0, iters=800, max_levels=4, init="normal",
                  z_pairs=None, np_sample=None),
@@ -57,8 +61,8 @@ def graph_for(name):
         g = synthetic.rgg(200_000, seed=0, device="host")
     elif name == "mesh":
         g = synthetic.mesh3d(120, device="host")
-    elif name == "rmat18":
-        g = synthetic.rmat(18, 16, seed=0, device="host")
+    elif name in ("rmat18", "rmat20"):
+        g = synthetic.rmat(int(name[4:]), 16, seed=0, device="host")
     elif name == "ba":
         g = synthetic.barabasi_albert(1_000_000, 4, seed=0, device="host")
     else:
