@@ -337,8 +337,10 @@ int drg_shard_epoch(void *ctx, const int64_t *indptr, const uint64_t *row_span,
  * epochs per launch one chunk ahead.  DRG_SHARD_LAGGED overlaps epoch t's exchange with
  * epoch t + 1 (two snapshot / delta buffers): epoch t reads the snapshot of the end of
  * epoch t - 2 at the latest, its reactions are folded in by the end of epoch t + 1 (the
- * emulation, rank -1, runs exactly that worst case).  Needs the NCCL communicator (or
- * rank -1). */
+ * emulation, rank -1, runs exactly that worst case).  exchange_every = r > 1 (not
+ * lagged): the exchange after every r-th epoch (and the last) only -- negatives read
+ * a snapshot up to r epochs old, reactions fold in after up to r epochs.  Needs the
+ * NCCL communicator (or rank -1). */
 #define DRG_SHARD_LAGGED 1
 int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *row_span,
                   const uint64_t *row_alias,
@@ -348,7 +350,8 @@ int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *row_span,
                   const int64_t *seg_n, const int64_t *seg_lo, const int64_t *step_lo,
                   const int64_t *n_steps, int t0, int n_iter, int iters, double lr0, double gamma,
                   double eps, double clip, int b, int M, uint64_t seed, int level,
-                  int64_t max_threads, int flags, uint64_t *evals, void *stream);
+                  int64_t max_threads, int flags, int exchange_every, uint64_t *evals,
+                  void *stream);
 
 /* --- single-row / single-interaction drop-ins -----------------------------------
  * precompute_gaussian_table (similarity.py:110-119): out[d-1] = exp(-d^2 / (2 sigma^2)),

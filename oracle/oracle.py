@@ -916,6 +916,25 @@ def deferred_drawn_epoch(pos, draws, lr, gamma, eps, clip, b, snap=None, fold=Tr
     return pos
 
 
+def periodic_drawn_epochs(pos, draws_per_epoch, lrs, gamma, eps, clip, b, every):
+    """drg_shard_run with exchange_every = r: the negatives read the snapshot taken at
+    the last exchange, their reactions accumulate until it; exchanges after every r-th
+    epoch and after the last."""
+    pos = np.array(pos, dtype=np.float64)
+    snap = pos.copy()
+    delta = np.zeros_like(pos)
+    n = len(draws_per_epoch)
+    for j in range(n):
+        pos, d = deferred_drawn_epoch(pos, draws_per_epoch[j], lrs[j], gamma, eps, clip, b,
+                                      snap=snap, fold=False)
+        delta += d
+        if (j + 1) % every == 0 or j + 1 == n:
+            pos += delta
+            delta[:] = 0.0
+            snap = pos.copy()
+    return pos
+
+
 def lagged_drawn_epochs(pos, draws_per_epoch, lrs, gamma, eps, clip, b):
     """drg_shard_run with DRG_SHARD_LAGGED as its emulation runs it (the worst case of
     the overlapped exchange): epoch j reads the negatives from the snapshot taken at

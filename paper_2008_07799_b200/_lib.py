@@ -64,7 +64,7 @@ SIGNATURES = {
     "drg_shard_epoch": [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _P, _I32, _P, _P, _P, _P, _P, _I32, _I32,
                         _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _P, _P, _P],
     "drg_shard_run": [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _P, _I32, _P, _P, _P, _P, _P, _I32, _I32,
-                      _I32, _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _I32, _P, _P],
+                      _I32, _F64, _F64, _F64, _F64, _I32, _I32, _U64, _I32, _I64, _I32, _I32, _P, _P],
     "drg_khop_source": [_P, _P, _I64, _I32, _I64, _P, _P, _I64, _P, _P],
     "drg_similarity": [_P, _P, _P, _I64, _I64, _I32, _F64, _F64, _I32, _F64, _F64, _P, _P, _P,
                        _P, _P, _P],

@@ -2201,9 +2201,10 @@ extern "C" int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *r
                              const int64_t *seg_lo, const int64_t *step_lo,
                              const int64_t *n_steps, int t0, int n_iter, int iters, double lr0,
                              double gamma, double eps, double clip, int b, int M, uint64_t seed,
-                             int level, int64_t max_threads, int flags, uint64_t *evals,
-                             void *stream) {
+                             int level, int64_t max_threads, int flags, int exchange_every,
+                             uint64_t *evals, void *stream) {
     ShardCtx *c = static_cast<ShardCtx *>(ctx);
+    if (exchange_every < 1) return fail(DRG_ERR_INVALID, "exchange_every must be >= 1");
     cudaStream_t st = as_stream(stream);
     if (M < 0 || b < 1 || iters < 1) return fail(DRG_ERR_INVALID, "bad optimizer parameters");
     if (nseg < 1 || nseg > kMaxParts) return fail(DRG_ERR_INVALID, "bad segment count");
@@ -2214,6 +2215,8 @@ extern "C" int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *r
     int64_t total = 0;
     for (int s = 0; s < nseg; ++s) total += n_steps[s];
     const bool lagged = (flags & DRG_SHARD_LAGGED) && c->world > 1;
+    if (lagged && exchange_every > 1)
+        return fail(DRG_ERR_INVALID, "the lagged exchange runs after every epoch");
     const size_t nbuf = (size_t)c->view.pad * c->world;
     if (lagged && c->buf2_cap < (int64_t)nbuf) {
         if (c->snap2) cudaFree(c->snap2);
@@ -2236,7 +2239,9 @@ extern "C" int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *r
     EvalSlots evs(st);
     DRG_TRY(evs.init(reinterpret_cast<unsigned long long *>(evals), st));
     if (total == 0) {   // nothing drawn here; the exchanges still pair with the peers'
-        for (int j = 0; j < n_iter; ++j) DRG_TRY(shard_exchange(c, snap[0], delta[0], st));
+        for (int j = 0; j < n_iter; ++j)
+            if (lagged || (j + 1) % exchange_every == 0 || j + 1 == n_iter)
+                DRG_TRY(shard_exchange(c, snap[0], delta[0], st));
         return evs.finish(st);
     }
     const DArgs D = shard_dargs(indptr, row_span, row_alias, collapse, neg_alias, map, n_tab,
@@ -2281,9 +2286,10 @@ extern "C" int drg_shard_run(void *ctx, const int64_t *indptr, const uint64_t *r
             const int j = q * K + e, t = t0 + j;
             P.lr = lr_of(lr0, t, iters);
             P.draws = chunk_buf(q) + (size_t)e * (rec_bytes / 4);
-            if (!lagged) {
+            if (!lagged) {   // exchange after every exchange_every-th epoch and the last
                 DRG_TRY(launch_shard_apply(P, V, max_threads, st));
-                DRG_TRY(shard_exchange(c, snap[0], delta[0], st));
+                if ((j + 1) % exchange_every == 0 || j + 1 == n_iter)
+                    DRG_TRY(shard_exchange(c, snap[0], delta[0], st));
                 continue;
             }
             // epoch j reads snap[j & 1] and writes delta[j & 1]: both last touched

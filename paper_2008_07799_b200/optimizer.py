@@ -122,6 +122,9 @@ class OptimizerParams:
     # (negatives read positions up to two epochs old, reactions fold in one epoch
     # later; DRG_SHARD_LAGGED) instead of exchanging between epochs
     shard_lagged: bool = False
+    # multi-GPU sampled levels: exchange after every this-many epochs (1 = every epoch;
+    # r > 1 lets negatives read positions up to r epochs old)
+    shard_exchange_every: int = 1
 
     def __post_init__(self) -> None:
         if self.neg_samples < 0:
@@ -141,6 +144,8 @@ class OptimizerParams:
         for c in (self.sampled_concurrency, self.sampled_concurrency_coarse):
             if c is not None and c < 1:
                 raise ValueError("sampled concurrency divisors must be >= 1")
+        if self.shard_exchange_every < 1:
+            raise ValueError("shard_exchange_every must be >= 1")
         if not 0 <= self.virtual_ranks <= 8:
             raise ValueError("virtual_ranks must be in [0, 8]")
         if self.init not in ("normal", "uniform"):
@@ -999,7 +1004,7 @@ class LayoutPlan:
                   t0, n_iter, o.iters, float(o.lr0), float(gamma), float(o.eps),
                   float(o.grad_clip), o.b, o.neg_samples, seed, level,
                   max_threads or self._shard_threads(level, lay, segs), flags,
-                  _lib.ptr(self.evals),
+                  1 if o.shard_lagged else o.shard_exchange_every, _lib.ptr(self.evals),
                   _lib.stream_ptr())
 
     def shard_epoch(self, level: int, world: int, ctx, t: int, max_threads: int | None = None,

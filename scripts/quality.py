@@ -126,6 +126,10 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
             if upd == "sampledv":   # the multi-GPU path on W ranks emulated on this GPU
                 upd, extra = "sampled", {"virtual_ranks": int(div), "threads": 16,
                                          "shard_min_nodes": 65536}
+            elif upd.startswith("sampledvr"):   # ... exchanging every r epochs: sampledvrR:W
+                r = int(upd[len("sampledvr"):])
+                upd, extra = "sampled", {"virtual_ranks": int(div), "threads": 16,
+                                         "shard_exchange_every": r, "shard_min_nodes": 65536}
             elif upd == "sampledvl":   # ... with the lagged (overlapped) exchange
                 upd, extra = "sampled", {"virtual_ranks": int(div), "threads": 16,
                                          "shard_lagged": True, "shard_min_nodes": 65536}

@@ -73,8 +73,8 @@ def test_emulated_epoch_matches_sequential_restatement(world):
             float(err.max())
 
 
-@pytest.mark.parametrize("lagged", [False, True])
-def test_shard_run_matches_epoch_restatement(lagged):
+@pytest.mark.parametrize("lagged,every", [(False, 1), (True, 1), (False, 2)])
+def test_shard_run_matches_epoch_restatement(lagged, every):
     """drg_shard_run (a level's epochs and exchanges in one call, emulated 3 ranks,
     one step in flight) against the oracle's sequential restatement on the same
     draws: exchange after every epoch, or the lagged worst case (negatives from the
@@ -83,6 +83,7 @@ def test_shard_run_matches_epoch_restatement(lagged):
     plan, _ = _plan(world=world)
     o = plan.opt
     o.shard_lagged = lagged
+    o.shard_exchange_every = every
     o.lr0 = 0.05   # chained epochs at lr ~ 1 amplify fp32-vs-fp64 rounding chaotically
     for level in sorted({0, plan.depth}):
         n = plan.levels[level].n
@@ -106,6 +107,8 @@ def test_shard_run_matches_epoch_restatement(lagged):
         y = y0.cpu().numpy().astype(np.float64)
         if lagged:
             want = O.lagged_drawn_epochs(y, draws, lrs, gamma, o.eps, o.grad_clip, o.b)
+        elif every > 1:
+            want = O.periodic_drawn_epochs(y, draws, lrs, gamma, o.eps, o.grad_clip, o.b, every)
         else:
             want = y
             for j in range(n_ep):
@@ -114,7 +117,7 @@ def test_shard_run_matches_epoch_restatement(lagged):
         err = np.abs(got - want) / np.maximum(1.0, np.abs(want))
         assert np.median(err) <= 1e-6 and np.quantile(err, 0.99) <= 1e-4 and err.max() <= 1e-3, \
             float(err.max())
-        if not lagged:   # one call == the epoch-by-epoch host loop, bit for bit
+        if not lagged and every == 1:   # one call == the epoch-by-epoch host loop, bit for bit
             ctx.level(lay, "cuda")
             ctx.load(y0)
             for j in range(n_ep):
