@@ -428,8 +428,9 @@ def run_ours(args):
         M = opt.neg_samples
         n0 = L0.n // (world if group is not None else 1)
         # update: y_i, y_j, M y_c gathers + the same M + 2 reductions; draws: source
-        # alias, the two row bounds, the row-alias record and M negative alias loads
-        upd, drw = n0 * 2 * (M + 2), n0 * (4 + M)
+        # alias, the row span (one {start, length} record), the row-alias record and M
+        # negative alias loads
+        upd, drw = n0 * 2 * (M + 2), n0 * (3 + M)
         t_min = upd / (ceil["gather+red 1:1"] * 1e9) + drw / (ceil["gather 8B"] * 1e9)
         random_access = {"accesses_per_launch": upd + drw,
                          "achieved_G_per_s": (upd + drw) / l0_launch_s / 1e9,

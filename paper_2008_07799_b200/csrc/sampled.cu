@@ -774,7 +774,7 @@ __device__ __forceinline__ float hot_sum(const int *a, float inv_scale) {
 }
 
 template <bool AGG, int B>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(1024)
     apply_hot_kernel(PArgs A, float2 *y, const int32_t *__restrict__ hot, int n_hot) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ unsigned s_filter[kHotFilterWords];
@@ -978,6 +978,17 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
     void *args[] = {&Q, &y, &hot, &n_hot};
     const int64_t threads = (int64_t)grid * block;
     void *fn;
+    if (hot && n_hot > 0) {
+        // one block per SM: each block stages the hot nodes and publishes their
+        // increments once per round, so fewer, larger blocks mean fewer same-address
+        // reductions and reloads on the hubs per round (R-MAT: 512 blocks of 128
+        // published 32 k hub updates per round at 64 k steps in flight)
+        const int64_t per_sm = ceil_div(threads, (int64_t)sm_count());
+        const int hb = (int)std::min<int64_t>(threads, std::min<int64_t>(
+                                                          1024, std::max<int64_t>(32, ceil_div(per_sm, 32) * 32)));
+        cfg.blockDim = dim3((unsigned)hb);
+        cfg.gridDim = dim3((unsigned)ceil_div(threads, hb));
+    }
     if (hot && n_hot > 0)   // hub level: the hottest nodes staged per block
         fn = agg ? (P.b == 2 ? (void *)apply_hot_kernel<true, 2> : (void *)apply_hot_kernel<true, 0>)
                  : (P.b == 2 ? (void *)apply_hot_kernel<false, 2> : (void *)apply_hot_kernel<false, 0>);
@@ -1578,10 +1589,13 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
     P.b = b;
     P.M = M;
     P.probe = probe;
-    // hub levels whose hottest nodes are staged: the draws inline, no draw pass
-    static const bool hot_fused = [] {   // DRG_HOT_FUSED=0: the split form there too
+    // hub levels whose hottest nodes are staged, draws inline (DRG_HOT_FUSED=1): faster
+    // at full concurrency (R-MAT 270 -> 306 iters/s), but those levels run capped at
+    // HOT_MAX_THREADS steps in flight for fidelity, and there the split form wins
+    // (the draw pass keeps its full occupancy): 208 inline vs 240 split at 64 k
+    static const bool hot_fused = [] {
         const char *e = getenv("DRG_HOT_FUSED");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     if (hot && n_hot > 0 && !det && M <= kMaxNeg && hot_fused) {
         for (int j = 0; j < n_iter; ++j) {

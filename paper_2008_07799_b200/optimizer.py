@@ -512,6 +512,13 @@ L2_HINT_NODES = 1 << 22
 # source of up to a third of an epoch's steps, and the C3 BA coarsest level.
 HOT_STEPS = int(os.environ.get("DRG_HOT_STEPS", 4096))   # (env: experiments)
 HOT_NODES = 64
+# Steps in flight on those levels.  A staged hub no longer serialises its steps on
+# its L2 line, so every concurrent step that touches it really reads the same
+# position: R-MAT scale 20 (hub in ~1/3 of a coarse epoch's steps) keeps KL within
+# 0.2% of the reference at 50-100 k steps in flight and drifts -10% at the ~150 k the
+# n/4 default reaches (profiles/r02_quality_rmat20_*).  The plain (unstaged) kernel
+# is faithful at n/4 because the hub's atomics serialise -- and 4x slower.
+HOT_MAX_THREADS = int(os.environ.get("DRG_HOT_MAX_THREADS", 65536))   # (env: experiments)
 # Above this per-node rate the sampled epoch serialises on the hub's atomics even
 # warp-aggregated, and the gather (K7 + heavy-row split) is faster: R-MAT's coarse
 # levels (busiest node 2.4e5 - 4.8e6 steps per epoch) -- while R-MAT's level 0
@@ -831,10 +838,17 @@ class LayoutPlan:
                   o.iters,
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
                   o.neg_samples, seed, level,
-                  max_threads if max_threads is not None else max(32, L.n // max(1, div)),
+                  max_threads if max_threads is not None else self._steps_in_flight(level, div),
                   flags, L.n, _lib.ptr(self.evals) if count else None,
                   _lib.ptr(S.hot) if (S.hot is not None and not det) else None,
                   0 if S.hot is None else S.hot.numel(), _lib.stream_ptr())
+
+    def _steps_in_flight(self, level: int, div: int) -> int:
+        """n_l / divisor, capped at HOT_MAX_THREADS on levels with staged hub nodes."""
+        L = self.levels[level]
+        c = max(32, L.n // max(1, div))
+        hot = L.sampled.hot is not None and not (self.opt.threads == 1)
+        return min(c, HOT_MAX_THREADS) if hot else c
 
     def _collapse(self, level: int):
         """Collapse probabilities of ``level`` (NULL at level 0 and for mapped draws)."""
