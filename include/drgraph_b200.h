@@ -246,6 +246,10 @@ int drg_row_spans(const int64_t *indptr, int64_t n, uint64_t *out_span, void *st
 /* hub levels drawn inline: L2 eviction-priority hints on the draws' table reads (for
  * tables far above L2: R-MAT scale 24 +3.5%, BA-1M -7% on its hub level) */
 #define DRG_SAMPLED_L2_HINTS 8
+/* src_alias points at 32-byte source records (drg_src_records): each source draw
+ * reads the Vose bucket, the row span and the collapse probability of both of the
+ * bucket's outcomes from one sector (split form only) */
+#define DRG_SAMPLED_SRC_RECORDS 16
 
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_span, const uint64_t *rec,
                        const uint64_t *row_alias,
@@ -266,6 +270,16 @@ int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_span, const ui
  * attempts hit i or j) -- exactly the steps drg_layout_sampled runs.
  * drg_sampled_apply: one epoch of those steps on y, at most max_threads steps in
  * flight (max_threads = 1: sequential, the reference kernel's order). */
+/* 32-byte source records of a source Vose table over nodes [0, n_src) (src_alias
+ * as drg_alias_build writes it) for DRG_SAMPLED_SRC_RECORDS: per bucket b,
+ * out[4b..4b+3] = {threshold | alias << 32, row start of b | row length of b << 32,
+ * row start | row length of the alias, collapse of b | collapse of the alias << 32}
+ * (fp32 bits; collapse NULL: 0).  Needs nnz < 2^32.  Replaces the separate
+ * alias / drg_row_spans / collapse reads of the reference's source draw
+ * (_kernels.py:66-75; optimizer.py:111-139). */
+int drg_src_records(const uint64_t *src_alias, int64_t n_src, const int64_t *indptr,
+                    const float *collapse, uint64_t *out, void *stream);
+
 int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_span, const uint64_t *row_alias,
                       const uint64_t *src_alias, const float *collapse,
                       const uint64_t *neg_alias, const int32_t *map, int64_t n,

@@ -30,6 +30,7 @@ DRG_SAMPLED_FUSED = 2
 DRG_SAMPLED_DETERMINISTIC = 4
 DRG_SHARD_LAGGED = 1
 DRG_SAMPLED_L2_HINTS = 8
+DRG_SAMPLED_SRC_RECORDS = 16
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -87,6 +88,7 @@ SIGNATURES = {
     "drg_sampled_draws": [_P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _F64, _I64, _I64, _I32, _I32, _I32, _U64, _I32,
                           _P, _P],
     "drg_row_spans": [_P, _I64, _P, _P],
+    "drg_src_records": [_P, _I64, _P, _P, _P, _P],
     "drg_sampled_apply": [_P, _I64, _P, _F64, _F64, _F64, _F64, _I32, _I32, _I64, _I32, _P],
     "drg_text_lines": [_P, _I64, _I32, _P, _P, _P, _P],
     "drg_parse_lines": [_P, _I64, _P, _I64, _I32, _I64, _I64, _P, _P, _P, _P, _P, _P],

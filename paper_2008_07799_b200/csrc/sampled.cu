@@ -96,6 +96,12 @@ __device__ __forceinline__ int64_t ld_hint(const int64_t *a, uint64_t pol) {
     asm volatile("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(r) : "l"(a), "l"(pol));
     return r;
 }
+__device__ __forceinline__ uint4 ld_hint(const uint4 *a, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(a), "l"(pol));
+    return r;
+}
 __device__ __forceinline__ int32_t ld_hint(const int32_t *a, uint64_t pol) {
     int32_t r;
     asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
@@ -394,6 +400,11 @@ struct DArgs {
     int64_t n_src, src_lo;
     const int32_t *src_perm;
     int64_t out_stride;   // field stride of out (>= n_steps; ranks' slices of one buffer)
+    // optional 32-byte source records (drg_src_records; 1-GPU draws, src_lo = 0, no
+    // src_perm): bucket b's {threshold, alias, span of b} and {span of the alias,
+    // collapse of b, collapse of the alias} -- one random sector per drawn source
+    // instead of three table reads (alias record, row span, collapse)
+    const uint4 *src_rec = nullptr;
 };
 
 // small blocks: they fit beside the update pass's resident blocks
@@ -418,7 +429,14 @@ __device__ __forceinline__ void draw_step(const DArgs &A, int64_t s, uint32_t c1
     const u32x4 r2 = philox4x32<7>(u32x4{(uint32_t)s, c1, (A.level << 24) | 0xfe00u, 0x3c6ef372u},
                                    A.key0, A.key1);
     const int64_t sb = bucket(A.n_src, r.x, r.y);
-    const uint2 srec = HINT ? ld_hint(A.src_alias + sb, once) : __ldg(A.src_alias + sb);
+    uint2 srec = make_uint2(0u, 0u);
+    uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = q0;
+    if (A.src_rec) {   // both halves of one 32-byte record: one sector
+        q0 = HINT ? ld_hint(A.src_rec + 2 * sb, once) : __ldg(A.src_rec + 2 * sb);
+        q1 = HINT ? ld_hint(A.src_rec + 2 * sb + 1, once) : __ldg(A.src_rec + 2 * sb + 1);
+    } else {
+        srec = HINT ? ld_hint(A.src_alias + sb, once) : __ldg(A.src_alias + sb);
+    }
     const int Me = min(A.M, kMaxNeg);
     int32_t cand[kMaxNeg];
 #pragma unroll
@@ -427,18 +445,27 @@ __device__ __forceinline__ void draw_step(const DArgs &A, int64_t s, uint32_t c1
             cand[m] = (int32_t)pick_neg<HINT>(A.neg, neg_draw(K, s, c1, m, 0), keep);
         }
     }
-    int64_t i = accept(srec, sb, r.z);
-    i = A.src_perm ? (int64_t)__ldg(A.src_perm + A.src_lo + i) : A.src_lo + i;
-    int64_t lo, hi;
-    if (A.span) {
-        const uint2 sp = HINT ? ld_hint(A.span + i, once) : __ldg(A.span + i);
-        lo = sp.x;
-        hi = lo + sp.y;
+    int64_t i, lo, hi;
+    float cprob;
+    if (A.src_rec) {
+        const bool own = u32_to_unit(r.z) < __uint_as_float(q0.x);   // accept()
+        i = own ? sb : (int64_t)q0.y;
+        lo = own ? q0.z : q1.x;
+        hi = lo + (own ? q0.w : q1.y);
+        cprob = __uint_as_float(own ? q1.z : q1.w);
     } else {
-        lo = HINT ? ld_hint(A.indptr + i, once) : __ldg(A.indptr + i);
-        hi = HINT ? ld_hint(A.indptr + i + 1, once) : __ldg(A.indptr + i + 1);
+        i = accept(srec, sb, r.z);
+        i = A.src_perm ? (int64_t)__ldg(A.src_perm + A.src_lo + i) : A.src_lo + i;
+        if (A.span) {
+            const uint2 sp = HINT ? ld_hint(A.span + i, once) : __ldg(A.span + i);
+            lo = sp.x;
+            hi = lo + sp.y;
+        } else {
+            lo = HINT ? ld_hint(A.indptr + i, once) : __ldg(A.indptr + i);
+            hi = HINT ? ld_hint(A.indptr + i + 1, once) : __ldg(A.indptr + i + 1);
+        }
+        cprob = A.collapse ? __ldg(A.collapse + i) : 0.0f;   // NULL: none
     }
-    const float cprob = A.collapse ? __ldg(A.collapse + i) : 0.0f;   // NULL: none
     int64_t j = i;
     if ((A.probe & 2) && hi > lo) {
         j = (int64_t)bucket(A.n, r2.x, r2.y);
@@ -1397,6 +1424,40 @@ extern "C" int drg_row_spans(const int64_t *indptr, int64_t n, uint64_t *out_spa
     return DRG_OK;
 }
 
+namespace drg {
+namespace {
+__global__ void src_records_kernel(const uint2 *__restrict__ alias, int64_t n,
+                                   const int64_t *__restrict__ indptr,
+                                   const float *__restrict__ collapse, uint4 *out) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * blockDim.x) {
+        const uint2 rec = alias[b];
+        const int64_t a = rec.y;
+        const int64_t lb = indptr[b], la = indptr[a];
+        const float cb = collapse ? collapse[b] : 0.0f, ca = collapse ? collapse[a] : 0.0f;
+        out[2 * b] = make_uint4(rec.x, rec.y, (uint32_t)lb, (uint32_t)(indptr[b + 1] - lb));
+        out[2 * b + 1] = make_uint4((uint32_t)la, (uint32_t)(indptr[a + 1] - la),
+                                    __float_as_uint(cb), __float_as_uint(ca));
+    }
+}
+}  // namespace
+}  // namespace drg
+
+extern "C" int drg_src_records(const uint64_t *src_alias, int64_t n_src, const int64_t *indptr,
+                               const float *collapse, uint64_t *out, void *stream) {
+    if (n_src <= 0) return DRG_OK;
+    cudaStream_t st = as_stream(stream);
+    int64_t last = 0;
+    DRG_CUDA(cudaMemcpyAsync(&last, indptr + n_src, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    DRG_CUDA(cudaStreamSynchronize(st));
+    if (last >= (int64_t)1 << 32) return fail(DRG_ERR_UNSUPPORTED, "source records need nnz < 2^32");
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n_src, 256), sm_count() * 16);
+    src_records_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint2 *>(src_alias), n_src,
+                                             indptr, collapse, reinterpret_cast<uint4 *>(out));
+    DRG_LAUNCHED("src_records_kernel");
+    return DRG_OK;
+}
+
 extern "C" int drg_sampled_draws(const int64_t *indptr, const uint64_t *row_span,
                                  const uint64_t *row_alias,
                                  const uint64_t *src_alias, const float *collapse,
@@ -1502,6 +1563,8 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
     while (block > 32 && threads / block < 2 * (int64_t)sm_count()) block /= 2;
     const unsigned grid = (unsigned)(threads / block);
     auto lr_at = [&](int t) { return (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0); };
+    if ((flags & DRG_SAMPLED_SRC_RECORDS) && (flags & DRG_SAMPLED_FUSED))
+        return fail(DRG_ERR_UNSUPPORTED, "source records serve the split form");
     if ((flags & DRG_SAMPLED_FUSED) && map)
         return fail(DRG_ERR_UNSUPPORTED, "the fused form draws from level tables (map == NULL)");
     if (flags & DRG_SAMPLED_FUSED) {   // one kernel per epoch, draws inline
@@ -1569,6 +1632,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
     D.src_lo = 0;
     D.src_perm = nullptr;
     D.out_stride = n_steps;
+    if (flags & DRG_SAMPLED_SRC_RECORDS) D.src_rec = reinterpret_cast<const uint4 *>(src_alias);
     auto chunk_buf = [&](int c) { return buf.as<int32_t>() + (size_t)(c & 1) * K * (rec_bytes / 4); };
     auto draw = [&](int c) -> int {
         D.t_first = t0 + c * K;

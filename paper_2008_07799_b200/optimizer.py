@@ -446,6 +446,9 @@ class SampledTables:
     # the level's negative table Q^l (NegTable); None: the level's own full table
     neg: "NegTable | None" = None
     span: torch.Tensor | None = None        # int64 [n_0] {row start, length} (drg_row_spans)
+    # 32-byte source records (drg_src_records): bucket + both outcomes' spans and
+    # collapse probabilities in one sector (DRG_SAMPLED_SRC_RECORDS)
+    src_rec: torch.Tensor | None = None
 
 
 @dataclass
@@ -527,6 +530,22 @@ HOT_MAX_THREADS = int(os.environ.get("DRG_HOT_MAX_THREADS", 65536))   # (env: ex
 GATHER_STEPS = 32768
 
 
+# Source draws from 32-byte records (drg_src_records) on 1-GPU sampled levels
+# (DRG_SRC_RECORDS env for experiments: 1 = on)
+SRC_RECORDS = os.environ.get("DRG_SRC_RECORDS", "0") == "1"
+
+
+def src_records(S: SampledTables, indptr: torch.Tensor, collapse) -> torch.Tensor | None:
+    """drg_src_records over S.src_alias (None when nnz >= 2^32)."""
+    k = S.src_alias.numel()
+    if int(indptr[-1]) >= (1 << 32):
+        return None
+    out = torch.empty((max(k, 1), 4), dtype=torch.int64, device=indptr.device)
+    _lib.call("drg_src_records", _lib.ptr(S.src_alias), k, _lib.ptr(indptr),
+              _lib.ptr(collapse), _lib.ptr(out), _lib.stream_ptr())
+    return out
+
+
 def build_sampled_tables(ip, tg, P, R, Wn=None) -> SampledTables:
     """Per-row Vose over P (16-byte records), Vose over R -- over the connected
     prefix only (isolated nodes have R = 0 and are never a source) -- collapse
@@ -552,8 +571,15 @@ def build_sampled_tables(ip, tg, P, R, Wn=None) -> SampledTables:
                          neg=None if Wn is None else build_neg_table(Wn, R), span=span)
 
 
+# Coarse levels that draw from their own pair tables (P^l aggregated, level-l form of
+# the law) instead of level 0's through the composed map: "hub" = the hub-staged
+# levels (DRG_LEVEL_TABLES env for experiments: none | hub | all)
+LEVEL_TABLES = os.environ.get("DRG_LEVEL_TABLES", "none")
+
+
 def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
-                            neg_power: float = 0.75) -> list[LevelData]:
+                            neg_power: float = 0.75,
+                            level_tables: str | None = None) -> list[LevelData]:
     """update="sampled" without level aggregation: the reference draws every pair
     and negative at level 0 and maps it to the current level (_kernels.py:76-81,
     115), so the level-0 tables (per-row Vose over P, Vose over R and Q) serve all
@@ -564,13 +590,20 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
     Wn = device_negative_weights(R, neg_power)
     S0 = build_sampled_tables(ip, tg, P, R, Wn)
     S0.collapse = None   # no pair collapses at level 0
+    if SRC_RECORDS:
+        S0.src_rec = src_records(S0, ip, None)
     n0 = dh.levels[0].node_count
     out = [LevelData(n0, tg.numel(), ip, None, None, None, None, S0)]
     flat = None
     st = _lib.stream_ptr()
+    mode = LEVEL_TABLES if level_tables is None else level_tables
+    pairs = (ip, tg, P)   # P^l pulled up level by level (only when some level uses it)
+    need = mode != "none"
     for level in range(1, dh.depth + 1):
         n_l = dh.levels[level].node_count
         parent = dh.maps[level - 1]
+        if need:
+            pairs = _aggregate_pairs(*pairs, parent, n_l)
         if flat is None:   # level 1: the parent map itself
             flat = parent.to(torch.int32).contiguous()
         else:              # out[i] = parent[flat[i]]
@@ -580,8 +613,16 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
         R = _aggregate_nodes(R, parent, n_l)
         Wn = _aggregate_nodes(Wn, parent, n_l)   # Q^l: drawn at the level (same law)
         hubs = _is_hub_level(R)
+        if mode == "all" or (mode == "hub" and _hot_nodes(R) is not None):
+            # the level's own tables: source ~ R^l, collapse c_a, target ~ P^l_a.
+            S = build_sampled_tables(*pairs, R, Wn)
+            if SRC_RECORDS:
+                S.src_rec = src_records(S, pairs[0], S.collapse)
+            out.append(LevelData(n_l, pairs[1].numel(), pairs[0], None, None, None, None, S))
+            continue
         S = SampledTables(S0.src_alias, S0.row_alias, None, None, hubs, map=flat, indptr=ip,
-                          mass=R, hot=_hot_nodes(R), neg=build_neg_table(Wn, R), span=S0.span)
+                          mass=R, hot=_hot_nodes(R), neg=build_neg_table(Wn, R), span=S0.span,
+                          src_rec=S0.src_rec)
         out.append(LevelData(n_l, 0, None, None, None, None, None, S))
     return out
 
@@ -825,14 +866,17 @@ class LayoutPlan:
         div = fine if level == 0 else coarse
         ip, n_tab, mp, neg = self._tables(level)
         det = o.threads == 1 and not o.sampled_fused
+        rec = S.src_rec is not None and not o.sampled_fused
         flags = (int(S.hubs) * _lib.DRG_SAMPLED_AGGREGATE
+                 | (_lib.DRG_SAMPLED_SRC_RECORDS if rec else 0)
                  | (_lib.DRG_SAMPLED_FUSED if o.sampled_fused else 0)
                  | (_lib.DRG_SAMPLED_DETERMINISTIC if det else 0)
                  | (_lib.DRG_SAMPLED_L2_HINTS if self.levels[0].n >= L2_HINT_NODES else 0))
         if self.evals is None:
             self.evals = torch.zeros(1, dtype=torch.int64, device=y.device)
         _lib.call("drg_layout_sampled", _lib.ptr(ip), _lib.ptr(S.span), None,
-                  _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), self._collapse(level),
+                  _lib.ptr(S.row_alias), _lib.ptr(S.src_rec if rec else S.src_alias),
+                  self._collapse(level),
                   _lib.ptr(neg.alias), _lib.ptr(mp), n_tab, neg.n, neg.tail_n, float(neg.tail_p),
                   _lib.ptr(y), step_lo, n_steps, t0, n_iter,
                   o.iters,
