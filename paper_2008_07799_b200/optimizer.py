@@ -522,6 +522,7 @@ HOT_NODES = 64
 # n/4 default reaches (profiles/r02_quality_rmat20_*).  The plain (unstaged) kernel
 # is faithful at n/4 because the hub's atomics serialise -- and 4x slower.
 HOT_MAX_THREADS = int(os.environ.get("DRG_HOT_MAX_THREADS", 65536))   # (env: experiments)
+HOT_CAP_SHARE = 0.01   # busiest node's share of the steps from which the cap is flat
 # Above this per-node rate the sampled epoch serialises on the hub's atomics even
 # warp-aggregated, and the gather (K7 + heavy-row split) is faster: R-MAT's coarse
 # levels (busiest node 2.4e5 - 4.8e6 steps per epoch) -- while R-MAT's level 0
@@ -532,7 +533,7 @@ GATHER_STEPS = 32768
 
 # Source draws from 32-byte records (drg_src_records) on 1-GPU sampled levels
 # (DRG_SRC_RECORDS env for experiments: 1 = on)
-SRC_RECORDS = os.environ.get("DRG_SRC_RECORDS", "0") == "1"
+SRC_RECORDS = os.environ.get("DRG_SRC_RECORDS", "1") == "1"
 
 
 def src_records(S: SampledTables, indptr: torch.Tensor, collapse) -> torch.Tensor | None:
@@ -574,7 +575,7 @@ def build_sampled_tables(ip, tg, P, R, Wn=None) -> SampledTables:
 # Coarse levels that draw from their own pair tables (P^l aggregated, level-l form of
 # the law) instead of level 0's through the composed map: "hub" = the hub-staged
 # levels (DRG_LEVEL_TABLES env for experiments: none | hub | all)
-LEVEL_TABLES = os.environ.get("DRG_LEVEL_TABLES", "none")
+LEVEL_TABLES = os.environ.get("DRG_LEVEL_TABLES", "hub")
 
 
 def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
@@ -888,11 +889,25 @@ class LayoutPlan:
                   0 if S.hot is None else S.hot.numel(), _lib.stream_ptr())
 
     def _steps_in_flight(self, level: int, div: int) -> int:
-        """n_l / divisor, capped at HOT_MAX_THREADS on levels with staged hub nodes."""
+        """n_l / divisor, capped on levels with staged hub nodes: at HOT_MAX_THREADS
+        where the busiest node's share of the steps is >= HOT_CAP_SHARE, and where
+        it is below (R-MAT scale 24's level 0: 8.7e-4) at the steps in flight that
+        keep the concurrent steps on the hub (threads x share) at the cap's value
+        for HOT_CAP_SHARE -- 25x below the products measured faithful on R-MAT
+        scale 20 (64 k x 0.116 - 0.255, profiles/r02_quality_rmat20_*)."""
         L = self.levels[level]
         c = max(32, L.n // max(1, div))
         hot = L.sampled.hot is not None and not (self.opt.threads == 1)
-        return min(c, HOT_MAX_THREADS) if hot else c
+        if not hot:
+            return c
+        key = ("share", level)
+        if key not in self._shard_cache:   # (host syncs once per plan and level)
+            R = L.sampled.mass
+            self._shard_cache[key] = (float(R.max()) / max(float(R.sum()), 1e-300)
+                                      if R is not None else 1.0)
+        share = self._shard_cache[key]
+        cap = HOT_MAX_THREADS * max(1.0, HOT_CAP_SHARE / max(share, 1e-300))
+        return int(min(c, cap))
 
     def _collapse(self, level: int):
         """Collapse probabilities of ``level`` (NULL at level 0 and for mapped draws)."""

@@ -261,3 +261,71 @@ def test_hub_level_inline_draws_run_the_drawn_steps(threads):
         want = O.drawn_steps(y.astype(np.float64), d.cpu().numpy(), 0.02 * (1.0 - t / 10),
                              gamma, 1e-3, 5.0, plan.opt.b)
         np.testing.assert_allclose(got, want, rtol=0, atol=1e-4)
+
+
+def _setup_level_tables(golden, mode="all"):
+    """_setup with the coarse levels drawing from their own aggregated pair tables
+    (build_mapped_level_data(level_tables=mode)): the level-l form of the law."""
+    from paper_2008_07799_b200.optimizer import build_mapped_level_data
+    from paper_2008_07799_b200.graph import DeviceGraph
+    from paper_2008_07799_b200.optimizer import prepare_layout
+    g = golden_graph(golden, "r500")
+    gg = B.Graph(np.asarray(g.indptr, dtype=np.int64), np.asarray(g.indices, dtype=np.int32))
+    prep = prepare_layout(DeviceGraph.from_host(gg), B.SimilarityParams(k=2),
+                          B.OptimizerParams(seed=0, neg_samples=5, iters=10), min_size=8)
+    plan = prep.plan
+    plan.levels = build_mapped_level_data(prep.similarity, prep.hierarchy, plan.opt.neg_power,
+                                          level_tables=mode)
+    ns = O.build_sparse_similarity(O.all_k_neighborhoods(g, 2))
+    dh = prep.hierarchy
+    oh = O.Hierarchy([lv.to_host() for lv in dh.levels], [m.cpu().numpy() for m in dh.maps],
+                     0.8, 8)
+    return plan, ns, oh
+
+
+@pytest.mark.parametrize("pick", ["middle", "coarsest"])
+def test_level_tables_pair_law(golden, pick):
+    """Coarse levels drawing from their own tables (source ~ R^l, collapse c_a,
+    target ~ P^l_a.) follow the reference's draw-at-level-0-then-map law."""
+    plan, ns, oh = _setup_level_tables(golden)
+    level = _level(plan, pick)
+    S = plan.levels[level].sampled
+    assert S.map is None and S.collapse is not None
+    n = plan.levels[level].n
+    ip, tg, P, R, Q = O.level_data(ns, oh, level)
+    epochs = max(1, 3_000_000 // n)
+    d = plan.sampled_draws(level, 0, n, 2, epochs).cpu().numpy()
+    i = d[:, 0, :].ravel().astype(np.int64)
+    j = d[:, 1, :].ravel().astype(np.int64)
+    counts = np.bincount(i * n + j, minlength=n * n).astype(np.float64)
+    expected = np.zeros(n * n)
+    rows = np.repeat(np.arange(n), np.diff(ip))
+    np.add.at(expected, rows * n + tg, P)
+    inner = R - np.bincount(rows, weights=P, minlength=n)
+    expected[np.arange(n) * n + np.arange(n)] += np.maximum(inner, 0.0)
+    assert _chi2(counts, expected) > 1e-6
+
+
+@pytest.mark.parametrize("mode", ["none", "all"])
+def test_source_records_draw_the_same_steps(golden, mode):
+    """32-byte source records (drg_src_records, DRG_SAMPLED_SRC_RECORDS) make the same
+    source, span and collapse decisions as the separate tables: with one step in
+    flight a whole epoch is bitwise identical, at every level, for the mapped
+    (level-0 tables) and the level-table plans."""
+    from paper_2008_07799_b200.optimizer import src_records
+    plan, _, _ = _setup_level_tables(golden, mode)
+    rng = np.random.default_rng(21)
+    for level in range(plan.depth + 1):
+        L = plan.levels[level]
+        S = L.sampled
+        y0 = torch.from_numpy(rng.normal(0, 1.0, size=(L.n, 2)).astype(np.float32)).cuda()
+        outs = []
+        for use in (False, True):
+            S.src_rec = (src_records(S, S.indptr if S.map is not None else L.indptr,
+                                     S.collapse if level > 0 else None) if use else None)
+            y = y0.clone()
+            plan.sampled_steps(level, y, 0, L.n, 3, 1, max_threads=1)
+            outs.append(y)
+        S.src_rec = None
+        assert not torch.equal(outs[0], y0)
+        assert torch.equal(outs[0], outs[1])
