@@ -563,6 +563,7 @@ struct PArgs {
     float hot_scale;        // apply_hot_kernel's fixed-point scale (set by launch_apply)
     int b, M;
     int probe;
+    int *locks = nullptr;   // per-node step locks (DRG_SAMPLED_LOCKS), see locked_step
 };
 
 // The reference step (_kernels.py:82-140) on drawn (i, j, negatives): the source's
@@ -684,6 +685,42 @@ __device__ __forceinline__ void step_body(const PArgs &A, const St &st, int64_t 
     st.add((gix != 0.f || giy != 0.f) ? i : -1, gix, giy);
 }
 
+// A step under per-node locks on its source and attraction partner: the steps in
+// flight then touch disjoint (i, j) pairs, so the attraction -- the local structure
+// NP measures -- never reads a position another in-flight step is about to move,
+// at any number of steps in flight (the negatives stay Hogwild: their staleness is
+// harmless, as the multi-GPU form's epoch-old snapshots show).  Both locks are
+// tried at once (one L2 round trip); a step that fails releases what it took and
+// retries a bounded number of times, then runs unlocked (plain Hogwild) -- no
+// waiting cycle can form.  The step's reductions are fenced before the release.
+constexpr int kLockTries = 16;
+
+template <int B, class St>
+__device__ __forceinline__ void locked_step(const PArgs &A, const St &st, int64_t i, int64_t j,
+                                            const int32_t *cand, int64_t sl) {
+    int *L = A.locks;
+    bool got = false;
+    if (L) {
+        for (int tries = 0; tries < kLockTries; ++tries) {
+            const int ri = atomicCAS(L + i, 0, 1);
+            const int rj = i != j ? atomicCAS(L + j, 0, 1) : 0;
+            if (ri == 0 && rj == 0) {
+                got = true;
+                break;
+            }
+            if (ri == 0) atomicExch(L + i, 0);
+            if (rj == 0 && i != j) atomicExch(L + j, 0);
+            __nanosleep(100 + 50 * (threadIdx.x & 7));
+        }
+    }
+    step_body<B>(A, st, i, j, cand, sl);
+    if (got) {
+        __threadfence();
+        atomicExch(L + i, 0);
+        if (i != j) atomicExch(L + j, 0);
+    }
+}
+
 // grid-stride over the launch's steps; the next step's record is prefetched while
 // this step runs
 // The columns of several ranks' draws (emulated multi-GPU: rank after rank in one
@@ -695,7 +732,7 @@ __device__ __forceinline__ int64_t column(const PArgs &A, int64_t sl) {
     return SPREAD ? (int64_t)(((uint64_t)sl * A.spread) % (uint64_t)A.n_steps) : sl;
 }
 
-template <int B, class St, bool SPREAD = false>
+template <int B, class St, bool SPREAD = false, bool LOCK = false>
 __device__ __forceinline__ void apply_steps(const PArgs &A, const St &st, int64_t sl,
                                             const int64_t nthreads) {
     const int Me = min(A.M, kMaxNeg);
@@ -720,7 +757,8 @@ __device__ __forceinline__ void apply_steps(const PArgs &A, const St &st, int64_
             for (int m = 0; m < kMaxNeg; ++m)
                 if (m < Me) cc[m] = __ldcs(A.draws + (2 + m) * sd + col);
         }
-        step_body<B>(A, st, i, j, cand, cur);
+        if (LOCK) locked_step<B>(A, st, i, j, cand, cur);
+        else step_body<B>(A, st, i, j, cand, cur);
     }
 }
 
@@ -929,6 +967,15 @@ __global__ void __launch_bounds__(256, 1) apply_kernel_lc(PArgs A, float2 *y) {
                         (int64_t)gridDim.x * blockDim.x);
 }
 
+// steps under (i, j) locks (DRG_SAMPLED_LOCKS)
+template <int B>
+__global__ void __launch_bounds__(256, 1) apply_locked_kernel(PArgs A, float2 *y) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    apply_steps<B, GlobalStore<false>, false, true>(
+        A, GlobalStore<false>{y, A.probe}, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+        (int64_t)gridDim.x * blockDim.x);
+}
+
 // deterministic sub-batch: one step per thread, positions frozen for the launch
 template <int B>
 __global__ void __launch_bounds__(256) apply_det_kernel(PArgs A, float2 *y) {
@@ -1016,7 +1063,9 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
         cfg.blockDim = dim3((unsigned)hb);
         cfg.gridDim = dim3((unsigned)ceil_div(threads, hb));
     }
-    if (hot && n_hot > 0)   // hub level: the hottest nodes staged per block
+    if (P.locks && !(hot && n_hot > 0) && !agg)
+        fn = P.b == 2 ? (void *)apply_locked_kernel<2> : (void *)apply_locked_kernel<0>;
+    else if (hot && n_hot > 0)   // hub level: the hottest nodes staged per block
         fn = agg ? (P.b == 2 ? (void *)apply_hot_kernel<true, 2> : (void *)apply_hot_kernel<true, 0>)
                  : (P.b == 2 ? (void *)apply_hot_kernel<false, 2> : (void *)apply_hot_kernel<false, 0>);
     else
@@ -1604,6 +1653,15 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
     const int nchunks = (n_iter + K - 1) / K;
     Scratch buf(st);
     DRG_CUDA(buf.alloc(rec_bytes * (size_t)K * (nchunks > 1 ? 2 : 1)));
+    static const bool use_locks = [] {
+        const char *e = getenv("DRG_SAMPLED_LOCKS");
+        return e && e[0] == '1';
+    }();
+    Scratch locks(st);
+    if (use_locks && !det && !agg && !(hot && n_hot > 0)) {
+        DRG_CUDA(locks.alloc(sizeof(int) * (size_t)n_y));
+        DRG_CUDA(cudaMemsetAsync(locks.p, 0, sizeof(int) * (size_t)n_y, st));
+    }
     SideStreams ss;
     DRG_CUDA(side_streams(&ss));
     Events ev;   // 0 start, 1-2 drawn[2], 3-4 applied[2], 5 draws done
@@ -1673,6 +1731,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
         DRG_CUDA(cudaStreamWaitEvent(st, ev.e[0], 0));
         return evs.finish(st);
     }
+    P.locks = locks.as<int>();   // NULL unless DRG_SAMPLED_LOCKS
     int rc = draw(0);
     if (rc) return rc;
     Scratch delta(st);

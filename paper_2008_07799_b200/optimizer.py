@@ -531,9 +531,17 @@ HOT_CAP_SHARE = 0.01   # busiest node's share of the steps from which the cap is
 GATHER_STEPS = 32768
 
 
-# Source draws from 32-byte records (drg_src_records) on 1-GPU sampled levels
-# (DRG_SRC_RECORDS env for experiments: 1 = on)
-SRC_RECORDS = os.environ.get("DRG_SRC_RECORDS", "1") == "1"
+# Source draws from 32-byte records (drg_src_records) on 1-GPU sampled levels whose
+# per-node tables are far above L2 (>= L2_HINT_NODES level-0 nodes: R-MAT scale 24,
+# one DRAM miss per drawn source instead of three).  Below that the three 8-byte
+# tables stay in L2 and the records only add traffic: the C4 mesh's draw pass read
+# 280 MB of DRAM per epoch with them against 235 MB without, at the same speed.
+# (DRG_SRC_RECORDS env for experiments: 1 = always, 0 = never)
+SRC_RECORDS = os.environ.get("DRG_SRC_RECORDS", "auto")
+
+
+def _use_src_records(n0: int) -> bool:
+    return SRC_RECORDS == "1" or (SRC_RECORDS == "auto" and n0 >= L2_HINT_NODES)
 
 
 def src_records(S: SampledTables, indptr: torch.Tensor, collapse) -> torch.Tensor | None:
@@ -591,19 +599,25 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
     Wn = device_negative_weights(R, neg_power)
     S0 = build_sampled_tables(ip, tg, P, R, Wn)
     S0.collapse = None   # no pair collapses at level 0
-    if SRC_RECORDS:
-        S0.src_rec = src_records(S0, ip, None)
     n0 = dh.levels[0].node_count
+    use_rec = _use_src_records(n0)
+    if use_rec:
+        S0.src_rec = src_records(S0, ip, None)
     out = [LevelData(n0, tg.numel(), ip, None, None, None, None, S0)]
     flat = None
     st = _lib.stream_ptr()
     mode = LEVEL_TABLES if level_tables is None else level_tables
-    pairs = (ip, tg, P)   # P^l pulled up level by level (only when some level uses it)
-    need = mode != "none"
+    pairs = (ip, tg, P)   # P^l pulled up level by level, as far as some level uses it
+    own, Rl = {}, R        # levels that draw from their own tables (R^l is cheap)
+    for level in range(1, dh.depth + 1):
+        Rl = _aggregate_nodes(Rl, dh.maps[level - 1], dh.levels[level].node_count)
+        own[level] = mode == "all" or (mode == "hub" and _hot_nodes(Rl) is not None)
+    last_own = max((lv for lv, o in own.items() if o), default=0)
+    del Rl
     for level in range(1, dh.depth + 1):
         n_l = dh.levels[level].node_count
         parent = dh.maps[level - 1]
-        if need:
+        if level <= last_own:
             pairs = _aggregate_pairs(*pairs, parent, n_l)
         if flat is None:   # level 1: the parent map itself
             flat = parent.to(torch.int32).contiguous()
@@ -614,10 +628,10 @@ def build_mapped_level_data(ds: DeviceSimilarity, dh: DeviceHierarchy,
         R = _aggregate_nodes(R, parent, n_l)
         Wn = _aggregate_nodes(Wn, parent, n_l)   # Q^l: drawn at the level (same law)
         hubs = _is_hub_level(R)
-        if mode == "all" or (mode == "hub" and _hot_nodes(R) is not None):
+        if own[level]:
             # the level's own tables: source ~ R^l, collapse c_a, target ~ P^l_a.
             S = build_sampled_tables(*pairs, R, Wn)
-            if SRC_RECORDS:
+            if use_rec:
                 S.src_rec = src_records(S, pairs[0], S.collapse)
             out.append(LevelData(n_l, pairs[1].numel(), pairs[0], None, None, None, None, S))
             continue
