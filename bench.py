@@ -79,6 +79,8 @@ def parse():
                     help="level-0 steps in flight = n / this (default: by graph size)")
     ap.add_argument("--sampled-concurrency-coarse", type=int, default=None,
                     help="coarse-level steps in flight = n_l / this (default: by graph size)")
+    ap.add_argument("--sampled-locks", choices=["auto", "on", "off"], default="auto",
+                    help="steps under (i, j) locks on plain sampled levels (auto: by graph size)")
     ap.add_argument("--hub-levels", choices=["jacobi", "sampled"], default="sampled",
                     help="update the hub-heavy levels of update=sampled run")
     return ap.parse_args()
@@ -161,7 +163,7 @@ def build_workload(name):
 
 
 def params_for(name, iters_override=None, update="sampled", concurrency=None,
-               hub_levels="sampled", concurrency_coarse=None):
+               hub_levels="sampled", concurrency_coarse=None, locks="auto"):
     import paper_2008_07799_b200 as B
     w = WORKLOADS[name]
     sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"], neighbor_cap=w.get("cap"))
@@ -171,6 +173,7 @@ def params_for(name, iters_override=None, update="sampled", concurrency=None,
     opt = B.OptimizerParams(neg_samples=w["M"], iters=iters_override or w["iters"], seed=0,
                             init=w["init"], update=update, sampled_concurrency=concurrency,
                             sampled_concurrency_coarse=concurrency_coarse, hub_levels=hub_levels,
+                            sampled_locks={"auto": None, "on": True, "off": False}[locks],
                             threads=max(2, os.cpu_count() or 2))
     return sim, opt, dict(w["hier"])
 
@@ -287,7 +290,8 @@ def run_ours(args):
         group = dist.group.WORLD
     name = args.workload
     sim, opt, hier = params_for(name, args.iters, args.update, args.sampled_concurrency,
-                                args.hub_levels, args.sampled_concurrency_coarse)
+                                args.hub_levels, args.sampled_concurrency_coarse,
+                                args.sampled_locks)
 
     dg = build_workload(name)
     torch.cuda.synchronize()
@@ -295,6 +299,7 @@ def run_ours(args):
                           force_levels=hier.get("force_levels"), timed=True)
     plan = prep.plan
     sizes = prep.hierarchy.sizes
+    plan_locked = [opt.update == "sampled" and plan.locked_level(lv) for lv in range(len(sizes))]
     nnzs = [lv.nnz for lv in plan.levels]
     prep_ms = {k: round(v, 3) for k, v in prep.timings.items()}
     # the same preparation again, warm (module loading / pool growth excluded)
@@ -361,6 +366,7 @@ def run_ours(args):
         variants = {"jacobi": {}, "inplace": {}, "sampled": {"sampled_fused": False},
                     "sampled_fused": {"update": "sampled", "sampled_fused": True},
                     "sampled_deterministic": {"update": "sampled", "threads": 1},
+                    "sampled_hogwild": {"update": "sampled", "sampled_locks": False},
                     "sgather": {}}
         for label, extra in variants.items():
             kw2 = {"update": label, **extra}
@@ -368,6 +374,8 @@ def run_ours(args):
                 kw2["threads"] = opt.threads
             if all(getattr(opt, k) == v for k, v in kw2.items()):
                 continue
+            if label == "sampled_hogwild" and not any(plan_locked):
+                continue   # the default already is the Hogwild form
             o2 = B.OptimizerParams(**{**opt.__dict__, **kw2})
             mode = kw2["update"]
             p2 = build_plan(prep.similarity, prep.hierarchy, o2)
@@ -485,6 +493,8 @@ def run_ours(args):
             "config": {"workload": name, "desc": WORKLOADS[name]["desc"], "levels": sizes,
                        "nnz_per_level": nnzs,
                        "iters_per_level": T, "update": opt.update, "hub_levels": opt.hub_levels,
+                       "locked_levels": [lv for lv in range(len(sizes))
+                                         if opt.update == "sampled" and plan_locked[lv]],
                        "l2": "256 MiB flush between steps; level-0 stream "
                              f"{alg_bytes / 1e9:.2f} GB/iteration > 126 MB L2",
                        "parallelism": f"node-range x{world}" if world > 1 else "single GPU"},

@@ -250,6 +250,16 @@ int drg_row_spans(const int64_t *indptr, int64_t n, uint64_t *out_span, void *st
  * reads the Vose bucket, the row span and the collapse probability of both of the
  * bucket's outcomes from one sector (split form only) */
 #define DRG_SAMPLED_SRC_RECORDS 16
+/* steps under per-node locks on the source i and the attraction partner j: the
+ * steps in flight touch disjoint (i, j) pairs, so attraction never reads a position
+ * another in-flight step is about to move -- the reference's sequential semantics
+ * for the pair (_kernels.py:82-105) at any number of steps in flight; the negatives
+ * stay Hogwild.  Try-locks (CAS) released without a fence: the updates of i and j
+ * are returning atomics and the release depends on their results.  A step that
+ * cannot get both locks retries while the warp's other lanes run, and after 64
+ * failures runs unlocked.  Plain levels only (not with AGGREGATE, hot nodes, FUSED
+ * or DETERMINISTIC: DRG_ERR_UNSUPPORTED).  Also accepted by drg_sampled_apply. */
+#define DRG_SAMPLED_LOCKED 32
 
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_span, const uint64_t *rec,
                        const uint64_t *row_alias,

@@ -31,6 +31,7 @@ DRG_SAMPLED_DETERMINISTIC = 4
 DRG_SHARD_LAGGED = 1
 DRG_SAMPLED_L2_HINTS = 8
 DRG_SAMPLED_SRC_RECORDS = 16
+DRG_SAMPLED_LOCKED = 32
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

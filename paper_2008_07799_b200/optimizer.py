@@ -107,6 +107,11 @@ class OptimizerParams:
     # value on coarser levels; None = by graph size (sampled_divisors)
     sampled_concurrency: int | None = None
     sampled_concurrency_coarse: int | None = None
+    # update="sampled", threads > 1: steps under per-node locks on the source and the
+    # attraction partner (DRG_SAMPLED_LOCKED) on plain (non-hub) levels.  None = by
+    # graph size: on for graphs below FAST_CONCURRENCY_NODES nodes, whose Hogwild
+    # form is held to n/256 steps in flight by fidelity (locked_divisors)
+    sampled_locks: bool | None = None
     att_samples: int = 2           # update="sgather": attraction partners drawn per node
     # update="sampled": the update of levels above GATHER_STEPS.  "sampled" (default)
     # keeps the reference's step there too; "jacobi" gathers them -- 3-6x faster on
@@ -506,6 +511,28 @@ def sampled_divisors(n0: int, opt: "OptimizerParams") -> tuple[int, int]:
     return fine, coarse
 
 
+# Steps under (i, j) locks (DRG_SAMPLED_LOCKED): the steps in flight touch disjoint
+# (source, partner) pairs, so the fidelity no longer depends on how many there are.
+# C1 (100 seeds, profiles/r02_quality_grid_locks.jsonl): Hogwild at n/4 steps in
+# flight KL +2.4% / NP -11.6%, at n/16 +0.6% / -4.1%; locked at n/1 KL +0.03% / NP
+# +1.1% +- 2.0%.  C2 (48 seeds, r02_quality_rgg_48seeds_locks.jsonl): locked at n/1
+# on every level KL -0.01% / NP +1.4% +- 1.7%, at n/2 (n/1 coarse) +0.14% / +0.5% +-
+# 1.6% (Hogwild n/256: +0.07% / +0.5% +- 1.7%).  A locked step costs two more L2
+# round trips (acquire, returning update) and retries while its nodes are held, so
+# it pays where Hogwild is fidelity-capped far below the machine: graphs under
+# FAST_CONCURRENCY_NODES (C1 2 528 -> 23 181 iters/s, C2 4 788 -> 21 397,
+# r02_bench_locks_sweep.jsonl).  On the C4 mesh the Hogwild levels are faster:
+# level 0 is bound by random L2 operations, to which the locks add four per step
+# (174 -> 253 ms), and its small coarse levels run n/4 Hogwild -- measured faithful
+# there -- in 8-15 ms against 37-48 ms locked.
+LOCKED_DIVISORS = (1, 1)
+
+
+def locked_divisors(opt: "OptimizerParams") -> tuple[int, int]:
+    return (opt.sampled_concurrency or LOCKED_DIVISORS[0],
+            opt.sampled_concurrency_coarse or LOCKED_DIVISORS[1])
+
+
 HUB_STEPS = 512   # warp-aggregate the sampled updates above this per-node rate
 # level-0 node count from which the per-node tables (8 B per node each) are far above
 # L2 and the inline draws of hub levels take L2 eviction hints (DRG_SAMPLED_L2_HINTS)
@@ -877,12 +904,14 @@ class LayoutPlan:
         if S is None:
             raise RuntimeError("plan was built without sampled-mode tables")
         o = self.opt
-        fine, coarse = sampled_divisors(self.levels[0].n, o)
+        locked = self.locked_level(level)
+        fine, coarse = locked_divisors(o) if locked else sampled_divisors(self.levels[0].n, o)
         div = fine if level == 0 else coarse
         ip, n_tab, mp, neg = self._tables(level)
         det = o.threads == 1 and not o.sampled_fused
         rec = S.src_rec is not None and not o.sampled_fused
         flags = (int(S.hubs) * _lib.DRG_SAMPLED_AGGREGATE
+                 | (_lib.DRG_SAMPLED_LOCKED if locked else 0)
                  | (_lib.DRG_SAMPLED_SRC_RECORDS if rec else 0)
                  | (_lib.DRG_SAMPLED_FUSED if o.sampled_fused else 0)
                  | (_lib.DRG_SAMPLED_DETERMINISTIC if det else 0)
@@ -901,6 +930,18 @@ class LayoutPlan:
                   flags, L.n, _lib.ptr(self.evals) if count else None,
                   _lib.ptr(S.hot) if (S.hot is not None and not det) else None,
                   0 if S.hot is None else S.hot.numel(), _lib.stream_ptr())
+
+    def locked_level(self, level: int) -> bool:
+        """Whether ``level``'s sampled epochs run under (i, j) locks: plain Hogwild
+        levels (no hub aggregation / staging, threads > 1, split form) of graphs
+        below FAST_CONCURRENCY_NODES nodes, or as OptimizerParams.sampled_locks says."""
+        o = self.opt
+        S = self.levels[level].sampled
+        if S is None or o.threads == 1 or o.sampled_fused or S.hubs or S.hot is not None:
+            return False
+        if o.sampled_locks is not None:
+            return bool(o.sampled_locks)
+        return self.levels[0].n < FAST_CONCURRENCY_NODES
 
     def _steps_in_flight(self, level: int, div: int) -> int:
         """n_l / divisor, capped on levels with staged hub nodes: at HOT_MAX_THREADS
@@ -958,16 +999,17 @@ class LayoutPlan:
         return out
 
     def sampled_apply(self, level: int, draws: torch.Tensor, y: torch.Tensor, t: int,
-                      max_threads: int = 1) -> None:
+                      max_threads: int = 1, locked: bool = False) -> None:
         """drg_sampled_apply: one epoch's drawn steps (int32 [2 + M, n_steps]) on y in
-        place at epoch t's learning rate, <= max_threads steps in flight."""
+        place at epoch t's learning rate, <= max_threads steps in flight; ``locked``:
+        under (i, j) locks (DRG_SAMPLED_LOCKED)."""
         _, gamma, _ = self._level_args(level)
         o = self.opt
         draws = draws.contiguous()
         lr = max(o.lr0 * (1.0 - t / o.iters), 0.0)
         _lib.call("drg_sampled_apply", _lib.ptr(draws), draws.shape[-1], _lib.ptr(y), lr,
                   float(gamma), float(o.eps), float(o.grad_clip), o.b, o.neg_samples,
-                  max_threads, 0, _lib.stream_ptr())
+                  max_threads, _lib.DRG_SAMPLED_LOCKED if locked else 0, _lib.stream_ptr())
 
     def _run_level_sampled(self, level, y, t0, n_iter, group=None, step_fn=None):
         """Reference-faithful epochs: n_l sampled steps each, Hogwild on y.  Levels of

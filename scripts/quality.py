@@ -114,6 +114,10 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
             extra = {}
             if upd == "sampledf":   # the fused one-kernel form of "sampled"
                 upd, extra = "sampled", {"sampled_fused": True}
+            if upd == "sampledL":   # steps under (i, j) locks on plain levels
+                upd, extra = "sampled", {"sampled_locks": True}
+            if upd == "sampledH":   # plain Hogwild (no locks) on every level
+                upd, extra = "sampled", {"sampled_locks": False}
             if upd == "sampledh":   # "sampled" on every level, hub-heavy ones included
                 upd, extra = "sampled", {"hub_levels": "sampled"}
             if div and upd == "sampled":

@@ -69,7 +69,7 @@ def _check(rows):
 def test_c1_grid_final_layout_parity(threads):
     """BASELINE C1: 100 x 100 grid, k=2, perplexity 30, 300 iterations, single level,
     uniform init; 40 seeds; threads = 1 (deterministic sub-batches, the default) and
-    threads = 16 (Hogwild)."""
+    threads = 16 (steps under (i, j) locks, n/2 in flight)."""
     from paper_2008_07799_b200 import synthetic
     g = synthetic.grid(100, 100, device="host")
     og, bg = O.Graph(g.indptr, g.indices), B.Graph(g.indptr, g.indices)
@@ -77,11 +77,13 @@ def test_c1_grid_final_layout_parity(threads):
     _check(rows)
 
 
-def test_c2_reduced_rgg_final_layout_parity():
+@pytest.mark.parametrize("threads", [1, 16])
+def test_c2_reduced_rgg_final_layout_parity(threads):
     """BASELINE C2 reduced to 50 000 points (mean degree 10), k=3, perplexity 30,
-    500 iterations, 3 levels; 20 seeds, the default threads = 1."""
+    500 iterations, 3 levels; 20 seeds; threads = 1 (the default, deterministic) and
+    threads = 16 (steps under (i, j) locks on every level)."""
     from paper_2008_07799_b200 import synthetic
     g = synthetic.rgg(50_000, seed=0, device="host")
     og, bg = O.Graph(g.indptr, g.indices), B.Graph(g.indptr, g.indices)
-    rows = _arms(og, bg, 3, 30.0, 500, 3, "normal", range(700, 720), 1)
+    rows = _arms(og, bg, 3, 30.0, 500, 3, "normal", range(700, 720), threads)
     _check(rows)

@@ -329,3 +329,82 @@ def test_source_records_draw_the_same_steps(golden, mode):
         S.src_rec = None
         assert not torch.equal(outs[0], y0)
         assert torch.equal(outs[0], outs[1])
+
+
+# ---- steps under (i, j) locks (DRG_SAMPLED_LOCKED) ---------------------------------
+
+@pytest.mark.parametrize("pick", ["finest", "coarsest"])
+def test_locked_step_and_sequential_epoch_parity(golden, pick):
+    """The locked form runs the reference step: single steps within 1e-5 max(1, |g|)
+    of the oracle's drawn_steps, a whole epoch with one step in flight equal to the
+    oracle's sequential replay."""
+    plan, _, _ = _setup(golden)
+    level = _level(plan, pick)
+    n = plan.levels[level].n
+    t = 3
+    lr = 1.0 - t / 10
+    _, gamma, _ = plan._level_args(level)
+    d = plan.sampled_draws(level, 0, n, t)[0]
+    y = np.random.default_rng(5).normal(0, 1.0, size=(n, 2)).astype(np.float32)
+    yd = torch.from_numpy(y).cuda()
+    for s in range(min(n, 24)):
+        out = yd.clone()
+        plan.sampled_apply(level, d[:, s:s + 1], out, t, locked=True)
+        got = out.cpu().numpy().astype(np.float64)
+        want = O.drawn_steps(y.astype(np.float64), d[:, s:s + 1].cpu().numpy(), lr, gamma,
+                             1e-3, 5.0, plan.opt.b)
+        g_got, g_want = (got - y) / lr, (want - y) / lr
+        assert np.all(np.abs(g_got - g_want) <= 1e-5 * np.maximum(1.0, np.abs(g_want))), s
+    out = yd.clone()
+    plan.sampled_apply(level, d, out, t, max_threads=1, locked=True)
+    want = O.drawn_steps(y.astype(np.float64), d.cpu().numpy(), lr, gamma, 1e-3, 5.0, plan.opt.b)
+    np.testing.assert_allclose(out.cpu().numpy(), want, rtol=0, atol=1e-4)
+
+
+def test_locked_steps_on_one_pair_serialise():
+    """Mutual exclusion and visibility of the locks: 8192 attraction-only steps over
+    128 disjoint pairs, 256 in flight (every pair contended).  Steps on one pair all
+    apply the same map to (y_i, y_j) and the pairs are disjoint, so ANY serial order
+    gives bit for bit the sequential result -- the locked run must equal it; plain
+    Hogwild at the same concurrency (stale reads, same-address increments from old
+    positions) does not."""
+    from paper_2008_07799_b200.graph import DeviceGraph
+    from paper_2008_07799_b200.optimizer import prepare_layout
+    from paper_2008_07799_b200 import synthetic
+    g = synthetic.grid(16, 16, device="host")
+    prep = prepare_layout(DeviceGraph.from_host(B.Graph(g.indptr, g.indices)),
+                          B.SimilarityParams(k=1),
+                          B.OptimizerParams(seed=0, neg_samples=0, iters=10, threads=4),
+                          max_levels=1)
+    plan = prep.plan
+    n, pairs, steps = 256, 128, 8192
+    rng = np.random.default_rng(3)
+    p = rng.integers(0, pairs, size=steps)
+    d = torch.from_numpy(np.stack([2 * p, 2 * p + 1]).astype(np.int32)).cuda()
+    y = rng.normal(0, 1.0, size=(n, 2)).astype(np.float32)
+    seq = torch.from_numpy(y).cuda()
+    plan.sampled_apply(0, d, seq, 2, max_threads=1)
+    locked = torch.from_numpy(y).cuda()
+    plan.sampled_apply(0, d, locked, 2, max_threads=256, locked=True)
+    assert torch.equal(locked, seq)
+    hog = torch.from_numpy(y).cuda()
+    plan.sampled_apply(0, d, hog, 2, max_threads=256)
+    assert not torch.equal(hog, seq)
+
+
+def test_locked_levels_policy(golden):
+    """Auto policy: plain levels of small graphs run locked at threads > 1; threads = 1
+    (deterministic), the fused form and sampled_locks=False do not."""
+    plan, _, _ = _setup(golden)
+    for kw, want in (({"threads": 8}, True), ({"threads": 1}, False),
+                     ({"threads": 8, "sampled_fused": True}, False),
+                     ({"threads": 8, "sampled_locks": False}, False)):
+        plan.opt = B.OptimizerParams(seed=0, neg_samples=5, iters=10, **kw)
+        hubs = plan.levels[0].sampled.hubs or plan.levels[0].sampled.hot is not None
+        assert plan.locked_level(0) == (want and not hubs), kw
+    plan.opt = B.OptimizerParams(seed=0, neg_samples=5, iters=10, threads=8)
+    y = torch.from_numpy(np.random.default_rng(1).normal(0, 1, (plan.levels[0].n, 2))
+                         .astype(np.float32)).cuda()
+    y0 = y.clone()
+    plan.sampled_steps(0, y, 0, plan.levels[0].n, 0, 2)      # two locked epochs run
+    assert torch.isfinite(y).all() and not torch.equal(y, y0)
