@@ -355,9 +355,16 @@ def test_locked_step_and_sequential_epoch_parity(golden, pick):
                              1e-3, 5.0, plan.opt.b)
         g_got, g_want = (got - y) / lr, (want - y) / lr
         assert np.all(np.abs(g_got - g_want) <= 1e-5 * np.maximum(1.0, np.abs(g_want))), s
-    out = yd.clone()
-    plan.sampled_apply(level, d, out, t, max_threads=1, locked=True)
-    want = O.drawn_steps(y.astype(np.float64), d.cpu().numpy(), lr, gamma, 1e-3, 5.0, plan.opt.b)
+    # one step in flight: the same fp32 operations in the same order as the plain
+    # form (bit for bit), and the oracle's sequential replay at the late-epoch
+    # learning rate of test_sampled_sequential_epoch_parity
+    for t2 in (3, 8):
+        out, plain = yd.clone(), yd.clone()
+        plan.sampled_apply(level, d, out, t2, max_threads=1, locked=True)
+        plan.sampled_apply(level, d, plain, t2, max_threads=1)
+        assert torch.equal(out, plain)
+    want = O.drawn_steps(y.astype(np.float64), d.cpu().numpy(), 1.0 - 8 / 10, gamma, 1e-3, 5.0,
+                         plan.opt.b)
     np.testing.assert_allclose(out.cpu().numpy(), want, rtol=0, atol=1e-4)
 
 
