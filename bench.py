@@ -81,6 +81,8 @@ def parse():
                     help="coarse-level steps in flight = n_l / this (default: by graph size)")
     ap.add_argument("--sampled-locks", choices=["auto", "on", "off"], default="auto",
                     help="steps under (i, j) locks on plain sampled levels (auto: by graph size)")
+    ap.add_argument("--sampled-snapshot", choices=["auto", "on", "off"], default="auto",
+                    help="negatives read from a per-epoch snapshot on Hogwild levels")
     ap.add_argument("--hub-levels", choices=["jacobi", "sampled"], default="sampled",
                     help="update the hub-heavy levels of update=sampled run")
     return ap.parse_args()
@@ -163,7 +165,7 @@ def build_workload(name):
 
 
 def params_for(name, iters_override=None, update="sampled", concurrency=None,
-               hub_levels="sampled", concurrency_coarse=None, locks="auto"):
+               hub_levels="sampled", concurrency_coarse=None, locks="auto", snapshot="auto"):
     import paper_2008_07799_b200 as B
     w = WORKLOADS[name]
     sim = B.SimilarityParams(k=w["k"], perplexity=w["perplexity"], neighbor_cap=w.get("cap"))
@@ -174,6 +176,7 @@ def params_for(name, iters_override=None, update="sampled", concurrency=None,
                             init=w["init"], update=update, sampled_concurrency=concurrency,
                             sampled_concurrency_coarse=concurrency_coarse, hub_levels=hub_levels,
                             sampled_locks={"auto": None, "on": True, "off": False}[locks],
+                            sampled_snapshot={"auto": None, "on": True, "off": False}[snapshot],
                             threads=max(2, os.cpu_count() or 2))
     return sim, opt, dict(w["hier"])
 
@@ -291,7 +294,7 @@ def run_ours(args):
     name = args.workload
     sim, opt, hier = params_for(name, args.iters, args.update, args.sampled_concurrency,
                                 args.hub_levels, args.sampled_concurrency_coarse,
-                                args.sampled_locks)
+                                args.sampled_locks, args.sampled_snapshot)
 
     dg = build_workload(name)
     torch.cuda.synchronize()
@@ -367,6 +370,7 @@ def run_ours(args):
                     "sampled_fused": {"update": "sampled", "sampled_fused": True},
                     "sampled_deterministic": {"update": "sampled", "threads": 1},
                     "sampled_hogwild": {"update": "sampled", "sampled_locks": False},
+                    "sampled_live_negatives": {"update": "sampled", "sampled_snapshot": False},
                     "sgather": {}}
         for label, extra in variants.items():
             kw2 = {"update": label, **extra}
@@ -376,6 +380,8 @@ def run_ours(args):
                 continue
             if label == "sampled_hogwild" and not any(plan_locked):
                 continue   # the default already is the Hogwild form
+            if label == "sampled_live_negatives" and (any(plan_locked) or opt.update != "sampled"):
+                continue
             o2 = B.OptimizerParams(**{**opt.__dict__, **kw2})
             mode = kw2["update"]
             p2 = build_plan(prep.similarity, prep.hierarchy, o2)

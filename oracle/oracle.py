@@ -865,14 +865,17 @@ def drawn_steps(pos, draws, lr, gamma, eps, clip, b):
     return pos
 
 
-def deferred_drawn_epoch(pos, draws, lr, gamma, eps, clip, b, snap=None, fold=True):
+def deferred_drawn_epoch(pos, draws, lr, gamma, eps, clip, b, snap=None, fold=True,
+                         defer=True):
     """The multi-GPU epoch of paper_2008_07799_b200/shard.py on given draws, as a
     sequential fp64 restatement: the reference step (_kernels.py:82-140) with the
     source and the attraction partner read and moved in place, each negative read
     from the epoch-start snapshot (plus this step's own earlier reactions on it) and
     its reaction deferred into a delta added at the epoch end.  ``snap``: an older
     snapshot to read the negatives from; ``fold=False`` returns (pos, delta)
-    without adding the delta."""
+    without adding the delta.  ``defer=False``: the 1-GPU snapshot form
+    (DRG_SAMPLED_SNAPSHOT) -- the negatives are still read from the snapshot, but
+    their reactions move ``pos`` at once, like every other update."""
     snap = pos.copy() if snap is None else snap
     delta = np.zeros_like(pos)
     bf = float(b)
@@ -905,7 +908,10 @@ def deferred_drawn_epoch(pos, draws, lr, gamma, eps, clip, b, snap=None, fold=Tr
                 coef = gamma * 2.0 * bf / ((ld2 + eps) * (1.0 + pw * ld2))
                 g = np.array([min(max(coef * dx, -clip), clip),
                               min(max(coef * dy, -clip), clip)]) * lr
-                delta[t] -= g
+                if defer:
+                    delta[t] -= g
+                else:
+                    pos[t] -= g
                 own[t] = own.get(t, 0.0) - g
                 yi += g
                 gi += g

@@ -32,6 +32,7 @@ DRG_SHARD_LAGGED = 1
 DRG_SAMPLED_L2_HINTS = 8
 DRG_SAMPLED_SRC_RECORDS = 16
 DRG_SAMPLED_LOCKED = 32
+DRG_SAMPLED_SNAPSHOT = 64
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

@@ -563,6 +563,7 @@ struct PArgs {
     float hot_scale;        // apply_hot_kernel's fixed-point scale (set by launch_apply)
     int b, M;
     int probe;
+    const float2 *snap = nullptr;   // DRG_SAMPLED_SNAPSHOT: epoch-start copy of y (negatives' reads)
     int *locks = nullptr;   // per-node step locks (apply_steps_locked), node v at v & lock_mask
     uint32_t lock_mask = 0xffffffffu;
     int zero = 0;           // 0 (a value the compiler cannot fold: release dependency)
@@ -611,6 +612,39 @@ struct FixedStore {    // deterministic sub-batch: y frozen, fixed-point increme
         add_fixed(delta, v, dx, dy);
     }
 };
+
+// Negatives read from a read-only snapshot of the positions (refreshed between
+// epochs by snap_copy_kernel); every update -- the negatives' reactions too -- still
+// goes to y at once.  Random gathers and float2 reductions on the SAME array run at
+// 148 G/s on this B200, on separate arrays at 260 G/s (scripts/l2_random_peak.cu,
+// profiles/r02_l2_random_peak.txt: reductions invalidate the lines the gathers
+// replicate across the two L2 partitions); with the five negative gathers of a step
+// moved to the snapshot the step's 14 accesses run at 213 G/s.  A negative's
+// position is then up to one epoch old -- the weak long-range repulsion tolerates
+// far more (the multi-GPU form, epoch-old reads AND deferred reactions: KL +0.00%,
+// NP within noise on the C4 mesh); source and partner stay live.
+struct SnapStore {
+    float2 *y;
+    const float2 *snap;
+    int probe;
+    __device__ __forceinline__ float2 load(int64_t v) const { return ld_y(y, v); }
+    __device__ __forceinline__ float2 load_neg(int64_t v) const { return __ldg(snap + v); }
+    __device__ __forceinline__ void add(int64_t v, float dx, float dy) const {
+        add_y_w<false>(y, v, dx, dy, probe);
+    }
+    __device__ __forceinline__ void add_neg(int64_t v, float dx, float dy) const { add(v, dx, dy); }
+};
+
+__global__ void snap_copy_kernel(const float2 *y, float2 *snap, int64_t n) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const float4 *s4 = reinterpret_cast<const float4 *>(y);
+    float4 *d4 = reinterpret_cast<float4 *>(snap);
+    const int64_t n4 = n / 2;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n4;
+         v += (int64_t)gridDim.x * blockDim.x)
+        d4[v] = __ldcg(s4 + v);
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) snap[n - 1] = __ldcg(y + n - 1);
+}
 
 __global__ void flush_kernel(float2 *y, unsigned long long *d, int64_t n) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1002,6 +1036,14 @@ __global__ void __launch_bounds__(256, 4) apply_kernel(PArgs A, float2 *y) {
                         (int64_t)gridDim.x * blockDim.x);
 }
 
+template <int B>
+__global__ void __launch_bounds__(256, 4) apply_snap_kernel(PArgs A, float2 *y) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    apply_steps<B>(A, SnapStore{y, A.snap, A.probe},
+                   (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                   (int64_t)gridDim.x * blockDim.x);
+}
+
 // Few steps in flight (small or fidelity-capped levels): the step is a dependent
 // chain issued by one or two warps per SM, so this instance drops the 4-blocks-per-SM
 // register cap (no parameter reloads / rematerialisation in the chain).
@@ -1109,6 +1151,8 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
     }
     if (P.locks && !(hot && n_hot > 0) && !agg)
         fn = P.b == 2 ? (void *)apply_locked_kernel<2> : (void *)apply_locked_kernel<0>;
+    else if (P.snap && !(hot && n_hot > 0) && !agg)
+        fn = P.b == 2 ? (void *)apply_snap_kernel<2> : (void *)apply_snap_kernel<0>;
     else if (hot && n_hot > 0)   // hub level: the hottest nodes staged per block
         fn = agg ? (P.b == 2 ? (void *)apply_hot_kernel<true, 2> : (void *)apply_hot_kernel<true, 0>)
                  : (P.b == 2 ? (void *)apply_hot_kernel<false, 2> : (void *)apply_hot_kernel<false, 0>);
@@ -1116,6 +1160,24 @@ int launch_apply(const PArgs &P, float2 *y, unsigned grid, int block, bool agg, 
         fn = agg ? apply_instance<true>(P.b, threads) : apply_instance<false>(P.b, threads);
     DRG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
     DRG_LAUNCHED("apply_kernel");
+    return DRG_OK;
+}
+
+// refresh of the negatives' snapshot (DRG_SAMPLED_SNAPSHOT), in the epochs' PDL chain
+int launch_snap_copy(const float2 *y, float2 *snap, int64_t n, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::min<int64_t>(ceil_div(std::max<int64_t>(n / 2, 1), 256),
+                                                   (int64_t)sm_count() * 8));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void *args[] = {&y, &snap, &n};
+    DRG_CUDA(cudaLaunchKernelExC(&cfg, (void *)snap_copy_kernel, args));
+    DRG_LAUNCHED("snap_copy_kernel");
     return DRG_OK;
 }
 
@@ -1724,6 +1786,18 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
         DRG_CUDA(locks.alloc(sizeof(int) * (size_t)n_y));
         DRG_CUDA(cudaMemsetAsync(locks.p, 0, sizeof(int) * (size_t)n_y, st));
     }
+    Scratch snap(st);
+    const bool use_snap = flags & DRG_SAMPLED_SNAPSHOT;
+    if (use_snap) {
+        if (det || agg || (hot && n_hot > 0) || (flags & (DRG_SAMPLED_FUSED | DRG_SAMPLED_LOCKED)))
+            return fail(DRG_ERR_UNSUPPORTED,
+                        "snapshot reads serve plain Hogwild levels in the split form");
+        DRG_CUDA(snap.alloc(sizeof(float2) * (size_t)n_y));
+    }
+    static const int snap_every = [] {   // (experiments: refresh every r-th epoch)
+        const char *e = getenv("DRG_SNAP_EVERY");
+        return e ? std::max(1, atoi(e)) : 1;
+    }();
     SideStreams ss;
     DRG_CUDA(side_streams(&ss));
     Events ev;   // 0 start, 1-2 drawn[2], 3-4 applied[2], 5 draws done
@@ -1794,6 +1868,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
         return evs.finish(st);
     }
     P.locks = locks.as<int>();   // NULL unless DRG_SAMPLED_LOCKED
+    P.snap = use_snap ? snap.as<float2>() : nullptr;
     int rc = draw(0);
     if (rc) return rc;
     Scratch delta(st);
@@ -1817,6 +1892,9 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
                 DRG_TRY(launch_det_epoch(P, reinterpret_cast<float2 *>(y), threads, n_y, ss.hi));
                 continue;
             }
+            if (use_snap && (c * K + e) % snap_every == 0)
+                DRG_TRY(launch_snap_copy(reinterpret_cast<const float2 *>(y), snap.as<float2>(),
+                                         n_y, ss.hi));
             DRG_TRY(launch_apply(P, reinterpret_cast<float2 *>(y), grid, block, agg, ss.hi, hot,
                                  n_hot));
         }

@@ -112,6 +112,11 @@ class OptimizerParams:
     # graph size: on for graphs below FAST_CONCURRENCY_NODES nodes, whose Hogwild
     # form is held to n/256 steps in flight by fidelity (locked_divisors)
     sampled_locks: bool | None = None
+    # update="sampled", Hogwild levels: the negatives' positions read from a read-only
+    # snapshot of y refreshed before every epoch (DRG_SAMPLED_SNAPSHOT).  None = on
+    # for plain levels with at least SNAPSHOT_MIN_THREADS steps in flight (the levels
+    # bound by random L2 operations: the C4 mesh's level 0)
+    sampled_snapshot: bool | None = None
     att_samples: int = 2           # update="sgather": attraction partners drawn per node
     # update="sampled": the update of levels above GATHER_STEPS.  "sampled" (default)
     # keeps the reference's step there too; "jacobi" gathers them -- 3-6x faster on
@@ -526,6 +531,12 @@ def sampled_divisors(n0: int, opt: "OptimizerParams") -> tuple[int, int]:
 # (174 -> 253 ms), and its small coarse levels run n/4 Hogwild -- measured faithful
 # there -- in 8-15 ms against 37-48 ms locked.
 LOCKED_DIVISORS = (1, 1)
+# Hogwild levels with at least this many steps in flight are bound by the L2's
+# random-operation rate, not by a step's latency: there the negatives are gathered
+# from a read-only snapshot (DRG_SAMPLED_SNAPSHOT) -- gathers and reductions on
+# separate arrays run at 213 G/s per step mix against 148 G/s on one array
+# (profiles/r02_l2_random_peak.txt).
+SNAPSHOT_MIN_THREADS = 40960
 
 
 def locked_divisors(opt: "OptimizerParams") -> tuple[int, int]:
@@ -910,8 +921,12 @@ class LayoutPlan:
         ip, n_tab, mp, neg = self._tables(level)
         det = o.threads == 1 and not o.sampled_fused
         rec = S.src_rec is not None and not o.sampled_fused
+        in_flight = (max_threads if max_threads is not None
+                     else self._steps_in_flight(level, div))
+        snapshot = self.snapshot_level(level, locked, det, min(in_flight, n_steps))
         flags = (int(S.hubs) * _lib.DRG_SAMPLED_AGGREGATE
                  | (_lib.DRG_SAMPLED_LOCKED if locked else 0)
+                 | (_lib.DRG_SAMPLED_SNAPSHOT if snapshot else 0)
                  | (_lib.DRG_SAMPLED_SRC_RECORDS if rec else 0)
                  | (_lib.DRG_SAMPLED_FUSED if o.sampled_fused else 0)
                  | (_lib.DRG_SAMPLED_DETERMINISTIC if det else 0)
@@ -926,7 +941,7 @@ class LayoutPlan:
                   o.iters,
                   float(o.lr0), float(gamma), float(o.eps), float(o.grad_clip), o.b,
                   o.neg_samples, seed, level,
-                  max_threads if max_threads is not None else self._steps_in_flight(level, div),
+                  in_flight,
                   flags, L.n, _lib.ptr(self.evals) if count else None,
                   _lib.ptr(S.hot) if (S.hot is not None and not det) else None,
                   0 if S.hot is None else S.hot.numel(), _lib.stream_ptr())
@@ -942,6 +957,16 @@ class LayoutPlan:
         if o.sampled_locks is not None:
             return bool(o.sampled_locks)
         return self.levels[0].n < FAST_CONCURRENCY_NODES
+
+    def snapshot_level(self, level: int, locked: bool, det: bool, in_flight: int) -> bool:
+        """Whether ``level``'s Hogwild epochs read the negatives from a snapshot."""
+        o = self.opt
+        S = self.levels[level].sampled
+        if locked or det or o.sampled_fused or S.hubs or S.hot is not None:
+            return False
+        if o.sampled_snapshot is not None:
+            return bool(o.sampled_snapshot)
+        return in_flight >= SNAPSHOT_MIN_THREADS
 
     def _steps_in_flight(self, level: int, div: int) -> int:
         """n_l / divisor, capped on levels with staged hub nodes: at HOT_MAX_THREADS

@@ -19,8 +19,15 @@ K=layout_iter; S=60; C=1
 # each, level 0 (256 MB draw chunks = 5 epochs) 4 draws + 20 applies -> 87 matching
 # launches per step; the timed step's level 0 starts at launch 87 + 63 = 150 with
 # draw(chunk 0), draw(chunk 1), apply(epoch 0)
-[ "$U" = "sampled" ] && K="draw_kernel|apply_kernel" && S=150 && C=3
+# (level 0 of the mesh runs apply_snap_kernel after a snap_copy_kernel per epoch)
+[ "$U" = "sampled" ] && K="draw_kernel|apply_kernel|apply_snap_kernel" && S=150 && C=3
 $CMD > $OUT/plain2_${W}_${U}.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k "regex:$K" -s $S -c $C -f \
       -o $OUT/full_${W}_${U} $CMD > $OUT/ncu_full_${W}_${U}.log 2>&1
 echo "full capture rc=$?"
+# 3) the per-epoch snapshot refresh of the sampled form
+if [ "$U" = "sampled" ]; then
+  ncu --set full --clock-control none -k "regex:snap_copy_kernel" -s 30 -c 1 -f \
+      -o $OUT/full_${W}_${U}_snapcopy $CMD > $OUT/ncu_full_${W}_${U}_snapcopy.log 2>&1
+  echo "snap copy capture rc=$?"
+fi

@@ -116,6 +116,10 @@ def main(name="grid", n_seeds=10, modes=("jacobi", "inplace", "sampled"), evalua
                 upd, extra = "sampled", {"sampled_fused": True}
             if upd == "sampledL":   # steps under (i, j) locks on plain levels
                 upd, extra = "sampled", {"sampled_locks": True}
+            if upd == "sampledS":   # negatives from a per-epoch snapshot on every plain level
+                upd, extra = "sampled", {"sampled_snapshot": True}
+            if upd == "sampledN":   # negatives read live (no snapshot)
+                upd, extra = "sampled", {"sampled_snapshot": False}
             if upd == "sampledH":   # plain Hogwild (no locks) on every level
                 upd, extra = "sampled", {"sampled_locks": False}
             if upd == "sampledh":   # "sampled" on every level, hub-heavy ones included

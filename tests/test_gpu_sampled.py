@@ -415,3 +415,30 @@ def test_locked_levels_policy(golden):
     y0 = y.clone()
     plan.sampled_steps(0, y, 0, plan.levels[0].n, 0, 2)      # two locked epochs run
     assert torch.isfinite(y).all() and not torch.equal(y, y0)
+
+
+# ---- negatives read from a per-epoch snapshot (DRG_SAMPLED_SNAPSHOT) ----------------
+
+@pytest.mark.parametrize("pick", ["finest", "coarsest"])
+def test_snapshot_epoch_matches_its_sequential_restatement(golden, pick):
+    """One step in flight: source and partner live, the negatives read from the
+    epoch-start copy (plus the step's own earlier reactions), every update applied at
+    once == the oracle's deferred_drawn_epoch(defer=False); and it differs from the
+    live-negatives epoch (the flag does something)."""
+    plan, _, _ = _setup(golden)
+    plan.opt = B.OptimizerParams(seed=0, neg_samples=5, iters=10, threads=4,
+                                 sampled_locks=False, sampled_snapshot=True)
+    level = _level(plan, pick)
+    n = plan.levels[level].n
+    t = 8
+    _, gamma, _ = plan._level_args(level)
+    d = plan.sampled_draws(level, 0, n, t)[0]
+    y = np.random.default_rng(11).normal(0, 1.0, size=(n, 2)).astype(np.float32)
+    yd = torch.from_numpy(y).cuda()
+    plan.sampled_steps(level, yd, 0, n, t, 1, max_threads=1)
+    want = O.deferred_drawn_epoch(y.astype(np.float64), d.cpu().numpy(), 1.0 - t / 10, gamma,
+                                  1e-3, 5.0, plan.opt.b, defer=False)
+    np.testing.assert_allclose(yd.cpu().numpy(), want, rtol=0, atol=1e-4)
+    live = O.drawn_steps(y.astype(np.float64), d.cpu().numpy(), 1.0 - t / 10, gamma, 1e-3, 5.0,
+                         plan.opt.b)
+    assert np.abs(want - live).max() > 1e-3
