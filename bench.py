@@ -303,6 +303,7 @@ def run_ours(args):
     plan = prep.plan
     sizes = prep.hierarchy.sizes
     plan_locked = [opt.update == "sampled" and plan.locked_level(lv) for lv in range(len(sizes))]
+    level_modes = [plan.level_mode(lv) for lv in range(len(sizes))]
     nnzs = [lv.nnz for lv in plan.levels]
     prep_ms = {k: round(v, 3) for k, v in prep.timings.items()}
     # the same preparation again, warm (module loading / pool growth excluded)
@@ -432,7 +433,7 @@ def run_ours(args):
     # update pass issues M + 2 gathers + M + 2 float2 reductions (1:1 mix ceiling),
     # the draw pass 4 + M random table loads (gather ceiling)
     random_access = None
-    ceil_path = os.path.join(ROOT, "profiles", "r01_l2_random_peak.txt")
+    ceil_path = os.path.join(ROOT, "profiles", "r02_l2_random_peak.txt")
     if kname.startswith("draw_kernel") and os.path.exists(ceil_path):
         ceil = {}
         for ln in open(ceil_path):
@@ -445,12 +446,16 @@ def run_ours(args):
         # alias, the row span (one {start, length} record), the row-alias record and M
         # negative alias loads
         upd, drw = n0 * 2 * (M + 2), n0 * (3 + M)
-        t_min = upd / (ceil["gather+red 1:1"] * 1e9) + drw / (ceil["gather 8B"] * 1e9)
+        # (with the negatives read from the per-epoch snapshot the update pass's mix is
+        # 5 read-only gathers + 2 gathers and 7 reductions on y: its own probe mode)
+        mix = ("snapshot-read mix 5gA+2g7rC" if level_modes[0] == "snapshot"
+               else "gather+red 1:1")
+        t_min = upd / (ceil[mix] * 1e9) + drw / (ceil["gather 8B"] * 1e9)
         random_access = {"accesses_per_launch": upd + drw,
                          "achieved_G_per_s": (upd + drw) / l0_launch_s / 1e9,
                          "ceiling_G_per_s": ceil, "t_min_us": t_min * 1e6,
-                         "frac": t_min / l0_launch_s,
-                         "source": "profiles/r01_l2_random_peak.txt"}
+                         "frac": t_min / l0_launch_s, "update_mix": mix,
+                         "source": "profiles/r02_l2_random_peak.txt"}
 
     # e2e through the public API: pinned host CSR in, host positions out
     e2e = None
@@ -499,8 +504,7 @@ def run_ours(args):
             "config": {"workload": name, "desc": WORKLOADS[name]["desc"], "levels": sizes,
                        "nnz_per_level": nnzs,
                        "iters_per_level": T, "update": opt.update, "hub_levels": opt.hub_levels,
-                       "locked_levels": [lv for lv in range(len(sizes))
-                                         if opt.update == "sampled" and plan_locked[lv]],
+                       "level_modes": level_modes,
                        "l2": "256 MiB flush between steps; level-0 stream "
                              f"{alg_bytes / 1e9:.2f} GB/iteration > 126 MB L2",
                        "parallelism": f"node-range x{world}" if world > 1 else "single GPU"},

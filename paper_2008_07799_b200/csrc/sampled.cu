@@ -1044,6 +1044,148 @@ __global__ void __launch_bounds__(256, 4) apply_snap_kernel(PArgs A, float2 *y) 
                    (int64_t)gridDim.x * blockDim.x);
 }
 
+// ---- snapshot form with the negatives drawn in the update pass -------------------
+// One table of 16-byte records {fp32 threshold, alias, y.x, y.y} per node: Q^l's Vose
+// bucket v next to node v's snapshot position.  A negative's draw (bucket -> record)
+// then brings the position of the bucket's own node in the same sector: one random
+// L2 read per negative instead of two (the alias record in the draw pass, the
+// position in the update pass; a second 8-byte read only when the alias is taken or
+// a redraw is needed).  The draws use draw_step's counters and the same records, so
+// the negatives are bit for bit those drg_sampled_draws reports; the draw pass then
+// resolves only the pair (i, j) (8-byte draw records instead of 28).  M <= kMaxNeg.
+struct NArgs {
+    uint4 *rec;             // [n_y]; .xy = Q^l bucket (zeros past neg.n), .zw = snapshot position
+    int64_t n, tail_n;      // NegTab: Vose over [0, n), uniform tail [n, n + tail_n)
+    uint32_t tail_thr;
+    uint32_t key0, key1, level;
+    int t;
+    int64_t step_lo;
+    unsigned long long *evals;
+};
+
+__global__ void negsnap_init_kernel(const uint2 *__restrict__ alias, int64_t n_alias, uint4 *rec,
+                                    int64_t n) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const uint2 a = v < n_alias ? alias[v] : make_uint2(0u, 0u);
+        rec[v] = make_uint4(a.x, a.y, 0u, 0u);
+    }
+}
+
+__global__ void negsnap_refresh_kernel(const float2 *y, uint4 *rec, int64_t n) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<float2 *>(rec + v)[1] = __ldcg(y + v);
+}
+
+struct NegSnapStore {   // source / partner live on y; negatives resolved by the caller
+    float2 *y;
+    int probe;
+    int32_t c[kMaxNeg];
+    float2 p[kMaxNeg];
+    __device__ __forceinline__ float2 load(int64_t v) const { return ld_y(y, v); }
+    __device__ __forceinline__ float2 load_neg(int64_t v) const {
+        float2 r = p[0];
+#pragma unroll
+        for (int q = 1; q < kMaxNeg; ++q)
+            if (c[q] == (int32_t)v) r = p[q];
+        return r;
+    }
+    __device__ __forceinline__ void add(int64_t v, float dx, float dy) const {
+        add_y_w<false>(y, v, dx, dy, probe);
+    }
+    __device__ __forceinline__ void add_neg(int64_t v, float dx, float dy) const { add(v, dx, dy); }
+};
+
+__device__ __forceinline__ float2 negsnap_pos(const uint4 *rec, int64_t v) {
+    return __ldg(reinterpret_cast<const float2 *>(rec + v) + 1);
+}
+
+// MC > 0: M known at compile time (the default M = 5: no dead sixth negative held in
+// registers, no predication on m < M)
+template <int B, int MC>
+__global__ void __launch_bounds__(256, 3) apply_negsnap_kernel(PArgs A0, NArgs N, float2 *y) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    PArgs A = A0;
+    if (MC > 0) A.M = MC;
+    const int Me = MC > 0 ? MC : min(A.M, kMaxNeg);
+    const int64_t ns = A.n_steps, sd = A.stride;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const uint4 *rec = N.rec;
+    SArgs K;   // the counter layout of draw_step
+    K.key0 = N.key0;
+    K.key1 = N.key1;
+    K.level = N.level;
+    unsigned nev = 0;
+    int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (sl < ns) {
+        int32_t ci = __ldcs(A.draws + sl), cj = __ldcs(A.draws + sd + sl);
+        for (; sl < ns; sl += nthreads) {
+            const int64_t i = ci, j = cj, cur = sl;
+            const int64_t s = N.step_lo + sl;
+            const uint32_t c1 = (uint32_t)(s >> 32) ^ ((uint32_t)N.t << 1);
+            if (sl + nthreads < ns) {
+                ci = __ldcs(A.draws + sl + nthreads);
+                cj = __ldcs(A.draws + sd + sl + nthreads);
+            }
+            NegSnapStore st;
+            st.y = y;
+            st.probe = A.probe;
+            // first attempt of every negative: one record each, all in flight
+            uint4 r[kMaxNeg];
+            int32_t bk[kMaxNeg];
+            uint32_t coin[kMaxNeg];
+#pragma unroll
+            for (int m = 0; m < kMaxNeg; ++m) {
+                if (m < Me) {
+                    const u32x4 q = neg_draw(K, s, c1, m, 0);
+                    const bool tail = q.w < N.tail_thr;
+                    bk[m] = (int32_t)(tail ? N.n + bucket(N.tail_n, q.x, q.y)
+                                           : bucket(N.n, q.x, q.y));
+                    coin[m] = tail ? 0u : q.z;   // (a tail pick is always its own node)
+                    r[m] = __ldg(rec + bk[m]);
+                    if (tail) r[m].x = 0x7f800000u;   // threshold +inf: accept
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < kMaxNeg; ++m) {
+                st.c[m] = -1;
+                st.p[m] = make_float2(0.f, 0.f);
+                if (m < Me) {
+                    const bool own = u32_to_unit(coin[m]) < __uint_as_float(r[m].x);
+                    int64_t c = own ? bk[m] : (int64_t)r[m].y;
+                    bool have = own;
+                    float2 pos = make_float2(__uint_as_float(r[m].z), __uint_as_float(r[m].w));
+                    for (int attempt = 1; (c == i || c == j) && attempt < 9; ++attempt) {
+                        const u32x4 q = neg_draw(K, s, c1, m, attempt);
+                        have = false;
+                        if (q.w < N.tail_thr) {
+                            c = N.n + bucket(N.tail_n, q.x, q.y);
+                        } else {
+                            const int64_t b2 = bucket(N.n, q.x, q.y);
+                            const uint4 r2 = __ldg(rec + b2);
+                            const bool own2 = u32_to_unit(q.z) < __uint_as_float(r2.x);
+                            c = own2 ? b2 : (int64_t)r2.y;
+                            if (own2) {
+                                have = true;
+                                pos = make_float2(__uint_as_float(r2.z), __uint_as_float(r2.w));
+                            }
+                        }
+                    }
+                    if (c != i && c != j) {
+                        st.c[m] = (int32_t)c;
+                        st.p[m] = have ? pos : negsnap_pos(rec, c);
+                        ++nev;
+                    }
+                }
+            }
+            step_body<B>(A, st, i, j, st.c, cur);
+        }
+    }
+    count_evals(N.evals, nev);
+}
+
 // Few steps in flight (small or fidelity-capped levels): the step is a dependent
 // chain issued by one or two warps per SM, so this instance drops the 4-blocks-per-SM
 // register cap (no parameter reloads / rematerialisation in the chain).
@@ -1178,6 +1320,37 @@ int launch_snap_copy(const float2 *y, float2 *snap, int64_t n, cudaStream_t st) 
     void *args[] = {&y, &snap, &n};
     DRG_CUDA(cudaLaunchKernelExC(&cfg, (void *)snap_copy_kernel, args));
     DRG_LAUNCHED("snap_copy_kernel");
+    return DRG_OK;
+}
+
+int launch_negsnap_epoch(const PArgs &P, const NArgs &N, float2 *y, int64_t n_y, unsigned grid,
+                         int block, bool refresh, cudaStream_t st) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (refresh) {
+        cfg.gridDim = dim3((unsigned)std::min<int64_t>(ceil_div(n_y, 256), (int64_t)sm_count() * 8));
+        cfg.blockDim = dim3(256);
+        const float2 *yc = y;
+        uint4 *rec = N.rec;
+        void *rargs[] = {&yc, &rec, &n_y};
+        DRG_CUDA(cudaLaunchKernelExC(&cfg, (void *)negsnap_refresh_kernel, rargs));
+        DRG_LAUNCHED("negsnap_refresh_kernel");
+    }
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3((unsigned)block);
+    PArgs Q = P;
+    NArgs M = N;
+    void *args[] = {&Q, &M, &y};
+    void *fn = P.b == 2 ? (P.M == 5 ? (void *)apply_negsnap_kernel<2, 5>
+                                    : (void *)apply_negsnap_kernel<2, 0>)
+                        : (void *)apply_negsnap_kernel<0, 0>;
+    DRG_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+    DRG_LAUNCHED("apply_negsnap_kernel");
     return DRG_OK;
 }
 
@@ -1772,7 +1945,18 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
     }
     // split: draw_kernel (K epochs per launch, double-buffered, low-priority stream)
     // -> apply_kernel per epoch (high-priority stream); joined back into `stream`
-    const size_t rec_bytes = (size_t)(2 + M) * sizeof(int32_t) * (size_t)n_steps;
+    // snapshot form with the negatives drawn in the update pass (apply_negsnap_kernel):
+    // the draw pass resolves only the pairs.  (DRG_NEGSNAP=0: the negatives stay in the
+    // draw pass and only their positions come from the snapshot, apply_snap_kernel)
+    static const bool negsnap_on = [] {
+        const char *e = getenv("DRG_NEGSNAP");
+        return !(e && e[0] == '0');
+    }();
+    const bool use_negsnap = (flags & DRG_SAMPLED_SNAPSHOT) && negsnap_on && M >= 1 &&
+                             M <= kMaxNeg && !det && !agg && !(hot && n_hot > 0) &&
+                             !(flags & DRG_SAMPLED_LOCKED);
+    const int Md = use_negsnap ? 0 : M;   // negatives in the draw records
+    const size_t rec_bytes = (size_t)(2 + Md) * sizeof(int32_t) * (size_t)n_steps;
     const int K = (int)std::max<int64_t>(1, std::min<int64_t>(n_iter, (int64_t)(kDrawBudget / rec_bytes)));
     const int nchunks = (n_iter + K - 1) / K;
     Scratch buf(st);
@@ -1792,7 +1976,14 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
         if (det || agg || (hot && n_hot > 0) || (flags & (DRG_SAMPLED_FUSED | DRG_SAMPLED_LOCKED)))
             return fail(DRG_ERR_UNSUPPORTED,
                         "snapshot reads serve plain Hogwild levels in the split form");
-        DRG_CUDA(snap.alloc(sizeof(float2) * (size_t)n_y));
+        DRG_CUDA(snap.alloc((use_negsnap ? sizeof(uint4) : sizeof(float2)) * (size_t)n_y));
+        if (use_negsnap) {
+            negsnap_init_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_y, 256),
+                                                              (int64_t)sm_count() * 8),
+                                  256, 0, st>>>(reinterpret_cast<const uint2 *>(neg_alias), neg_n,
+                                                snap.as<uint4>(), n_y);
+            DRG_LAUNCHED("negsnap_init_kernel");
+        }
     }
     static const int snap_every = [] {   // (experiments: refresh every r-th epoch)
         const char *e = getenv("DRG_SNAP_EVERY");
@@ -1816,7 +2007,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
     D.n = n;
     D.step_lo = step_lo;
     D.n_steps = n_steps;
-    D.M = M;
+    D.M = Md;
     D.key0 = (uint32_t)seed;
     D.key1 = (uint32_t)(seed >> 32);
     D.level = (uint32_t)level;
@@ -1868,7 +2059,7 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
         return evs.finish(st);
     }
     P.locks = locks.as<int>();   // NULL unless DRG_SAMPLED_LOCKED
-    P.snap = use_snap ? snap.as<float2>() : nullptr;
+    P.snap = use_snap && !use_negsnap ? snap.as<float2>() : nullptr;
     int rc = draw(0);
     if (rc) return rc;
     Scratch delta(st);
@@ -1890,6 +2081,22 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
             P.draws = chunk_buf(c) + (size_t)e * (rec_bytes / 4);
             if (det) {
                 DRG_TRY(launch_det_epoch(P, reinterpret_cast<float2 *>(y), threads, n_y, ss.hi));
+                continue;
+            }
+            if (use_negsnap) {
+                NArgs N;
+                N.rec = snap.as<uint4>();
+                N.n = D.neg.n;
+                N.tail_n = D.neg.tail_n;
+                N.tail_thr = D.neg.tail_thr;
+                N.key0 = D.key0;
+                N.key1 = D.key1;
+                N.level = D.level;
+                N.t = t;
+                N.step_lo = step_lo;
+                N.evals = ev_ctr;
+                DRG_TRY(launch_negsnap_epoch(P, N, reinterpret_cast<float2 *>(y), n_y, grid, block,
+                                             (c * K + e) % snap_every == 0, ss.hi));
                 continue;
             }
             if (use_snap && (c * K + e) % snap_every == 0)

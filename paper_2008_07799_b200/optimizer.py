@@ -958,6 +958,27 @@ class LayoutPlan:
             return bool(o.sampled_locks)
         return self.levels[0].n < FAST_CONCURRENCY_NODES
 
+    def level_mode(self, level: int) -> str:
+        """How ``level``'s sampled epochs run at the plan's parameters: "deterministic",
+        "fused", "hub" (warp-aggregated / staged hot nodes), "locked", "snapshot"
+        (Hogwild, negatives from the per-epoch snapshot) or "hogwild"."""
+        o = self.opt
+        S = self.levels[level].sampled
+        if S is None or o.update != "sampled":
+            return o.update
+        if o.sampled_fused:
+            return "fused"
+        if o.threads == 1:
+            return "deterministic"
+        if S.hubs or S.hot is not None:
+            return "hub"
+        if self.locked_level(level):
+            return "locked"
+        fine, coarse = sampled_divisors(self.levels[0].n, o)
+        in_flight = min(self._steps_in_flight(level, fine if level == 0 else coarse),
+                        self.levels[level].n)
+        return "snapshot" if self.snapshot_level(level, False, False, in_flight) else "hogwild"
+
     def snapshot_level(self, level: int, locked: bool, det: bool, in_flight: int) -> bool:
         """Whether ``level``'s Hogwild epochs read the negatives from a snapshot."""
         o = self.opt

@@ -435,10 +435,20 @@ def test_snapshot_epoch_matches_its_sequential_restatement(golden, pick):
     d = plan.sampled_draws(level, 0, n, t)[0]
     y = np.random.default_rng(11).normal(0, 1.0, size=(n, 2)).astype(np.float32)
     yd = torch.from_numpy(y).cuda()
+    plan.evals = None
     plan.sampled_steps(level, yd, 0, n, t, 1, max_threads=1)
     want = O.deferred_drawn_epoch(y.astype(np.float64), d.cpu().numpy(), 1.0 - t / 10, gamma,
                                   1e-3, 5.0, plan.opt.b, defer=False)
     np.testing.assert_allclose(yd.cpu().numpy(), want, rtol=0, atol=1e-4)
+    # the update pass draws the negatives itself here (apply_negsnap_kernel): the same
+    # ones as the draw pass reports, counted by the distance-evaluation counter
+    dn = d.cpu().numpy()
+    assert int(plan.evals) == int((dn[0] != dn[1]).sum() + (dn[2:] >= 0).sum())
+    # ... and concurrently (Hogwild): finite, and close to the sequential result
+    yc = torch.from_numpy(y).cuda()
+    plan.sampled_steps(level, yc, 0, n, t, 1, max_threads=64)
+    assert torch.isfinite(yc).all()
+    assert float((yc - yd).abs().mean()) < 0.05 * float((yd - torch.from_numpy(y).cuda()).abs().mean()) + 1e-3
     live = O.drawn_steps(y.astype(np.float64), d.cpu().numpy(), 1.0 - t / 10, gamma, 1e-3, 5.0,
                          plan.opt.b)
     assert np.abs(want - live).max() > 1e-3
