@@ -264,7 +264,11 @@ int drg_row_spans(const int64_t *indptr, int64_t n, uint64_t *out_span, void *st
  * every epoch (their reactions, like every other update, still go to y at once):
  * random gathers and reductions on separate arrays run 1.8x faster than on one
  * (the two L2 partitions keep replicas of read-only lines).  A negative's position
- * is up to one epoch old.  Plain Hogwild levels in the split form only. */
+ * is up to one epoch old.  Plain Hogwild levels in the split form only.  For M <= 6
+ * the copy is a table of 16-byte records {Q^l bucket v, position of v} and the
+ * update pass draws the negatives itself (same counters and records as the draw
+ * pass: the same negatives), so a negative costs one random read instead of two
+ * and the draw pass resolves only the pairs. */
 #define DRG_SAMPLED_SNAPSHOT 64
 
 int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_span, const uint64_t *rec,
