@@ -446,6 +446,11 @@ def run_ours(args):
         # alias, the row span (one {start, length} record), the row-alias record and M
         # negative alias loads
         upd, drw = n0 * 2 * (M + 2), n0 * (3 + M)
+        if level_modes[0] == "snapshot" and M <= 6:
+            # the update pass draws the negatives itself from {bucket, position}
+            # records (one read per negative in place of alias + position): the M
+            # record reads replace its M position gathers, the draw pass keeps 3
+            drw = n0 * 3
         # (with the negatives read from the per-epoch snapshot the update pass's mix is
         # 5 read-only gathers + 2 gathers and 7 reductions on y: its own probe mode)
         mix = ("snapshot-read mix 5gA+2g7rC" if level_modes[0] == "snapshot"
