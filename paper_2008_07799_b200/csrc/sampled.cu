@@ -1907,8 +1907,8 @@ extern "C" int drg_layout_sampled(const int64_t *indptr, const uint64_t *row_spa
     while (block > 32 && threads / block < 2 * (int64_t)sm_count()) block /= 2;
     const unsigned grid = (unsigned)(threads / block);
     auto lr_at = [&](int t) { return (float)std::max(lr0 * (1.0 - (double)t / (double)iters), 0.0); };
-    if ((flags & DRG_SAMPLED_LOCKED) && (flags & DRG_SAMPLED_FUSED))
-        return fail(DRG_ERR_UNSUPPORTED, "locked steps serve the split form");
+    if ((flags & (DRG_SAMPLED_LOCKED | DRG_SAMPLED_SNAPSHOT)) && (flags & DRG_SAMPLED_FUSED))
+        return fail(DRG_ERR_UNSUPPORTED, "locked steps and snapshot reads serve the split form");
     if ((flags & DRG_SAMPLED_SRC_RECORDS) && (flags & DRG_SAMPLED_FUSED))
         return fail(DRG_ERR_UNSUPPORTED, "source records serve the split form");
     if ((flags & DRG_SAMPLED_FUSED) && map)

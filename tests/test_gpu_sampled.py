@@ -453,3 +453,35 @@ def test_snapshot_epoch_matches_its_sequential_restatement(golden, pick):
     live = O.drawn_steps(y.astype(np.float64), d.cpu().numpy(), 1.0 - t / 10, gamma, 1e-3, 5.0,
                          plan.opt.b)
     assert np.abs(want - live).max() > 1e-3
+
+
+def test_sampled_flag_combinations_are_rejected(golden):
+    """DRG_SAMPLED_LOCKED / DRG_SAMPLED_SNAPSHOT serve plain Hogwild levels in the split
+    form: with the deterministic mode, the fused form or each other the library
+    answers DRG_ERR_UNSUPPORTED (NotImplementedError), never a silent fallback."""
+    from paper_2008_07799_b200 import _lib
+    plan, _, _ = _setup(golden)
+    L = plan.levels[0]
+    S = L.sampled
+    ip, n_tab, mp, neg = plan._tables(0)
+    y = torch.zeros((L.n, 2), dtype=torch.float32, device="cuda")
+
+    def run(flags):
+        _lib.call("drg_layout_sampled", _lib.ptr(ip), _lib.ptr(S.span), None,
+                  _lib.ptr(S.row_alias), _lib.ptr(S.src_alias), None, _lib.ptr(neg.alias),
+                  _lib.ptr(mp), n_tab, neg.n, neg.tail_n, float(neg.tail_p), _lib.ptr(y), 0, L.n,
+                  0, 1, 10, 1.0, 0.1, 1e-3, 5.0, 2, 5, 1, 0, 64, flags, L.n, None, None, 0,
+                  _lib.stream_ptr())
+
+    run(_lib.DRG_SAMPLED_LOCKED)
+    run(_lib.DRG_SAMPLED_SNAPSHOT)
+    for bad in (_lib.DRG_SAMPLED_LOCKED | _lib.DRG_SAMPLED_DETERMINISTIC,
+                _lib.DRG_SAMPLED_LOCKED | _lib.DRG_SAMPLED_FUSED,
+                _lib.DRG_SAMPLED_LOCKED | _lib.DRG_SAMPLED_AGGREGATE,
+                _lib.DRG_SAMPLED_SNAPSHOT | _lib.DRG_SAMPLED_LOCKED,
+                _lib.DRG_SAMPLED_SNAPSHOT | _lib.DRG_SAMPLED_DETERMINISTIC,
+                _lib.DRG_SAMPLED_SNAPSHOT | _lib.DRG_SAMPLED_FUSED):
+        with pytest.raises((NotImplementedError, RuntimeError, ValueError)):
+            run(bad)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all()
