@@ -628,7 +628,10 @@ struct SnapStore {
     const float2 *snap;
     int probe;
     __device__ __forceinline__ float2 load(int64_t v) const { return ld_y(y, v); }
-    __device__ __forceinline__ float2 load_neg(int64_t v) const { return __ldg(snap + v); }
+    // (ld.cg, not the non-coherent path: with programmatic dependent launches this
+    // kernel's blocks can become resident while the previous epoch's blocks still
+    // fill the SM's L1 with the old snapshot)
+    __device__ __forceinline__ float2 load_neg(int64_t v) const { return __ldcg(snap + v); }
     __device__ __forceinline__ void add(int64_t v, float dx, float dy) const {
         add_y_w<false>(y, v, dx, dy, probe);
     }
@@ -1098,8 +1101,11 @@ struct NegSnapStore {   // source / partner live on y; negatives resolved by the
     __device__ __forceinline__ void add_neg(int64_t v, float dx, float dy) const { add(v, dx, dy); }
 };
 
+// (record reads through L2 (ld.cg), not the non-coherent path: with programmatic
+// dependent launches this kernel's blocks can become resident while the previous
+// epoch's blocks still fill the SM's L1 with the old positions)
 __device__ __forceinline__ float2 negsnap_pos(const uint4 *rec, int64_t v) {
-    return __ldg(reinterpret_cast<const float2 *>(rec + v) + 1);
+    return __ldcg(reinterpret_cast<const float2 *>(rec + v) + 1);
 }
 
 // MC > 0: M known at compile time (the default M = 5: no dead sixth negative held in
@@ -1144,7 +1150,7 @@ __global__ void __launch_bounds__(256, 3) apply_negsnap_kernel(PArgs A0, NArgs N
                     bk[m] = (int32_t)(tail ? N.n + bucket(N.tail_n, q.x, q.y)
                                            : bucket(N.n, q.x, q.y));
                     coin[m] = tail ? 0u : q.z;   // (a tail pick is always its own node)
-                    r[m] = __ldg(rec + bk[m]);
+                    r[m] = __ldcg(rec + bk[m]);
                     if (tail) r[m].x = 0x7f800000u;   // threshold +inf: accept
                 }
             }
@@ -1164,7 +1170,7 @@ __global__ void __launch_bounds__(256, 3) apply_negsnap_kernel(PArgs A0, NArgs N
                             c = N.n + bucket(N.tail_n, q.x, q.y);
                         } else {
                             const int64_t b2 = bucket(N.n, q.x, q.y);
-                            const uint4 r2 = __ldg(rec + b2);
+                            const uint4 r2 = __ldcg(rec + b2);
                             const bool own2 = u32_to_unit(q.z) < __uint_as_float(r2.x);
                             c = own2 ? b2 : (int64_t)r2.y;
                             if (own2) {
