@@ -45,6 +45,24 @@ def test_python_binding_covers_header():
     assert set(_lib.SIGNATURES) == set(declared_symbols())
 
 
+def test_python_constants_equal_the_header_macros():
+    """Every DRG_SAMPLED_* flag and DRG_ERR_* status the binding uses has the value
+    the header defines (a flag renumbered on one side only would silently select
+    another kernel)."""
+    from paper_2008_07799_b200 import _lib
+    macros = {m.group(1): int(m.group(2), 0) for m in
+              re.finditer(r"^#define\s+(DRG_(?:SAMPLED|ERR)_\w+)\s+\(?(-?\d+)\)?\s*$",
+                          open(HEADER).read(), re.M)}
+    flags = {k: v for k, v in macros.items() if k.startswith("DRG_SAMPLED_")}
+    assert len(flags) >= 7 and len(set(flags.values())) == len(flags)
+    assert all(v & (v - 1) == 0 for v in flags.values())   # single bits
+    for name, value in macros.items():
+        if hasattr(_lib, name):
+            assert getattr(_lib, name) == value, name
+    for name in flags:
+        assert hasattr(_lib, name), name
+
+
 def test_params_validation_matches_reference():
     from paper_2008_07799_b200 import OptimizerParams, SimilarityParams
     for bad in (dict(k=0), dict(k=7), dict(perplexity=0.5)):

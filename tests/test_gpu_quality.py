@@ -7,10 +7,14 @@ the reference's own layouts by tests/test_oracle_golden.py) on this box's host
 cores; KL with the reference's unnormalised t-kernel and exact Z, NP =
 metrics.py:114-145 with k_eval = 2.
 
-The reference's own seed-to-seed spread of NP is ~13% per layout,
-so the NP gap is asserted as "consistent with |gap| <= 2%": the paired mean
-relative gap over the seeds must lie within 2% + 2 standard errors.  KL (spread
-~0.3%) is asserted within 2% directly.
+The reference's own seed-to-seed spread of NP is ~13% per layout (SURVEY §8(d));
+the paired per-seed gap between two layouts of the same seed is as wide (-30% ..
++40% on the reduced C2, for every GPU form AND between two runs of the reference's
+own Hogwild: scripts/diag_c2_locks.py).  So the NP gap is asserted as "consistent
+with |gap| <= 2%": the paired mean relative gap over the seeds must lie within 2% +
+3 standard errors (a 2-sigma bar fails a faithful run about once in 100; 40 seeds
+keep the bar near 8%, below the -11.6% a Hogwild run without the locks shows).  KL
+(spread ~0.3%) is asserted within 2% directly.
 """
 
 from __future__ import annotations
@@ -61,7 +65,7 @@ def _check(rows):
     d = np_ours / np_ref - 1
     np_gap, np_se = float(d.mean()), float(d.std(ddof=1) / np.sqrt(len(d)))
     assert abs(kl_gap) <= 0.02, kl_gap
-    assert abs(np_gap) <= 0.02 + 2 * np_se, (np_gap, np_se)
+    assert abs(np_gap) <= 0.02 + 3 * np_se, (np_gap, np_se, kl_gap)
     return kl_gap, np_gap, np_se
 
 
@@ -74,16 +78,16 @@ def test_c1_grid_final_layout_parity(threads):
     g = synthetic.grid(100, 100, device="host")
     og, bg = O.Graph(g.indptr, g.indices), B.Graph(g.indptr, g.indices)
     rows = _arms(og, bg, 2, 30.0, 300, 1, "uniform", range(5000, 5040), threads)
-    _check(rows)
+    print("C1, threads", threads, _check(rows))
 
 
 @pytest.mark.parametrize("threads", [1, 16])
 def test_c2_reduced_rgg_final_layout_parity(threads):
     """BASELINE C2 reduced to 50 000 points (mean degree 10), k=3, perplexity 30,
-    500 iterations, 3 levels; 20 seeds; threads = 1 (the default, deterministic) and
+    500 iterations, 3 levels; 40 seeds; threads = 1 (the default, deterministic) and
     threads = 16 (steps under (i, j) locks on every level)."""
     from paper_2008_07799_b200 import synthetic
     g = synthetic.rgg(50_000, seed=0, device="host")
     og, bg = O.Graph(g.indptr, g.indices), B.Graph(g.indptr, g.indices)
-    rows = _arms(og, bg, 3, 30.0, 500, 3, "normal", range(700, 720), threads)
-    _check(rows)
+    rows = _arms(og, bg, 3, 30.0, 500, 3, "normal", range(700, 740), threads)
+    print("reduced C2, threads", threads, _check(rows))
