@@ -779,7 +779,15 @@ class LayoutPlan:
                 self.opt.hub_levels == "jacobi":
             u = "jacobi"
         if u == "sampled":
-            k = "sampled_kernel" if self.opt.sampled_fused else "draw_kernel + apply_kernel"
+            mode = self.level_mode(level)
+            k = {"fused": "sampled_kernel",
+                 "locked": "draw_kernel + apply_locked_kernel",
+                 "deterministic": "draw_kernel + apply_det_kernel / flush_kernel",
+                 "hub": ("draw_kernel + apply_hot_kernel" if L.sampled.hot is not None
+                         else "draw_kernel + apply_kernel<AGG>"),
+                 "snapshot": ("draw_kernel + negsnap_refresh_kernel + apply_negsnap_kernel"
+                              if M <= 6 else "draw_kernel + snap_copy_kernel + apply_snap_kernel"),
+                 }.get(mode, "draw_kernel + apply_kernel")
             return k, L.n * (92 + 32 * M)
         if u == "sgather":
             S = self.opt.att_samples
