@@ -264,6 +264,7 @@ def run_reference_arm(args):
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": name, "desc": WORKLOADS[name]["desc"], "levels": sizes,
+                   "iters_per_level": opt.iters, "update": "sampled",
                    "step": "one epoch at every level (bounded sample of the layout stage)"},
         "interactions_per_s": inter,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
